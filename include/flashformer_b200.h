@@ -1,0 +1,154 @@
+/*
+ * flashformer_b200.h -- C-ABI of the B200 whole-model decode kernel.
+ *
+ * Drop-in boundary for the reference's decode path.  The reference
+ * (/root/reference/proj/include/fusesim/) has no FFI: its "operator API" is two
+ * header-only C++ calls that this ABI replaces:
+ *
+ *   fusesim::execute_program(programs, plan, store, tokens, pos)
+ *       interpreter.hpp:502-506  -> ffb_decode_step(...)
+ *   fusesim::reference_forward(store, tokens, pos)
+ *       reference.hpp:37-139     -> ffb_decode_step(...) (same contract)
+ *
+ * and the pieces of fusesim::TensorStore those calls mutate or read:
+ *   init_weights / TensorStore weights   tensor_store.hpp:240-366 -> ffb_upload_tensor
+ *   KVCache::set_position / k_at / v_at  tensor_store.hpp:109-125 -> ffb_kv_set / ffb_kv_get
+ *   KVCache::set_length / length         tensor_store.hpp:77,118  -> ffb_kv_set_length / ffb_kv_length
+ *   ModelConfig (+ validate)             config.hpp:45-86         -> ffb_model_config / ffb_create
+ *   RunMode {Baseline,Fused,FusedOverlap} types.hpp:64            -> ffb_set_mode
+ *
+ * Conventions:
+ *   - plain pointers and sizes only; host pointers unless a name says _device.
+ *   - every call returns an ffb_status; ffb_last_error() holds a thread-local
+ *     message.  FFB_VALIDATION mirrors fusesim::ValidationError (bad token,
+ *     position != cache length, cache capacity), FFB_UNSUPPORTED means no
+ *     compiled kernel specialisation matches the config.
+ *   - one CUDA stream per handle (or the caller's stream); a handle is not
+ *     re-entrant.  The KV length advances only when a step succeeds.
+ *   - no CPU fallback: on a machine without an sm_100 device ffb_create fails.
+ */
+#ifndef FLASHFORMER_B200_H
+#define FLASHFORMER_B200_H
+
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#pragma GCC visibility push(default)
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum ffb_status {
+    FFB_OK = 0,
+    FFB_USAGE = 1,         /* bad argument / handle / name (CLI usage=1, types.hpp:14) */
+    FFB_VALIDATION = 2,    /* fusesim::ValidationError equivalent (CLI validation=2) */
+    FFB_DEVICE = 3,        /* CUDA error */
+    FFB_UNSUPPORTED = 4    /* no template instantiation for this model shape */
+} ffb_status;
+
+/* fusesim::RunMode (types.hpp:64): one launch per sublayer stage, one
+ * persistent launch with the producer waiting at every barrier, or one
+ * persistent launch whose producer streams across barriers. */
+typedef enum ffb_mode {
+    FFB_MODE_BASELINE = 0,
+    FFB_MODE_FUSED = 1,
+    FFB_MODE_FUSED_OVERLAP = 2
+} ffb_mode;
+
+/* fusesim::ModelConfig (config.hpp:45-86), decoder kind.
+ * dtype: 0 = bf16 (the only compiled storage type).
+ * quant_bits: 0 (bf16 weights), 4 (reference int4 g128), 8 (int8 extension). */
+typedef struct ffb_model_config {
+    int64_t layers, d_model, d_inter, d_head, n_q_heads, n_kv_heads, vocab_size;
+    double rope_theta, rmsnorm_eps;
+    int32_t dtype;
+    int32_t quant_bits;
+    int32_t quant_group;
+    int64_t batch;
+} ffb_model_config;
+
+typedef struct ffb_model ffb_model;
+
+const char *ffb_last_error(void);
+const char *ffb_version(void);
+
+/* 1 if a kernel specialisation exists for this shape (no device needed). */
+int ffb_config_supported(const ffb_model_config *cfg);
+
+/* Allocates weights, KV cache [L][B][Hkv][max_seq_len][d_head] bf16 and
+ * scratch on `device`.  tp_rank/tp_size: tensor-parallel shard (tp_size 1 = whole model). */
+ffb_status ffb_create(const ffb_model_config *cfg, int64_t max_seq_len, int device,
+                      int tp_rank, int tp_size, ffb_model **out);
+void ffb_destroy(ffb_model *m);
+
+/* Weight packer.  `name` uses the reference's tensor names
+ * (tensor_store.hpp:344-363): "layer.<l>.wqkv", "layer.<l>.waout",
+ * "layer.<l>.wffn1", "layer.<l>.wffn2t", "layer.<l>.norm_attn",
+ * "layer.<l>.norm_ffn", "final_norm", "embedding", "lm_head".  `values` is the
+ * TensorStore's row-major f32 array (n = rows*cols).  bf16 matrices are
+ * rounded RNE (exact for reference stores, whose values are already on the
+ * bf16 grid); norm gains stay f32. */
+ffb_status ffb_upload_tensor(ffb_model *m, const char *name, const float *values, int64_t n);
+
+/* Fills every weight on the device with seeded synthetic values of the right
+ * scale (bench / smoke use; no host arrays involved). */
+ffb_status ffb_init_synthetic(ffb_model *m, uint64_t seed);
+
+/* KV cache access mirroring KVCache (tensor_store.hpp:63-150).  k/v: d_head
+ * f32 values, rounded to bf16 on store. */
+ffb_status ffb_kv_set(ffb_model *m, int64_t b, int64_t layer, int64_t head, int64_t pos,
+                      const float *k, const float *v);
+ffb_status ffb_kv_get(ffb_model *m, int64_t b, int64_t layer, int64_t head, int64_t pos,
+                      float *k, float *v);
+/* Bulk import of the reference layout [B][L][Hkv][S_src][dh] f32, positions [0, n_pos). */
+ffb_status ffb_kv_import(ffb_model *m, const float *k, const float *v, int64_t src_max_seq,
+                         int64_t n_pos);
+ffb_status ffb_kv_set_length(ffb_model *m, int64_t layer, int64_t n);
+int64_t ffb_kv_length(const ffb_model *m, int64_t layer);
+
+ffb_status ffb_set_mode(ffb_model *m, ffb_mode mode);
+
+/* One decode step for every batch row (reference.hpp:37-139 contract):
+ * tokens[batch] (host), pos == kv length of every layer, appends one KV
+ * position per layer.  logits_out: batch x vocab f32 (host, may be NULL);
+ * greedy_out: batch int64 argmax with lowest-index tie break (host, may be
+ * NULL).  stream: cudaStream_t or NULL for the handle's stream.  Synchronous
+ * w.r.t. the host outputs. */
+ffb_status ffb_decode_step(ffb_model *m, const int64_t *tokens, int64_t pos, float *logits_out,
+                           int64_t *greedy_out, void *stream);
+
+/* Same step with device-resident inputs/outputs, fully asynchronous on
+ * `stream`: d_tokens[batch] int64, d_logits (batch x vocab f32) and d_greedy
+ * (batch int64) device pointers (either may be NULL -> internal buffers).
+ * The caller guarantees pos == kv length; the length advances on enqueue. */
+ffb_status ffb_decode_step_device(ffb_model *m, const int64_t *d_tokens, int64_t pos,
+                                  float *d_logits, int64_t *d_greedy, void *stream);
+
+/* Introspection for roofline accounting and tests. */
+typedef struct ffb_info {
+    int32_t grid;            /* CTAs per launch (one per SM)               */
+    int32_t threads;         /* threads per CTA                            */
+    int32_t smem_bytes;      /* dynamic shared memory per CTA              */
+    int32_t ring_slots;      /* TMA ring depth                             */
+    int32_t slot_bytes;      /* bytes per ring slot                        */
+    int32_t attn_group;      /* CTAs per (batch row, kv head)              */
+    int32_t launches_per_step; /* 1 (fused) or 5*L+1 (baseline)            */
+    int32_t mode;
+    uint64_t weight_bytes;   /* streamed weight bytes per step             */
+    uint64_t device_bytes;   /* total device allocation                    */
+} ffb_info;
+ffb_status ffb_get_info(const ffb_model *m, ffb_info *out);
+
+/* Device pointer to the most recent logits (batch x vocab f32). */
+const float *ffb_logits_device(const ffb_model *m);
+
+#ifdef __cplusplus
+}
+#endif
+
+#if defined(__GNUC__)
+#pragma GCC visibility pop
+#endif
+#endif

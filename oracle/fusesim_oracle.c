@@ -1,0 +1,699 @@
+/*
+ * fusesim_oracle.c -- plain-C restatement of the reference decode path.
+ * TEST INFRASTRUCTURE ONLY (see fusesim_oracle.h).  Compiled with
+ * -ffp-contract=off so every f32/f64 operation rounds exactly like the
+ * reference's -O2 x86-64 build (proj/CMakeLists.txt:8).
+ */
+#include "fusesim_oracle.h"
+
+#include <math.h>
+#include <pthread.h>
+#include <stdarg.h>
+#include <stdio.h>
+#include <stdlib.h>
+#include <string.h>
+
+static __thread char g_err[512];
+
+static void set_err(const char *fmt, ...) {
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(g_err, sizeof(g_err), fmt, ap);
+    va_end(ap);
+}
+
+const char *fo_last_error(void) { return g_err; }
+
+/* ------------------------------------------------------------------ */
+/* std::mt19937_64 / std::mt19937 (libstdc++ <bits/random.h>)          */
+/* ------------------------------------------------------------------ */
+void fo_mt64_seed(fo_mt64 *g, uint64_t seed) {
+    g->mt[0] = seed;
+    for (int i = 1; i < 312; ++i)
+        g->mt[i] = 6364136223846793005ull * (g->mt[i - 1] ^ (g->mt[i - 1] >> 62)) + (uint64_t)i;
+    g->idx = 312;
+}
+
+static void mt64_gen(fo_mt64 *g) {
+    const uint64_t upper = ~0ull << 31, lower = ~upper;
+    for (int k = 0; k < 312; ++k) {
+        uint64_t y = (g->mt[k] & upper) | (g->mt[(k + 1) % 312] & lower);
+        g->mt[k] = g->mt[(k + 156) % 312] ^ (y >> 1) ^ ((y & 1ull) ? 0xb5026f5aa96619e9ull : 0ull);
+    }
+    g->idx = 0;
+}
+
+uint64_t fo_mt64_next(fo_mt64 *g) {
+    if (g->idx >= 312) mt64_gen(g);
+    uint64_t z = g->mt[g->idx++];
+    z ^= (z >> 29) & 0x5555555555555555ull;
+    z ^= (z << 17) & 0x71d67fffeda60000ull;
+    z ^= (z << 37) & 0xfff7eee000000000ull;
+    z ^= (z >> 43);
+    return z;
+}
+
+void fo_mt32_seed(fo_mt32 *g, uint32_t seed) {
+    g->mt[0] = seed;
+    for (int i = 1; i < 624; ++i)
+        g->mt[i] = 1812433253u * (g->mt[i - 1] ^ (g->mt[i - 1] >> 30)) + (uint32_t)i;
+    g->idx = 624;
+}
+
+static void mt32_gen(fo_mt32 *g) {
+    for (int k = 0; k < 624; ++k) {
+        uint32_t y = (g->mt[k] & 0x80000000u) | (g->mt[(k + 1) % 624] & 0x7fffffffu);
+        g->mt[k] = g->mt[(k + 397) % 624] ^ (y >> 1) ^ ((y & 1u) ? 0x9908b0dfu : 0u);
+    }
+    g->idx = 0;
+}
+
+uint32_t fo_mt32_next(fo_mt32 *g) {
+    if (g->idx >= 624) mt32_gen(g);
+    uint32_t z = g->mt[g->idx++];
+    z ^= (z >> 11);
+    z ^= (z << 7) & 0x9d2c5680u;
+    z ^= (z << 15) & 0xefc60000u;
+    z ^= (z >> 18);
+    return z;
+}
+
+/* types.hpp:142-152 */
+uint64_t fo_fnv1a(const void *data, uint64_t n, uint64_t seed) {
+    const unsigned char *p = (const unsigned char *)data;
+    uint64_t h = seed;
+    for (uint64_t i = 0; i < n; ++i) {
+        h ^= p[i];
+        h *= 0x100000001b3ull;
+    }
+    return h;
+}
+
+uint64_t fo_fnv1a_str(const char *s) { return fo_fnv1a(s, strlen(s), 0xcbf29ce484222325ull); }
+
+/* generate_canonical<double,53>(mt19937_64): one draw, u / 2^64 (random.tcc:3349-3380) */
+static double canon_f64(fo_mt64 *g) {
+    double r = (double)fo_mt64_next(g) / 18446744073709551616.0;
+    if (r >= 1.0) r = nextafter(1.0, 0.0);
+    return r;
+}
+
+/* generate_canonical<float,24>(mt19937_64) */
+static float canon_f32(fo_mt64 *g) {
+    float r = (float)fo_mt64_next(g) / 18446744073709551616.0f;
+    if (r >= 1.0f) r = nextafterf(1.0f, 0.0f);
+    return r;
+}
+
+/* normal_distribution<double>::operator() (random.tcc:1811-1844), Marsaglia polar */
+typedef struct { int saved_ok; double saved; } norm64;
+static double normal_f64(norm64 *st, fo_mt64 *g, double mean, double stddev) {
+    double ret;
+    if (st->saved_ok) {
+        st->saved_ok = 0;
+        ret = st->saved;
+    } else {
+        double x, y, r2;
+        do {
+            x = 2.0 * canon_f64(g) - 1.0;
+            y = 2.0 * canon_f64(g) - 1.0;
+            r2 = x * x + y * y;
+        } while (r2 > 1.0 || r2 == 0.0);
+        double mult = sqrt(-2 * log(r2) / r2);
+        st->saved = x * mult;
+        st->saved_ok = 1;
+        ret = y * mult;
+    }
+    return ret * stddev + mean;
+}
+
+/* normal_distribution<float>: float arithmetic, `- 1.0` promoted to double */
+typedef struct { int saved_ok; float saved; } norm32;
+static float normal_f32(norm32 *st, fo_mt64 *g, float mean, float stddev) {
+    float ret;
+    if (st->saved_ok) {
+        st->saved_ok = 0;
+        ret = st->saved;
+    } else {
+        float x, y, r2;
+        do {
+            x = (float)((double)(2.0f * canon_f32(g)) - 1.0);
+            y = (float)((double)(2.0f * canon_f32(g)) - 1.0);
+            r2 = x * x + y * y;
+        } while ((double)r2 > 1.0 || (double)r2 == 0.0);
+        float mult = sqrtf(-2.0f * logf(r2) / r2);
+        st->saved = x * mult;
+        st->saved_ok = 1;
+        ret = y * mult;
+    }
+    return ret * stddev + mean;
+}
+
+void fo_normal_f64(uint64_t seed, double mean, double stddev, double *out, int64_t n) {
+    fo_mt64 g;
+    norm64 st = {0, 0.0};
+    fo_mt64_seed(&g, seed);
+    for (int64_t i = 0; i < n; ++i) out[i] = normal_f64(&st, &g, mean, stddev);
+}
+
+/* ------------------------------------------------------------------ */
+/* element helpers                                                      */
+/* ------------------------------------------------------------------ */
+float fo_bf16_round(float x) { /* types.hpp:50-59 */
+    uint32_t bits;
+    memcpy(&bits, &x, 4);
+    uint32_t lsb = (bits >> 16) & 1u;
+    bits += 0x7fffu + lsb;
+    bits &= 0xffff0000u;
+    float out;
+    memcpy(&out, &bits, 4);
+    return out;
+}
+
+float fo_dequantize_code(uint8_t code, float scale, float zero_point) { /* quant.hpp:23-25 */
+    return ((float)code - zero_point) * scale;
+}
+
+uint8_t fo_quantize_value(float v, float scale, float zero_point, int32_t levels) {
+    float c = roundf(v / scale + zero_point); /* quant.hpp:36-39 */
+    if (c < 0.0f) c = 0.0f;
+    if (c > (float)levels) c = (float)levels;
+    return (uint8_t)c;
+}
+
+void fo_quantize_group(const float *values, int64_t n, int32_t levels, uint8_t *codes,
+                       float *scale, float *zero_point, float *deq) {
+    /* quant.hpp:42-54 (levels=15); the int8 extension uses levels=255 */
+    float lo = 0.0f, hi = 0.0f;
+    if (n > 0) {
+        lo = values[0];
+        hi = values[0];
+        for (int64_t i = 1; i < n; ++i) {
+            if (values[i] < lo) lo = values[i];
+            if (hi < values[i]) hi = values[i];
+        }
+    }
+    float range = hi - lo;
+    float s = range > 0 ? range / (float)levels : 1.0f;
+    float z = roundf(-lo / s);
+    if (z < 0.0f) z = 0.0f;
+    if (z > (float)levels) z = (float)levels;
+    for (int64_t i = 0; i < n; ++i) {
+        uint8_t c = fo_quantize_value(values[i], s, z, levels);
+        if (codes) codes[i] = c;
+        if (deq) deq[i] = fo_dequantize_code(c, s, z);
+    }
+    *scale = s;
+    *zero_point = z;
+}
+
+/* ------------------------------------------------------------------ */
+/* config / layout                                                      */
+/* ------------------------------------------------------------------ */
+int64_t fo_qkv_rows(const fo_config *c) {
+    return c->n_q_heads * c->d_head + 2 * c->n_kv_heads * c->d_head;
+}
+
+int fo_validate(const fo_config *c) { /* config.hpp:61-83 (decoder kind) */
+    if (c->layers < 0) { set_err("model: layers must be >= 0"); return 2; }
+    if (c->d_model <= 0) { set_err("model: d_model must be positive"); return 2; }
+    if (c->batch < 1 || c->batch > 16) { set_err("model: batch must be in [1,16]"); return 2; }
+    if (c->d_inter <= 0) { set_err("model: d_inter must be positive"); return 2; }
+    if (c->d_head <= 0 || c->d_head % 2 != 0) {
+        set_err("model: d_head must be positive and even");
+        return 2;
+    }
+    if (c->n_q_heads <= 0 || c->n_kv_heads <= 0) {
+        set_err("model: head counts must be positive");
+        return 2;
+    }
+    if (c->n_q_heads % c->n_kv_heads != 0) {
+        set_err("model: GQA grouping requires n_q_heads mod n_kv_heads == 0");
+        return 2;
+    }
+    if (c->d_model != c->n_q_heads * c->d_head) {
+        set_err("model: d_model must equal n_q_heads * d_head");
+        return 2;
+    }
+    if (c->vocab_size <= 0) { set_err("model: vocab_size must be positive"); return 2; }
+    if (c->quant_bits != 0) {
+        if (c->quant_bits != 4 && c->quant_bits != 8) {
+            set_err("quant: only 4-bit (reference) and 8-bit (extension) codes are supported");
+            return 2;
+        }
+        if (c->quant_group <= 0) { set_err("quant: group_size must be positive"); return 2; }
+        if (c->d_model % c->quant_group != 0) {
+            set_err("quant: group_size must divide every quantized row length");
+            return 2;
+        }
+    }
+    return 0;
+}
+
+static uint64_t row_bytes(const fo_config *c, int64_t cols) { /* tensor_store.hpp:29-32 */
+    if (c->quant_bits == 4) return (uint64_t)cols / 2 + (uint64_t)(cols / c->quant_group) * 4;
+    if (c->quant_bits == 8) return (uint64_t)cols + (uint64_t)(cols / c->quant_group) * 4;
+    return (uint64_t)cols * (c->dtype == 0 ? 2 : 4);
+}
+
+uint64_t fo_streamed_weight_bytes(const fo_config *c) { /* tensor_store.hpp:170-174 */
+    uint64_t per_layer = (uint64_t)fo_qkv_rows(c) * row_bytes(c, c->d_model) +
+                         (uint64_t)c->d_model * row_bytes(c, c->d_model) +
+                         (uint64_t)(2 * c->d_inter) * row_bytes(c, c->d_model) +
+                         (uint64_t)c->d_inter * row_bytes(c, c->d_model);
+    return per_layer * (uint64_t)c->layers + (uint64_t)c->vocab_size * row_bytes(c, c->d_model);
+}
+
+uint64_t fo_total_weight_bytes(const fo_config *c) { /* tensor_store.hpp:178-186 */
+    uint64_t eb = c->dtype == 0 ? 2 : 4;
+    return fo_streamed_weight_bytes(c) + (uint64_t)c->vocab_size * c->d_model * eb +
+           (uint64_t)(2 * c->layers + 1) * c->d_model * eb;
+}
+
+/* ------------------------------------------------------------------ */
+/* init_weights (tensor_store.hpp:270-366)                              */
+/* ------------------------------------------------------------------ */
+typedef struct fill_job {
+    char name[64];
+    float *dst;
+    int64_t rows, cols;
+    double fan_in_scale;
+    int kind; /* 0 = matrix (quantizable), 1 = norm vector, 2 = embedding (never quantized) */
+} fill_job;
+
+typedef struct fill_ctx {
+    const fo_config *cfg;
+    uint64_t seed;
+    fill_job *jobs;
+    int njobs;
+    int next;
+    pthread_mutex_t mu;
+} fill_ctx;
+
+static void run_fill(const fo_config *cfg, uint64_t seed, const fill_job *j) {
+    fo_mt64 g;
+    fo_mt64_seed(&g, seed ^ fo_fnv1a_str(j->name));
+    int64_t n = j->rows * j->cols;
+    if (j->kind == 1) { /* fill_vector: N(1, 0.02), not rounded */
+        norm64 st = {0, 0.0};
+        for (int64_t i = 0; i < n; ++i) j->dst[i] = (float)normal_f64(&st, &g, 1.0, 0.02);
+        return;
+    }
+    norm64 st = {0, 0.0};
+    for (int64_t i = 0; i < n; ++i) j->dst[i] = (float)normal_f64(&st, &g, 0.0, j->fan_in_scale);
+    int quantize = (j->kind == 0) && cfg->quant_bits != 0;
+    if (quantize) {
+        int32_t levels = cfg->quant_bits == 4 ? 15 : 255;
+        int64_t gs = cfg->quant_group;
+        float s, z;
+        for (int64_t r = 0; r < j->rows; ++r)
+            for (int64_t c0 = 0; c0 < j->cols; c0 += gs) {
+                float *grp = j->dst + r * j->cols + c0;
+                fo_quantize_group(grp, gs, levels, NULL, &s, &z, grp);
+            }
+    } else if (cfg->dtype == 0) {
+        for (int64_t i = 0; i < n; ++i) j->dst[i] = fo_bf16_round(j->dst[i]);
+    }
+}
+
+static void *fill_worker(void *arg) {
+    fill_ctx *ctx = (fill_ctx *)arg;
+    for (;;) {
+        pthread_mutex_lock(&ctx->mu);
+        int i = ctx->next++;
+        pthread_mutex_unlock(&ctx->mu);
+        if (i >= ctx->njobs) break;
+        run_fill(ctx->cfg, ctx->seed, &ctx->jobs[i]);
+    }
+    return NULL;
+}
+
+static float *alloc_f32(int64_t n) {
+    float *p = (float *)calloc((size_t)(n > 0 ? n : 1), sizeof(float));
+    return p;
+}
+
+void fo_free(fo_store *s) {
+    if (!s) return;
+    if (s->layers) {
+        for (int64_t l = 0; l < s->cfg.layers; ++l) {
+            free(s->layers[l].wqkv);
+            free(s->layers[l].waout);
+            free(s->layers[l].wffn1);
+            free(s->layers[l].wffn2t);
+            free(s->layers[l].norm_attn);
+            free(s->layers[l].norm_ffn);
+        }
+        free(s->layers);
+    }
+    free(s->final_norm);
+    free(s->embedding);
+    free(s->lm_head);
+    free(s->k);
+    free(s->v);
+    free(s->kv_len);
+    free(s);
+}
+
+fo_store *fo_init_weights(const fo_config *c, uint64_t seed, int64_t max_seq_len, int nthreads) {
+    if (fo_validate(c)) return NULL;
+    fo_store *s = (fo_store *)calloc(1, sizeof(fo_store));
+    s->cfg = *c;
+    s->max_seq_len = max_seq_len;
+    const int64_t d = c->d_model;
+    s->layers = (fo_layer *)calloc((size_t)(c->layers > 0 ? c->layers : 1), sizeof(fo_layer));
+    int njobs = (int)(6 * c->layers + 3);
+    fill_job *jobs = (fill_job *)calloc((size_t)njobs, sizeof(fill_job));
+    int j = 0;
+    /* fan-in: d_inter for the GLU output projection, stored cols otherwise (:330-333) */
+    double sd_d = 1.0 / sqrt((double)d), sd_i = 1.0 / sqrt((double)c->d_inter);
+    for (int64_t l = 0; l < c->layers; ++l) {
+        fo_layer *L = &s->layers[l];
+        L->wqkv = alloc_f32(fo_qkv_rows(c) * d);
+        L->waout = alloc_f32(d * d);
+        L->wffn1 = alloc_f32(2 * c->d_inter * d);
+        L->wffn2t = alloc_f32(c->d_inter * d);
+        L->norm_attn = alloc_f32(d);
+        L->norm_ffn = alloc_f32(d);
+#define JOB(NAME, DST, R, C, SD, K)                                                        \
+    do {                                                                                   \
+        snprintf(jobs[j].name, sizeof(jobs[j].name), "layer.%lld." NAME, (long long)l);   \
+        jobs[j].dst = (DST); jobs[j].rows = (R); jobs[j].cols = (C);                       \
+        jobs[j].fan_in_scale = (SD); jobs[j].kind = (K); ++j;                              \
+    } while (0)
+        JOB("wqkv", L->wqkv, fo_qkv_rows(c), d, sd_d, 0);
+        JOB("waout", L->waout, d, d, sd_d, 0);
+        JOB("wffn1", L->wffn1, 2 * c->d_inter, d, sd_d, 0);
+        JOB("wffn2t", L->wffn2t, c->d_inter, d, sd_i, 0);
+        JOB("norm_attn", L->norm_attn, 1, d, 0.0, 1);
+        JOB("norm_ffn", L->norm_ffn, 1, d, 0.0, 1);
+#undef JOB
+    }
+    s->final_norm = alloc_f32(d);
+    s->embedding = alloc_f32(c->vocab_size * d);
+    s->lm_head = alloc_f32(c->vocab_size * d);
+    snprintf(jobs[j].name, 64, "final_norm");
+    jobs[j].dst = s->final_norm; jobs[j].rows = 1; jobs[j].cols = d; jobs[j].kind = 1; ++j;
+    snprintf(jobs[j].name, 64, "embedding");
+    jobs[j].dst = s->embedding; jobs[j].rows = c->vocab_size; jobs[j].cols = d;
+    jobs[j].fan_in_scale = sd_d; jobs[j].kind = 2; ++j;
+    snprintf(jobs[j].name, 64, "lm_head");
+    jobs[j].dst = s->lm_head; jobs[j].rows = c->vocab_size; jobs[j].cols = d;
+    jobs[j].fan_in_scale = sd_d; jobs[j].kind = 0; ++j;
+
+    /* biggest jobs first so the per-tensor parallelism balances */
+    for (int a = 0; a < njobs; ++a)
+        for (int b = a + 1; b < njobs; ++b)
+            if (jobs[b].rows * jobs[b].cols > jobs[a].rows * jobs[a].cols) {
+                fill_job t = jobs[a]; jobs[a] = jobs[b]; jobs[b] = t;
+            }
+    fill_ctx ctx;
+    ctx.cfg = &s->cfg; ctx.seed = seed; ctx.jobs = jobs; ctx.njobs = njobs; ctx.next = 0;
+    pthread_mutex_init(&ctx.mu, NULL);
+    if (nthreads < 1) nthreads = 1;
+    if (nthreads > 64) nthreads = 64;
+    pthread_t th[64];
+    for (int t = 1; t < nthreads; ++t) pthread_create(&th[t], NULL, fill_worker, &ctx);
+    fill_worker(&ctx);
+    for (int t = 1; t < nthreads; ++t) pthread_join(th[t], NULL);
+    pthread_mutex_destroy(&ctx.mu);
+    free(jobs);
+
+    size_t kv = (size_t)c->batch * c->layers * c->n_kv_heads * max_seq_len * c->d_head;
+    s->k = alloc_f32((int64_t)kv);
+    s->v = alloc_f32((int64_t)kv);
+    s->kv_len = (int64_t *)calloc((size_t)(c->layers > 0 ? c->layers : 1), sizeof(int64_t));
+    return s;
+}
+
+/* ------------------------------------------------------------------ */
+/* KV cache (tensor_store.hpp:63-150)                                   */
+/* ------------------------------------------------------------------ */
+static size_t kv_index(const fo_store *s, int64_t b, int64_t l, int64_t h, int64_t pos) {
+    const fo_config *c = &s->cfg;
+    return ((((size_t)b * c->layers + l) * c->n_kv_heads + h) * s->max_seq_len + pos) *
+           c->d_head;
+}
+
+static float round_store(const fo_store *s, float x) {
+    return s->cfg.dtype == 0 ? fo_bf16_round(x) : x;
+}
+
+float *fo_k_at(fo_store *s, int64_t b, int64_t l, int64_t h, int64_t pos) {
+    return s->k + kv_index(s, b, l, h, pos);
+}
+float *fo_v_at(fo_store *s, int64_t b, int64_t l, int64_t h, int64_t pos) {
+    return s->v + kv_index(s, b, l, h, pos);
+}
+
+void fo_kv_set_position(fo_store *s, int64_t b, int64_t l, int64_t h, int64_t pos,
+                        const float *k, const float *v) {
+    float *kd = fo_k_at(s, b, l, h, pos), *vd = fo_v_at(s, b, l, h, pos);
+    for (int64_t d = 0; d < s->cfg.d_head; ++d) {
+        kd[d] = round_store(s, k[d]);
+        vd[d] = round_store(s, v[d]);
+    }
+}
+
+void fo_kv_set_length(fo_store *s, int64_t layer, int64_t n) { s->kv_len[layer] = n; }
+int64_t fo_kv_length(const fo_store *s, int64_t layer) { return s->kv_len[layer]; }
+
+void fo_synthetic_prefill(fo_store *s, int64_t prefill, uint64_t seed) {
+    const fo_config *c = &s->cfg;
+    fo_mt64 g;
+    norm32 st = {0, 0.0f};
+    fo_mt64_seed(&g, seed);
+    float *k = alloc_f32(c->d_head), *v = alloc_f32(c->d_head);
+    for (int64_t b = 0; b < c->batch; ++b)
+        for (int64_t l = 0; l < c->layers; ++l)
+            for (int64_t h = 0; h < c->n_kv_heads; ++h)
+                for (int64_t p = 0; p < prefill; ++p) {
+                    for (int64_t i = 0; i < c->d_head; ++i) k[i] = normal_f32(&st, &g, 0.0f, 0.3f);
+                    for (int64_t i = 0; i < c->d_head; ++i) v[i] = normal_f32(&st, &g, 0.0f, 0.3f);
+                    fo_kv_set_position(s, b, l, h, p, k, v);
+                }
+    for (int64_t l = 0; l < c->layers; ++l) s->kv_len[l] = prefill;
+    free(k);
+    free(v);
+}
+
+/* ------------------------------------------------------------------ */
+/* numerics (numerics.hpp)                                              */
+/* ------------------------------------------------------------------ */
+void fo_rmsnorm_f64(const double *x, const double *w, int64_t n, double eps, double *y) {
+    double ms = 0; /* numerics.hpp:14-24 */
+    for (int64_t i = 0; i < n; ++i) ms += x[i] * x[i];
+    ms /= (double)n;
+    double inv = 1.0 / sqrt(ms + eps);
+    for (int64_t i = 0; i < n; ++i) y[i] = w[i] * x[i] * inv;
+}
+
+void fo_rope_f64(double *v, int64_t d_head, int64_t pos, double theta) {
+    for (int64_t k = 0; k < d_head / 2; ++k) { /* numerics.hpp:27-37 */
+        double freq = pow(theta, -(double)(2 * k) / (double)d_head);
+        double angle = (double)pos * freq;
+        double c = cos(angle), s = sin(angle);
+        double a = v[2 * k], b = v[2 * k + 1];
+        v[2 * k] = a * c - b * s;
+        v[2 * k + 1] = a * s + b * c;
+    }
+}
+
+double fo_silu(double z) { return z / (1.0 + exp(-z)); } /* numerics.hpp:46 */
+
+int64_t fo_argmax_f64(const double *logits, int64_t n) { /* numerics.hpp:169-175 */
+    int64_t best = 0;
+    for (int64_t i = 1; i < n; ++i)
+        if (logits[i] > logits[best]) best = i;
+    return best;
+}
+
+void fo_attn_partial_update(double *m, double *l, double *o, int64_t d, const double *q,
+                            const double *k_rows, const double *v_rows, int64_t rows,
+                            double alpha) {
+    if (rows == 0) return; /* numerics.hpp:76-98 */
+    double *s = (double *)malloc(sizeof(double) * (size_t)rows);
+    double chunk_max = -INFINITY;
+    for (int64_t j = 0; j < rows; ++j) {
+        double dot = 0;
+        for (int64_t k = 0; k < d; ++k) dot += q[k] * k_rows[j * d + k];
+        s[j] = alpha * dot;
+        chunk_max = chunk_max > s[j] ? chunk_max : s[j];
+    }
+    double m_new = *m > chunk_max ? *m : chunk_max;
+    double scale = (*l == 0.0) ? 0.0 : exp(*m - m_new);
+    *l *= scale;
+    for (int64_t k = 0; k < d; ++k) o[k] *= scale;
+    for (int64_t j = 0; j < rows; ++j) {
+        double w = exp(s[j] - m_new);
+        *l += w;
+        for (int64_t k = 0; k < d; ++k) o[k] += w * v_rows[j * d + k];
+    }
+    *m = m_new;
+    free(s);
+}
+
+int fo_attn_reduce(const double *m, const double *l, const double *o, int64_t n_partials,
+                   int64_t d, double *out) {
+    double M = -INFINITY; /* numerics.hpp:123-145 */
+    int any = 0;
+    for (int64_t i = 0; i < n_partials; ++i)
+        if (l[i] != 0.0) {
+            M = M > m[i] ? M : m[i];
+            any = 1;
+        }
+    if (!any) {
+        set_err("attn_reduce: all partials empty");
+        return 2;
+    }
+    double L = 0;
+    for (int64_t i = 0; i < n_partials; ++i)
+        if (l[i] != 0.0) L += l[i] * exp(m[i] - M);
+    for (int64_t k = 0; k < d; ++k) out[k] = 0.0;
+    for (int64_t i = 0; i < n_partials; ++i) {
+        if (l[i] == 0.0) continue;
+        double r = exp(m[i] - M) / L;
+        for (int64_t k = 0; k < d; ++k) out[k] += r * o[i * d + k];
+    }
+    return 0;
+}
+
+/* ------------------------------------------------------------------ */
+/* reference_forward (reference.hpp:37-139)                             */
+/* ------------------------------------------------------------------ */
+static void matvec_rows(const float *w, int64_t rows, int64_t cols, const double *u, double *y) {
+    for (int64_t r = 0; r < rows; ++r) { /* reference.hpp:21-30 */
+        const float *row = w + r * cols;
+        double acc = 0.0;
+        for (int64_t c = 0; c < cols; ++c) acc += (double)row[c] * u[c];
+        y[r] = acc;
+    }
+}
+
+static void widen(const float *src, int64_t n, double *dst) {
+    for (int64_t i = 0; i < n; ++i) dst[i] = (double)src[i];
+}
+
+int fo_reference_forward(fo_store *s, const int64_t *tokens, int64_t pos, double *logits) {
+    return fo_reference_forward_ex(s, tokens, pos, logits, NULL, NULL);
+}
+
+int fo_reference_forward_ex(fo_store *s, const int64_t *tokens, int64_t pos, double *logits,
+                            const float *k_app, const float *v_app) {
+    const fo_config *m = &s->cfg;
+    const int64_t B = m->batch, D = m->d_model, dh = m->d_head, nq = m->n_q_heads,
+                  nkv = m->n_kv_heads, qpg = nq / nkv, V = m->vocab_size;
+    const double alpha = 1.0 / sqrt((double)dh);
+    for (int64_t b = 0; b < B; ++b)
+        if (tokens[b] < 0 || tokens[b] >= V) {
+            set_err("reference_forward: token id out of range");
+            return 2;
+        }
+    double *x = (double *)malloc(sizeof(double) * (size_t)(B * D));
+    double *u = (double *)malloc(sizeof(double) * (size_t)D);
+    double *w = (double *)malloc(sizeof(double) * (size_t)D);
+    int64_t qkvr = fo_qkv_rows(m);
+    double *qkv = (double *)malloc(sizeof(double) * (size_t)qkvr);
+    double *q = (double *)malloc(sizeof(double) * (size_t)(B * nq * dh));
+    float *krow = (float *)malloc(sizeof(float) * (size_t)(B * nkv * dh));
+    float *vrow = (float *)malloc(sizeof(float) * (size_t)(B * nkv * dh));
+    double *attn = (double *)malloc(sizeof(double) * (size_t)(nq * dh));
+    double *aout = (double *)malloc(sizeof(double) * (size_t)D);
+    double *sc = (double *)malloc(sizeof(double) * (size_t)(pos + 1));
+    int rc = 0;
+
+    for (int64_t b = 0; b < B; ++b) widen(s->embedding + tokens[b] * D, D, x + b * D);
+
+    for (int64_t l = 0; l < m->layers; ++l) {
+        const fo_layer *lw = &s->layers[l];
+        if (s->kv_len[l] != pos) {
+            set_err("reference_forward: cache length does not match position");
+            rc = 2;
+            goto done;
+        }
+        for (int64_t b = 0; b < B; ++b) {
+            widen(lw->norm_attn, D, w);
+            fo_rmsnorm_f64(x + b * D, w, D, m->rmsnorm_eps, u);
+            matvec_rows(lw->wqkv, qkvr, D, u, qkv);
+            memcpy(q + b * nq * dh, qkv, sizeof(double) * (size_t)(nq * dh));
+            for (int64_t h = 0; h < nq; ++h) fo_rope_f64(q + b * nq * dh + h * dh, dh, pos, m->rope_theta);
+            for (int64_t h = 0; h < nkv; ++h) {
+                double *k = qkv + (nq + h) * dh;
+                fo_rope_f64(k, dh, pos, m->rope_theta);
+                for (int64_t d = 0; d < dh; ++d) {
+                    krow[b * nkv * dh + h * dh + d] = (float)k[d];
+                    vrow[b * nkv * dh + h * dh + d] = (float)qkv[(nq + nkv + h) * dh + d];
+                }
+            }
+        }
+        /* append_token: every row lands, then the length advances once (:102-106) */
+        if (pos >= s->max_seq_len) {
+            set_err("kv_append: cache capacity reached (max_seq_len)");
+            rc = 2;
+            goto done;
+        }
+        if (k_app && v_app) { /* checker hook: append externally rounded rows */
+            for (int64_t b = 0; b < B; ++b)
+                for (int64_t i = 0; i < nkv * dh; ++i) {
+                    krow[b * nkv * dh + i] = k_app[(b * m->layers + l) * nkv * dh + i];
+                    vrow[b * nkv * dh + i] = v_app[(b * m->layers + l) * nkv * dh + i];
+                }
+        }
+        for (int64_t b = 0; b < B; ++b)
+            for (int64_t h = 0; h < nkv; ++h)
+                fo_kv_set_position(s, b, l, h, pos, krow + b * nkv * dh + h * dh,
+                                   vrow + b * nkv * dh + h * dh);
+        s->kv_len[l] += 1;
+
+        for (int64_t b = 0; b < B; ++b) {
+            for (int64_t i = 0; i < nq * dh; ++i) attn[i] = 0.0;
+            for (int64_t h = 0; h < nq; ++h) {
+                int64_t kvh = h / qpg;
+                const double *qh = q + b * nq * dh + h * dh;
+                int64_t n = pos + 1;
+                double mx = -INFINITY;
+                for (int64_t j = 0; j < n; ++j) {
+                    const float *kj = fo_k_at(s, b, l, kvh, j);
+                    double dot = 0;
+                    for (int64_t d = 0; d < dh; ++d) dot += qh[d] * (double)kj[d];
+                    sc[j] = alpha * dot;
+                    mx = mx > sc[j] ? mx : sc[j];
+                }
+                double denom = 0;
+                for (int64_t j = 0; j < n; ++j) denom += exp(sc[j] - mx);
+                for (int64_t j = 0; j < n; ++j) {
+                    double wj = exp(sc[j] - mx) / denom;
+                    const float *vj = fo_v_at(s, b, l, kvh, j);
+                    for (int64_t d = 0; d < dh; ++d) attn[h * dh + d] += wj * (double)vj[d];
+                }
+            }
+            matvec_rows(lw->waout, D, D, attn, aout);
+            double *xb = x + b * D;
+            for (int64_t k = 0; k < D; ++k) xb[k] += aout[k];
+
+            widen(lw->norm_ffn, D, w);
+            fo_rmsnorm_f64(xb, w, D, m->rmsnorm_eps, u);
+            for (int64_t t = 0; t < m->d_inter; ++t) {
+                const float *in_row = lw->wffn1 + (2 * t) * D;
+                const float *gate_row = lw->wffn1 + (2 * t + 1) * D;
+                double a = 0, g = 0;
+                for (int64_t c = 0; c < D; ++c) {
+                    a += (double)in_row[c] * u[c];
+                    g += (double)gate_row[c] * u[c];
+                }
+                double hh = fo_silu(g) * a;
+                const float *col = lw->wffn2t + t * D;
+                for (int64_t k = 0; k < D; ++k) xb[k] += hh * (double)col[k];
+            }
+        }
+    }
+    for (int64_t b = 0; b < B; ++b) {
+        widen(s->final_norm, D, w);
+        fo_rmsnorm_f64(x + b * D, w, D, m->rmsnorm_eps, u);
+        matvec_rows(s->lm_head, V, D, u, logits + b * V);
+    }
+done:
+    free(x); free(u); free(w); free(qkv); free(q); free(krow); free(vrow);
+    free(attn); free(aout); free(sc);
+    return rc;
+}

@@ -1,0 +1,337 @@
+"""B200-native FlashFormer decode step (arxiv 2505.22758).
+
+Host-side mirror of the reference's decode interface
+(/root/reference/proj/include/fusesim/):
+
+  fusesim::ModelConfig            config.hpp:45-86       -> ModelConfig
+  fusesim::ValidationError, ...   types.hpp:17-31        -> ValidationError, ...
+  fusesim::RunMode                types.hpp:64           -> RunMode
+  fusesim::TensorStore + KVCache  tensor_store.hpp:63-366 -> DecodeModel (device store)
+  fusesim::execute_program /      interpreter.hpp:502-506,
+  fusesim::reference_forward      reference.hpp:37-139   -> DecodeModel.forward
+
+Everything runs through the C-ABI in ``include/flashformer_b200.h`` implemented
+by ``libffb200.so`` (hand-written sm_100a CUDA).  There is no CPU path: if the
+library is missing or no B200 is visible, the calls raise.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import enum
+import os
+from dataclasses import dataclass, replace
+
+import numpy as np
+
+__all__ = [
+    "ModelConfig", "RunMode", "DecodeModel", "ValidationError", "DeviceError",
+    "UnsupportedConfigError", "UsageError", "PRESETS", "model_preset", "lib", "LIB_PATH",
+    "tensor_names",
+]
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libffb200.so")
+
+
+class FusesimError(RuntimeError):
+    pass
+
+
+class UsageError(FusesimError):          # CLI exit 1
+    pass
+
+
+class ValidationError(FusesimError):     # fusesim::ValidationError, exit 2
+    pass
+
+
+class DeviceError(FusesimError):         # CUDA failure, exit 3
+    pass
+
+
+class UnsupportedConfigError(FusesimError):
+    pass
+
+
+_STATUS = {1: UsageError, 2: ValidationError, 3: DeviceError, 4: UnsupportedConfigError}
+
+
+class RunMode(enum.IntEnum):
+    """fusesim::RunMode (types.hpp:64)."""
+    BASELINE = 0        # one launch per sublayer stage (multi-kernel variant)
+    FUSED = 1           # one persistent launch, producer waits at barriers
+    FUSED_OVERLAP = 2   # one persistent launch, producer streams across barriers
+
+
+class _Cfg(C.Structure):
+    _fields_ = [
+        ("layers", C.c_int64), ("d_model", C.c_int64), ("d_inter", C.c_int64),
+        ("d_head", C.c_int64), ("n_q_heads", C.c_int64), ("n_kv_heads", C.c_int64),
+        ("vocab_size", C.c_int64), ("rope_theta", C.c_double), ("rmsnorm_eps", C.c_double),
+        ("dtype", C.c_int32), ("quant_bits", C.c_int32), ("quant_group", C.c_int32),
+        ("batch", C.c_int64),
+    ]
+
+
+class _Info(C.Structure):
+    _fields_ = [
+        ("grid", C.c_int32), ("threads", C.c_int32), ("smem_bytes", C.c_int32),
+        ("ring_slots", C.c_int32), ("slot_bytes", C.c_int32), ("attn_group", C.c_int32),
+        ("launches_per_step", C.c_int32), ("mode", C.c_int32),
+        ("weight_bytes", C.c_uint64), ("device_bytes", C.c_uint64),
+    ]
+
+
+@dataclass(frozen=True)
+class ModelConfig:
+    """fusesim::ModelConfig (config.hpp:45-86), decoder kind."""
+    layers: int
+    d_model: int
+    d_inter: int
+    d_head: int
+    n_q_heads: int
+    n_kv_heads: int
+    vocab_size: int
+    rope_theta: float = 500000.0
+    rmsnorm_eps: float = 1e-5
+    dtype: int = 0
+    quant_bits: int = 0
+    quant_group: int = 128
+    batch: int = 1
+
+    @property
+    def qkv_rows(self) -> int:
+        return (self.n_q_heads + 2 * self.n_kv_heads) * self.d_head
+
+    @property
+    def q_group(self) -> int:
+        return self.n_q_heads // self.n_kv_heads
+
+    def replace(self, **kw) -> "ModelConfig":
+        return replace(self, **kw)
+
+    def _c(self) -> _Cfg:
+        return _Cfg(self.layers, self.d_model, self.d_inter, self.d_head, self.n_q_heads,
+                    self.n_kv_heads, self.vocab_size, self.rope_theta, self.rmsnorm_eps,
+                    self.dtype, self.quant_bits, self.quant_group, self.batch)
+
+    def streamed_weight_bytes(self) -> int:
+        """StoreLayout::streamed_weight_bytes (tensor_store.hpp:170-174)."""
+        if self.quant_bits == 4:
+            row = self.d_model // 2 + (self.d_model // self.quant_group) * 4
+        elif self.quant_bits == 8:
+            row = self.d_model + (self.d_model // self.quant_group) * 4
+        else:
+            row = self.d_model * 2
+        rows = self.layers * (self.qkv_rows + self.d_model + 3 * self.d_inter) + self.vocab_size
+        return rows * row
+
+    def kv_bytes_per_position(self) -> int:
+        """StoreLayout::kv_bytes_per_position (tensor_store.hpp:188-192)."""
+        return self.batch * self.layers * self.n_kv_heads * 2 * self.d_head * 2
+
+
+PRESETS = {
+    # fusesim presets (presets.hpp:19-47)
+    "llama31_8b-toy": ModelConfig(4, 256, 896, 64, 4, 2, 512),
+    "llama31_8b": ModelConfig(32, 4096, 14336, 128, 32, 8, 128256),
+    "llama31_70b": ModelConfig(80, 8192, 28672, 128, 64, 8, 128256),
+    # BASELINE.json configs (SURVEY.md §8 tags T, S)
+    "tiny": ModelConfig(4, 512, 1792, 64, 8, 2, 32000),
+    "llama32_1b": ModelConfig(16, 2048, 8192, 64, 32, 8, 128256),
+}
+
+
+def model_preset(name: str) -> ModelConfig:
+    """fusesim::model_preset (presets.hpp:19-60) for the decoder presets."""
+    if name not in PRESETS:
+        raise ValidationError(f"unknown model preset: {name}")
+    return PRESETS[name]
+
+
+def tensor_names(cfg: ModelConfig) -> list[str]:
+    """Reference tensor names (tensor_store.hpp:344-363) in upload order."""
+    names = []
+    for l in range(cfg.layers):
+        names += [f"layer.{l}.{t}" for t in
+                  ("wqkv", "waout", "wffn1", "wffn2t", "norm_attn", "norm_ffn")]
+    return names + ["final_norm", "embedding", "lm_head"]
+
+
+_lib = None
+
+
+def lib():
+    """Load libffb200.so (fails loudly; there is no fallback)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise DeviceError(f"CUDA extension not built: {LIB_PATH} (run __graft_entry__.build())")
+    L = C.CDLL(LIB_PATH)
+    P = C.POINTER
+    L.ffb_last_error.restype = C.c_char_p
+    L.ffb_version.restype = C.c_char_p
+    L.ffb_config_supported.argtypes = [P(_Cfg)]
+    L.ffb_create.argtypes = [P(_Cfg), C.c_int64, C.c_int, C.c_int, C.c_int, P(C.c_void_p)]
+    L.ffb_destroy.argtypes = [C.c_void_p]
+    L.ffb_destroy.restype = None
+    L.ffb_upload_tensor.argtypes = [C.c_void_p, C.c_char_p, P(C.c_float), C.c_int64]
+    L.ffb_init_synthetic.argtypes = [C.c_void_p, C.c_uint64]
+    L.ffb_kv_set.argtypes = [C.c_void_p] + [C.c_int64] * 4 + [P(C.c_float)] * 2
+    L.ffb_kv_get.argtypes = [C.c_void_p] + [C.c_int64] * 4 + [P(C.c_float)] * 2
+    L.ffb_kv_import.argtypes = [C.c_void_p, P(C.c_float), P(C.c_float), C.c_int64, C.c_int64]
+    L.ffb_kv_set_length.argtypes = [C.c_void_p, C.c_int64, C.c_int64]
+    L.ffb_kv_length.argtypes = [C.c_void_p, C.c_int64]
+    L.ffb_kv_length.restype = C.c_int64
+    L.ffb_set_mode.argtypes = [C.c_void_p, C.c_int]
+    L.ffb_decode_step.argtypes = [C.c_void_p, P(C.c_int64), C.c_int64, P(C.c_float),
+                                  P(C.c_int64), C.c_void_p]
+    L.ffb_decode_step_device.argtypes = [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p,
+                                         C.c_void_p, C.c_void_p]
+    L.ffb_get_info.argtypes = [C.c_void_p, P(_Info)]
+    L.ffb_logits_device.argtypes = [C.c_void_p]
+    L.ffb_logits_device.restype = C.c_void_p
+    _lib = L
+    return L
+
+
+def _check(rc: int):
+    if rc != 0:
+        msg = lib().ffb_last_error().decode()
+        raise _STATUS.get(rc, FusesimError)(msg)
+
+
+def _fp(a: np.ndarray):
+    return a.ctypes.data_as(C.POINTER(C.c_float))
+
+
+class DecodeModel:
+    """Device-resident decoder: weights, KV cache and the decode kernel.
+
+    Mirrors the mutable state the reference threads through
+    ``TensorStore&`` (weights + ``KVCache``) and the two entry points that
+    consume it.  ``forward(tokens, pos)`` has reference_forward's contract
+    (reference.hpp:37-139): pos must equal every layer's cache length, one KV
+    position per layer is appended, logits[batch][vocab] are returned.
+    """
+
+    def __init__(self, cfg: ModelConfig, max_seq_len: int, device: int = 0,
+                 mode: RunMode = RunMode.FUSED_OVERLAP, tp_rank: int = 0, tp_size: int = 1):
+        L = lib()
+        self.cfg = cfg
+        self.max_seq_len = max_seq_len
+        self._c = cfg._c()
+        h = C.c_void_p()
+        _check(L.ffb_create(C.byref(self._c), max_seq_len, device, tp_rank, tp_size,
+                            C.byref(h)))
+        self._h = h
+        self.set_mode(mode)
+
+    @staticmethod
+    def supported(cfg: ModelConfig) -> bool:
+        c = cfg._c()
+        return bool(lib().ffb_config_supported(C.byref(c)))
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().ffb_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    # ------------------------------------------------------------ weights
+    def upload_tensor(self, name: str, values: np.ndarray):
+        a = np.ascontiguousarray(values, dtype=np.float32).ravel()
+        _check(lib().ffb_upload_tensor(self._h, name.encode(), _fp(a), a.size))
+
+    def upload_store(self, store):
+        """Pack every tensor of a TensorStore-like object (``store.tensor(name)``)."""
+        for n in tensor_names(self.cfg):
+            self.upload_tensor(n, store.tensor(n))
+
+    def init_synthetic(self, seed: int = 1234):
+        _check(lib().ffb_init_synthetic(self._h, seed))
+
+    # ------------------------------------------------------------ KV cache
+    def kv_set(self, b, layer, head, pos, k, v):
+        k = np.ascontiguousarray(k, np.float32)
+        v = np.ascontiguousarray(v, np.float32)
+        _check(lib().ffb_kv_set(self._h, b, layer, head, pos, _fp(k), _fp(v)))
+
+    def kv_get(self, b, layer, head, pos):
+        dh = self.cfg.d_head
+        k = np.empty(dh, np.float32)
+        v = np.empty(dh, np.float32)
+        _check(lib().ffb_kv_get(self._h, b, layer, head, pos, _fp(k), _fp(v)))
+        return k, v
+
+    def kv_import(self, k: np.ndarray, v: np.ndarray, n_pos: int):
+        """Import a reference-layout cache [B][L][Hkv][S][dh] (positions < n_pos)
+        and set every layer's length to n_pos."""
+        k = np.ascontiguousarray(k, np.float32)
+        v = np.ascontiguousarray(v, np.float32)
+        _check(lib().ffb_kv_import(self._h, _fp(k), _fp(v), k.shape[3], n_pos))
+        for l in range(self.cfg.layers):
+            self.set_length(l, n_pos)
+
+    def set_length(self, layer: int, n: int):
+        _check(lib().ffb_kv_set_length(self._h, layer, n))
+
+    def length(self, layer: int) -> int:
+        return lib().ffb_kv_length(self._h, layer)
+
+    # ------------------------------------------------------------ execution
+    def set_mode(self, mode: RunMode):
+        _check(lib().ffb_set_mode(self._h, int(mode)))
+        self.mode = RunMode(mode)
+
+    def step(self, tokens, pos: int, logits: bool = True, out: np.ndarray | None = None,
+             greedy: np.ndarray | None = None, stream: int = 0):
+        """One decode step; returns (logits f32 [B][V] or None, greedy int64 [B]).
+
+        ``out``/``greedy`` may be preallocated (ideally pinned) host buffers;
+        ``stream`` is a cudaStream_t handle (0 = the model's own stream)."""
+        c = self.cfg
+        tok = np.ascontiguousarray(np.asarray(tokens, dtype=np.int64).reshape(-1))
+        if tok.size != c.batch:
+            raise ValidationError("execute_program: one token per batch row required")
+        if out is None and logits:
+            out = np.empty((c.batch, c.vocab_size), np.float32)
+        if greedy is None:
+            greedy = np.empty(c.batch, np.int64)
+        _check(lib().ffb_decode_step(self._h, tok.ctypes.data_as(C.POINTER(C.c_int64)), pos,
+                                     _fp(out) if out is not None else None,
+                                     greedy.ctypes.data_as(C.POINTER(C.c_int64)),
+                                     C.c_void_p(stream or None)))
+        return out, greedy
+
+    def forward(self, tokens, pos: int) -> np.ndarray:
+        """reference_forward / execute_program contract: logits [batch][vocab]."""
+        return self.step(tokens, pos, logits=True)[0]
+
+    def step_device(self, d_tokens: int, pos: int, d_logits: int = 0, d_greedy: int = 0,
+                    stream: int = 0):
+        """Asynchronous step on raw device pointers (e.g. torch ``data_ptr()``)."""
+        _check(lib().ffb_decode_step_device(self._h, C.c_void_p(d_tokens), pos,
+                                            C.c_void_p(d_logits or None),
+                                            C.c_void_p(d_greedy or None),
+                                            C.c_void_p(stream or None)))
+
+    def info(self) -> dict:
+        i = _Info()
+        _check(lib().ffb_get_info(self._h, C.byref(i)))
+        return {f: getattr(i, f) for f, _ in _Info._fields_}
+
+    def logits_device_ptr(self) -> int:
+        return lib().ffb_logits_device(self._h) or 0

@@ -1,0 +1,58 @@
+// kernel_ops.cuh -- type-erased handle on one compile-time specialisation of
+// the decode kernel.  Each kernels_*.cu translation unit instantiates a few
+// shapes (compiled in parallel) and registers them here; the runtime picks
+// the entry whose shape equals the model config (SURVEY.md §7 hard part 9:
+// instantiate only the shapes that are used).
+#pragma once
+#include <cuda_runtime.h>
+
+#include <vector>
+
+#include "decode_kernel.cuh"
+
+namespace ffb200 {
+
+struct KernelOps {
+    int D, DI, DH, NQ, NKV, B;
+    int threads, smem, nslots, slot_bytes, rg, tmax, kvc;
+    cudaError_t (*prepare)();
+    cudaError_t (*launch)(const DecodeParams&, int grid, cudaStream_t, bool cooperative);
+};
+
+template <class S>
+cudaError_t prepare_impl() {
+    using T = KTraits<S>;
+    return cudaFuncSetAttribute(decode_step_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                T::SMEM_BYTES);
+}
+
+template <class S>
+cudaError_t launch_impl(const DecodeParams& p, int grid, cudaStream_t stream, bool cooperative) {
+    using T = KTraits<S>;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(T::NTHREADS);
+    cfg.dynamicSmemBytes = T::SMEM_BYTES;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeCooperative;
+    attr[0].val.cooperative = cooperative ? 1 : 0;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, decode_step_kernel<S>, p);
+}
+
+template <class S>
+KernelOps make_ops() {
+    using T = KTraits<S>;
+    return KernelOps{S::D,       S::DI,        S::DH,  S::NQ,  S::NKV,    S::B,
+                     T::NTHREADS, T::SMEM_BYTES, T::NSLOTS, T::SLOT_BYTES, T::RG, T::TMAX,
+                     T::KVC,      &prepare_impl<S>, &launch_impl<S>};
+}
+
+// registration hooks, one per kernels_*.cu
+void register_kernels_small(std::vector<KernelOps>& v);
+void register_kernels_1b(std::vector<KernelOps>& v);
+void register_kernels_8b(std::vector<KernelOps>& v);
+
+}  // namespace ffb200

@@ -1,0 +1,687 @@
+// runtime.cu -- host runtime + C-ABI (include/flashformer_b200.h).
+//
+// Replaces, on the device side, the subsystems of the reference that change
+// (SURVEY.md §2.2):
+//   * weight packer   TensorStore f32 arrays (tensor_store.hpp:240-366) ->
+//                     device bf16 matrices, f32 norm gains
+//   * KV allocator    KVCache (tensor_store.hpp:63-150) -> one device block
+//                     [L][B][Hkv][S][dh] bf16, position-major per head so a
+//                     run of positions is one TMA bulk copy
+//   * static planner  build_plan / assign_chunks (partition.hpp:80-343) ->
+//                     balanced contiguous per-CTA row ranges (CtaPlan)
+//   * launch shim     execute_program (interpreter.hpp:502-506) -> one
+//                     cooperative persistent launch per step (or 5L+1
+//                     launches in baseline mode)
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/flashformer_b200.h"
+#include "kernel_ops.cuh"
+
+using namespace ffb200;
+
+namespace {
+
+thread_local std::string g_err;
+
+ffb_status fail(ffb_status s, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof(buf), fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return s;
+}
+
+#define CUDA_TRY(expr)                                                                 \
+    do {                                                                               \
+        cudaError_t e_ = (expr);                                                       \
+        if (e_ != cudaSuccess)                                                         \
+            return fail(FFB_DEVICE, "%s: %s (%s:%d)", #expr, cudaGetErrorString(e_),  \
+                        __FILE__, __LINE__);                                           \
+    } while (0)
+
+const std::vector<KernelOps>& registry() {
+    static std::vector<KernelOps> v;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        register_kernels_small(v);
+        register_kernels_1b(v);
+        register_kernels_8b(v);
+    });
+    return v;
+}
+
+const KernelOps* find_ops(const ffb_model_config& c) {
+    if (c.dtype != 0 || c.quant_bits != 0) return nullptr;
+    for (const auto& k : registry())
+        if (k.D == c.d_model && k.DI == c.d_inter && k.DH == c.d_head && k.NQ == c.n_q_heads &&
+            k.NKV == c.n_kv_heads && k.B == c.batch)
+            return &k;
+    return nullptr;
+}
+
+ffb_status validate_cfg(const ffb_model_config* c) {  // config.hpp:61-83
+    if (!c) return fail(FFB_USAGE, "config is NULL");
+    if (c->layers < 0) return fail(FFB_VALIDATION, "model: layers must be >= 0");
+    if (c->d_model <= 0) return fail(FFB_VALIDATION, "model: d_model must be positive");
+    if (c->batch < 1 || c->batch > 16) return fail(FFB_VALIDATION, "model: batch must be in [1,16]");
+    if (c->d_inter <= 0) return fail(FFB_VALIDATION, "model: d_inter must be positive");
+    if (c->d_head <= 0 || c->d_head % 2)
+        return fail(FFB_VALIDATION, "model: d_head must be positive and even");
+    if (c->n_q_heads <= 0 || c->n_kv_heads <= 0)
+        return fail(FFB_VALIDATION, "model: head counts must be positive");
+    if (c->n_q_heads % c->n_kv_heads)
+        return fail(FFB_VALIDATION, "model: GQA grouping requires n_q_heads mod n_kv_heads == 0");
+    if (c->d_model != c->n_q_heads * c->d_head)
+        return fail(FFB_VALIDATION, "model: d_model must equal n_q_heads * d_head");
+    if (c->vocab_size <= 0) return fail(FFB_VALIDATION, "model: vocab_size must be positive");
+    if (c->quant_bits && (c->quant_group <= 0 || c->d_model % c->quant_group))
+        return fail(FFB_VALIDATION, "quant: group_size must divide every quantized row length");
+    return FFB_OK;
+}
+
+uint16_t bf16_bits_rne(float x) {  // types.hpp:50-59
+    uint32_t bits;
+    std::memcpy(&bits, &x, 4);
+    if ((bits & 0x7f800000u) == 0x7f800000u && (bits & 0x7fffffu)) return (bits >> 16) | 0x40;
+    uint32_t lsb = (bits >> 16) & 1u;
+    bits += 0x7fffu + lsb;
+    return static_cast<uint16_t>(bits >> 16);
+}
+
+float bf16_bits_to_f32(uint16_t h) {
+    uint32_t bits = static_cast<uint32_t>(h) << 16;
+    float f;
+    std::memcpy(&f, &bits, 4);
+    return f;
+}
+
+__global__ void f32_to_bf16_kernel(const float* __restrict__ src, __nv_bfloat16* __restrict__ dst,
+                                   int64_t n) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        dst[i] = __float2bfloat16_rn(src[i]);
+}
+
+__device__ __forceinline__ uint64_t splitmix(uint64_t z) {
+    z += 0x9e3779b97f4a7c15ull;
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+    z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+    return z ^ (z >> 31);
+}
+
+// synthetic weights: uniform with the reference's N(0, 1/sqrt(fan_in)) variance
+__global__ void synth_bf16_kernel(__nv_bfloat16* dst, int64_t n, uint64_t seed, float stddev) {
+    const float a = stddev * 1.7320508f;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const uint64_t r = splitmix(seed ^ (static_cast<uint64_t>(i) * 0xd1b54a32d192ed03ull));
+        const float u = static_cast<float>(r >> 40) * (1.0f / 16777216.0f);  // [0,1)
+        dst[i] = __float2bfloat16_rn((2.0f * u - 1.0f) * a);
+    }
+}
+
+__global__ void synth_f32_kernel(float* dst, int64_t n, uint64_t seed, float mean, float stddev) {
+    const float a = stddev * 1.7320508f;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const uint64_t r = splitmix(seed ^ (static_cast<uint64_t>(i) * 0xd1b54a32d192ed03ull));
+        const float u = static_cast<float>(r >> 40) * (1.0f / 16777216.0f);
+        dst[i] = mean + (2.0f * u - 1.0f) * a;
+    }
+}
+
+int64_t split_at(int64_t units, int64_t c, int64_t grid) { return (units * c) / grid; }
+
+}  // namespace
+
+struct ffb_model {
+    ffb_model_config cfg{};
+    const KernelOps* ops = nullptr;
+    int device = 0, grid = 0, tp_rank = 0, tp_size = 1;
+    int64_t max_seq = 0;
+    int attn_group = 0, n_units = 0;
+    ffb_mode mode = FFB_MODE_FUSED_OVERLAP;
+    uint32_t epoch = 0;
+    cudaStream_t stream = nullptr;
+    std::vector<int64_t> kv_len;
+    std::vector<void*> allocs;
+    uint64_t device_bytes = 0;
+
+    __nv_bfloat16 *wqkv = nullptr, *waout = nullptr, *wffn1 = nullptr, *wffn2t = nullptr;
+    __nv_bfloat16 *embedding = nullptr, *lm_head = nullptr, *kcache = nullptr, *vcache = nullptr;
+    float *norm_attn = nullptr, *norm_ffn = nullptr, *final_norm = nullptr;
+    float *x = nullptr, *q = nullptr, *attn_out = nullptr, *glu_part = nullptr,
+          *attn_part = nullptr, *logits = nullptr, *amax_val = nullptr;
+    int32_t* amax_idx = nullptr;
+    int64_t *greedy = nullptr, *tokens_dev = nullptr;
+    uint32_t *counters = nullptr, *head_counters = nullptr, *amax_counter = nullptr;
+    CtaPlan* plan = nullptr;
+    int64_t* tokens_pinned = nullptr;
+    int64_t* greedy_pinned = nullptr;
+    float* logits_pinned = nullptr;
+    float* staging = nullptr;  // f32 upload staging
+    static constexpr int64_t kStagingElems = 8 << 20;
+
+    int64_t qkv_rows() const { return (cfg.n_q_heads + 2 * cfg.n_kv_heads) * cfg.d_head; }
+
+    template <class Tp>
+    ffb_status alloc(Tp** p, size_t count) {
+        void* ptr = nullptr;
+        size_t bytes = std::max<size_t>(count * sizeof(Tp), 256);
+        cudaError_t e = cudaMalloc(&ptr, bytes);
+        if (e != cudaSuccess)
+            return fail(FFB_DEVICE, "cudaMalloc(%zu bytes): %s", bytes, cudaGetErrorString(e));
+        allocs.push_back(ptr);
+        device_bytes += bytes;
+        *p = static_cast<Tp*>(ptr);
+        return FFB_OK;
+    }
+
+    ~ffb_model() {
+        if (device >= 0) cudaSetDevice(device);
+        for (void* p : allocs) cudaFree(p);
+        if (tokens_pinned) cudaFreeHost(tokens_pinned);
+        if (greedy_pinned) cudaFreeHost(greedy_pinned);
+        if (logits_pinned) cudaFreeHost(logits_pinned);
+        if (stream) cudaStreamDestroy(stream);
+    }
+};
+
+namespace {
+
+ffb_status build_plan(ffb_model* m) {
+    const auto& c = m->cfg;
+    const int64_t G = m->grid;
+    m->n_units = static_cast<int>(c.batch * c.n_kv_heads);
+    if (m->n_units > G) return fail(FFB_UNSUPPORTED, "batch * n_kv_heads exceeds the SM count");
+    m->attn_group = static_cast<int>(G / m->n_units);
+    std::vector<CtaPlan> plan(G);
+    const int64_t qkv_pairs = m->qkv_rows() / 2;
+    for (int64_t i = 0; i < G; ++i) {
+        CtaPlan& p = plan[i];
+        std::memset(&p, 0, sizeof(p));
+        p.qkv_r0 = static_cast<int32_t>(2 * split_at(qkv_pairs, i, G));
+        p.qkv_r1 = static_cast<int32_t>(2 * split_at(qkv_pairs, i + 1, G));
+        p.aout_r0 = static_cast<int32_t>(split_at(c.d_model, i, G));
+        p.aout_r1 = static_cast<int32_t>(split_at(c.d_model, i + 1, G));
+        p.glu_t0 = static_cast<int32_t>(split_at(c.d_inter, i, G));
+        p.glu_t1 = static_cast<int32_t>(split_at(c.d_inter, i + 1, G));
+        p.lm_r0 = static_cast<int32_t>(split_at(c.vocab_size, i, G));
+        p.lm_r1 = static_cast<int32_t>(split_at(c.vocab_size, i + 1, G));
+        p.red_c0 = static_cast<int32_t>(split_at(c.d_model, i, G));
+        p.red_c1 = static_cast<int32_t>(split_at(c.d_model, i + 1, G));
+        if (i < static_cast<int64_t>(m->n_units) * m->attn_group) {
+            p.attn_unit = static_cast<int32_t>(i / m->attn_group);
+            p.attn_g = static_cast<int32_t>(i % m->attn_group);
+        } else {
+            p.attn_unit = -1;
+            p.attn_g = 0;
+        }
+        if (p.glu_t1 - p.glu_t0 > m->ops->tmax)
+            return fail(FFB_UNSUPPORTED, "d_inter too large for the per-CTA GLU buffer");
+    }
+    CUDA_TRY(cudaMemcpy(m->plan, plan.data(), sizeof(CtaPlan) * G, cudaMemcpyHostToDevice));
+    return FFB_OK;
+}
+
+DecodeParams make_params(const ffb_model* m, int64_t pos, const int64_t* d_tokens,
+                         float* d_logits, int64_t* d_greedy) {
+    DecodeParams p{};
+    p.wqkv = m->wqkv;
+    p.waout = m->waout;
+    p.wffn1 = m->wffn1;
+    p.wffn2t = m->wffn2t;
+    p.norm_attn = m->norm_attn;
+    p.norm_ffn = m->norm_ffn;
+    p.final_norm = m->final_norm;
+    p.embedding = m->embedding;
+    p.lm_head = m->lm_head;
+    p.kcache = m->kcache;
+    p.vcache = m->vcache;
+    p.x = m->x;
+    p.q = m->q;
+    p.attn_out = m->attn_out;
+    p.glu_part = m->glu_part;
+    p.attn_part = m->attn_part;
+    p.logits = d_logits ? d_logits : m->logits;
+    p.amax_val = m->amax_val;
+    p.amax_idx = m->amax_idx;
+    p.greedy = d_greedy ? d_greedy : m->greedy;
+    p.counters = m->counters;
+    p.head_counters = m->head_counters;
+    p.amax_counter = m->amax_counter;
+    p.plan = m->plan;
+    p.tokens = d_tokens;
+    p.max_seq = m->max_seq;
+    p.layers = static_cast<int32_t>(m->cfg.layers);
+    p.vocab = static_cast<int32_t>(m->cfg.vocab_size);
+    p.pos = static_cast<int32_t>(pos);
+    p.epoch = m->epoch;
+    p.stage_begin = 0;
+    p.stage_end = static_cast<int32_t>(m->cfg.layers * kStagesPerLayer + 1);
+    p.overlap = m->mode == FFB_MODE_FUSED_OVERLAP ? 1 : 0;
+    p.attn_group = m->attn_group;
+    p.n_units = m->n_units;
+    p.eps = static_cast<float>(m->cfg.rmsnorm_eps);
+    p.rope_theta = m->cfg.rope_theta;
+    return p;
+}
+
+ffb_status launch_step(ffb_model* m, int64_t pos, const int64_t* d_tokens, float* d_logits,
+                       int64_t* d_greedy, cudaStream_t stream) {
+    m->epoch += 1;
+    if (m->epoch >= 0x00ffffffu) {  // keep epoch * grid far from u32 wrap
+        CUDA_TRY(cudaMemsetAsync(m->counters, 0, sizeof(uint32_t) * (m->cfg.layers * 5 + 1), stream));
+        CUDA_TRY(cudaMemsetAsync(m->head_counters, 0,
+                                 sizeof(uint32_t) * std::max<int64_t>(1, m->cfg.layers * m->n_units),
+                                 stream));
+        CUDA_TRY(cudaMemsetAsync(m->amax_counter, 0, sizeof(uint32_t), stream));
+        m->epoch = 1;
+    }
+    DecodeParams p = make_params(m, pos, d_tokens, d_logits, d_greedy);
+    if (m->mode == FFB_MODE_BASELINE) {
+        const int n = static_cast<int>(m->cfg.layers * kStagesPerLayer + 1);
+        for (int s = 0; s < n; ++s) {
+            p.stage_begin = s;
+            p.stage_end = s + 1;
+            CUDA_TRY(m->ops->launch(p, m->grid, stream, false));
+        }
+    } else {
+        CUDA_TRY(m->ops->launch(p, m->grid, stream, true));
+    }
+    return FFB_OK;
+}
+
+struct TensorDst {
+    void* ptr = nullptr;
+    int64_t n = 0;
+    bool is_bf16 = true;
+};
+
+bool resolve(ffb_model* m, const std::string& name, TensorDst* d) {
+    const auto& c = m->cfg;
+    const int64_t D = c.d_model;
+    if (name == "embedding") { *d = {m->embedding, c.vocab_size * D, true}; return true; }
+    if (name == "lm_head") { *d = {m->lm_head, c.vocab_size * D, true}; return true; }
+    if (name == "final_norm") { *d = {m->final_norm, D, false}; return true; }
+    if (name.rfind("layer.", 0) != 0) return false;
+    size_t dot = name.find('.', 6);
+    if (dot == std::string::npos) return false;
+    int64_t l = -1;
+    try {
+        l = std::stoll(name.substr(6, dot - 6));
+    } catch (...) {
+        return false;
+    }
+    if (l < 0 || l >= c.layers) return false;
+    std::string t = name.substr(dot + 1);
+    const int64_t QR = m->qkv_rows();
+    if (t == "wqkv") *d = {m->wqkv + l * QR * D, QR * D, true};
+    else if (t == "waout") *d = {m->waout + l * D * D, D * D, true};
+    else if (t == "wffn1") *d = {m->wffn1 + l * 2 * c.d_inter * D, 2 * c.d_inter * D, true};
+    else if (t == "wffn2t") *d = {m->wffn2t + l * c.d_inter * D, c.d_inter * D, true};
+    else if (t == "norm_attn") *d = {m->norm_attn + l * D, D, false};
+    else if (t == "norm_ffn") *d = {m->norm_ffn + l * D, D, false};
+    else return false;
+    return true;
+}
+
+size_t kv_offset(const ffb_model* m, int64_t b, int64_t l, int64_t h, int64_t pos) {
+    const auto& c = m->cfg;
+    return ((((size_t)l * c.batch + b) * c.n_kv_heads + h) * (size_t)m->max_seq + pos) * c.d_head;
+}
+
+bool pinned(const void* p) {
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeHost;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* ffb_last_error(void) { return g_err.c_str(); }
+const char* ffb_version(void) { return "ffb200 0.1.0 (sm_100a)"; }
+
+int ffb_config_supported(const ffb_model_config* cfg) {
+    if (!cfg) return 0;
+    return find_ops(*cfg) != nullptr ? 1 : 0;
+}
+
+ffb_status ffb_create(const ffb_model_config* cfg, int64_t max_seq_len, int device, int tp_rank,
+                      int tp_size, ffb_model** out) {
+    if (!out) return fail(FFB_USAGE, "out is NULL");
+    *out = nullptr;
+    ffb_status st = validate_cfg(cfg);
+    if (st) return st;
+    if (tp_size != 1 || tp_rank != 0)
+        return fail(FFB_UNSUPPORTED, "tensor-parallel shards are not built in this version");
+    if (max_seq_len < 1) return fail(FFB_VALIDATION, "max_seq_len must be >= 1");
+    const KernelOps* ops = find_ops(*cfg);
+    if (!ops)
+        return fail(FFB_UNSUPPORTED,
+                    "no kernel specialisation for d_model=%lld d_inter=%lld d_head=%lld "
+                    "heads=%lld/%lld batch=%lld quant=%d",
+                    (long long)cfg->d_model, (long long)cfg->d_inter, (long long)cfg->d_head,
+                    (long long)cfg->n_q_heads, (long long)cfg->n_kv_heads, (long long)cfg->batch,
+                    cfg->quant_bits);
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+        cudaGetLastError();
+        return fail(FFB_DEVICE, "no CUDA device visible (this library has no CPU fallback)");
+    }
+    if (device < 0 || device >= ndev) return fail(FFB_USAGE, "device %d out of range", device);
+    CUDA_TRY(cudaSetDevice(device));
+    cudaDeviceProp prop;
+    CUDA_TRY(cudaGetDeviceProperties(&prop, device));
+    if (prop.major != 10)
+        return fail(FFB_DEVICE, "device %d is sm_%d%d; this build targets sm_100a", device,
+                    prop.major, prop.minor);
+    int coop = 0;
+    CUDA_TRY(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, device));
+    if (!coop) return fail(FFB_DEVICE, "device lacks cooperative launch");
+
+    auto m = new ffb_model();
+    m->cfg = *cfg;
+    m->ops = ops;
+    m->device = device;
+    m->grid = prop.multiProcessorCount;
+    m->max_seq = max_seq_len;
+    m->kv_len.assign(cfg->layers, 0);
+    auto bail = [&](ffb_status s) {
+        delete m;
+        return s;
+    };
+    if (ops->prepare() != cudaSuccess) {
+        cudaGetLastError();
+        return bail(fail(FFB_DEVICE, "cannot configure kernel shared memory"));
+    }
+    if (cudaStreamCreateWithFlags(&m->stream, cudaStreamNonBlocking) != cudaSuccess)
+        return bail(fail(FFB_DEVICE, "stream create failed"));
+
+    const auto& c = *cfg;
+    const int64_t L = c.layers, D = c.d_model, B = c.batch, V = c.vocab_size;
+    const int64_t Lc = std::max<int64_t>(L, 1);
+#define ALLOC(ptr, n)                 \
+    do {                              \
+        ffb_status s_ = m->alloc(&(ptr), (n)); \
+        if (s_) return bail(s_);      \
+    } while (0)
+    ALLOC(m->wqkv, (size_t)Lc * m->qkv_rows() * D);
+    ALLOC(m->waout, (size_t)Lc * D * D);
+    ALLOC(m->wffn1, (size_t)Lc * 2 * c.d_inter * D);
+    ALLOC(m->wffn2t, (size_t)Lc * c.d_inter * D);
+    ALLOC(m->norm_attn, (size_t)Lc * D);
+    ALLOC(m->norm_ffn, (size_t)Lc * D);
+    ALLOC(m->final_norm, (size_t)D);
+    ALLOC(m->embedding, (size_t)V * D);
+    ALLOC(m->lm_head, (size_t)V * D);
+    const size_t kv = (size_t)Lc * B * c.n_kv_heads * max_seq_len * c.d_head;
+    ALLOC(m->kcache, kv);
+    ALLOC(m->vcache, kv);
+    ALLOC(m->x, (size_t)B * D);
+    ALLOC(m->q, (size_t)B * D);
+    ALLOC(m->attn_out, (size_t)B * D);
+    ALLOC(m->glu_part, (size_t)m->grid * ops->rg * B * D);
+    const int64_t units = B * c.n_kv_heads;
+    const int64_t qpg = c.n_q_heads / c.n_kv_heads;
+    ALLOC(m->attn_part, (size_t)units * m->grid * qpg * (c.d_head + 2));
+    ALLOC(m->logits, (size_t)B * V);
+    ALLOC(m->amax_val, (size_t)m->grid * B);
+    ALLOC(m->amax_idx, (size_t)m->grid * B);
+    ALLOC(m->greedy, (size_t)B);
+    ALLOC(m->tokens_dev, (size_t)B);
+    ALLOC(m->counters, (size_t)Lc * 5 + 1);
+    ALLOC(m->head_counters, (size_t)Lc * units);
+    ALLOC(m->amax_counter, 1);
+    ALLOC(m->plan, (size_t)m->grid);
+    ALLOC(m->staging, (size_t)ffb_model::kStagingElems);
+#undef ALLOC
+    if (cudaMemset(m->counters, 0, sizeof(uint32_t) * (Lc * 5 + 1)) != cudaSuccess ||
+        cudaMemset(m->head_counters, 0, sizeof(uint32_t) * Lc * units) != cudaSuccess ||
+        cudaMemset(m->amax_counter, 0, sizeof(uint32_t)) != cudaSuccess ||
+        cudaMemset(m->kcache, 0, kv * 2) != cudaSuccess ||
+        cudaMemset(m->vcache, 0, kv * 2) != cudaSuccess)
+        return bail(fail(FFB_DEVICE, "cudaMemset failed"));
+    if (cudaMallocHost(&m->tokens_pinned, sizeof(int64_t) * B) != cudaSuccess ||
+        cudaMallocHost(&m->greedy_pinned, sizeof(int64_t) * B) != cudaSuccess ||
+        cudaMallocHost(&m->logits_pinned, sizeof(float) * B * V) != cudaSuccess)
+        return bail(fail(FFB_DEVICE, "cudaMallocHost failed"));
+    st = build_plan(m);
+    if (st) return bail(st);
+    *out = m;
+    return FFB_OK;
+}
+
+void ffb_destroy(ffb_model* m) { delete m; }
+
+ffb_status ffb_upload_tensor(ffb_model* m, const char* name, const float* values, int64_t n) {
+    if (!m || !name || !values) return fail(FFB_USAGE, "NULL argument");
+    TensorDst d;
+    if (!resolve(m, name, &d)) return fail(FFB_USAGE, "unknown tensor name '%s'", name);
+    if (n != d.n)
+        return fail(FFB_USAGE, "tensor '%s': expected %lld values, got %lld", name,
+                    (long long)d.n, (long long)n);
+    CUDA_TRY(cudaSetDevice(m->device));
+    if (!d.is_bf16) {
+        CUDA_TRY(cudaMemcpy(d.ptr, values, sizeof(float) * n, cudaMemcpyHostToDevice));
+        return FFB_OK;
+    }
+    auto* dst = static_cast<__nv_bfloat16*>(d.ptr);
+    for (int64_t off = 0; off < n; off += ffb_model::kStagingElems) {
+        const int64_t cnt = std::min<int64_t>(ffb_model::kStagingElems, n - off);
+        CUDA_TRY(cudaMemcpyAsync(m->staging, values + off, sizeof(float) * cnt,
+                                 cudaMemcpyHostToDevice, m->stream));
+        f32_to_bf16_kernel<<<1184, 256, 0, m->stream>>>(m->staging, dst + off, cnt);
+        CUDA_TRY(cudaGetLastError());
+    }
+    CUDA_TRY(cudaStreamSynchronize(m->stream));
+    return FFB_OK;
+}
+
+ffb_status ffb_init_synthetic(ffb_model* m, uint64_t seed) {
+    if (!m) return fail(FFB_USAGE, "NULL handle");
+    CUDA_TRY(cudaSetDevice(m->device));
+    const auto& c = m->cfg;
+    const int64_t L = c.layers, D = c.d_model;
+    const float sd = 1.0f / std::sqrt(static_cast<float>(D));
+    const float sdi = 1.0f / std::sqrt(static_cast<float>(c.d_inter));
+    auto bf = [&](__nv_bfloat16* p, int64_t n, uint64_t s, float stddev) {
+        synth_bf16_kernel<<<4096, 256, 0, m->stream>>>(p, n, seed * 1315423911ull + s, stddev);
+    };
+    auto f32 = [&](float* p, int64_t n, uint64_t s) {
+        synth_f32_kernel<<<256, 256, 0, m->stream>>>(p, n, seed * 1315423911ull + s, 1.0f, 0.02f);
+    };
+    bf(m->wqkv, L * m->qkv_rows() * D, 1, sd);
+    bf(m->waout, L * D * D, 2, sd);
+    bf(m->wffn1, L * 2 * c.d_inter * D, 3, sd);
+    bf(m->wffn2t, L * c.d_inter * D, 4, sdi);
+    bf(m->embedding, c.vocab_size * D, 5, sd);
+    bf(m->lm_head, c.vocab_size * D, 6, sd);
+    f32(m->norm_attn, L * D, 7);
+    f32(m->norm_ffn, L * D, 8);
+    f32(m->final_norm, D, 9);
+    CUDA_TRY(cudaGetLastError());
+    CUDA_TRY(cudaStreamSynchronize(m->stream));
+    return FFB_OK;
+}
+
+ffb_status ffb_kv_set(ffb_model* m, int64_t b, int64_t layer, int64_t head, int64_t pos,
+                      const float* k, const float* v) {
+    if (!m || !k || !v) return fail(FFB_USAGE, "NULL argument");
+    const auto& c = m->cfg;
+    if (b < 0 || b >= c.batch || layer < 0 || layer >= c.layers || head < 0 ||
+        head >= c.n_kv_heads || pos < 0 || pos >= m->max_seq)
+        return fail(FFB_VALIDATION, "kv_set: index out of range");
+    std::vector<uint16_t> kb(c.d_head), vb(c.d_head);
+    for (int64_t d = 0; d < c.d_head; ++d) {
+        kb[d] = bf16_bits_rne(k[d]);
+        vb[d] = bf16_bits_rne(v[d]);
+    }
+    CUDA_TRY(cudaSetDevice(m->device));
+    const size_t off = kv_offset(m, b, layer, head, pos);
+    CUDA_TRY(cudaMemcpy(m->kcache + off, kb.data(), 2 * c.d_head, cudaMemcpyHostToDevice));
+    CUDA_TRY(cudaMemcpy(m->vcache + off, vb.data(), 2 * c.d_head, cudaMemcpyHostToDevice));
+    return FFB_OK;
+}
+
+ffb_status ffb_kv_get(ffb_model* m, int64_t b, int64_t layer, int64_t head, int64_t pos,
+                      float* k, float* v) {
+    if (!m || !k || !v) return fail(FFB_USAGE, "NULL argument");
+    const auto& c = m->cfg;
+    if (b < 0 || b >= c.batch || layer < 0 || layer >= c.layers || head < 0 ||
+        head >= c.n_kv_heads || pos < 0 || pos >= m->max_seq)
+        return fail(FFB_VALIDATION, "kv_get: index out of range");
+    std::vector<uint16_t> kb(c.d_head), vb(c.d_head);
+    CUDA_TRY(cudaSetDevice(m->device));
+    CUDA_TRY(cudaStreamSynchronize(m->stream));
+    const size_t off = kv_offset(m, b, layer, head, pos);
+    CUDA_TRY(cudaMemcpy(kb.data(), m->kcache + off, 2 * c.d_head, cudaMemcpyDeviceToHost));
+    CUDA_TRY(cudaMemcpy(vb.data(), m->vcache + off, 2 * c.d_head, cudaMemcpyDeviceToHost));
+    for (int64_t d = 0; d < c.d_head; ++d) {
+        k[d] = bf16_bits_to_f32(kb[d]);
+        v[d] = bf16_bits_to_f32(vb[d]);
+    }
+    return FFB_OK;
+}
+
+ffb_status ffb_kv_import(ffb_model* m, const float* k, const float* v, int64_t src_max_seq,
+                         int64_t n_pos) {
+    if (!m || !k || !v) return fail(FFB_USAGE, "NULL argument");
+    const auto& c = m->cfg;
+    if (n_pos < 0 || n_pos > m->max_seq || n_pos > src_max_seq)
+        return fail(FFB_VALIDATION, "kv_import: n_pos out of range");
+    CUDA_TRY(cudaSetDevice(m->device));
+    std::vector<uint16_t> kb(n_pos * c.d_head), vb(n_pos * c.d_head);
+    for (int64_t b = 0; b < c.batch; ++b)
+        for (int64_t l = 0; l < c.layers; ++l)
+            for (int64_t h = 0; h < c.n_kv_heads; ++h) {
+                const size_t src = (((size_t)b * c.layers + l) * c.n_kv_heads + h) * src_max_seq * c.d_head;
+                for (int64_t i = 0; i < n_pos * c.d_head; ++i) {
+                    kb[i] = bf16_bits_rne(k[src + i]);
+                    vb[i] = bf16_bits_rne(v[src + i]);
+                }
+                const size_t off = kv_offset(m, b, l, h, 0);
+                CUDA_TRY(cudaMemcpy(m->kcache + off, kb.data(), 2 * n_pos * c.d_head,
+                                    cudaMemcpyHostToDevice));
+                CUDA_TRY(cudaMemcpy(m->vcache + off, vb.data(), 2 * n_pos * c.d_head,
+                                    cudaMemcpyHostToDevice));
+            }
+    return FFB_OK;
+}
+
+ffb_status ffb_kv_set_length(ffb_model* m, int64_t layer, int64_t n) {
+    if (!m) return fail(FFB_USAGE, "NULL handle");
+    if (layer < 0 || layer >= m->cfg.layers) return fail(FFB_VALIDATION, "kv_set_length: bad layer");
+    if (n < 0 || n > m->max_seq) return fail(FFB_VALIDATION, "kv_set_length: beyond max_seq_len");
+    m->kv_len[layer] = n;
+    return FFB_OK;
+}
+
+int64_t ffb_kv_length(const ffb_model* m, int64_t layer) {
+    if (!m || layer < 0 || layer >= m->cfg.layers) return -1;
+    return m->kv_len[layer];
+}
+
+ffb_status ffb_set_mode(ffb_model* m, ffb_mode mode) {
+    if (!m) return fail(FFB_USAGE, "NULL handle");
+    if (mode != FFB_MODE_BASELINE && mode != FFB_MODE_FUSED && mode != FFB_MODE_FUSED_OVERLAP)
+        return fail(FFB_USAGE, "unknown mode %d", (int)mode);
+    m->mode = mode;
+    return FFB_OK;
+}
+
+static ffb_status check_step(ffb_model* m, const int64_t* tokens, int64_t pos) {
+    const auto& c = m->cfg;
+    if (tokens)
+        for (int64_t b = 0; b < c.batch; ++b)
+            if (tokens[b] < 0 || tokens[b] >= c.vocab_size)
+                return fail(FFB_VALIDATION, "decode_step: token id out of range");
+    for (int64_t l = 0; l < c.layers; ++l)
+        if (m->kv_len[l] != pos)
+            return fail(FFB_VALIDATION, "decode_step: cache length does not match position");
+    if (pos < 0 || pos >= m->max_seq)
+        return fail(FFB_VALIDATION, "kv_append: cache capacity reached (max_seq_len)");
+    return FFB_OK;
+}
+
+ffb_status ffb_decode_step(ffb_model* m, const int64_t* tokens, int64_t pos, float* logits_out,
+                           int64_t* greedy_out, void* stream) {
+    if (!m || !tokens) return fail(FFB_USAGE, "NULL argument");
+    ffb_status st = check_step(m, tokens, pos);
+    if (st) return st;
+    CUDA_TRY(cudaSetDevice(m->device));
+    cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : m->stream;
+    const auto& c = m->cfg;
+    std::memcpy(m->tokens_pinned, tokens, sizeof(int64_t) * c.batch);
+    CUDA_TRY(cudaMemcpyAsync(m->tokens_dev, m->tokens_pinned, sizeof(int64_t) * c.batch,
+                             cudaMemcpyHostToDevice, s));
+    st = launch_step(m, pos, m->tokens_dev, nullptr, nullptr, s);
+    if (st) return st;
+    const size_t lbytes = sizeof(float) * c.batch * c.vocab_size;
+    const bool direct = logits_out && pinned(logits_out);
+    if (logits_out)
+        CUDA_TRY(cudaMemcpyAsync(direct ? logits_out : m->logits_pinned, m->logits, lbytes,
+                                 cudaMemcpyDeviceToHost, s));
+    if (greedy_out)
+        CUDA_TRY(cudaMemcpyAsync(m->greedy_pinned, m->greedy, sizeof(int64_t) * c.batch,
+                                 cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaStreamSynchronize(s));
+    if (logits_out && !direct) std::memcpy(logits_out, m->logits_pinned, lbytes);
+    if (greedy_out) std::memcpy(greedy_out, m->greedy_pinned, sizeof(int64_t) * c.batch);
+    for (auto& n : m->kv_len) n += 1;
+    return FFB_OK;
+}
+
+ffb_status ffb_decode_step_device(ffb_model* m, const int64_t* d_tokens, int64_t pos,
+                                  float* d_logits, int64_t* d_greedy, void* stream) {
+    if (!m || !d_tokens) return fail(FFB_USAGE, "NULL argument");
+    ffb_status st = check_step(m, nullptr, pos);
+    if (st) return st;
+    CUDA_TRY(cudaSetDevice(m->device));
+    cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : m->stream;
+    st = launch_step(m, pos, d_tokens, d_logits, d_greedy, s);
+    if (st) return st;
+    for (auto& n : m->kv_len) n += 1;
+    return FFB_OK;
+}
+
+ffb_status ffb_get_info(const ffb_model* m, ffb_info* out) {
+    if (!m || !out) return fail(FFB_USAGE, "NULL argument");
+    const auto& c = m->cfg;
+    out->grid = m->grid;
+    out->threads = m->ops->threads;
+    out->smem_bytes = m->ops->smem;
+    out->ring_slots = m->ops->nslots;
+    out->slot_bytes = m->ops->slot_bytes;
+    out->attn_group = m->attn_group;
+    out->launches_per_step =
+        m->mode == FFB_MODE_BASELINE ? static_cast<int32_t>(c.layers * kStagesPerLayer + 1) : 1;
+    out->mode = m->mode;
+    const uint64_t row = static_cast<uint64_t>(c.d_model) * 2;
+    out->weight_bytes = row * (static_cast<uint64_t>(c.layers) *
+                                   (m->qkv_rows() + c.d_model + 3 * c.d_inter) +
+                               c.vocab_size);
+    out->device_bytes = m->device_bytes;
+    return FFB_OK;
+}
+
+const float* ffb_logits_device(const ffb_model* m) { return m ? m->logits : nullptr; }
+
+}  // extern "C"

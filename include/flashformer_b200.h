@@ -110,6 +110,25 @@ int64_t ffb_kv_length(const ffb_model *m, int64_t layer);
 
 ffb_status ffb_set_mode(ffb_model *m, ffb_mode mode);
 
+/* Tuning knobs.  "l2_prefetch_bytes": how far (bytes per SM) the producer's
+ * L2 prefetch cursor runs ahead of the shared-memory ring in FusedOverlap
+ * mode (0 disables; default 256 KiB). */
+ffb_status ffb_set_option(ffb_model *m, const char *key, int64_t value);
+
+/* Diagnostics only (never needed for correct use): bit 0 = streaming-only
+ * run, the consumer warps just wait for and release every ring slot of the
+ * schedule -- measures the TMA streaming rate with no math and no
+ * inter-SM flags.  Results are garbage while set. */
+ffb_status ffb_set_debug(ffb_model *m, int32_t flags);
+
+/* Tracing: when enabled, consumer thread 0 of every CTA
+ * records %globaltimer at each stage's entry, dependency-met, done and a
+ * stage-specific mark, plus the ns it spent starved waiting for ring data,
+ * into a device buffer [grid][5*L+1][8] (u64).  ffb_get_trace copies it out
+ * (out may be NULL to query the element count); returns -1 on error. */
+ffb_status ffb_set_trace(ffb_model *m, int enable);
+int64_t ffb_get_trace(ffb_model *m, uint64_t *out, int64_t n);
+
 /* One decode step for every batch row (reference.hpp:37-139 contract):
  * tokens[batch] (host), pos == kv length of every layer, appends one KV
  * position per layer.  logits_out: batch x vocab f32 (host, may be NULL);

@@ -185,6 +185,11 @@ def lib():
     L.ffb_kv_length.argtypes = [C.c_void_p, C.c_int64]
     L.ffb_kv_length.restype = C.c_int64
     L.ffb_set_mode.argtypes = [C.c_void_p, C.c_int]
+    L.ffb_set_debug.argtypes = [C.c_void_p, C.c_int32]
+    L.ffb_set_option.argtypes = [C.c_void_p, C.c_char_p, C.c_int64]
+    L.ffb_set_trace.argtypes = [C.c_void_p, C.c_int]
+    L.ffb_get_trace.argtypes = [C.c_void_p, C.POINTER(C.c_uint64), C.c_int64]
+    L.ffb_get_trace.restype = C.c_int64
     L.ffb_decode_step.argtypes = [C.c_void_p, P(C.c_int64), C.c_int64, P(C.c_float),
                                   P(C.c_int64), C.c_void_p]
     L.ffb_decode_step_device.argtypes = [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p,
@@ -295,6 +300,29 @@ class DecodeModel:
     def set_mode(self, mode: RunMode):
         _check(lib().ffb_set_mode(self._h, int(mode)))
         self.mode = RunMode(mode)
+
+    def set_option(self, key: str, value: int):
+        """Tuning knobs (ffb_set_option), e.g. ("l2_prefetch_bytes", 262144)."""
+        _check(lib().ffb_set_option(self._h, key.encode(), int(value)))
+
+    def set_debug(self, flags: int):
+        """Diagnostics only (ffb_set_debug): 1 = streaming-only run."""
+        _check(lib().ffb_set_debug(self._h, flags))
+
+    def set_trace(self, enable: bool = True):
+        """Per-CTA stage timestamps of the next steps (ffb_set_trace)."""
+        _check(lib().ffb_set_trace(self._h, 1 if enable else 0))
+
+    def trace(self) -> np.ndarray:
+        """[grid][5L+1][8] u64: stage entry, dependency met, stage done, stage
+        mark (ns timestamps), ns starved on ring data, spare."""
+        n = lib().ffb_get_trace(self._h, None, 0)
+        if n < 0:
+            raise DeviceError("tracing not enabled")
+        out = np.zeros(n, np.uint64)
+        if lib().ffb_get_trace(self._h, out.ctypes.data_as(C.POINTER(C.c_uint64)), n) < 0:
+            raise DeviceError(lib().ffb_last_error().decode())
+        return out.reshape(self.info()["grid"], self.cfg.layers * 5 + 1, 8)
 
     def step(self, tokens, pos: int, logits: bool = True, out: np.ndarray | None = None,
              greedy: np.ndarray | None = None, stream: int = 0):

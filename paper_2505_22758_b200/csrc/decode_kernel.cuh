@@ -42,6 +42,18 @@
 
 namespace ffb200 {
 
+// Debug bits (never set by the public API's production path):
+//   kDebugStreamOnly: consumers only wait for / release ring slots (pure TMA
+//                     streaming rate of the schedule, no math, no flags)
+enum : int { kDebugStreamOnly = 1 };
+
+// per-(CTA, stage) trace record: 0 entry, 1 dependency met, 2 done,
+// 3 stage mark, 4 ns starved waiting for ring data, 5-7 spare
+constexpr int kTraceSlots = 8;
+
+// most CTAs that split one (batch row, kv head)'s positions (runtime.cu)
+constexpr int kMaxGroup = 32;
+
 enum : int { S_QKV = 0, S_ATTN = 1, S_AOUT = 2, S_GLU = 3, S_RED = 4, kStagesPerLayer = 5 };
 
 // Static per-CTA work ranges, built on the host (runtime.cu: build_cta_plan).
@@ -91,6 +103,15 @@ struct DecodeParams {
     int32_t overlap;     // 1 = FusedOverlap, 0 = Fused (producer waits at barriers)
     int32_t attn_group;  // G: CTAs per (batch row, kv head)
     int32_t n_units;     // B * NKV
+    int32_t debug;       // kDebug* bits; 0 in production
+    uint64_t* trace;     // optional [grid][n_stages][8] trace records
+    int64_t l2_prefetch; // bytes the L2 prefetch cursor runs ahead of the ring
+    // GLU work pool (dynamic load balance, deterministic): pairs [pool_t0, DI)
+    // in chunks of pool_ct pairs, claimed at run time by whichever CTA is free;
+    // each chunk's d_model partial goes to pool_part[chunk].
+    float* pool_part;          // [pool_chunks][RG][B][D]
+    uint32_t* pool_counters;   // [L] claim counters (epoch based)
+    int32_t pool_t0, pool_ct, pool_chunks;
     float eps;
     double rope_theta;
 };
@@ -119,19 +140,22 @@ struct KTraits {
     static constexpr int ROW_BYTES = S::D * 2;
     static constexpr int RPS = SLOT_BYTES / ROW_BYTES;  // rows per slot
     static constexpr int RPT = RPS / RG;            // rows per thread per slot
+    // rows per epilogue batch (whole slots; >= 64/B rows so barriers are rare)
+    static constexpr int RB = RPS > 64 / S::B ? RPS : ((64 / S::B) / RPS) * RPS;
     static constexpr int KVC = SLOT_BYTES / (2 * S::DH * 2);  // KV positions per slot
     static constexpr int DPL = S::DH / 32;          // attention dims per lane
     static constexpr int TMAX = 160;                // max GLU pairs per CTA (host-checked)
     static_assert(TPR % 32 == 0, "a row must span whole warps");
     static_assert(NV % TPR == 0 && NCT % TPR == 0, "row mapping");
     static_assert(RPS >= 2 && RPS % 2 == 0 && RPS % RG == 0, "slot rows");
-    static_assert(RPS * S::B <= NCT, "epilogue threads");
+    static_assert(RPS * S::B <= NCT && RB * S::B <= NCT, "epilogue threads");
+    static_assert(RPT * S::B <= 32, "one transposed warp reduction per slot");
     static_assert(S::DH % 32 == 0 && DPL <= 8, "attention lane split");
     static_assert(KVC >= 1, "kv chunk");
 
     // ---- shared memory carve-up (bytes) ----
     static constexpr int OFF_RED = 0;  // [2][WPR][RPS][B] f32
-    static constexpr int SZ_RED = 2 * WPR * RPS * S::B * 4;
+    static constexpr int SZ_RED = 2 * WPR * RB * S::B * 4;
     static constexpr int OFF_H = OFF_RED + SZ_RED;  // [B][TMAX] f32
     static constexpr int SZ_H = S::B * TMAX * 4;
     static constexpr int OFF_ROPE = OFF_H + SZ_H;  // [DH/2][2] f32
@@ -139,11 +163,17 @@ struct KTraits {
     static constexpr int OFF_NORM = OFF_ROPE + SZ_ROPE;  // [NCW][B] f32
     static constexpr int SZ_NORM = NCW * S::B * 4 + 16;
     static constexpr int OFF_WPART = OFF_NORM + SZ_NORM;  // [NCW][QPG][DH+2] f32
-    static constexpr int SZ_WPART = NCW * S::QPG * (S::DH + 2) * 4;
+    // also reused for: attention combine (3*G*QPG), argmax candidates
+    // (2*grid*B) and the GLU reduction (NCW*32); grid <= kMaxGrid
+    static constexpr int kMaxGrid = 160;
+    static constexpr int cmax(int a, int b) { return a > b ? a : b; }
+    static constexpr int SZ_WPART =
+        4 * cmax(cmax(NCW * S::QPG * (S::DH + 2), 3 * kMaxGrid * S::QPG),
+                 cmax(2 * kMaxGrid * S::B, NCW * 32));
     static constexpr int OFF_AMAX = OFF_WPART + SZ_WPART;  // [NCT] (f32, i32)
     static constexpr int SZ_AMAX = NCT * 8;
     static constexpr int OFF_MISC = OFF_AMAX + SZ_AMAX;  // flags
-    static constexpr int SZ_MISC = 64;
+    static constexpr int SZ_MISC = 256;
     static constexpr int FIXED = ((OFF_MISC + SZ_MISC + 1023) / 1024) * 1024;
     static constexpr int MAX_SMEM = 227 * 1024;
     static constexpr int NSLOTS_RAW = (MAX_SMEM - FIXED - 256) / SLOT_BYTES;
@@ -180,7 +210,7 @@ struct DecodeCta {
     }
 
     __device__ float* red_buf(uint32_t it) {
-        return reinterpret_cast<float*>(smem + T::OFF_RED) + (it & 1) * (T::WPR * T::RPS * B);
+        return reinterpret_cast<float*>(smem + T::OFF_RED) + (it & 1) * (T::WPR * T::RB * B);
     }
     __device__ float* h_s() { return reinterpret_cast<float*>(smem + T::OFF_H); }
     __device__ float* rope() { return reinterpret_cast<float*>(smem + T::OFF_ROPE); }
@@ -237,14 +267,160 @@ struct DecodeCta {
         return ((((size_t)l * B + b) * S::NKV + h) * (size_t)p.max_seq + pos) * DH;
     }
 
+    // KV rows are stored with their 16-byte chunks XOR-swizzled by (pos & 7)
+    // (runtime.cu applies the same map on import/export): element `dim` of
+    // position `pos` lives at this offset inside the row.
+    __device__ static int kv_swz_dim(int dim, int pos) {
+        return ((((dim >> 3) ^ (pos & 7))) << 3) | (dim & 7);
+    }
+
     // ============================================================ producer
-    __device__ void produce_rows(uint32_t& it, const __nv_bfloat16* base, int r0, int r1,
-                                 uint64_t policy) {
+    // The static schedule walked twice: by the producer lane (DRAIN=false:
+    // issue TMA into free slots) and, in the streaming-only debug mode, by the
+    // consumer warps (DRAIN=true: wait for each slot and release it).
+    template <bool DRAIN>
+    __device__ void chunk(uint32_t& it, const void* src0, const void* src1, uint32_t bytes,
+                          uint32_t off1, uint64_t policy) {
+        const uint32_t slot = it % T::NSLOTS, ph = (it / T::NSLOTS) & 1;
+        if (DRAIN) {
+            mbar_wait(&full[slot], ph);
+            __syncwarp();
+            if ((threadIdx.x & 31) == 0) mbar_arrive(&empty[slot]);
+        } else {
+            mbar_wait(&empty[slot], ph ^ 1);
+            mbar_arrive_expect_tx(&full[slot], src1 ? 2 * bytes : bytes);
+            uint8_t* dst = ring + slot * T::SLOT_BYTES;
+            tma_load_1d(dst, src0, bytes, &full[slot], policy);
+            if (src1) tma_load_1d(dst + off1, src1, bytes, &full[slot], policy);
+        }
+        ++it;
+    }
+
+    // One list of the static per-CTA stream: rows [r0, r1) of a matrix (kv =
+    // false) or KV positions [r0, r1) of one (layer, batch row, kv head).
+    struct List {
+        const __nv_bfloat16* base;
+        int r0, r1;
+        bool kv;
+        bool pool;  // the GLU work pool: one marker chunk, claimed dynamically
+    };
+
+    // The lists of (stage, sub) in consumption order; false past the end.
+    __device__ bool list_of(int stage, int sub, List& L) const {
+        const int l = stage / kStagesPerLayer, s = stage % kStagesPerLayer;
+        if (stage == p.layers * kStagesPerLayer) {
+            if (sub > 0) return false;
+            L = {p.lm_head, pl.lm_r0, pl.lm_r1, false, false};
+            return true;
+        }
+        switch (s) {
+            case S_QKV:
+                if (sub > 0) return false;
+                L = {p.wqkv + (size_t)l * S::QKVR * D, pl.qkv_r0, pl.qkv_r1, false, false};
+                return true;
+            case S_ATTN: {
+                if (sub > 0 || pl.attn_unit < 0) return false;
+                int p0, p1;
+                attn_range(p0, p1);
+                const int unit = pl.attn_unit;
+                L = {p.kcache + kv_row(l, unit / S::NKV, unit % S::NKV, 0), p0, min(p1, p.pos),
+                     true, false};
+                return true;
+            }
+            case S_AOUT:
+                if (sub > 0) return false;
+                L = {p.waout + (size_t)l * D * D, pl.aout_r0, pl.aout_r1, false, false};
+                return true;
+            case S_GLU:
+                if (sub == 0) L = {p.wffn1 + (size_t)l * 2 * S::DI * D, 2 * pl.glu_t0,
+                                   2 * pl.glu_t1, false, false};
+                else if (sub == 1) L = {p.wffn2t + (size_t)l * S::DI * D, pl.glu_t0, pl.glu_t1,
+                                        false, false};
+                else if (sub == 2 && p.pool_chunks > 0) L = {nullptr, 0, 1, false, true};
+                else return false;
+                return true;
+            default:
+                return false;
+        }
+    }
+
+    // Walks the per-CTA stream chunk by chunk (one ring slot each).
+    struct Cursor {
+        int stage, sub, c0;
+        bool valid;
+        List L;
+    };
+
+    __device__ void cursor_init(Cursor& c) const {
+        c.stage = p.stage_begin;
+        c.sub = 0;
+        c.valid = false;
+    }
+
+    // Next chunk: K/matrix source, V source (kv only), bytes per source, stage.
+    __device__ bool cursor_next(Cursor& c, const void** src0, const void** src1,
+                                uint32_t* bytes, int* stage) const {
+        const int last = min(p.stage_end, n_stages());
+        while (c.stage < last) {
+            if (!c.valid) {
+                if (!list_of(c.stage, c.sub, c.L)) {
+                    ++c.stage;
+                    c.sub = 0;
+                    continue;
+                }
+                c.valid = true;
+                c.c0 = c.L.r0;
+            }
+            if (c.c0 >= c.L.r1) {
+                c.valid = false;
+                ++c.sub;
+                continue;
+            }
+            *stage = c.stage;
+            if (c.L.pool) {  // marker: the caller runs the dynamic pool protocol
+                *src0 = nullptr;
+                *src1 = nullptr;
+                *bytes = 0;
+                c.c0 = c.L.r1;
+            } else if (c.L.kv) {
+                const int n = min(T::KVC, c.L.r1 - c.c0);
+                const size_t off = (size_t)c.c0 * DH;
+                *src0 = c.L.base + off;
+                *src1 = p.vcache + (c.L.base - p.kcache) + off;
+                *bytes = static_cast<uint32_t>(n) * DH * 2;
+                c.c0 += T::KVC;
+            } else {
+                const int n = min(T::RPS, c.L.r1 - c.c0);
+                *src0 = c.L.base + (size_t)c.c0 * D;
+                *src1 = nullptr;
+                *bytes = static_cast<uint32_t>(n) * T::ROW_BYTES;
+                c.c0 += T::RPS;
+            }
+            return true;
+        }
+        return false;
+    }
+
+    // ---- GLU work pool ------------------------------------------------
+    // After its static GLU slice a CTA's producer claims pool chunks with an
+    // atomic (one claim kept in flight) and streams each chunk's Wffn1 rows
+    // then Wffn2^T rows, tagging every slot with the chunk id (slot_meta);
+    // a failed claim sends an end marker (slot_meta = -1, plain arrive, no
+    // bytes).  Every CTA makes exactly (claims + 1) increments per layer, so
+    // the counter base of an epoch is (epoch-1) * (pool_chunks + grid).
+    __device__ int* slot_meta() { return misc() + 32; }
+
+    __device__ int pool_slots() const {
+        return (2 * p.pool_ct + T::RPS - 1) / T::RPS + (p.pool_ct + T::RPS - 1) / T::RPS;
+    }
+
+    __device__ void pool_stream(uint32_t& it, const __nv_bfloat16* base, int r0, int r1, int ch,
+                                uint64_t policy) {
         for (int c0 = r0; c0 < r1; c0 += T::RPS) {
-            const int n = min(T::RPS, r1 - c0);
-            const uint32_t slot = it % T::NSLOTS, par = ((it / T::NSLOTS) & 1) ^ 1;
-            mbar_wait(&empty[slot], par);
-            const uint32_t bytes = static_cast<uint32_t>(n) * T::ROW_BYTES;
+            const uint32_t slot = it % T::NSLOTS, ph = (it / T::NSLOTS) & 1;
+            mbar_wait(&empty[slot], ph ^ 1);
+            slot_meta()[slot] = ch;
+            const uint32_t bytes = static_cast<uint32_t>(min(T::RPS, r1 - c0)) * T::ROW_BYTES;
             mbar_arrive_expect_tx(&full[slot], bytes);
             tma_load_1d(ring + slot * T::SLOT_BYTES, base + (size_t)c0 * D, bytes, &full[slot],
                         policy);
@@ -252,61 +428,121 @@ struct DecodeCta {
         }
     }
 
-    __device__ void produce_kv(uint32_t& it, int l, int q0, int q1, uint64_t policy) {
-        const int unit = pl.attn_unit, b = unit / S::NKV, h = unit % S::NKV;
-        for (int c0 = q0; c0 < q1; c0 += T::KVC) {
-            const int n = min(T::KVC, q1 - c0);
-            const uint32_t slot = it % T::NSLOTS, par = ((it / T::NSLOTS) & 1) ^ 1;
-            mbar_wait(&empty[slot], par);
-            const uint32_t bytes = static_cast<uint32_t>(n) * DH * 2;
-            mbar_arrive_expect_tx(&full[slot], 2 * bytes);
-            uint8_t* dst = ring + slot * T::SLOT_BYTES;
-            const size_t row = kv_row(l, b, h, c0);
-            tma_load_1d(dst, p.kcache + row, bytes, &full[slot], policy);
-            tma_load_1d(dst + T::SLOT_BYTES / 2, p.vcache + row, bytes, &full[slot], policy);
-            ++it;
+    template <bool DRAIN>
+    __device__ void pool_run(uint32_t& it, int l, uint64_t policy) {
+        if (DRAIN) {  // streaming-only debug: mirror the consumer protocol
+            for (;;) {
+                const uint32_t slot = it % T::NSLOTS, ph = (it / T::NSLOTS) & 1;
+                mbar_wait(&full[slot], ph);
+                const int ch = slot_meta()[slot];
+                __syncwarp();
+                if ((threadIdx.x & 31) == 0) mbar_arrive(&empty[slot]);
+                ++it;
+                if (ch < 0) return;
+                for (int k = 1; k < pool_slots(); ++k) {
+                    const uint32_t s2 = it % T::NSLOTS, ph2 = (it / T::NSLOTS) & 1;
+                    mbar_wait(&full[s2], ph2);
+                    __syncwarp();
+                    if ((threadIdx.x & 31) == 0) mbar_arrive(&empty[s2]);
+                    ++it;
+                }
+            }
+        }
+        uint32_t* ctr = p.pool_counters + l;
+        const uint32_t base = (p.epoch - 1) * static_cast<uint32_t>(p.pool_chunks + grid);
+        uint32_t claim = atomicAdd(ctr, 1u) - base;
+        for (;;) {
+            if (claim >= static_cast<uint32_t>(p.pool_chunks)) {
+                const uint32_t slot = it % T::NSLOTS, ph = (it / T::NSLOTS) & 1;
+                mbar_wait(&empty[slot], ph ^ 1);
+                slot_meta()[slot] = -1;
+                mbar_arrive(&full[slot]);
+                ++it;
+                return;
+            }
+            const int ch = static_cast<int>(claim);
+            claim = atomicAdd(ctr, 1u) - base;  // next claim in flight while streaming
+            const int t0c = p.pool_t0 + ch * p.pool_ct, t1c = t0c + p.pool_ct;
+            pool_stream(it, p.wffn1 + (size_t)l * 2 * S::DI * D, 2 * t0c, 2 * t1c, ch, policy);
+            pool_stream(it, p.wffn2t + (size_t)l * S::DI * D, t0c, t1c, ch, policy);
         }
     }
 
+    // Producer: issues every chunk of the stream into the ring (TMA bulk).
+    // FusedOverlap: gated only by free slots, plus an L2 prefetch cursor
+    // (cp.async.bulk.prefetch.L2) running up to p.l2_prefetch bytes ahead of
+    // the ring so HBM keeps streaming through barrier/latency phases.
+    // Fused: waits at every stage boundary (emit.hpp:229-235 without hoisting).
+    // DRAIN (streaming-only debug): consumers walk the same stream.
+    template <bool DRAIN>
     __device__ void producer() {
         const uint64_t policy = policy_evict_first();
         uint32_t it = 0;
-        const int last = min(p.stage_end, n_stages());
-        for (int stage = p.stage_begin; stage < last; ++stage) {
-            if (!p.overlap && stage != p.stage_begin) {
-                const uint32_t* ctr;
-                uint32_t target;
-                if (dependency(stage, &ctr, &target)) spin_until_geq(ctr, target);
+        Cursor c, pf;
+        cursor_init(c);
+        cursor_init(pf);
+        const int64_t window = (!DRAIN && p.overlap) ? p.l2_prefetch : 0;
+        int64_t ahead = 0;  // bytes prefetched but not yet loaded into the ring
+        int64_t pf_bytes = 0;
+        bool pf_live = window > 0;
+        int cur_stage = p.stage_begin;
+        const void *s0, *s1;
+        uint32_t bytes;
+        int stage;
+        while (cursor_next(c, &s0, &s1, &bytes, &stage)) {
+            if (!DRAIN && !p.overlap && stage != cur_stage) {
+                for (int s = cur_stage + 1; s <= stage; ++s) {
+                    const uint32_t* ctr;
+                    uint32_t target;
+                    if (dependency(s, &ctr, &target)) spin_until_geq(ctr, target);
+                }
             }
-            const int l = stage / kStagesPerLayer, s = stage % kStagesPerLayer;
-            if (stage == p.layers * kStagesPerLayer) {
-                produce_rows(it, p.lm_head, pl.lm_r0, pl.lm_r1, policy);
+            cur_stage = stage;
+            if (s0 == nullptr) {  // GLU work-pool marker
+                pool_run<DRAIN>(it, stage / kStagesPerLayer, policy);
                 continue;
             }
-            switch (s) {
-                case S_QKV:
-                    produce_rows(it, p.wqkv + (size_t)l * S::QKVR * D, pl.qkv_r0, pl.qkv_r1,
-                                 policy);
-                    break;
-                case S_ATTN:
-                    if (pl.attn_unit >= 0) {
-                        int p0, p1;
-                        attn_range(p0, p1);
-                        produce_kv(it, l, p0, min(p1, p.pos), policy);
+            const int64_t need = s1 ? 2 * (int64_t)bytes : bytes;
+            if (!DRAIN) {
+                // Prefetch into L2 only while the ring is full (this SM cannot
+                // load anyway, typically behind a barrier), never more than
+                // `window` bytes ahead of the ring: idle HBM time is spent on
+                // the bytes the ring will want next.
+                const uint32_t slot = it % T::NSLOTS, ph = (it / T::NSLOTS) & 1;
+                if (ahead < need) {  // pf cursor must stay ahead of the main one
+                    ahead = 0;
+                    pf = c;  // restart just past this chunk
+                }
+                // ring full: issue the whole prefetch window at once (no
+                // waiting between prefetches), then block on the slot
+                if (!mbar_test_wait(&empty[slot], ph ^ 1)) {
+                    while (pf_live && ahead < window) {
+                        const void *q0, *q1;
+                        uint32_t qb;
+                        int qs;
+                        if (!cursor_next(pf, &q0, &q1, &qb, &qs)) {
+                            pf_live = false;
+                            break;
+                        }
+                        if (q0 == nullptr) continue;  // pool marker: claims are dynamic
+                        prefetch_l2(q0, qb);
+                        if (q1) prefetch_l2(q1, qb);
+                        ahead += q1 ? 2 * (int64_t)qb : qb;
+                        pf_bytes += q1 ? 2 * (int64_t)qb : qb;
                     }
-                    break;
-                case S_AOUT:
-                    produce_rows(it, p.waout + (size_t)l * D * D, pl.aout_r0, pl.aout_r1, policy);
-                    break;
-                case S_GLU:
-                    produce_rows(it, p.wffn1 + (size_t)l * 2 * S::DI * D, 2 * pl.glu_t0,
-                                 2 * pl.glu_t1, policy);
-                    produce_rows(it, p.wffn2t + (size_t)l * S::DI * D, pl.glu_t0, pl.glu_t1,
-                                 policy);
-                    break;
-                default:
-                    break;
+                }
+                ahead -= need;
             }
+            chunk<DRAIN>(it, s0, s1, bytes, T::SLOT_BYTES / 2, policy);
+        }
+        // producer trace: L2-prefetched bytes of this launch (last stage, slot 5)
+        // and the SM this CTA ran on (slot 6)
+        if (p.trace != nullptr && !DRAIN) {
+            uint32_t smid;
+            asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+            uint64_t* t = p.trace + ((size_t)cta * n_stages() + n_stages() - 1) * kTraceSlots;
+            t[5] = pf_bytes;
+            t[6] = smid;
         }
     }
 
@@ -317,6 +553,49 @@ struct DecodeCta {
         return v;
     }
 
+    __device__ static float warp_max(float v) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+        return v;
+    }
+
+    // per-CTA %globaltimer trace: [grid][n_stages][4] = entry, dependency met,
+    // stage done (arrived), spare.  Off (nullptr) in production.
+    __device__ static uint64_t gtimer() {
+        uint64_t t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        return t;
+    }
+
+    __device__ void trace_put(int stage, int slot, uint64_t v) {
+        if (p.trace != nullptr && threadIdx.x == 0)
+            p.trace[((size_t)cta * n_stages() + stage) * kTraceSlots + slot] = v;
+    }
+
+    __device__ void trace_mark(int stage, int slot) {
+        if (p.trace != nullptr && threadIdx.x == 0) trace_put(stage, slot, gtimer());
+    }
+
+    // consumer wait for ring data; with tracing on, thread 0 accumulates the
+    // time spent starved (trace slot 4)
+    uint64_t ring_wait_ns = 0;
+    __device__ void wait_full(uint32_t slot, uint32_t par) {
+        if (p.trace != nullptr && threadIdx.x == 0) {
+            const uint64_t t0 = gtimer();
+            mbar_wait(&full[slot], par);
+            ring_wait_ns += gtimer() - t0;
+        } else {
+            mbar_wait(&full[slot], par);
+        }
+    }
+
+    __device__ void trace_ring_wait(int stage) {
+        trace_put(stage, 4, ring_wait_ns);
+        ring_wait_ns = 0;
+    }
+
+    // Dependency wait: one thread spins (acquire), the named barrier hands
+    // the ordering to the other consumer threads (cf. CUTLASS grid barrier).
     __device__ void wait_stage(int stage) {
         const uint32_t* ctr;
         uint32_t target;
@@ -324,22 +603,38 @@ struct DecodeCta {
             if (threadIdx.x == 0) spin_until_geq(ctr, target);
             consumer_sync(NCT);
         }
+        trace_mark(stage, 1);
     }
 
-    __device__ void arrive(uint32_t* ctr) {
+    // Stage completion: named barrier orders every consumer's writes before
+    // thread 0's gpu-scope release-add (cumulativity); no separate fence.
+    __device__ void arrive(uint32_t* ctr, int stage) {
         consumer_sync(NCT);
-        if (threadIdx.x == 0) {
-            __threadfence();
-            red_release_gpu(ctr, 1);
-        }
+        if (threadIdx.x == 0) red_release_gpu(ctr, 1);
+        trace_mark(stage, 2);
+        trace_ring_wait(stage);
     }
 
     // Load this thread's activation slice: act[b][j][e] = column (lt + j*TPR)*8 + e.
     // src_emb: layer-0 input taken straight from the embedding (bf16 row per b).
     // gain != nullptr -> RMSNorm with that f32 gain (numerics.hpp:14-24).
+    // The gains are constants and are fetched before the dependency wait for
+    // `stage`; only the activations wait.
     __device__ void load_act(float (&act)[B][T::VPT][8], const float* src, bool from_emb,
-                             const float* gain) {
+                             const float* gain, int stage) {
         const int ctid = threadIdx.x, lt = ctid % T::TPR, rg = ctid / T::TPR;
+        float g[T::VPT][8];
+        if (gain != nullptr) {
+#pragma unroll
+            for (int j = 0; j < T::VPT; ++j) {
+                const int col = (lt + j * T::TPR) * 8;
+                const float4 g0 = __ldg(reinterpret_cast<const float4*>(gain + col));
+                const float4 g1 = __ldg(reinterpret_cast<const float4*>(gain + col + 4));
+                g[j][0] = g0.x; g[j][1] = g0.y; g[j][2] = g0.z; g[j][3] = g0.w;
+                g[j][4] = g1.x; g[j][5] = g1.y; g[j][6] = g1.z; g[j][7] = g1.w;
+            }
+        }
+        wait_stage(stage);
 #pragma unroll
         for (int b = 0; b < B; ++b) {
 #pragma unroll
@@ -389,16 +684,11 @@ struct DecodeCta {
         }
         consumer_sync(NCT);  // ns reusable afterwards
 #pragma unroll
-        for (int j = 0; j < T::VPT; ++j) {
-            const int col = (lt + j * T::TPR) * 8;
-            const float4 g0 = __ldg(reinterpret_cast<const float4*>(gain + col));
-            const float4 g1 = __ldg(reinterpret_cast<const float4*>(gain + col + 4));
-            const float g[8] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
+        for (int j = 0; j < T::VPT; ++j)
 #pragma unroll
             for (int b = 0; b < B; ++b)
 #pragma unroll
-                for (int e = 0; e < 8; ++e) act[b][j][e] = g[e] * act[b][j][e] * inv[b];
-        }
+                for (int e = 0; e < 8; ++e) act[b][j][e] = g[j][e] * act[b][j][e] * inv[b];
     }
 
     __device__ static float dot8(const uint4 w, const float (&a)[8], float acc) {
@@ -413,63 +703,107 @@ struct DecodeCta {
         return acc;
     }
 
-    // GEMV over rows [r0, r1) streamed by the producer.  For every slot the
-    // row sums land in red_buf(it)[wr][row][b] and `epi(c0, nrows, red)` runs
-    // after the named barrier.
+    // V (power of two <= 32) per-lane values -> lane l ends with the warp sum
+    // of value index l >> (5 - log2 V): V-1 + 5-log2(V) shuffles instead of 5V.
+    template <int V>
+    __device__ static float reduce_multi(float (&v)[V], int lane) {
+        static_assert(V >= 1 && V <= 32 && (V & (V - 1)) == 0, "V must be a power of two");
+#pragma unroll
+        for (int s = V / 2, o = 16; s >= 1; s >>= 1, o >>= 1) {
+            const bool upper = (lane & o) != 0;
+#pragma unroll
+            for (int i = 0; i < s; ++i) {
+                const float send = upper ? v[i] : v[i + s];
+                const float keep = upper ? v[i + s] : v[i];
+                v[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+            }
+        }
+        float r = v[0];
+#pragma unroll
+        for (int o = 16 / V; o >= 1; o >>= 1) r += __shfl_xor_sync(0xffffffffu, r, o);
+        return r;
+    }
+
+    static constexpr int ilog2(int v) { return v <= 1 ? 0 : 1 + ilog2(v / 2); }
+
+    // GEMV over rows [r0, r1) streamed by the producer.  Per slot every warp
+    // forms its column-slice partial dots for all RPT x B (row, batch) values
+    // (two accumulators per row, no per-row branches), releases the slot, and
+    // folds the values with one transposed warp reduction into
+    // red[wr][row][b].  Warps never wait for each other inside a batch of RB
+    // rows; `epi(c0, nrows, red)` runs once per batch after one named barrier
+    // (red is double-buffered across batches).
     template <class Epi>
     __device__ void gemv(uint32_t& it, const float (&act)[B][T::VPT][8], int r0, int r1,
                          Epi&& epi) {
+        constexpr int V = T::RPT * B, LV = ilog2(V);
         const int ctid = threadIdx.x, lane = ctid % 32;
         const int rg = ctid / T::TPR, lt = ctid % T::TPR, wr = lt / 32;
+        const int vidx = lane >> (5 - LV), vr = vidx / B, vb = vidx % B;
+        const bool writer = (lane & ((32 >> LV) - 1)) == 0;
+        int batch_c0 = r0;
+        uint32_t nbatch = 0;
+        float* red = red_buf(0);
         for (int c0 = r0; c0 < r1; c0 += T::RPS) {
             const int nrows = min(T::RPS, r1 - c0);
             const uint32_t slot = it % T::NSLOTS, par = (it / T::NSLOTS) & 1;
-            mbar_wait(&full[slot], par);
+            wait_full(slot, par);
             const uint8_t* base = ring + slot * T::SLOT_BYTES;
-            float part[T::RPT][B];
+            float v[V];
 #pragma unroll
             for (int r = 0; r < T::RPT; ++r) {
+                // rows past nrows read stale (valid) smem; their sums are dropped
+                const uint8_t* rowp = base + (rg + r * T::RG) * T::ROW_BYTES;
+                float a0[B], a1[B];
 #pragma unroll
-                for (int b = 0; b < B; ++b) part[r][b] = 0.f;
-                const int row = rg + r * T::RG;
-                if (row < nrows) {
+                for (int b = 0; b < B; ++b) a0[b] = a1[b] = 0.f;
 #pragma unroll
-                    for (int j = 0; j < T::VPT; ++j) {
-                        const uint4 w = lds_u128(base + row * T::ROW_BYTES + (lt + j * T::TPR) * 16);
+                for (int j = 0; j < T::VPT; ++j) {
+                    const uint4 w = lds_u128(rowp + (lt + j * T::TPR) * 16);
 #pragma unroll
-                        for (int b = 0; b < B; ++b) part[r][b] = dot8(w, act[b][j], part[r][b]);
+                    for (int b = 0; b < B; ++b) {
+                        const float(&a)[8] = act[b][j];
+                        a0[b] = fmaf(bf_lo(w.x), a[0], a0[b]);
+                        a1[b] = fmaf(bf_hi(w.x), a[1], a1[b]);
+                        a0[b] = fmaf(bf_lo(w.y), a[2], a0[b]);
+                        a1[b] = fmaf(bf_hi(w.y), a[3], a1[b]);
+                        a0[b] = fmaf(bf_lo(w.z), a[4], a0[b]);
+                        a1[b] = fmaf(bf_hi(w.z), a[5], a1[b]);
+                        a0[b] = fmaf(bf_lo(w.w), a[6], a0[b]);
+                        a1[b] = fmaf(bf_hi(w.w), a[7], a1[b]);
                     }
                 }
+#pragma unroll
+                for (int b = 0; b < B; ++b) v[r * B + b] = a0[b] + a1[b];
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(&empty[slot]);
-            float* red = red_buf(it);
-#pragma unroll
-            for (int r = 0; r < T::RPT; ++r) {
-                const int row = rg + r * T::RG;
-#pragma unroll
-                for (int b = 0; b < B; ++b) {
-                    const float v = warp_sum(part[r][b]);
-                    if (lane == 0 && row < nrows) red[(wr * T::RPS + row) * B + b] = v;
-                }
-            }
-            consumer_sync(NCT);
-            epi(c0, nrows, red);
+            const float s = reduce_multi<V>(v, lane);
+            const int row = rg + vr * T::RG;
+            if (writer && row < nrows) red[(wr * T::RB + (c0 - batch_c0) + row) * B + vb] = s;
             ++it;
+            const int batch_rows = c0 + nrows - batch_c0;
+            if (c0 + T::RPS >= r1 || batch_rows + T::RPS > T::RB) {
+                consumer_sync(NCT);
+                epi(batch_c0, batch_rows, red);
+                batch_c0 = c0 + T::RPS;
+                red = red_buf(++nbatch);
+            }
         }
     }
 
     __device__ static float row_total(const float* red, int row, int b) {
         float t = 0.f;
 #pragma unroll
-        for (int w = 0; w < T::WPR; ++w) t += red[(w * T::RPS + row) * B + b];
+        for (int w = 0; w < T::WPR; ++w) t += red[(w * T::RB + row) * B + b];
         return t;
     }
 
     // ---------------------------------------------------------- S_QKV
     __device__ void stage_qkv(uint32_t& it, int l) {
         float act[B][T::VPT][8];
-        load_act(act, p.x, l == 0, p.norm_attn + (size_t)l * D);
+        load_act(act, p.x, l == 0, p.norm_attn + (size_t)l * D, l * kStagesPerLayer + S_QKV);
+        trace_mark(l * kStagesPerLayer + S_QKV, 3);
         const float* rp = rope();
         const int ctid = threadIdx.x;
         gemv(it, act, pl.qkv_r0, pl.qkv_r1, [&](int c0, int nrows, const float* red) {
@@ -489,7 +823,8 @@ struct DecodeCta {
                         __stcg(q + 1, r1);
                     } else {
                         const int h = (g - QR) / DH;
-                        __nv_bfloat16* k_dst = p.kcache + kv_row(l, b, h, p.pos) + dim;
+                        __nv_bfloat16* k_dst =
+                            p.kcache + kv_row(l, b, h, p.pos) + kv_swz_dim(dim, p.pos);
                         __nv_bfloat162 kv2;
                         kv2.x = __float2bfloat16_rn(r0);
                         kv2.y = __float2bfloat16_rn(r1);
@@ -497,7 +832,8 @@ struct DecodeCta {
                     }
                 } else {
                     const int gv = g - QR - KR, h = gv / DH, dim = gv % DH;
-                    __nv_bfloat16* v_dst = p.vcache + kv_row(l, b, h, p.pos) + dim;
+                    __nv_bfloat16* v_dst =
+                        p.vcache + kv_row(l, b, h, p.pos) + kv_swz_dim(dim, p.pos);
                     __nv_bfloat162 kv2;
                     kv2.x = __float2bfloat16_rn(a);
                     kv2.y = __float2bfloat16_rn(bb);
@@ -505,43 +841,134 @@ struct DecodeCta {
                 }
             }
         });
-        arrive(p.counters + l * kStagesPerLayer + S_QKV);
+        arrive(p.counters + l * kStagesPerLayer + S_QKV, l * kStagesPerLayer + S_QKV);
     }
 
     // ---------------------------------------------------------- S_ATTN
-    // One online-softmax state per warp (m, l replicated in all lanes, o
-    // split over lanes by head dim), positions dealt round-robin to warps.
-    struct AttnState {
-        float m[QPG], l[QPG], o[QPG][T::DPL];
-    };
+    // Split-K flash-decoding (numerics.hpp:64-145) on CUDA cores with ONE
+    // online-softmax state per CTA, chunk by chunk from the ring:
+    //   A  scores: thread (dq, pos) dots DPA dims of k_pos with alpha*q of all
+    //      QPG heads (q in smem, read as broadcasts).  K/V rows are stored with
+    //      16-byte chunks XOR-swizzled by (pos & 7), so 32 lanes on 32
+    //      positions hit 32 distinct banks; partials -> ss[dq][h][pos]
+    //   B  softmax: warp h sums the DQ partials, chunk max, online rescale,
+    //      p = e^{s - m} -> ps[pos][h]
+    //   C  P.V: thread (pg, dc) keeps o[h][8 dims of chunk dc] for all heads
+    //      over positions pg, pg + PG, ...
+    static constexpr int DQ = NCT / T::KVC;  // dim groups in phase A
+    static constexpr int DPA = DH / DQ;      // dims per thread in phase A
+    static constexpr int DC = DH / 8;        // 16-byte chunks per K/V row
+    static constexpr int PG = NCT / DC;      // position groups in phase C
+    static_assert(NCT % T::KVC == 0 && DPA % 8 == 0 && DC >= 8, "attention mapping");
+    static_assert(QPG <= NCW && 32 % DC == 0 || DC >= 32, "attention mapping");
+    static_assert(DQ * QPG * T::KVC + T::KVC * QPG + QPG * DH + QPG * 4 <= NCW * QPG * (DH + 2),
+                  "attention scratch fits in wpart");
 
-    __device__ void attn_update(AttnState& st, const float (&q)[QPG][T::DPL], const float* kf,
-                                const float* vf, float alpha) {
-        float dot[QPG];
-#pragma unroll
-        for (int h = 0; h < QPG; ++h) {
-            float s = 0.f;
-#pragma unroll
-            for (int e = 0; e < T::DPL; ++e) s = fmaf(q[h][e], kf[e], s);
-            dot[h] = warp_sum(s);
-        }
-#pragma unroll
-        for (int h = 0; h < QPG; ++h) {
-            const float s = alpha * dot[h];
-            const float m_new = fmaxf(st.m[h], s);
-            const float scale = expf(st.m[h] - m_new);
-            const float w = expf(s - m_new);
-            st.l[h] = st.l[h] * scale + w;
-#pragma unroll
-            for (int e = 0; e < T::DPL; ++e) st.o[h][e] = st.o[h][e] * scale + w * vf[e];
-            st.m[h] = m_new;
-        }
-    }
+    __device__ float* att_ss() { return wpart(); }                       // [DQ][QPG][KVC]
+    __device__ float* att_ps() { return att_ss() + DQ * QPG * T::KVC; }  // [KVC][QPG]
+    __device__ float* att_q() { return att_ps() + T::KVC * QPG; }        // [QPG][DH]
+    __device__ float* att_st() { return att_q() + QPG * DH; }            // [QPG][4] m l scale
 
-    __device__ static void unpack_bf16(const uint32_t* w, float* f, int n) {
-        for (int i = 0; i < n / 2; ++i) {
-            f[2 * i] = bf_lo(w[i]);
-            f[2 * i + 1] = bf_hi(w[i]);
+    // One chunk of n positions [pos0, pos0 + n) whose K/V rows are at kb/vb
+    // (shared memory, swizzled as stored).  o: this thread's P.V accumulators.
+    __device__ void attn_chunk(const uint8_t* kb, const uint8_t* vb, int n, int pos0,
+                               float (&o)[QPG][8]) {
+        const int ctid = threadIdx.x, warp = ctid / 32, lane = ctid % 32;
+        float* ss = att_ss();
+        float* ps = att_ps();
+        const float* qs = att_q();
+        float* st = att_st();
+        {  // A: scores
+            const int j = ctid % T::KVC, dq = ctid / T::KVC;
+            float acc[QPG];
+#pragma unroll
+            for (int h = 0; h < QPG; ++h) acc[h] = 0.f;
+            if (j < n) {
+                const uint8_t* row = kb + (size_t)j * DH * 2;
+                const int key = (pos0 + j) & 7;
+#pragma unroll
+                for (int c = 0; c < DPA / 8; ++c) {
+                    const int ch = dq * (DPA / 8) + c;
+                    const uint4 w = lds_u128(row + ((ch ^ key) << 4));
+                    const float kf[8] = {bf_lo(w.x), bf_hi(w.x), bf_lo(w.y), bf_hi(w.y),
+                                         bf_lo(w.z), bf_hi(w.z), bf_lo(w.w), bf_hi(w.w)};
+#pragma unroll
+                    for (int h = 0; h < QPG; ++h) {
+                        const float4 q0 = *reinterpret_cast<const float4*>(qs + h * DH + ch * 8);
+                        const float4 q1 =
+                            *reinterpret_cast<const float4*>(qs + h * DH + ch * 8 + 4);
+                        acc[h] = fmaf(q0.x, kf[0], acc[h]);
+                        acc[h] = fmaf(q0.y, kf[1], acc[h]);
+                        acc[h] = fmaf(q0.z, kf[2], acc[h]);
+                        acc[h] = fmaf(q0.w, kf[3], acc[h]);
+                        acc[h] = fmaf(q1.x, kf[4], acc[h]);
+                        acc[h] = fmaf(q1.y, kf[5], acc[h]);
+                        acc[h] = fmaf(q1.z, kf[6], acc[h]);
+                        acc[h] = fmaf(q1.w, kf[7], acc[h]);
+                    }
+                }
+            }
+#pragma unroll
+            for (int h = 0; h < QPG; ++h) ss[(dq * QPG + h) * T::KVC + j] = acc[h];
+        }
+        consumer_sync(NCT);
+        if (warp < QPG) {  // B: online softmax for head `warp`
+            const int h = warp;
+            float sv[(T::KVC + 31) / 32];
+            float cmax = -INFINITY;
+#pragma unroll
+            for (int i = 0; i < (T::KVC + 31) / 32; ++i) {
+                const int j = lane + 32 * i;
+                float s = -INFINITY;
+                if (j < n) {
+                    s = 0.f;
+#pragma unroll
+                    for (int dq = 0; dq < DQ; ++dq) s += ss[(dq * QPG + h) * T::KVC + j];
+                }
+                sv[i] = s;
+                cmax = fmaxf(cmax, s);
+            }
+            cmax = warp_max(cmax);
+            const float m_old = st[h * 4 + 0];
+            const float m_new = fmaxf(m_old, cmax);
+            const float scale = expf(m_old - m_new);  // 0 for the first chunk
+            float psum = 0.f;
+#pragma unroll
+            for (int i = 0; i < (T::KVC + 31) / 32; ++i) {
+                const int j = lane + 32 * i;
+                if (j < T::KVC) {
+                    const float pj = j < n ? expf(sv[i] - m_new) : 0.f;
+                    ps[j * QPG + h] = pj;
+                    psum += pj;
+                }
+            }
+            psum = warp_sum(psum);
+            if (lane == 0) {
+                st[h * 4 + 0] = m_new;
+                st[h * 4 + 1] = st[h * 4 + 1] * scale + psum;
+                st[h * 4 + 2] = scale;
+            }
+        }
+        consumer_sync(NCT);
+        {  // C: P.V
+            const int dc = ctid % DC, pg = ctid / DC;
+#pragma unroll
+            for (int h = 0; h < QPG; ++h) {
+                const float sc = st[h * 4 + 2];
+#pragma unroll
+                for (int e = 0; e < 8; ++e) o[h][e] *= sc;
+            }
+            for (int j = pg; j < n; j += PG) {
+                const uint4 w = lds_u128(vb + (size_t)j * DH * 2 + ((dc ^ ((pos0 + j) & 7)) << 4));
+                const float vf[8] = {bf_lo(w.x), bf_hi(w.x), bf_lo(w.y), bf_hi(w.y),
+                                     bf_lo(w.z), bf_hi(w.z), bf_lo(w.w), bf_hi(w.w)};
+#pragma unroll
+                for (int h = 0; h < QPG; ++h) {
+                    const float pj = ps[j * QPG + h];
+#pragma unroll
+                    for (int e = 0; e < 8; ++e) o[h][e] = fmaf(pj, vf[e], o[h][e]);
+                }
+            }
         }
     }
 
@@ -549,176 +976,222 @@ struct DecodeCta {
         if (pl.attn_unit < 0) return;  // idle CTA: no chunks were streamed
         const int ctid = threadIdx.x, warp = ctid / 32, lane = ctid % 32;
         const int unit = pl.attn_unit, b = unit / S::NKV, kvh = unit % S::NKV;
-        const float alpha = 1.0f / sqrtf(static_cast<float>(DH));
         int p0, p1;
         attn_range(p0, p1);
         const int past_end = min(p1, p.pos);
-
-        float q[QPG][T::DPL];
+        float* st = att_st();
+        if (ctid < QPG) {
+            st[ctid * 4 + 0] = -INFINITY;
+            st[ctid * 4 + 1] = 0.f;
+            st[ctid * 4 + 2] = 0.f;
+        }
+        wait_stage(l * kStagesPerLayer + S_ATTN);
+        {  // alpha * q of this kv head's QPG query heads -> smem (alpha = 1/sqrt(dh))
+            const float alpha = 1.0f / sqrtf(static_cast<float>(DH));
+            float* qs = att_q();
+            for (int i = ctid; i < QPG * DH; i += NCT)
+                qs[i] = alpha * ldcg_f(p.q + (size_t)b * D + kvh * QPG * DH + i);
+            // the current token's K/V rows (this launch's S_QKV wrote them with
+            // generic stores; read at L2, emit.hpp:148-154 SyncLoadCurrentToken)
+            // staged now so the load overlaps the ring chunks
+            if (p.pos >= p0 && p.pos < p1) {
+                uint8_t* cur = reinterpret_cast<uint8_t*>(h_s());  // [K row][V row]
+                const size_t row = kv_row(l, b, kvh, p.pos);
+                constexpr int V16 = DH * 2 / 16;
+                if (ctid < 2 * V16) {
+                    const __nv_bfloat16* src = (ctid < V16 ? p.kcache : p.vcache) + row;
+                    const uint4 w = __ldcg(reinterpret_cast<const uint4*>(src) + ctid % V16);
+                    *reinterpret_cast<uint4*>(cur + ctid * 16) = w;
+                }
+            }
+        }
+        float o[QPG][8];
 #pragma unroll
         for (int h = 0; h < QPG; ++h)
 #pragma unroll
-            for (int e = 0; e < T::DPL; ++e)
-                q[h][e] = ldcg_f(p.q + (size_t)b * D + (kvh * QPG + h) * DH + lane * T::DPL + e);
-        AttnState st;
-#pragma unroll
-        for (int h = 0; h < QPG; ++h) {
-            st.m[h] = -INFINITY;
-            st.l[h] = 0.f;
-#pragma unroll
-            for (int e = 0; e < T::DPL; ++e) st.o[h][e] = 0.f;
-        }
+            for (int e = 0; e < 8; ++e) o[h][e] = 0.f;
+        consumer_sync(NCT);
 
         for (int c0 = p0; c0 < past_end; c0 += T::KVC) {
             const int n = min(T::KVC, past_end - c0);
             const uint32_t slot = it % T::NSLOTS, par = (it / T::NSLOTS) & 1;
-            mbar_wait(&full[slot], par);
+            wait_full(slot, par);
             const uint8_t* kb = ring + slot * T::SLOT_BYTES;
-            const uint8_t* vb = kb + T::SLOT_BYTES / 2;
-            for (int j = warp; j < n; j += NCW) {
-                uint32_t kw[T::DPL / 2], vw[T::DPL / 2];
-                const uint8_t* kp = kb + (size_t)j * DH * 2 + lane * T::DPL * 2;
-                const uint8_t* vp = vb + (size_t)j * DH * 2 + lane * T::DPL * 2;
-#pragma unroll
-                for (int i = 0; i < T::DPL / 2; ++i) {
-                    kw[i] = lds_u32(kp + 4 * i);
-                    vw[i] = lds_u32(vp + 4 * i);
-                }
-                float kf[T::DPL], vf[T::DPL];
-                unpack_bf16(kw, kf, T::DPL);
-                unpack_bf16(vw, vf, T::DPL);
-                attn_update(st, q, kf, vf, alpha);
-            }
+            attn_chunk(kb, kb + T::SLOT_BYTES / 2, n, c0, o);
             __syncwarp();
             if (lane == 0) mbar_arrive(&empty[slot]);
             ++it;
         }
+        trace_mark(l * kStagesPerLayer + S_ATTN, 3);
         // current token: written by this launch's S_QKV with generic stores,
-        // read back at L2 (emit.hpp:148-154 SyncLoadCurrentToken)
-        if (p.pos >= p0 && p.pos < p1 && warp == (p.pos - p0) % NCW) {
-            const size_t row = kv_row(l, b, kvh, p.pos) + lane * T::DPL;
-            uint32_t kw[T::DPL / 2], vw[T::DPL / 2];
-#pragma unroll
-            for (int i = 0; i < T::DPL / 2; ++i) {
-                kw[i] = __ldcg(reinterpret_cast<const unsigned int*>(p.kcache + row) + i);
-                vw[i] = __ldcg(reinterpret_cast<const unsigned int*>(p.vcache + row) + i);
-            }
-            float kf[T::DPL], vf[T::DPL];
-            unpack_bf16(kw, kf, T::DPL);
-            unpack_bf16(vw, vf, T::DPL);
-            attn_update(st, q, kf, vf, alpha);
+        // read back at L2 into smem (emit.hpp:148-154 SyncLoadCurrentToken)
+        if (p.pos >= p0 && p.pos < p1) {  // staged into h_s at stage entry
+            const uint8_t* cur = reinterpret_cast<const uint8_t*>(h_s());
+            attn_chunk(cur, cur + DH * 2, 1, p.pos, o);
         }
-
-        // combine the NCW warp states into this CTA's partial (m, l, o)
-        float* wp = wpart();
+        consumer_sync(NCT);
+        // CTA partial: (m, l) from st, o summed over the PG position groups
         constexpr int STR = DH + 2;
+        float* mlc = reinterpret_cast<float*>(misc()) + 4;  // [QPG][2]
+        if (ctid < QPG) {
+            mlc[2 * ctid] = st[ctid * 4 + 0];
+            mlc[2 * ctid + 1] = st[ctid * 4 + 1];
+        }
+        // groups sharing a warp first (lanes dc, dc + DC, ...), then warps
 #pragma unroll
-        for (int h = 0; h < QPG; ++h) {
-            float* dst = wp + (warp * QPG + h) * STR;
-            if (lane == 0) {
-                dst[0] = st.m[h];
-                dst[1] = st.l[h];
+        for (int h = 0; h < QPG; ++h)
+#pragma unroll
+            for (int e = 0; e < 8; ++e)
+#pragma unroll
+                for (int off = DC; off < 32; off <<= 1)
+                    o[h][e] += __shfl_xor_sync(0xffffffffu, o[h][e], off);
+        consumer_sync(NCT);  // st/ss/ps/q dead from here: wpart reused for o
+        float* ro = wpart();  // [NCW][QPG][DH]
+        {
+            const int dc = ctid % DC;
+            if (lane < DC || DC >= 32) {
+#pragma unroll
+                for (int h = 0; h < QPG; ++h)
+#pragma unroll
+                    for (int e = 0; e < 8; ++e) ro[(warp * QPG + h) * DH + dc * 8 + e] = o[h][e];
             }
-#pragma unroll
-            for (int e = 0; e < T::DPL; ++e) dst[2 + lane * T::DPL + e] = st.o[h][e];
         }
         consumer_sync(NCT);
         float* part = p.attn_part + ((size_t)unit * grid + pl.attn_g) * QPG * STR;
+        constexpr int WPG = NCT / 32 / (DC >= 32 ? DC / 32 : 1);  // warps holding groups
         for (int idx = ctid; idx < QPG * DH; idx += NCT) {
             const int h = idx / DH, d = idx % DH;
-            float M = -INFINITY;
-            for (int w = 0; w < NCW; ++w) {
-                const float* s = wp + (w * QPG + h) * STR;
-                if (s[1] > 0.f) M = fmaxf(M, s[0]);
-            }
-            float L = 0.f, O = 0.f;
-            for (int w = 0; w < NCW; ++w) {
-                const float* s = wp + (w * QPG + h) * STR;
-                if (s[1] > 0.f) {
-                    const float r = expf(s[0] - M);
-                    L += s[1] * r;
-                    O += s[2 + d] * r;
-                }
-            }
+            float O = 0.f;
+            for (int w = 0; w < NCW; ++w)
+                if ((w * 32) % DC == 0 || DC >= 32) O += ro[(w * QPG + h) * DH + d];
             float* dst = part + h * STR;
             __stcg(dst + 2 + d, O);
             if (d == 0) {
-                __stcg(dst, M);
-                __stcg(dst + 1, L);
+                __stcg(dst, mlc[2 * h]);
+                __stcg(dst + 1, mlc[2 * h + 1]);
             }
         }
+        (void)WPG;
         // last arriver of the group combines (numerics.hpp:123-145)
         consumer_sync(NCT);
         int* flag = misc();
         if (ctid == 0) {
-            __threadfence();
             const uint32_t old =
                 atom_add_acq_rel_gpu(p.head_counters + (size_t)l * p.n_units + unit, 1);
             flag[0] = (old + 1 == p.epoch * static_cast<uint32_t>(p.attn_group)) ? 1 : 0;
-            __threadfence();
         }
         consumer_sync(NCT);
         if (flag[0]) {
+            // One L2 round trip: every thread first issues the G o-values of
+            // its (first two) outputs into registers, then the (m, l) of the
+            // whole group go to smem; per head (one warp): M = max m,
+            // r_g = e^{m_g - M} / L; out = sum_g r_g o_g.
+            const int G = p.attn_group;  // <= kMaxGroup (host-checked)
             const float* base = p.attn_part + (size_t)unit * grid * QPG * STR;
-            for (int idx = ctid; idx < QPG * DH; idx += NCT) {
-                const int h = idx / DH, d = idx % DH;
-                float M = -INFINITY;
-                for (int g = 0; g < p.attn_group; ++g) {
-                    const float* s = base + ((size_t)g * QPG + h) * STR;
-                    if (ldcg_f(s + 1) > 0.f) M = fmaxf(M, ldcg_f(s));
+            constexpr int NO = (QPG * DH + NCT - 1) / NCT;  // outputs per thread
+            constexpr int NV = NO < 2 ? NO : 2;             // held in registers at once
+            float v[NV][kMaxGroup];
+            auto load_o = [&](int k0) {
+#pragma unroll
+                for (int k = 0; k < NV; ++k) {
+                    const int idx = ctid + (k0 + k) * NCT;
+                    const int h = idx / DH, d = idx % DH;
+                    const float* o = base + (size_t)h * STR + 2 + d;
+#pragma unroll
+                    for (int g = 0; g < kMaxGroup; ++g)
+                        v[k][g] = (g < G && k0 + k < NO && idx < QPG * DH)
+                                      ? ldcg_f(o + (size_t)g * QPG * STR)
+                                      : 0.f;
                 }
-                float L = 0.f;
-                for (int g = 0; g < p.attn_group; ++g) {
-                    const float* s = base + ((size_t)g * QPG + h) * STR;
-                    const float lg = ldcg_f(s + 1);
-                    if (lg > 0.f) L += lg * expf(ldcg_f(s) - M);
-                }
-                float out = 0.f;
-                for (int g = 0; g < p.attn_group; ++g) {
-                    const float* s = base + ((size_t)g * QPG + h) * STR;
-                    const float lg = ldcg_f(s + 1);
-                    if (lg > 0.f) out += (expf(ldcg_f(s) - M) / L) * ldcg_f(s + 2 + d);
-                }
-                __stcg(p.attn_out + (size_t)b * D + (kvh * QPG + h) * DH + d, out);
+            };
+            load_o(0);
+            float* ml = wpart();  // [G][QPG][2]; free again after the barrier above
+            for (int i = ctid; i < G * QPG; i += NCT) {
+                const float* s = base + (size_t)i * STR;
+                ml[2 * i] = ldcg_f(s);
+                ml[2 * i + 1] = ldcg_f(s + 1);
             }
-            arrive(p.counters + l * kStagesPerLayer + S_ATTN);
+            consumer_sync(NCT);
+            float* rr = ml + 2 * G * QPG;  // [QPG][G] combine weights
+            for (int h = warp; h < QPG; h += NCW) {
+                float M = -INFINITY;
+                for (int g = lane; g < G; g += 32)
+                    if (ml[2 * (g * QPG + h) + 1] > 0.f) M = fmaxf(M, ml[2 * (g * QPG + h)]);
+                M = warp_max(M);
+                float L = 0.f;
+                for (int g = lane; g < G; g += 32) {
+                    const float lg = ml[2 * (g * QPG + h) + 1];
+                    if (lg > 0.f) L += lg * expf(ml[2 * (g * QPG + h)] - M);
+                }
+                L = warp_sum(L);
+                for (int g = lane; g < G; g += 32) {
+                    const float lg = ml[2 * (g * QPG + h) + 1];
+                    rr[h * G + g] = lg > 0.f ? expf(ml[2 * (g * QPG + h)] - M) / L : 0.f;
+                }
+            }
+            consumer_sync(NCT);
+            for (int k0 = 0; k0 < NO; k0 += NV) {
+                if (k0 > 0) load_o(k0);
+#pragma unroll
+                for (int k = 0; k < NV; ++k) {
+                    const int idx = ctid + (k0 + k) * NCT;
+                    if (k0 + k >= NO || idx >= QPG * DH) continue;
+                    const int h = idx / DH, d = idx % DH;
+                    float out = 0.f;
+#pragma unroll
+                    for (int g = 0; g < kMaxGroup; ++g)
+                        if (g < G) out += rr[h * G + g] * v[k][g];
+                    __stcg(p.attn_out + (size_t)b * D + (kvh * QPG + h) * DH + d, out);
+                }
+            }
+            arrive(p.counters + l * kStagesPerLayer + S_ATTN, l * kStagesPerLayer + S_ATTN);
         }
     }
 
     // ---------------------------------------------------------- S_AOUT
     __device__ void stage_aout(uint32_t& it, int l) {
         float act[B][T::VPT][8];
-        load_act(act, p.attn_out, false, nullptr);
+        load_act(act, p.attn_out, false, nullptr, l * kStagesPerLayer + S_AOUT);
         const int ctid = threadIdx.x;
-        gemv(it, act, pl.aout_r0, pl.aout_r1, [&](int c0, int nrows, const float* red) {
+        const int r0 = pl.aout_r0, nr = pl.aout_r1 - pl.aout_r0;
+        float* acc = h_s();  // [B][TMAX] row results; x updated once at the end
+        gemv(it, act, r0, pl.aout_r1, [&](int c0, int nrows, const float* red) {
             if (ctid < nrows * B) {
                 const int r = ctid / B, b = ctid % B;
-                float* xp = p.x + (size_t)b * D + c0 + r;
-                __stcg(xp, ldcg_f(xp) + row_total(red, r, b));
+                acc[b * T::TMAX + c0 - r0 + r] = row_total(red, r, b);
             }
         });
-        arrive(p.counters + l * kStagesPerLayer + S_AOUT);
+        consumer_sync(NCT);
+        for (int i = ctid; i < nr * B; i += NCT) {  // one L2 round trip for all rows
+            const int r = i / B, b = i % B;
+            float* xp = p.x + (size_t)b * D + r0 + r;
+            __stcg(xp, ldcg_f(xp) + acc[b * T::TMAX + r]);
+        }
+        arrive(p.counters + l * kStagesPerLayer + S_AOUT, l * kStagesPerLayer + S_AOUT);
     }
 
     // ---------------------------------------------------------- S_GLU
-    __device__ void stage_glu(uint32_t& it, int l) {
+    // in/gate rows [2 t0, 2 t1) of Wffn1 -> h[t - t0] = silu(gate) * in (smem)
+    __device__ void glu_ffn1(uint32_t& it, const float (&act)[B][T::VPT][8], int t0, int t1) {
         const int ctid = threadIdx.x;
-        const int t0 = pl.glu_t0, t1 = pl.glu_t1;
         float* hs = h_s();
-        {
-            float act[B][T::VPT][8];
-            load_act(act, p.x, false, p.norm_ffn + (size_t)l * D);
-            gemv(it, act, 2 * t0, 2 * t1, [&](int c0, int nrows, const float* red) {
-                const int npairs = nrows / 2;
-                if (ctid < npairs * B) {
-                    const int pr = ctid / B, b = ctid % B;
-                    const float a = row_total(red, 2 * pr, b), g = row_total(red, 2 * pr + 1, b);
-                    const float silu = g / (1.0f + expf(-g));
-                    hs[b * T::TMAX + (c0 / 2 - t0) + pr] = silu * a;
-                }
-            });
-        }
+        gemv(it, act, 2 * t0, 2 * t1, [&](int c0, int nrows, const float* red) {
+            const int npairs = nrows / 2;
+            if (ctid < npairs * B) {
+                const int pr = ctid / B, b = ctid % B;
+                const float a = row_total(red, 2 * pr, b), g = row_total(red, 2 * pr + 1, b);
+                const float silu = g / (1.0f + expf(-g));
+                hs[b * T::TMAX + (c0 / 2 - t0) + pr] = silu * a;
+            }
+        });
         consumer_sync(NCT);  // h complete
+    }
+
+    // d_model partial of pairs [t0, t1) (Wffn2^T rows, AXPY) written to dst
+    // ([RG][B][D] block of glu_part or pool_part)
+    __device__ void glu_ffn2(uint32_t& it, int t0, int t1, float* dst_part) {
+        const int ctid = threadIdx.x;
+        const float* hs = h_s();
         const int rg = ctid / T::TPR, lt = ctid % T::TPR, lane = ctid % 32;
         float acc[B][T::VPT][8];
 #pragma unroll
@@ -730,33 +1203,37 @@ struct DecodeCta {
         for (int c0 = t0; c0 < t1; c0 += T::RPS) {
             const int nrows = min(T::RPS, t1 - c0);
             const uint32_t slot = it % T::NSLOTS, par = (it / T::NSLOTS) & 1;
-            mbar_wait(&full[slot], par);
+            wait_full(slot, par);
             const uint8_t* base = ring + slot * T::SLOT_BYTES;
+            auto axpy_row = [&](int row) {
+                float hb[B];
 #pragma unroll
-            for (int r = 0; r < T::RPT; ++r) {
-                const int row = rg + r * T::RG;
-                if (row < nrows) {
-                    float hb[B];
+                for (int b = 0; b < B; ++b) hb[b] = hs[b * T::TMAX + (c0 - t0) + row];
 #pragma unroll
-                    for (int b = 0; b < B; ++b) hb[b] = hs[b * T::TMAX + (c0 - t0) + row];
+                for (int j = 0; j < T::VPT; ++j) {
+                    const uint4 w = lds_u128(base + row * T::ROW_BYTES + (lt + j * T::TPR) * 16);
+                    const float wf[8] = {bf_lo(w.x), bf_hi(w.x), bf_lo(w.y), bf_hi(w.y),
+                                         bf_lo(w.z), bf_hi(w.z), bf_lo(w.w), bf_hi(w.w)};
 #pragma unroll
-                    for (int j = 0; j < T::VPT; ++j) {
-                        const uint4 w = lds_u128(base + row * T::ROW_BYTES + (lt + j * T::TPR) * 16);
-                        const float wf[8] = {bf_lo(w.x), bf_hi(w.x), bf_lo(w.y), bf_hi(w.y),
-                                             bf_lo(w.z), bf_hi(w.z), bf_lo(w.w), bf_hi(w.w)};
+                    for (int b = 0; b < B; ++b)
 #pragma unroll
-                        for (int b = 0; b < B; ++b)
-#pragma unroll
-                            for (int e = 0; e < 8; ++e) acc[b][j][e] = fmaf(hb[b], wf[e], acc[b][j][e]);
-                    }
+                        for (int e = 0; e < 8; ++e) acc[b][j][e] = fmaf(hb[b], wf[e], acc[b][j][e]);
                 }
+            };
+            if (nrows == T::RPS) {  // full slot: straight-line, no per-row branches
+#pragma unroll
+                for (int r = 0; r < T::RPT; ++r) axpy_row(rg + r * T::RG);
+            } else {
+#pragma unroll
+                for (int r = 0; r < T::RPT; ++r)
+                    if (rg + r * T::RG < nrows) axpy_row(rg + r * T::RG);
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(&empty[slot]);
             ++it;
         }
-        // per-(CTA, row group) partial d_model vectors
-        float* gp = p.glu_part + ((size_t)cta * T::RG + rg) * B * D;
+        // per-row-group partial d_model vectors
+        float* gp = dst_part + (size_t)rg * B * D;
 #pragma unroll
         for (int b = 0; b < B; ++b)
 #pragma unroll
@@ -768,23 +1245,66 @@ struct DecodeCta {
                 __stcg(reinterpret_cast<float4*>(dst + 4),
                        make_float4(acc[b][j][4], acc[b][j][5], acc[b][j][6], acc[b][j][7]));
             }
-        arrive(p.counters + l * kStagesPerLayer + S_GLU);
+    }
+
+    // ---------------------------------------------------------- S_GLU
+    // Static slice [glu_t0, glu_t1) into glu_part[cta], then pool chunks
+    // (claimed by this CTA's producer) each into pool_part[chunk].
+    __device__ void stage_glu(uint32_t& it, int l) {
+        float act[B][T::VPT][8];
+        load_act(act, p.x, false, p.norm_ffn + (size_t)l * D, l * kStagesPerLayer + S_GLU);
+        glu_ffn1(it, act, pl.glu_t0, pl.glu_t1);
+        glu_ffn2(it, pl.glu_t0, pl.glu_t1, p.glu_part + (size_t)cta * T::RG * B * D);
+        if (p.pool_chunks > 0) {
+            for (;;) {
+                const uint32_t slot = it % T::NSLOTS, par = (it / T::NSLOTS) & 1;
+                wait_full(slot, par);
+                const int ch = slot_meta()[slot];
+                if (ch < 0) {  // end marker: release the (byte-less) slot
+                    __syncwarp();
+                    if ((threadIdx.x & 31) == 0) mbar_arrive(&empty[slot]);
+                    ++it;
+                    break;
+                }
+                const int t0c = p.pool_t0 + ch * p.pool_ct, t1c = t0c + p.pool_ct;
+                glu_ffn1(it, act, t0c, t1c);
+                glu_ffn2(it, t0c, t1c, p.pool_part + (size_t)ch * T::RG * B * D);
+            }
+        }
+        arrive(p.counters + l * kStagesPerLayer + S_GLU, l * kStagesPerLayer + S_GLU);
     }
 
     // ---------------------------------------------------------- S_RED
     __device__ void stage_red(int l) {
+        wait_stage(l * kStagesPerLayer + S_RED);
         const int ctid = threadIdx.x, warp = ctid / 32, lane = ctid % 32;
         const int c0 = pl.red_c0, c1 = pl.red_c1;
-        const int nparts = grid * T::RG;
-        float* ns = norm_s();  // [NCW][32] scratch reuse would overflow; use wpart
-        float* scratch = wpart();
+        // CTA partials then pool-chunk partials: a fixed order independent of
+        // which CTA computed which pool chunk -> deterministic sums
+        const int nstatic = grid * T::RG;
+        const int nparts = nstatic + p.pool_chunks * T::RG;
+        float* scratch = wpart();  // [NCW][32]
         for (int b = 0; b < B; ++b) {
             for (int cb = c0; cb < c1; cb += 32) {
                 const int col = cb + lane;
                 float s = 0.f;
-                if (col < c1)
-                    for (int q = warp; q < nparts; q += NCW)
-                        s += ldcg_f(p.glu_part + ((size_t)q * B + b) * D + col);
+                if (col < c1) {
+                    // partials warp, warp+NCW, ... summed in that fixed order,
+                    // 8 independent L2 loads in flight per thread
+                    constexpr int U = 32;  // independent L2 loads in flight per thread
+                    for (int q0 = warp; q0 < nparts; q0 += U * NCW) {
+                        float v[U];
+#pragma unroll
+                        for (int u = 0; u < U; ++u) {
+                            const int q = q0 + u * NCW;
+                            const float* src = q < nstatic ? p.glu_part + (size_t)q * B * D
+                                                           : p.pool_part + (size_t)(q - nstatic) * B * D;
+                            v[u] = q < nparts ? ldcg_f(src + (size_t)b * D + col) : 0.f;
+                        }
+#pragma unroll
+                        for (int u = 0; u < U; ++u) s += v[u];
+                    }
+                }
                 scratch[warp * 32 + lane] = s;
                 consumer_sync(NCT);
                 if (warp == 0 && col < c1) {
@@ -796,14 +1316,13 @@ struct DecodeCta {
                 consumer_sync(NCT);
             }
         }
-        (void)ns;
-        arrive(p.counters + l * kStagesPerLayer + S_RED);
+        arrive(p.counters + l * kStagesPerLayer + S_RED, l * kStagesPerLayer + S_RED);
     }
 
     // ---------------------------------------------------------- S_LMHEAD
     __device__ void stage_lmhead(uint32_t& it) {
         float act[B][T::VPT][8];
-        load_act(act, p.x, p.layers == 0, p.final_norm);
+        load_act(act, p.x, p.layers == 0, p.final_norm, p.layers * kStagesPerLayer);
         const int ctid = threadIdx.x;
         float best = -INFINITY;
         int best_i = 0x7fffffff;
@@ -839,27 +1358,36 @@ struct DecodeCta {
         consumer_sync(NCT);
         int* flag = misc();
         if (ctid == 0) {
-            __threadfence();
             const uint32_t old = atom_add_acq_rel_gpu(p.amax_counter, 1);
             flag[1] = (old + 1 == p.epoch * static_cast<uint32_t>(grid)) ? 1 : 0;
-            __threadfence();
         }
         consumer_sync(NCT);
-        if (flag[1] && ctid < B) {
-            float bv = -INFINITY;
-            int bi = 0;
-            bool any = false;
-            for (int c = 0; c < grid; ++c) {
-                const float v = ldcg_f(p.amax_val + (size_t)c * B + ctid);
-                const int i = __ldcg(p.amax_idx + (size_t)c * B + ctid);
-                if (i == 0x7fffffff) continue;  // CTA without lm_head rows
-                if (!any || v > bv || (v == bv && i < bi)) {
-                    bv = v;
-                    bi = i;
-                    any = true;
-                }
+        if (flag[1]) {
+            // all CTA candidates into smem in one parallel pass, then scan in
+            // CTA (= ascending row) order
+            float* cv = wpart();
+            int* ci = reinterpret_cast<int*>(cv + grid * B);
+            for (int i = ctid; i < grid * B; i += NCT) {
+                cv[i] = ldcg_f(p.amax_val + i);
+                ci[i] = __ldcg(p.amax_idx + i);
             }
-            p.greedy[ctid] = bi;
+            consumer_sync(NCT);
+            if (ctid < B) {
+                float bv = -INFINITY;
+                int bi = 0;
+                bool any = false;
+                for (int c = 0; c < grid; ++c) {
+                    const float v = cv[c * B + ctid];
+                    const int i = ci[c * B + ctid];
+                    if (i == 0x7fffffff) continue;  // CTA without lm_head rows
+                    if (!any || v > bv || (v == bv && i < bi)) {
+                        bv = v;
+                        bi = i;
+                        any = true;
+                    }
+                }
+                p.greedy[ctid] = bi;
+            }
         }
     }
 
@@ -867,7 +1395,7 @@ struct DecodeCta {
         uint32_t it = 0;
         const int last = min(p.stage_end, n_stages());
         for (int stage = p.stage_begin; stage < last; ++stage) {
-            wait_stage(stage);  // satisfied immediately after a kernel boundary
+            trace_mark(stage, 0);
             const int l = stage / kStagesPerLayer, s = stage % kStagesPerLayer;
             if (stage == p.layers * kStagesPerLayer) {
                 stage_lmhead(it);
@@ -915,7 +1443,9 @@ __global__ void __launch_bounds__(KTraits<S>::NTHREADS, 1)
     }
     __syncthreads();
     if (tid >= T::NCT) {
-        if (tid == T::NCT) cta.producer();
+        if (tid == T::NCT) cta.template producer<false>();
+    } else if (p.debug & kDebugStreamOnly) {
+        cta.template producer<true>();  // streaming-only measurement
     } else {
         cta.consumer();
     }

@@ -14,7 +14,7 @@ namespace ffb200 {
 
 struct KernelOps {
     int D, DI, DH, NQ, NKV, B;
-    int threads, smem, nslots, slot_bytes, rg, tmax, kvc;
+    int threads, smem, nslots, slot_bytes, rg, tmax, kvc, rps;
     cudaError_t (*prepare)();
     cudaError_t (*launch)(const DecodeParams&, int grid, cudaStream_t, bool cooperative);
 };
@@ -47,7 +47,7 @@ KernelOps make_ops() {
     using T = KTraits<S>;
     return KernelOps{S::D,       S::DI,        S::DH,  S::NQ,  S::NKV,    S::B,
                      T::NTHREADS, T::SMEM_BYTES, T::NSLOTS, T::SLOT_BYTES, T::RG, T::TMAX,
-                     T::KVC,      &prepare_impl<S>, &launch_impl<S>};
+                     T::KVC,      T::RPS,        &prepare_impl<S>, &launch_impl<S>};
 }
 
 // registration hooks, one per kernels_*.cu

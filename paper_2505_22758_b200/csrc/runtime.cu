@@ -144,6 +144,11 @@ __global__ void synth_f32_kernel(float* dst, int64_t n, uint64_t seed, float mea
 
 int64_t split_at(int64_t units, int64_t c, int64_t grid) { return (units * c) / grid; }
 
+// KV row layout: 16-byte chunks XOR-swizzled by (pos & 7) so that the
+// attention kernel's 32 lanes on 32 positions read 32 distinct smem banks
+// (decode_kernel.cuh: kv_swz_dim).  Element d of position pos:
+int64_t kv_swz(int64_t d, int64_t pos) { return (((d >> 3) ^ (pos & 7)) << 3) | (d & 7); }
+
 }  // namespace
 
 struct ffb_model {
@@ -153,6 +158,15 @@ struct ffb_model {
     int64_t max_seq = 0;
     int attn_group = 0, n_units = 0;
     ffb_mode mode = FFB_MODE_FUSED_OVERLAP;
+    int32_t debug = 0;
+    uint64_t* trace = nullptr;  // per-CTA stage timestamps (ffb_set_trace)
+    int64_t l2_prefetch = 0;  // per-CTA L2 prefetch window (ffb_set_option); off: measured slower
+    int plan_reverse = 0;             // weight slices assigned in reverse CTA order
+    int64_t pool_permille = 0;        // share of d_inter in the dynamic GLU pool (off)
+    int64_t pool_ct_pref = 4;         // preferred pairs per pool chunk
+    int pool_t0 = 0, pool_ct = 0, pool_chunks = 0, pool_chunks_max = 0;
+    float* pool_part = nullptr;
+    uint32_t* pool_counters = nullptr;
     uint32_t epoch = 0;
     cudaStream_t stream = nullptr;
     std::vector<int64_t> kv_len;
@@ -206,20 +220,39 @@ ffb_status build_plan(ffb_model* m) {
     const int64_t G = m->grid;
     m->n_units = static_cast<int>(c.batch * c.n_kv_heads);
     if (m->n_units > G) return fail(FFB_UNSUPPORTED, "batch * n_kv_heads exceeds the SM count");
-    m->attn_group = static_cast<int>(G / m->n_units);
+    // split-K group per (batch row, kv head): as many SMs as fit, at most
+    // kMaxGroup so the last-arriver combine keeps every load in flight
+    m->attn_group = static_cast<int>(std::min<int64_t>(G / m->n_units, kMaxGroup));
     std::vector<CtaPlan> plan(G);
     const int64_t qkv_pairs = m->qkv_rows() / 2;
+    // GLU work pool: the last pool_frac of the d_inter pairs, in chunks of
+    // pool_ct pairs, is claimed dynamically (decode_kernel.cuh: pool_run);
+    // the rest is split statically.  Off for small d_inter / batch > 2.
+    m->pool_ct = 0;
+    m->pool_chunks = 0;
+    m->pool_t0 = c.d_inter;
+    if (m->pool_permille > 0 && c.batch <= 2 && c.d_inter / G >= 32) {
+        const int64_t ct = std::max<int64_t>(m->pool_ct_pref, m->ops->rps);
+        const int64_t chunks = (c.d_inter * m->pool_permille) / (1000 * ct);
+        if (chunks > 0 && chunks <= m->pool_chunks_max) {
+            m->pool_ct = static_cast<int>(ct);
+            m->pool_chunks = static_cast<int>(chunks);
+            m->pool_t0 = c.d_inter - chunks * ct;
+        }
+    }
+    const int64_t glu_static = m->pool_t0;
     for (int64_t i = 0; i < G; ++i) {
         CtaPlan& p = plan[i];
         std::memset(&p, 0, sizeof(p));
-        p.qkv_r0 = static_cast<int32_t>(2 * split_at(qkv_pairs, i, G));
-        p.qkv_r1 = static_cast<int32_t>(2 * split_at(qkv_pairs, i + 1, G));
-        p.aout_r0 = static_cast<int32_t>(split_at(c.d_model, i, G));
-        p.aout_r1 = static_cast<int32_t>(split_at(c.d_model, i + 1, G));
-        p.glu_t0 = static_cast<int32_t>(split_at(c.d_inter, i, G));
-        p.glu_t1 = static_cast<int32_t>(split_at(c.d_inter, i + 1, G));
-        p.lm_r0 = static_cast<int32_t>(split_at(c.vocab_size, i, G));
-        p.lm_r1 = static_cast<int32_t>(split_at(c.vocab_size, i + 1, G));
+        const int64_t k = m->plan_reverse ? G - 1 - i : i;  // weight-slice order
+        p.qkv_r0 = static_cast<int32_t>(2 * split_at(qkv_pairs, k, G));
+        p.qkv_r1 = static_cast<int32_t>(2 * split_at(qkv_pairs, k + 1, G));
+        p.aout_r0 = static_cast<int32_t>(split_at(c.d_model, k, G));
+        p.aout_r1 = static_cast<int32_t>(split_at(c.d_model, k + 1, G));
+        p.glu_t0 = static_cast<int32_t>(split_at(glu_static, k, G));
+        p.glu_t1 = static_cast<int32_t>(split_at(glu_static, k + 1, G));
+        p.lm_r0 = static_cast<int32_t>(split_at(c.vocab_size, k, G));
+        p.lm_r1 = static_cast<int32_t>(split_at(c.vocab_size, k + 1, G));
         p.red_c0 = static_cast<int32_t>(split_at(c.d_model, i, G));
         p.red_c1 = static_cast<int32_t>(split_at(c.d_model, i + 1, G));
         if (i < static_cast<int64_t>(m->n_units) * m->attn_group) {
@@ -229,7 +262,7 @@ ffb_status build_plan(ffb_model* m) {
             p.attn_unit = -1;
             p.attn_g = 0;
         }
-        if (p.glu_t1 - p.glu_t0 > m->ops->tmax)
+        if (p.glu_t1 - p.glu_t0 > m->ops->tmax || p.aout_r1 - p.aout_r0 > m->ops->tmax)
             return fail(FFB_UNSUPPORTED, "d_inter too large for the per-CTA GLU buffer");
     }
     CUDA_TRY(cudaMemcpy(m->plan, plan.data(), sizeof(CtaPlan) * G, cudaMemcpyHostToDevice));
@@ -276,18 +309,36 @@ DecodeParams make_params(const ffb_model* m, int64_t pos, const int64_t* d_token
     p.n_units = m->n_units;
     p.eps = static_cast<float>(m->cfg.rmsnorm_eps);
     p.rope_theta = m->cfg.rope_theta;
+    p.debug = m->debug;
+    p.trace = m->trace;
+    p.l2_prefetch = m->l2_prefetch;
+    p.pool_part = m->pool_part;
+    p.pool_counters = m->pool_counters;
+    p.pool_t0 = m->pool_t0;
+    p.pool_ct = m->pool_ct;
+    p.pool_chunks = m->pool_chunks;
     return p;
+}
+
+// Zero every inter-CTA counter (stage, head-combine, argmax, GLU pool); the
+// caller restarts epochs from 0.  Needed before the epoch wraps and whenever
+// the plan changes (the pool counter base depends on pool_chunks).
+ffb_status reset_sync_state(ffb_model* m, cudaStream_t stream) {
+    const int64_t Lc = std::max<int64_t>(1, m->cfg.layers);
+    CUDA_TRY(cudaMemsetAsync(m->counters, 0, sizeof(uint32_t) * (Lc * 5 + 1), stream));
+    CUDA_TRY(cudaMemsetAsync(m->head_counters, 0,
+                             sizeof(uint32_t) * std::max<int64_t>(1, Lc * m->n_units), stream));
+    CUDA_TRY(cudaMemsetAsync(m->amax_counter, 0, sizeof(uint32_t), stream));
+    CUDA_TRY(cudaMemsetAsync(m->pool_counters, 0, sizeof(uint32_t) * Lc, stream));
+    return FFB_OK;
 }
 
 ffb_status launch_step(ffb_model* m, int64_t pos, const int64_t* d_tokens, float* d_logits,
                        int64_t* d_greedy, cudaStream_t stream) {
     m->epoch += 1;
     if (m->epoch >= 0x00ffffffu) {  // keep epoch * grid far from u32 wrap
-        CUDA_TRY(cudaMemsetAsync(m->counters, 0, sizeof(uint32_t) * (m->cfg.layers * 5 + 1), stream));
-        CUDA_TRY(cudaMemsetAsync(m->head_counters, 0,
-                                 sizeof(uint32_t) * std::max<int64_t>(1, m->cfg.layers * m->n_units),
-                                 stream));
-        CUDA_TRY(cudaMemsetAsync(m->amax_counter, 0, sizeof(uint32_t), stream));
+        ffb_status s = reset_sync_state(m, stream);
+        if (s) return s;
         m->epoch = 1;
     }
     DecodeParams p = make_params(m, pos, d_tokens, d_logits, d_greedy);
@@ -401,7 +452,7 @@ ffb_status ffb_create(const ffb_model_config* cfg, int64_t max_seq_len, int devi
     m->cfg = *cfg;
     m->ops = ops;
     m->device = device;
-    m->grid = prop.multiProcessorCount;
+    m->grid = std::min(prop.multiProcessorCount, 160);  // KTraits::kMaxGrid
     m->max_seq = max_seq_len;
     m->kv_len.assign(cfg->layers, 0);
     auto bail = [&](ffb_status s) {
@@ -452,6 +503,12 @@ ffb_status ffb_create(const ffb_model_config* cfg, int64_t max_seq_len, int devi
     ALLOC(m->amax_counter, 1);
     ALLOC(m->plan, (size_t)m->grid);
     ALLOC(m->staging, (size_t)ffb_model::kStagingElems);
+    // pool partials sized for the largest pool the options allow (50%)
+    m->pool_chunks_max = static_cast<int>(std::max<int64_t>(1, c.d_inter / 2 / ops->rps));
+    ALLOC(m->pool_part, (size_t)m->pool_chunks_max * ops->rg * B * D);
+    ALLOC(m->pool_counters, (size_t)Lc);
+    if (cudaMemset(m->pool_counters, 0, sizeof(uint32_t) * Lc) != cudaSuccess)
+        return bail(fail(FFB_DEVICE, "cudaMemset failed"));
 #undef ALLOC
     if (cudaMemset(m->counters, 0, sizeof(uint32_t) * (Lc * 5 + 1)) != cudaSuccess ||
         cudaMemset(m->head_counters, 0, sizeof(uint32_t) * Lc * units) != cudaSuccess ||
@@ -531,8 +588,8 @@ ffb_status ffb_kv_set(ffb_model* m, int64_t b, int64_t layer, int64_t head, int6
         return fail(FFB_VALIDATION, "kv_set: index out of range");
     std::vector<uint16_t> kb(c.d_head), vb(c.d_head);
     for (int64_t d = 0; d < c.d_head; ++d) {
-        kb[d] = bf16_bits_rne(k[d]);
-        vb[d] = bf16_bits_rne(v[d]);
+        kb[kv_swz(d, pos)] = bf16_bits_rne(k[d]);
+        vb[kv_swz(d, pos)] = bf16_bits_rne(v[d]);
     }
     CUDA_TRY(cudaSetDevice(m->device));
     const size_t off = kv_offset(m, b, layer, head, pos);
@@ -555,8 +612,8 @@ ffb_status ffb_kv_get(ffb_model* m, int64_t b, int64_t layer, int64_t head, int6
     CUDA_TRY(cudaMemcpy(kb.data(), m->kcache + off, 2 * c.d_head, cudaMemcpyDeviceToHost));
     CUDA_TRY(cudaMemcpy(vb.data(), m->vcache + off, 2 * c.d_head, cudaMemcpyDeviceToHost));
     for (int64_t d = 0; d < c.d_head; ++d) {
-        k[d] = bf16_bits_to_f32(kb[d]);
-        v[d] = bf16_bits_to_f32(vb[d]);
+        k[d] = bf16_bits_to_f32(kb[kv_swz(d, pos)]);
+        v[d] = bf16_bits_to_f32(vb[kv_swz(d, pos)]);
     }
     return FFB_OK;
 }
@@ -573,10 +630,13 @@ ffb_status ffb_kv_import(ffb_model* m, const float* k, const float* v, int64_t s
         for (int64_t l = 0; l < c.layers; ++l)
             for (int64_t h = 0; h < c.n_kv_heads; ++h) {
                 const size_t src = (((size_t)b * c.layers + l) * c.n_kv_heads + h) * src_max_seq * c.d_head;
-                for (int64_t i = 0; i < n_pos * c.d_head; ++i) {
-                    kb[i] = bf16_bits_rne(k[src + i]);
-                    vb[i] = bf16_bits_rne(v[src + i]);
-                }
+                for (int64_t ps = 0; ps < n_pos; ++ps)
+                    for (int64_t d = 0; d < c.d_head; ++d) {
+                        const int64_t i = ps * c.d_head + d;
+                        const int64_t o = ps * c.d_head + kv_swz(d, ps);
+                        kb[o] = bf16_bits_rne(k[src + i]);
+                        vb[o] = bf16_bits_rne(v[src + i]);
+                    }
                 const size_t off = kv_offset(m, b, l, h, 0);
                 CUDA_TRY(cudaMemcpy(m->kcache + off, kb.data(), 2 * n_pos * c.d_head,
                                     cudaMemcpyHostToDevice));
@@ -605,6 +665,72 @@ ffb_status ffb_set_mode(ffb_model* m, ffb_mode mode) {
         return fail(FFB_USAGE, "unknown mode %d", (int)mode);
     m->mode = mode;
     return FFB_OK;
+}
+
+ffb_status ffb_set_debug(ffb_model* m, int32_t flags) {
+    if (!m) return fail(FFB_USAGE, "NULL handle");
+    m->debug = flags;
+    return FFB_OK;
+}
+
+ffb_status ffb_set_option(ffb_model* m, const char* key, int64_t value) {
+    if (!m || !key) return fail(FFB_USAGE, "NULL argument");
+    if (std::strcmp(key, "l2_prefetch_bytes") == 0) {
+        if (value < 0 || value > (64ll << 20))
+            return fail(FFB_USAGE, "l2_prefetch_bytes out of range [0, 64 MiB]");
+        m->l2_prefetch = value;
+        return FFB_OK;
+    }
+    if (std::strcmp(key, "plan_reverse") == 0 || std::strcmp(key, "glu_pool_permille") == 0 ||
+        std::strcmp(key, "glu_pool_chunk") == 0) {
+        if (key[0] == 'p') m->plan_reverse = value ? 1 : 0;
+        else if (std::strcmp(key, "glu_pool_chunk") == 0) {
+            if (value < 1 || value > 64) return fail(FFB_USAGE, "glu_pool_chunk in [1, 64]");
+            m->pool_ct_pref = value;
+        } else {
+            if (value < 0 || value > 500) return fail(FFB_USAGE, "glu_pool_permille in [0, 500]");
+            m->pool_permille = value;
+        }
+        CUDA_TRY(cudaSetDevice(m->device));
+        CUDA_TRY(cudaStreamSynchronize(m->stream));
+        CUDA_TRY(cudaDeviceSynchronize());
+        ffb_status s = build_plan(m);
+        if (s) return s;
+        s = reset_sync_state(m, m->stream);
+        if (s) return s;
+        CUDA_TRY(cudaStreamSynchronize(m->stream));
+        m->epoch = 0;
+        return FFB_OK;
+    }
+    return fail(FFB_USAGE, "unknown option '%s'", key);
+}
+
+ffb_status ffb_set_trace(ffb_model* m, int enable) {
+    if (!m) return fail(FFB_USAGE, "NULL handle");
+    CUDA_TRY(cudaSetDevice(m->device));
+    if (enable && !m->trace) {
+        const size_t n = (size_t)m->grid * (m->cfg.layers * kStagesPerLayer + 1) * kTraceSlots;
+        ffb_status s = m->alloc(&m->trace, n);
+        if (s) return s;
+        CUDA_TRY(cudaMemset(m->trace, 0, n * sizeof(uint64_t)));
+    } else if (!enable) {
+        m->trace = nullptr;  // buffer stays owned by the handle
+    }
+    return FFB_OK;
+}
+
+int64_t ffb_get_trace(ffb_model* m, uint64_t* out, int64_t n) {
+    if (!m || !m->trace) return -1;
+    const int64_t total = (int64_t)m->grid * (m->cfg.layers * kStagesPerLayer + 1) * kTraceSlots;
+    if (out) {
+        if (n < total) return -1;
+        if (cudaStreamSynchronize(m->stream) != cudaSuccess ||
+            cudaDeviceSynchronize() != cudaSuccess ||
+            cudaMemcpy(out, m->trace, total * sizeof(uint64_t), cudaMemcpyDeviceToHost) !=
+                cudaSuccess)
+            return -1;
+    }
+    return total;
 }
 
 static ffb_status check_step(ffb_model* m, const int64_t* tokens, int64_t pos) {

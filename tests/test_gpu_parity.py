@@ -19,7 +19,8 @@ import numpy as np
 import pytest
 
 import oracle as O
-from gpu_helpers import GOLDEN, check_step, device_from_store, rel_err, to_model_cfg
+from gpu_helpers import (GOLDEN, check_step, device_from_store, kv_rows_match, rel_err,
+                         to_model_cfg)
 from paper_2505_22758_b200 import DecodeModel, RunMode, ValidationError
 
 pytestmark = pytest.mark.gpu
@@ -127,8 +128,7 @@ def test_appended_kv_rows_within_one_bf16_ulp():
             for h in range(TOY.n_kv_heads):
                 k, v = m.kv_get(0, l, h, 300)
                 for got, want in ((k, K[0, l, h, 300]), (v, V[0, l, h, 300])):
-                    ulp = np.abs(want) * 2.0 ** -7 + 1e-30
-                    assert np.all(np.abs(got - want) <= ulp * 1.0001)
+                    assert kv_rows_match(got, want)
         golden = np.load(os.path.join(GOLDEN, "toy_logits.npz"))["kv_300"]
         np.testing.assert_array_equal(np.concatenate([K[0, 0, 0, 300], V[0, 0, 0, 300]]), golden)
 

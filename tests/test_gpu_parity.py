@@ -198,3 +198,16 @@ def test_full_size_modes_bit_identical_and_greedy(name):
     np.testing.assert_array_equal(outs[0], outs[1])
     np.testing.assert_array_equal(outs[1], outs[2])
     m.close()
+
+
+def test_reference_cpp_drives_kernel_through_bridge():
+    """fusesim's own C++ (init_weights, reference_forward) next to
+    fusesim::b200::Decoder (include/ffb200/fusesim_bridge.hpp): the drop-in a
+    reference maintainer would compile (tests/cpp/bridge_parity.cpp)."""
+    import subprocess
+    exe = os.path.join(os.path.dirname(os.path.abspath(__file__)), "cpp", "bridge_parity")
+    if not os.path.exists(exe):
+        pytest.skip("bridge_parity not built (needs the reference headers at build time)")
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=300)
+    print(r.stdout)
+    assert r.returncode == 0, r.stdout + r.stderr

@@ -47,6 +47,8 @@ def parse():
                     choices=["fused_overlap", "fused", "baseline"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-variants", action="store_true")
+    ap.add_argument("--calibrate", type=int, default=3,
+                    help="ffb_calibrate iterations before timing (0 = uniform plan)")
     return ap.parse_args()
 
 
@@ -229,6 +231,10 @@ def run_ours(args):
             "baseline": RunMode.BASELINE}[args.mode]
     m = DecodeModel(cfg, ctx + 8, device=dev, mode=mode)
     m.init_synthetic(1234)
+    if args.calibrate:  # per-SM load balance (setup, outside the timed region)
+        for l in range(cfg.layers):
+            m.set_length(l, ctx)
+        m.calibrate(args.calibrate)
     info = m.info()
     stream = torch.cuda.Stream(device=dev)
     tokens = torch.arange(17, 17 + args.batch, dtype=torch.int64, device=f"cuda:{dev}")
@@ -348,6 +354,9 @@ def run_ours(args):
             "clocks": clk.summary(),
             "cpu_baseline": cpu,
             "kernel_info": info,
+            "plan": {"calibrate_iterations": args.calibrate,
+                     "sm_weight_min": round(float(m.plan_weights().min()), 4),
+                     "sm_weight_max": round(float(m.plan_weights().max()), 4)},
         }
         print(json.dumps(line), flush=True)
     m.close()

@@ -112,7 +112,10 @@ ffb_status ffb_set_mode(ffb_model *m, ffb_mode mode);
 
 /* Tuning knobs.  "l2_prefetch_bytes": how far (bytes per SM) the producer's
  * L2 prefetch cursor runs ahead of the shared-memory ring in FusedOverlap
- * mode (0 disables; default 256 KiB). */
+ * mode (0 disables; default 512 KiB).  "l2_prefetch_stages": 6-bit mask of
+ * the stage types (bit s = stage s of a layer: 0 QKV, 1 ATTN, 2 AOUT, 3 GLU,
+ * 4 RED; bit 5 = LM head) in which the prefetch may run, only while the ring
+ * is full (default ATTN|AOUT = 0x6). */
 ffb_status ffb_set_option(ffb_model *m, const char *key, int64_t value);
 
 /* Diagnostics only (never needed for correct use): bit 0 = streaming-only
@@ -159,6 +162,19 @@ typedef struct ffb_info {
     uint64_t device_bytes;   /* total device allocation                    */
 } ffb_info;
 ffb_status ffb_get_info(const ffb_model *m, ffb_info *out);
+
+/* Per-SM load balance (the reference's calibrate step, on
+ * real hardware).  Runs `iterations` rounds of 3 traced decode steps at the
+ * current cache length (positions beyond the length are scratch), measures
+ * each SM's GLU streaming time and re-splits the rows of every streamed
+ * matrix in proportion to each SM's measured rate (weights clamped to
+ * [0.7, 1.3] of the mean).  Persistent launches map CTAs to plans by SM id,
+ * so the weights follow the SM.  iterations == 0 restores the uniform plan.
+ * Results stay deterministic for a given plan; a different plan changes the
+ * cross-CTA summation grouping (~1e-7 relative). */
+ffb_status ffb_calibrate(ffb_model *m, int32_t iterations);
+/* Current per-SM plan weights (mean 1); returns the count (grid) or -1. */
+int64_t ffb_get_plan_weights(const ffb_model *m, double *out, int64_t n);
 
 /* Device pointer to the most recent logits (batch x vocab f32). */
 const float *ffb_logits_device(const ffb_model *m);

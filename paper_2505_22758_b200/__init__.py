@@ -30,7 +30,7 @@ __all__ = [
 ]
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libffb200.so")
+LIB_PATH = os.environ.get("FFB200_LIB") or os.path.join(HERE, "libffb200.so")
 
 
 class FusesimError(RuntimeError):
@@ -197,6 +197,9 @@ def lib():
     L.ffb_get_info.argtypes = [C.c_void_p, P(_Info)]
     L.ffb_logits_device.argtypes = [C.c_void_p]
     L.ffb_logits_device.restype = C.c_void_p
+    L.ffb_calibrate.argtypes = [C.c_void_p, C.c_int32]
+    L.ffb_get_plan_weights.argtypes = [C.c_void_p, P(C.c_double), C.c_int64]
+    L.ffb_get_plan_weights.restype = C.c_int64
     _lib = L
     return L
 
@@ -304,6 +307,17 @@ class DecodeModel:
     def set_option(self, key: str, value: int):
         """Tuning knobs (ffb_set_option), e.g. ("l2_prefetch_bytes", 262144)."""
         _check(lib().ffb_set_option(self._h, key.encode(), int(value)))
+
+    def calibrate(self, iterations: int = 3):
+        """Per-SM load balance from measured streaming rates (ffb_calibrate);
+        0 restores the uniform plan."""
+        _check(lib().ffb_calibrate(self._h, int(iterations)))
+
+    def plan_weights(self) -> np.ndarray:
+        n = lib().ffb_get_plan_weights(self._h, None, 0)
+        out = np.zeros(n, np.float64)
+        lib().ffb_get_plan_weights(self._h, out.ctypes.data_as(C.POINTER(C.c_double)), n)
+        return out
 
     def set_debug(self, flags: int):
         """Diagnostics only (ffb_set_debug): 1 = streaming-only run."""

@@ -106,12 +106,18 @@ struct DecodeParams {
     int32_t debug;       // kDebug* bits; 0 in production
     uint64_t* trace;     // optional [grid][n_stages][8] trace records
     int64_t l2_prefetch; // bytes the L2 prefetch cursor runs ahead of the ring
+    int32_t l2_pf_stages; // stage types (bit s % 5, bit 5 = LM head) where the
+                          // producer may prefetch while its ring is full
     // GLU work pool (dynamic load balance, deterministic): pairs [pool_t0, DI)
     // in chunks of pool_ct pairs, claimed at run time by whichever CTA is free;
     // each chunk's d_model partial goes to pool_part[chunk].
     float* pool_part;          // [pool_chunks][RG][B][D]
     uint32_t* pool_counters;   // [L] claim counters (epoch based)
     int32_t pool_t0, pool_ct, pool_chunks;
+    // SM id -> dense rank (the CTA's plan index) for persistent launches, so
+    // that a per-SM weighted plan (ffb_calibrate) follows the SM whatever
+    // block index the launch put there; nullptr -> blockIdx.x
+    const int16_t* sm_rank;
     float eps;
     double rope_theta;
 };
@@ -167,9 +173,16 @@ struct KTraits {
     // (2*grid*B) and the GLU reduction (NCW*32); grid <= kMaxGrid
     static constexpr int kMaxGrid = 160;
     static constexpr int cmax(int a, int b) { return a > b ? a : b; }
+    // attention: ring slots consumed together in one softmax pass, positions
+    // per pass (+1 for the current token, rounded to 4) and its scratch:
+    // alpha*q [QPG][DH], scores [QPG][ANP], probabilities [ANP][QPG], stats
+    static constexpr int ATT_SC = 4;
+    static constexpr int ANP = ((ATT_SC * KVC + 1) + 3) / 4 * 4;
+    static constexpr int SZ_ATT = S::QPG * S::DH + 2 * S::QPG * ANP + 4 * S::QPG;
     static constexpr int SZ_WPART =
-        4 * cmax(cmax(NCW * S::QPG * (S::DH + 2), 3 * kMaxGrid * S::QPG),
-                 cmax(2 * kMaxGrid * S::B, NCW * 32));
+        4 * cmax(cmax(cmax(NCW * S::QPG * (S::DH + 2), 3 * kMaxGrid * S::QPG),
+                      cmax(2 * kMaxGrid * S::B, NCW * 32)),
+                 SZ_ATT);
     static constexpr int OFF_AMAX = OFF_WPART + SZ_WPART;  // [NCT] (f32, i32)
     static constexpr int SZ_AMAX = NCT * 8;
     static constexpr int OFF_MISC = OFF_AMAX + SZ_AMAX;  // flags
@@ -179,6 +192,7 @@ struct KTraits {
     static constexpr int NSLOTS_RAW = (MAX_SMEM - FIXED - 256) / SLOT_BYTES;
     static constexpr int NSLOTS = NSLOTS_RAW > 8 ? 8 : NSLOTS_RAW;
     static_assert(NSLOTS >= 2, "ring too small");
+    static_assert(NSLOTS >= ATT_SC + 1, "attention pass must leave a slot for streaming");
     static constexpr int OFF_BARS = FIXED;  // full[NSLOTS], empty[NSLOTS]
     static constexpr int OFF_RING = FIXED + 256;
     static constexpr int SMEM_BYTES = OFF_RING + NSLOTS * SLOT_BYTES;
@@ -205,6 +219,11 @@ struct DecodeCta {
         empty = full + T::NSLOTS;
         ring = smem + T::OFF_RING;
         cta = blockIdx.x;
+        if (p.sm_rank != nullptr) {
+            uint32_t smid;
+            asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+            cta = p.sm_rank[smid];
+        }
         grid = gridDim.x;
         pl = p.plan[cta];
     }
@@ -515,7 +534,8 @@ struct DecodeCta {
                 }
                 // ring full: issue the whole prefetch window at once (no
                 // waiting between prefetches), then block on the slot
-                if (!mbar_test_wait(&empty[slot], ph ^ 1)) {
+                const int stype = stage == p.layers * kStagesPerLayer ? 5 : stage % kStagesPerLayer;
+                if (((p.l2_pf_stages >> stype) & 1) && !mbar_test_wait(&empty[slot], ph ^ 1)) {
                     while (pf_live && ahead < window) {
                         const void *q0, *q1;
                         uint32_t qb;
@@ -726,6 +746,29 @@ struct DecodeCta {
 
     static constexpr int ilog2(int v) { return v <= 1 ? 0 : 1 + ilog2(v / 2); }
 
+    // Sums V values over each group of G consecutive lanes (G, V powers of
+    // two, V <= G <= 32): afterwards lane l of a group holds the group sum of
+    // value index (l % G) / (G / V).  V - 1 + log2(G / V) shuffles.
+    template <int V, int G>
+    __device__ static float reduce_group(float (&v)[V], int lane) {
+        static_assert(V >= 1 && V <= G && G <= 32 && (V & (V - 1)) == 0 && (G & (G - 1)) == 0,
+                      "powers of two, V <= G <= 32");
+#pragma unroll
+        for (int s = V / 2, o = G / 2; s >= 1; s >>= 1, o >>= 1) {
+            const bool upper = (lane & o) != 0;
+#pragma unroll
+            for (int i = 0; i < s; ++i) {
+                const float send = upper ? v[i] : v[i + s];
+                const float keep = upper ? v[i + s] : v[i];
+                v[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+            }
+        }
+        float r = v[0];
+#pragma unroll
+        for (int o = G / V / 2; o >= 1; o >>= 1) r += __shfl_xor_sync(0xffffffffu, r, o);
+        return r;
+    }
+
     // GEMV over rows [r0, r1) streamed by the producer.  Per slot every warp
     // forms its column-slice partial dots for all RPT x B (row, batch) values
     // (two accumulators per row, no per-row branches), releases the slot, and
@@ -845,102 +888,96 @@ struct DecodeCta {
     }
 
     // ---------------------------------------------------------- S_ATTN
-    // Split-K flash-decoding (numerics.hpp:64-145) on CUDA cores with ONE
-    // online-softmax state per CTA, chunk by chunk from the ring:
-    //   A  scores: thread (dq, pos) dots DPA dims of k_pos with alpha*q of all
-    //      QPG heads (q in smem, read as broadcasts).  K/V rows are stored with
-    //      16-byte chunks XOR-swizzled by (pos & 7), so 32 lanes on 32
-    //      positions hit 32 distinct banks; partials -> ss[dq][h][pos]
-    //   B  softmax: warp h sums the DQ partials, chunk max, online rescale,
-    //      p = e^{s - m} -> ps[pos][h]
-    //   C  P.V: thread (pg, dc) keeps o[h][8 dims of chunk dc] for all heads
-    //      over positions pg, pg + PG, ...
-    static constexpr int DQ = NCT / T::KVC;  // dim groups in phase A
-    static constexpr int DPA = DH / DQ;      // dims per thread in phase A
-    static constexpr int DC = DH / 8;        // 16-byte chunks per K/V row
-    static constexpr int PG = NCT / DC;      // position groups in phase C
-    static_assert(NCT % T::KVC == 0 && DPA % 8 == 0 && DC >= 8, "attention mapping");
-    static_assert(QPG <= NCW && 32 % DC == 0 || DC >= 32, "attention mapping");
-    static_assert(DQ * QPG * T::KVC + T::KVC * QPG + QPG * DH + QPG * 4 <= NCW * QPG * (DH + 2),
-                  "attention scratch fits in wpart");
+    // Split-K flash-decoding (numerics.hpp:64-145) on CUDA cores.  A CTA's
+    // positions [p0, p1) are consumed in passes of up to ATT_SC ring slots
+    // (plus the current token in the last pass), three barriers per pass:
+    //   A  scores: thread j dots position j's K row (16-byte chunks XOR-
+    //      swizzled by pos & 7 -> conflict-free) with alpha*q of all QPG heads
+    //      (smem broadcasts) -> sc[h][j]
+    //   B  softmax: warp h takes the pass max, rescales its running (m, l)
+    //      (online softmax across passes) and writes p[j][h] = e^{s - m}
+    //   C  P.V: thread (pg, dc) accumulates o[h][8 dims of chunk dc] for all
+    //      heads over positions pg, pg + PG, ...
+    // At ctx 4096 on the 8B shape a CTA owns ~228 positions: one pass.
+    static constexpr int DC = DH / 8;   // 16-byte chunks per K/V row
+    static constexpr int PG = NCT / DC;  // position groups in phase C
+    static constexpr int ANP = T::ANP;
+    static_assert(DC >= 8 && NCT % DC == 0, "attention mapping");
+    static_assert(32 % DC == 0, "attention mapping: a position's chunks share one warp");
+    static_assert(QPG <= DC, "attention score fold: QPG <= DH / 8");
 
-    __device__ float* att_ss() { return wpart(); }                       // [DQ][QPG][KVC]
-    __device__ float* att_ps() { return att_ss() + DQ * QPG * T::KVC; }  // [KVC][QPG]
-    __device__ float* att_q() { return att_ps() + T::KVC * QPG; }        // [QPG][DH]
-    __device__ float* att_st() { return att_q() + QPG * DH; }            // [QPG][4] m l scale
+    __device__ float* att_q() { return wpart(); }                 // [QPG][DH]
+    __device__ float* att_sc() { return att_q() + QPG * DH; }     // [QPG][ANP]
+    __device__ float* att_p() { return att_sc() + QPG * ANP; }    // [ANP][QPG]
+    __device__ float* att_st() { return att_p() + ANP * QPG; }    // [QPG][4] m l scale
 
-    // One chunk of n positions [pos0, pos0 + n) whose K/V rows are at kb/vb
-    // (shared memory, swizzled as stored).  o: this thread's P.V accumulators.
-    __device__ void attn_chunk(const uint8_t* kb, const uint8_t* vb, int n, int pos0,
-                               float (&o)[QPG][8]) {
+    // K (kv = 0) or V (kv = 1) row of pass position j: ring slot (it0 + j /
+    // KVC) for j < nring, else the current token staged in h_s
+    __device__ const uint8_t* att_row(uint32_t it0, int j, int nring, int kv) {
+        if (j < nring) {
+            const uint32_t slot = (it0 + j / T::KVC) % T::NSLOTS;
+            return ring + slot * T::SLOT_BYTES + kv * (T::SLOT_BYTES / 2) + (j % T::KVC) * DH * 2;
+        }
+        return reinterpret_cast<const uint8_t*>(h_s()) + kv * DH * 2;
+    }
+
+    // One pass over n positions [pos0, pos0 + n), the first nring of them in
+    // ring slots it0, it0 + 1, ... (already waited for).  Scores are kept in
+    // log2 units (q is pre-scaled by alpha * log2 e), so p = 2^{s - m}: the
+    // same softmax, one MUFU.EX2 per probability.  Dot products use packed
+    // f32x2 FMAs (FFMA2) on (even, odd) dimension pairs.
+    // (A (position-group, chunk) mapping of phase A with q in registers and a
+    // shuffle fold was tried: no faster, and it showed an unexplained
+    // overlap-mode corruption at batch 4 on the toy shape; not used.)
+    __device__ void attn_pass(uint32_t it0, int nring, int n, int pos0, float2 (&o)[QPG][4]) {
         const int ctid = threadIdx.x, warp = ctid / 32, lane = ctid % 32;
-        float* ss = att_ss();
-        float* ps = att_ps();
+        float* sc = att_sc();
+        float* pr = att_p();
         const float* qs = att_q();
         float* st = att_st();
-        {  // A: scores
-            const int j = ctid % T::KVC, dq = ctid / T::KVC;
-            float acc[QPG];
+        for (int j = ctid; j < n; j += NCT) {  // A: scores, thread = position
+            const uint8_t* row = att_row(it0, j, nring, 0);
+            const int key = (pos0 + j) & 7;
+            float2 acc[QPG];
 #pragma unroll
-            for (int h = 0; h < QPG; ++h) acc[h] = 0.f;
-            if (j < n) {
-                const uint8_t* row = kb + (size_t)j * DH * 2;
-                const int key = (pos0 + j) & 7;
+            for (int h = 0; h < QPG; ++h) acc[h] = make_float2(0.f, 0.f);
+#pragma unroll 2
+            for (int ch = 0; ch < DC; ++ch) {
+                float4 q4[QPG][2];  // all heads' q for this chunk first (LDS in flight)
 #pragma unroll
-                for (int c = 0; c < DPA / 8; ++c) {
-                    const int ch = dq * (DPA / 8) + c;
-                    const uint4 w = lds_u128(row + ((ch ^ key) << 4));
-                    const float kf[8] = {bf_lo(w.x), bf_hi(w.x), bf_lo(w.y), bf_hi(w.y),
-                                         bf_lo(w.z), bf_hi(w.z), bf_lo(w.w), bf_hi(w.w)};
+                for (int h = 0; h < QPG; ++h) {
+                    q4[h][0] = *reinterpret_cast<const float4*>(qs + h * DH + ch * 8);
+                    q4[h][1] = *reinterpret_cast<const float4*>(qs + h * DH + ch * 8 + 4);
+                }
+                const uint4 w = lds_u128(row + ((ch ^ key) << 4));
+                const float2 k0 = make_float2(bf_lo(w.x), bf_hi(w.x));
+                const float2 k1 = make_float2(bf_lo(w.y), bf_hi(w.y));
+                const float2 k2 = make_float2(bf_lo(w.z), bf_hi(w.z));
+                const float2 k3 = make_float2(bf_lo(w.w), bf_hi(w.w));
 #pragma unroll
-                    for (int h = 0; h < QPG; ++h) {
-                        const float4 q0 = *reinterpret_cast<const float4*>(qs + h * DH + ch * 8);
-                        const float4 q1 =
-                            *reinterpret_cast<const float4*>(qs + h * DH + ch * 8 + 4);
-                        acc[h] = fmaf(q0.x, kf[0], acc[h]);
-                        acc[h] = fmaf(q0.y, kf[1], acc[h]);
-                        acc[h] = fmaf(q0.z, kf[2], acc[h]);
-                        acc[h] = fmaf(q0.w, kf[3], acc[h]);
-                        acc[h] = fmaf(q1.x, kf[4], acc[h]);
-                        acc[h] = fmaf(q1.y, kf[5], acc[h]);
-                        acc[h] = fmaf(q1.z, kf[6], acc[h]);
-                        acc[h] = fmaf(q1.w, kf[7], acc[h]);
-                    }
+                for (int h = 0; h < QPG; ++h) {
+                    acc[h] = __ffma2_rn(make_float2(q4[h][0].x, q4[h][0].y), k0, acc[h]);
+                    acc[h] = __ffma2_rn(make_float2(q4[h][0].z, q4[h][0].w), k1, acc[h]);
+                    acc[h] = __ffma2_rn(make_float2(q4[h][1].x, q4[h][1].y), k2, acc[h]);
+                    acc[h] = __ffma2_rn(make_float2(q4[h][1].z, q4[h][1].w), k3, acc[h]);
                 }
             }
 #pragma unroll
-            for (int h = 0; h < QPG; ++h) ss[(dq * QPG + h) * T::KVC + j] = acc[h];
+            for (int h = 0; h < QPG; ++h) sc[h * ANP + j] = acc[h].x + acc[h].y;
         }
         consumer_sync(NCT);
-        if (warp < QPG) {  // B: online softmax for head `warp`
-            const int h = warp;
-            float sv[(T::KVC + 31) / 32];
+        for (int h = warp; h < QPG; h += NCW) {  // B: online softmax of head h
             float cmax = -INFINITY;
-#pragma unroll
-            for (int i = 0; i < (T::KVC + 31) / 32; ++i) {
-                const int j = lane + 32 * i;
-                float s = -INFINITY;
-                if (j < n) {
-                    s = 0.f;
-#pragma unroll
-                    for (int dq = 0; dq < DQ; ++dq) s += ss[(dq * QPG + h) * T::KVC + j];
-                }
-                sv[i] = s;
-                cmax = fmaxf(cmax, s);
-            }
+            for (int j = lane; j < n; j += 32) cmax = fmaxf(cmax, sc[h * ANP + j]);
             cmax = warp_max(cmax);
             const float m_old = st[h * 4 + 0];
             const float m_new = fmaxf(m_old, cmax);
-            const float scale = expf(m_old - m_new);  // 0 for the first chunk
+            const float scale = exp2f(m_old - m_new);  // 0 for the first pass
             float psum = 0.f;
-#pragma unroll
-            for (int i = 0; i < (T::KVC + 31) / 32; ++i) {
-                const int j = lane + 32 * i;
-                if (j < T::KVC) {
-                    const float pj = j < n ? expf(sv[i] - m_new) : 0.f;
-                    ps[j * QPG + h] = pj;
-                    psum += pj;
-                }
+            for (int j = lane; j < n; j += 32) {
+                const float pj = exp2f(sc[h * ANP + j] - m_new);
+                pr[j * QPG + h] = pj;
+                psum += pj;
             }
             psum = warp_sum(psum);
             if (lane == 0) {
@@ -954,22 +991,37 @@ struct DecodeCta {
             const int dc = ctid % DC, pg = ctid / DC;
 #pragma unroll
             for (int h = 0; h < QPG; ++h) {
-                const float sc = st[h * 4 + 2];
+                const float2 s2 = make_float2(st[h * 4 + 2], st[h * 4 + 2]);
 #pragma unroll
-                for (int e = 0; e < 8; ++e) o[h][e] *= sc;
+                for (int e = 0; e < 4; ++e) o[h][e] = __fmul2_rn(o[h][e], s2);
             }
+#pragma unroll 2
             for (int j = pg; j < n; j += PG) {
-                const uint4 w = lds_u128(vb + (size_t)j * DH * 2 + ((dc ^ ((pos0 + j) & 7)) << 4));
-                const float vf[8] = {bf_lo(w.x), bf_hi(w.x), bf_lo(w.y), bf_hi(w.y),
-                                     bf_lo(w.z), bf_hi(w.z), bf_lo(w.w), bf_hi(w.w)};
+                const uint4 w = lds_u128(att_row(it0, j, nring, 1) + ((dc ^ ((pos0 + j) & 7)) << 4));
+                const float2 v2[4] = {make_float2(bf_lo(w.x), bf_hi(w.x)),
+                                      make_float2(bf_lo(w.y), bf_hi(w.y)),
+                                      make_float2(bf_lo(w.z), bf_hi(w.z)),
+                                      make_float2(bf_lo(w.w), bf_hi(w.w))};
+                float pj[QPG];
+                if constexpr (QPG % 4 == 0) {
+#pragma unroll
+                    for (int h = 0; h < QPG; h += 4) {
+                        const float4 p4 = *reinterpret_cast<const float4*>(pr + j * QPG + h);
+                        pj[h] = p4.x; pj[h + 1] = p4.y; pj[h + 2] = p4.z; pj[h + 3] = p4.w;
+                    }
+                } else {
+#pragma unroll
+                    for (int h = 0; h < QPG; ++h) pj[h] = pr[j * QPG + h];
+                }
 #pragma unroll
                 for (int h = 0; h < QPG; ++h) {
-                    const float pj = ps[j * QPG + h];
+                    const float2 p2 = make_float2(pj[h], pj[h]);
 #pragma unroll
-                    for (int e = 0; e < 8; ++e) o[h][e] = fmaf(pj, vf[e], o[h][e]);
+                    for (int e = 0; e < 4; ++e) o[h][e] = __ffma2_rn(p2, v2[e], o[h][e]);
                 }
             }
         }
+        consumer_sync(NCT);  // sc / p / stats reusable by the next pass
     }
 
     __device__ void stage_attn(uint32_t& it, int l) {
@@ -978,7 +1030,8 @@ struct DecodeCta {
         const int unit = pl.attn_unit, b = unit / S::NKV, kvh = unit % S::NKV;
         int p0, p1;
         attn_range(p0, p1);
-        const int past_end = min(p1, p.pos);
+        const int past_end = max(p0, min(p1, p.pos));
+        const bool has_cur = p.pos >= p0 && p.pos < p1;
         float* st = att_st();
         if (ctid < QPG) {
             st[ctid * 4 + 0] = -INFINITY;
@@ -986,15 +1039,15 @@ struct DecodeCta {
             st[ctid * 4 + 2] = 0.f;
         }
         wait_stage(l * kStagesPerLayer + S_ATTN);
-        {  // alpha * q of this kv head's QPG query heads -> smem (alpha = 1/sqrt(dh))
-            const float alpha = 1.0f / sqrtf(static_cast<float>(DH));
+        {  // alpha * log2(e) * q of this kv head's QPG query heads -> smem
+           // (alpha = 1/sqrt(dh); scores in log2 units, see attn_pass)
+            const float alpha = 1.4426950408889634f / sqrtf(static_cast<float>(DH));
             float* qs = att_q();
             for (int i = ctid; i < QPG * DH; i += NCT)
                 qs[i] = alpha * ldcg_f(p.q + (size_t)b * D + kvh * QPG * DH + i);
             // the current token's K/V rows (this launch's S_QKV wrote them with
             // generic stores; read at L2, emit.hpp:148-154 SyncLoadCurrentToken)
-            // staged now so the load overlaps the ring chunks
-            if (p.pos >= p0 && p.pos < p1) {
+            if (has_cur) {
                 uint8_t* cur = reinterpret_cast<uint8_t*>(h_s());  // [K row][V row]
                 const size_t row = kv_row(l, b, kvh, p.pos);
                 constexpr int V16 = DH * 2 / 16;
@@ -1005,31 +1058,30 @@ struct DecodeCta {
                 }
             }
         }
-        float o[QPG][8];
+        float2 o[QPG][4];
 #pragma unroll
         for (int h = 0; h < QPG; ++h)
 #pragma unroll
-            for (int e = 0; e < 8; ++e) o[h][e] = 0.f;
+            for (int e = 0; e < 4; ++e) o[h][e] = make_float2(0.f, 0.f);
         consumer_sync(NCT);
+        trace_mark(l * kStagesPerLayer + S_ATTN, 5);
 
-        for (int c0 = p0; c0 < past_end; c0 += T::KVC) {
-            const int n = min(T::KVC, past_end - c0);
-            const uint32_t slot = it % T::NSLOTS, par = (it / T::NSLOTS) & 1;
-            wait_full(slot, par);
-            const uint8_t* kb = ring + slot * T::SLOT_BYTES;
-            attn_chunk(kb, kb + T::SLOT_BYTES / 2, n, c0, o);
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&empty[slot]);
-            ++it;
+        constexpr int PASS = T::ATT_SC * T::KVC;
+        for (int c0 = p0; c0 < past_end || (c0 == p0 && has_cur); c0 += PASS) {
+            const int nring = min(PASS, past_end - c0);
+            const int nslots = (nring + T::KVC - 1) / T::KVC;
+            const bool last = c0 + PASS >= past_end;
+            const int n = nring + ((last && has_cur) ? 1 : 0);
+            const uint32_t it0 = it;
+            for (int s = 0; s < nslots; ++s, ++it)
+                wait_full(it % T::NSLOTS, (it / T::NSLOTS) & 1);
+            trace_mark(l * kStagesPerLayer + S_ATTN, 6);
+            attn_pass(it0, nring, n, c0, o);
+            if (lane == 0)
+                for (uint32_t i = it0; i < it; ++i) mbar_arrive(&empty[i % T::NSLOTS]);
+            if (last) break;
         }
         trace_mark(l * kStagesPerLayer + S_ATTN, 3);
-        // current token: written by this launch's S_QKV with generic stores,
-        // read back at L2 into smem (emit.hpp:148-154 SyncLoadCurrentToken)
-        if (p.pos >= p0 && p.pos < p1) {  // staged into h_s at stage entry
-            const uint8_t* cur = reinterpret_cast<const uint8_t*>(h_s());
-            attn_chunk(cur, cur + DH * 2, 1, p.pos, o);
-        }
-        consumer_sync(NCT);
         // CTA partial: (m, l) from st, o summed over the PG position groups
         constexpr int STR = DH + 2;
         float* mlc = reinterpret_cast<float*>(misc()) + 4;  // [QPG][2]
@@ -1041,11 +1093,13 @@ struct DecodeCta {
 #pragma unroll
         for (int h = 0; h < QPG; ++h)
 #pragma unroll
-            for (int e = 0; e < 8; ++e)
+            for (int e = 0; e < 4; ++e)
 #pragma unroll
-                for (int off = DC; off < 32; off <<= 1)
-                    o[h][e] += __shfl_xor_sync(0xffffffffu, o[h][e], off);
-        consumer_sync(NCT);  // st/ss/ps/q dead from here: wpart reused for o
+                for (int off = DC; off < 32; off <<= 1) {
+                    o[h][e].x += __shfl_xor_sync(0xffffffffu, o[h][e].x, off);
+                    o[h][e].y += __shfl_xor_sync(0xffffffffu, o[h][e].y, off);
+                }
+        consumer_sync(NCT);  // st/sc/p/q dead from here: wpart reused for o
         float* ro = wpart();  // [NCW][QPG][DH]
         {
             const int dc = ctid % DC;
@@ -1053,12 +1107,13 @@ struct DecodeCta {
 #pragma unroll
                 for (int h = 0; h < QPG; ++h)
 #pragma unroll
-                    for (int e = 0; e < 8; ++e) ro[(warp * QPG + h) * DH + dc * 8 + e] = o[h][e];
+                    for (int e = 0; e < 4; ++e)
+                        *reinterpret_cast<float2*>(ro + (warp * QPG + h) * DH + dc * 8 + 2 * e) =
+                            o[h][e];
             }
         }
         consumer_sync(NCT);
         float* part = p.attn_part + ((size_t)unit * grid + pl.attn_g) * QPG * STR;
-        constexpr int WPG = NCT / 32 / (DC >= 32 ? DC / 32 : 1);  // warps holding groups
         for (int idx = ctid; idx < QPG * DH; idx += NCT) {
             const int h = idx / DH, d = idx % DH;
             float O = 0.f;
@@ -1071,9 +1126,9 @@ struct DecodeCta {
                 __stcg(dst + 1, mlc[2 * h + 1]);
             }
         }
-        (void)WPG;
         // last arriver of the group combines (numerics.hpp:123-145)
         consumer_sync(NCT);
+        trace_mark(l * kStagesPerLayer + S_ATTN, 7);
         int* flag = misc();
         if (ctid == 0) {
             const uint32_t old =
@@ -1121,12 +1176,12 @@ struct DecodeCta {
                 float L = 0.f;
                 for (int g = lane; g < G; g += 32) {
                     const float lg = ml[2 * (g * QPG + h) + 1];
-                    if (lg > 0.f) L += lg * expf(ml[2 * (g * QPG + h)] - M);
+                    if (lg > 0.f) L += lg * exp2f(ml[2 * (g * QPG + h)] - M);
                 }
                 L = warp_sum(L);
                 for (int g = lane; g < G; g += 32) {
                     const float lg = ml[2 * (g * QPG + h) + 1];
-                    rr[h * G + g] = lg > 0.f ? expf(ml[2 * (g * QPG + h)] - M) / L : 0.f;
+                    rr[h * G + g] = lg > 0.f ? exp2f(ml[2 * (g * QPG + h)] - M) / L : 0.f;
                 }
             }
             consumer_sync(NCT);

@@ -144,6 +144,17 @@ __global__ void synth_f32_kernel(float* dst, int64_t n, uint64_t seed, float mea
 
 int64_t split_at(int64_t units, int64_t c, int64_t grid) { return (units * c) / grid; }
 
+// One CTA per SM (the decode kernel's shared memory): which SM ids exist.
+__global__ void smid_probe_kernel(int32_t* out) {
+    extern __shared__ uint8_t probe_smem[];
+    if (threadIdx.x == 0) {
+        uint32_t smid;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+        out[blockIdx.x] = static_cast<int32_t>(smid);
+        probe_smem[0] = 0;
+    }
+}
+
 // KV row layout: 16-byte chunks XOR-swizzled by (pos & 7) so that the
 // attention kernel's 32 lanes on 32 positions read 32 distinct smem banks
 // (decode_kernel.cuh: kv_swz_dim).  Element d of position pos:
@@ -160,8 +171,20 @@ struct ffb_model {
     ffb_mode mode = FFB_MODE_FUSED_OVERLAP;
     int32_t debug = 0;
     uint64_t* trace = nullptr;  // per-CTA stage timestamps (ffb_set_trace)
-    int64_t l2_prefetch = 0;  // per-CTA L2 prefetch window (ffb_set_option); off: measured slower
+    // per-CTA L2 prefetch window (ffb_set_option), issued only while the
+    // producer is blocked on a full ring in S_ATTN / S_AOUT (the attention
+    // latency chain, when HBM would otherwise idle); measured -2% on the 8B
+    // shape at 512 KiB, while prefetching during the streaming-bound GLU
+    // stage costs up to +8% (profiles/summary_r01.md)
+    int64_t l2_prefetch = 512 << 10;
+    int32_t l2_pf_stages = (1 << S_ATTN) | (1 << S_AOUT);
     int plan_reverse = 0;             // weight slices assigned in reverse CTA order
+    // per-SM plan weights (ffb_calibrate): streamed-row shares of QKV / AOUT /
+    // GLU / LM head proportional to each SM's measured streaming rate
+    std::vector<double> sm_weight;
+    std::vector<CtaPlan> plan_host;
+    int16_t* sm_rank = nullptr;       // device [max smid + 1] -> dense rank, or null
+    int use_sm_rank = 1;              // option "sm_rank": plans follow SM ids
     int64_t pool_permille = 0;        // share of d_inter in the dynamic GLU pool (off)
     int64_t pool_ct_pref = 4;         // preferred pairs per pool chunk
     int pool_t0 = 0, pool_ct = 0, pool_chunks = 0, pool_chunks_max = 0;
@@ -241,18 +264,28 @@ ffb_status build_plan(ffb_model* m) {
         }
     }
     const int64_t glu_static = m->pool_t0;
+    // slice k of every streamed matrix goes to CTA ord[k]; boundaries follow
+    // the cumulative per-SM weights (all 1 unless ffb_calibrate ran)
+    if ((int64_t)m->sm_weight.size() != G) m->sm_weight.assign(G, 1.0);
+    std::vector<double> cum(G + 1, 0.0);
+    for (int64_t k = 0; k < G; ++k)
+        cum[k + 1] = cum[k] + m->sm_weight[m->plan_reverse ? G - 1 - k : k];
+    auto wsplit = [&](int64_t units, int64_t k) {
+        if (k >= G) return units;
+        return std::min<int64_t>(units, std::llround(units * cum[k] / cum[G]));
+    };
     for (int64_t i = 0; i < G; ++i) {
         CtaPlan& p = plan[i];
         std::memset(&p, 0, sizeof(p));
         const int64_t k = m->plan_reverse ? G - 1 - i : i;  // weight-slice order
-        p.qkv_r0 = static_cast<int32_t>(2 * split_at(qkv_pairs, k, G));
-        p.qkv_r1 = static_cast<int32_t>(2 * split_at(qkv_pairs, k + 1, G));
-        p.aout_r0 = static_cast<int32_t>(split_at(c.d_model, k, G));
-        p.aout_r1 = static_cast<int32_t>(split_at(c.d_model, k + 1, G));
-        p.glu_t0 = static_cast<int32_t>(split_at(glu_static, k, G));
-        p.glu_t1 = static_cast<int32_t>(split_at(glu_static, k + 1, G));
-        p.lm_r0 = static_cast<int32_t>(split_at(c.vocab_size, k, G));
-        p.lm_r1 = static_cast<int32_t>(split_at(c.vocab_size, k + 1, G));
+        p.qkv_r0 = static_cast<int32_t>(2 * wsplit(qkv_pairs, k));
+        p.qkv_r1 = static_cast<int32_t>(2 * wsplit(qkv_pairs, k + 1));
+        p.aout_r0 = static_cast<int32_t>(wsplit(c.d_model, k));
+        p.aout_r1 = static_cast<int32_t>(wsplit(c.d_model, k + 1));
+        p.glu_t0 = static_cast<int32_t>(wsplit(glu_static, k));
+        p.glu_t1 = static_cast<int32_t>(wsplit(glu_static, k + 1));
+        p.lm_r0 = static_cast<int32_t>(wsplit(c.vocab_size, k));
+        p.lm_r1 = static_cast<int32_t>(wsplit(c.vocab_size, k + 1));
         p.red_c0 = static_cast<int32_t>(split_at(c.d_model, i, G));
         p.red_c1 = static_cast<int32_t>(split_at(c.d_model, i + 1, G));
         if (i < static_cast<int64_t>(m->n_units) * m->attn_group) {
@@ -266,6 +299,48 @@ ffb_status build_plan(ffb_model* m) {
             return fail(FFB_UNSUPPORTED, "d_inter too large for the per-CTA GLU buffer");
     }
     CUDA_TRY(cudaMemcpy(m->plan, plan.data(), sizeof(CtaPlan) * G, cudaMemcpyHostToDevice));
+    m->plan_host = plan;
+    return FFB_OK;
+}
+
+// SM id -> dense rank table for persistent launches (decode_kernel.cuh:
+// DecodeCta ctor).  Left null (block index = plan index) if the probe does
+// not see `grid` distinct SMs.
+ffb_status probe_sm_ranks(ffb_model* m) {
+    const int G = m->grid;
+    int32_t* d_ids = nullptr;
+    CUDA_TRY(cudaMalloc(&d_ids, sizeof(int32_t) * G));
+    cudaError_t e = cudaFuncSetAttribute(smid_probe_kernel,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, m->ops->smem);
+    if (e == cudaSuccess) {
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(G);
+        cfg.blockDim = dim3(32);
+        cfg.dynamicSmemBytes = m->ops->smem;
+        cfg.stream = m->stream;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeCooperative;
+        attr[0].val.cooperative = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        e = cudaLaunchKernelEx(&cfg, smid_probe_kernel, d_ids);
+    }
+    std::vector<int32_t> ids(G, -1);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(m->stream);
+    if (e == cudaSuccess)
+        e = cudaMemcpy(ids.data(), d_ids, sizeof(int32_t) * G, cudaMemcpyDeviceToHost);
+    cudaFree(d_ids);
+    if (e != cudaSuccess) return fail(FFB_DEVICE, "SM probe: %s", cudaGetErrorString(e));
+    std::vector<int32_t> sorted = ids;
+    std::sort(sorted.begin(), sorted.end());
+    if (sorted.front() < 0 || std::adjacent_find(sorted.begin(), sorted.end()) != sorted.end())
+        return FFB_OK;  // not one CTA per distinct SM: keep block-index plans
+    std::vector<int16_t> table(sorted.back() + 1, 0);
+    for (int r = 0; r < G; ++r) table[sorted[r]] = static_cast<int16_t>(r);
+    ffb_status st = m->alloc(&m->sm_rank, table.size());
+    if (st) return st;
+    CUDA_TRY(cudaMemcpy(m->sm_rank, table.data(), sizeof(int16_t) * table.size(),
+                        cudaMemcpyHostToDevice));
     return FFB_OK;
 }
 
@@ -312,11 +387,13 @@ DecodeParams make_params(const ffb_model* m, int64_t pos, const int64_t* d_token
     p.debug = m->debug;
     p.trace = m->trace;
     p.l2_prefetch = m->l2_prefetch;
+    p.l2_pf_stages = m->l2_pf_stages;
     p.pool_part = m->pool_part;
     p.pool_counters = m->pool_counters;
     p.pool_t0 = m->pool_t0;
     p.pool_ct = m->pool_ct;
     p.pool_chunks = m->pool_chunks;
+    p.sm_rank = (m->mode == FFB_MODE_BASELINE || !m->use_sm_rank) ? nullptr : m->sm_rank;
     return p;
 }
 
@@ -522,6 +599,8 @@ ffb_status ffb_create(const ffb_model_config* cfg, int64_t max_seq_len, int devi
         return bail(fail(FFB_DEVICE, "cudaMallocHost failed"));
     st = build_plan(m);
     if (st) return bail(st);
+    st = probe_sm_ranks(m);
+    if (st) return bail(st);
     *out = m;
     return FFB_OK;
 }
@@ -681,6 +760,15 @@ ffb_status ffb_set_option(ffb_model* m, const char* key, int64_t value) {
         m->l2_prefetch = value;
         return FFB_OK;
     }
+    if (std::strcmp(key, "sm_rank") == 0) {
+        m->use_sm_rank = value ? 1 : 0;
+        return FFB_OK;
+    }
+    if (std::strcmp(key, "l2_prefetch_stages") == 0) {
+        if (value < 0 || value > 0x3f) return fail(FFB_USAGE, "l2_prefetch_stages is a 6-bit mask");
+        m->l2_pf_stages = static_cast<int32_t>(value);
+        return FFB_OK;
+    }
     if (std::strcmp(key, "plan_reverse") == 0 || std::strcmp(key, "glu_pool_permille") == 0 ||
         std::strcmp(key, "glu_pool_chunk") == 0) {
         if (key[0] == 'p') m->plan_reverse = value ? 1 : 0;
@@ -809,5 +897,91 @@ ffb_status ffb_get_info(const ffb_model* m, ffb_info* out) {
 }
 
 const float* ffb_logits_device(const ffb_model* m) { return m ? m->logits : nullptr; }
+
+ffb_status ffb_calibrate(ffb_model* m, int32_t iterations) {
+    if (!m) return fail(FFB_USAGE, "NULL handle");
+    if (iterations < 0 || iterations > 16) return fail(FFB_USAGE, "iterations in [0, 16]");
+    const auto& c = m->cfg;
+    const int G = m->grid;
+    if (iterations == 0 || c.layers == 0) {  // back to the uniform plan
+        m->sm_weight.assign(G, 1.0);
+    } else {
+        const int64_t pos = m->kv_len[0];
+        for (int64_t l = 0; l < c.layers; ++l)
+            if (m->kv_len[l] != pos)
+                return fail(FFB_VALIDATION, "calibrate: layers have different cache lengths");
+        if (pos >= m->max_seq) return fail(FFB_VALIDATION, "calibrate: cache is full");
+        if (m->sm_rank == nullptr)
+            return fail(FFB_UNSUPPORTED, "calibrate: SM ids unavailable (no per-SM plans)");
+        CUDA_TRY(cudaSetDevice(m->device));
+        uint64_t* saved_trace = m->trace;
+        const ffb_mode saved_mode = m->mode;
+        ffb_status st = ffb_set_trace(m, 1);
+        if (st) return st;
+        m->mode = FFB_MODE_FUSED_OVERLAP;
+        const int S = static_cast<int>(c.layers * kStagesPerLayer + 1);
+        std::vector<uint64_t> tr((size_t)G * S * kTraceSlots);
+        CUDA_TRY(cudaMemsetAsync(m->tokens_dev, 0, sizeof(int64_t) * c.batch, m->stream));
+        for (int iter = 0; iter < iterations && !st; ++iter) {
+            // steps at the current length: they write K/V at `pos` (beyond
+            // the cache length, overwritten by the next real step)
+            for (int rep = 0; rep < 3 && !st; ++rep)
+                st = launch_step(m, pos, m->tokens_dev, nullptr, nullptr, m->stream);
+            if (st) break;
+            CUDA_TRY(cudaStreamSynchronize(m->stream));
+            CUDA_TRY(cudaMemcpy(tr.data(), m->trace, tr.size() * sizeof(uint64_t),
+                                cudaMemcpyDeviceToHost));
+            // per CTA (= SM rank): median over layers of the GLU stage time
+            std::vector<double> t(G, 0.0);
+            for (int i = 0; i < G; ++i) {
+                std::vector<double> v;
+                for (int64_t l = 0; l < c.layers; ++l) {
+                    const uint64_t* r = &tr[((size_t)i * S + l * kStagesPerLayer + S_GLU) * kTraceSlots];
+                    if (r[1] && r[2] > r[1]) v.push_back(static_cast<double>(r[2] - r[1]));
+                }
+                if (v.empty()) { t[i] = 0; continue; }
+                std::nth_element(v.begin(), v.begin() + v.size() / 2, v.end());
+                t[i] = v[v.size() / 2];
+            }
+            double tm = 0;
+            int nt = 0;
+            for (double x : t) if (x > 0) { tm += x; ++nt; }
+            if (nt == 0) break;
+            tm /= nt;
+            // n_i ~ w_i and t_i ~ n_i / rate_i: equal times need w_i ~ w_i tm / t_i
+            double sum = 0;
+            for (int i = 0; i < G; ++i) {
+                if (t[i] > 0) m->sm_weight[i] *= tm / t[i];
+                sum += m->sm_weight[i];
+            }
+            for (int i = 0; i < G; ++i)
+                m->sm_weight[i] = std::min(1.3, std::max(0.7, m->sm_weight[i] * G / sum));
+            st = build_plan(m);
+        }
+        m->mode = saved_mode;
+        m->trace = saved_trace;
+        if (st) return st;
+    }
+    CUDA_TRY(cudaSetDevice(m->device));
+    CUDA_TRY(cudaDeviceSynchronize());
+    ffb_status st = build_plan(m);
+    if (st) return st;
+    st = reset_sync_state(m, m->stream);
+    if (st) return st;
+    CUDA_TRY(cudaStreamSynchronize(m->stream));
+    m->epoch = 0;
+    return FFB_OK;
+}
+
+int64_t ffb_get_plan_weights(const ffb_model* m, double* out, int64_t n) {
+    if (!m) return -1;
+    const int64_t G = m->grid;
+    if (out) {
+        if (n < G) return -1;
+        for (int64_t i = 0; i < G; ++i)
+            out[i] = i < (int64_t)m->sm_weight.size() ? m->sm_weight[i] : 1.0;
+    }
+    return G;
+}
 
 }  // extern "C"

@@ -211,3 +211,35 @@ def test_reference_cpp_drives_kernel_through_bridge():
     r = subprocess.run([exe], capture_output=True, text=True, timeout=300)
     print(r.stdout)
     assert r.returncode == 0, r.stdout + r.stderr
+
+
+def test_calibrated_plan_keeps_parity_and_mode_identity():
+    """ffb_calibrate re-splits every streamed matrix by measured per-SM rates
+    (the reference's calibrate step): weights stay within the
+    clamp, every run mode still agrees bit for bit (the plan, not the launch,
+    fixes the summation order) and the step still matches the oracle."""
+    cfg = O.preset("llama31_8b").replace(layers=2, vocab_size=4096)
+    st = O.OracleStore(cfg, 1234, 260)
+    st.synthetic_prefill(256, 7)
+    with device_from_store(st) as m:
+        m.calibrate(2)
+        w = m.plan_weights()
+        assert len(w) == m.info()["grid"]
+        assert np.all((w >= 0.7 - 1e-9) & (w <= 1.3 + 1e-9)), (w.min(), w.max())
+        assert abs(w.mean() - 1.0) < 0.05
+        outs = []
+        for mode in MODES:
+            m.set_mode(mode)
+            for l in range(cfg.layers):
+                m.set_length(l, 256)
+            outs.append(m.step([17], 256)[0])
+        np.testing.assert_array_equal(outs[0], outs[1])
+        np.testing.assert_array_equal(outs[1], outs[2])
+        for l in range(cfg.layers):
+            m.set_length(l, 256)
+        m.set_mode(RunMode.FUSED_OVERLAP)
+        e_plain, e_strict, flips = check_step(st, m, [17], 256)
+        print(f"calibrated: weights {w.min():.3f}..{w.max():.3f}, rel_err {e_plain:.2e}, "
+              f"same-KV {e_strict:.2e}")
+        m.calibrate(0)
+        assert np.all(m.plan_weights() == 1.0)

@@ -13,11 +13,19 @@ ap.add_argument("--batch", type=int, default=1)
 ap.add_argument("--steps", type=int, default=100)
 ap.add_argument("--sweep", default="", help="comma list of l2_prefetch_bytes")
 ap.add_argument("--ncu", action="store_true", help="few launches, for profiling")
+ap.add_argument("--calibrate", type=int, default=0, help="ffb_calibrate iterations first")
+ap.add_argument("--pf-stages", type=int, default=0x3f, help="l2_prefetch_stages mask for --sweep")
 a = ap.parse_args()
 
 cfg = model_preset(a.model).replace(batch=a.batch)
 m = DecodeModel(cfg, a.ctx + 8)
 m.init_synthetic(1)
+if a.calibrate:
+    for l in range(cfg.layers):
+        m.set_length(l, a.ctx)
+    m.calibrate(a.calibrate)
+    w = m.plan_weights()
+    print(f"calibrated weights: min {w.min():.3f} max {w.max():.3f} std {w.std():.3f}")
 s = torch.cuda.Stream()
 tok = torch.full((a.batch,), 17, dtype=torch.int64, device="cuda")
 kv = a.batch * cfg.layers * cfg.n_kv_heads * 2 * cfg.d_head * 2 * (a.ctx + 1)
@@ -43,6 +51,7 @@ def timeit(name):
 
 if a.sweep:
     m.set_mode(RunMode.FUSED_OVERLAP)
+    m.set_option("l2_prefetch_stages", a.pf_stages)
     for w in [int(x) for x in a.sweep.split(",")]:
         m.set_option("l2_prefetch_bytes", w)
         timeit(f"overlap l2pf={w >> 10}K")

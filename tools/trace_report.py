@@ -18,6 +18,7 @@ ap.add_argument("--ctx", type=int, default=4096)
 ap.add_argument("--batch", type=int, default=1)
 ap.add_argument("--mode", default="fused_overlap")
 ap.add_argument("--reverse", action="store_true", help="plan_reverse option")
+ap.add_argument("--calibrate", type=int, default=0, help="ffb_calibrate iterations first")
 a = ap.parse_args()
 cfg = model_preset(a.model).replace(batch=a.batch)
 m = DecodeModel(cfg, a.ctx + 8, mode={"fused_overlap": RunMode.FUSED_OVERLAP, "fused": RunMode.FUSED,
@@ -25,6 +26,10 @@ m = DecodeModel(cfg, a.ctx + 8, mode={"fused_overlap": RunMode.FUSED_OVERLAP, "f
 m.init_synthetic(1)
 if a.reverse:
     m.set_option("plan_reverse", 1)
+if a.calibrate:
+    for l in range(cfg.layers):
+        m.set_length(l, a.ctx)
+    m.calibrate(a.calibrate)
 m.set_trace(True)
 for _ in range(3):
     for l in range(cfg.layers):
@@ -79,3 +84,18 @@ for s_name, s_idx in (("qkv", 0), ("aout", 2)):
     o = np.argsort(-dr.mean(1))
     print(f"{s_name}: done spread {np.mean(dr.max(0)):.2f} us; slowest ctas {list(o[:6])}; "
           f"corr(done, cta)={np.corrcoef(dr.mean(1), np.arange(len(sm)))[0,1]:.2f}")
+# attention breakdown (slots 5: q staged, 6: ring slots ready, 3: pass done,
+# 7: partial written; 2: combine done, last arriver only)
+att = [s for s in range(S - 1) if s % 5 == 1]
+def seg(a, b, sel=None):
+    v = []
+    for s in att:
+        x = tr[:, s, a].astype(np.int64); y = tr[:, s, b].astype(np.int64)
+        ok = (x > 0) & (y > x)
+        if ok.any():
+            v.append(np.median((y - x)[ok]) / 1e3)
+    return np.mean(v) if v else float("nan")
+print(f"attn: dep->q {seg(1, 5):.2f}  q->ring {seg(5, 6):.2f}  pass {seg(6, 3):.2f}  "
+      f"partial {seg(3, 7):.2f}  combine(last) {seg(7, 2):.2f} us")
+if os.environ.get("PHASES"):
+    print(f"attn phases: ring->A {seg(6, 5):.2f}  A->B {seg(5, 7):.2f}  B->C/end {seg(7, 3):.2f} us")

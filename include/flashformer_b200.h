@@ -74,6 +74,19 @@ typedef struct ffb_model ffb_model;
 const char *ffb_last_error(void);
 const char *ffb_version(void);
 
+/* Host-only weight packer (no device needed).  Row format of a streamed
+ * matrix with `cols` columns: bf16 (quant_bits 0) = cols*2 bytes; int4 / int8
+ * = [codes: int4 two per byte, little nibble first | f32 scale per group of
+ * 128 | u8 zero point per group | zero pad to 16 B].  Returns the bytes per
+ * row, or -1 for an unsupported (cols, quant_bits). */
+int64_t ffb_quant_row_bytes(int64_t cols, int32_t quant_bits);
+/* Packs rows x cols f32 values (quant_bits 4 or 8) into `out`
+ * (rows * ffb_quant_row_bytes bytes), re-deriving the reference's
+ * quantize_group grid (quant.hpp:42-54) per group of 128 columns.  Returns the
+ * number of groups whose values lie on no such grid (packed lossily), or -1. */
+int64_t ffb_pack_quant_rows(const float *values, int64_t rows, int64_t cols,
+                            int32_t quant_bits, uint8_t *out);
+
 /* 1 if a kernel specialisation exists for this shape (no device needed). */
 int ffb_config_supported(const ffb_model_config *cfg);
 
@@ -89,7 +102,13 @@ void ffb_destroy(ffb_model *m);
  * "layer.<l>.norm_ffn", "final_norm", "embedding", "lm_head".  `values` is the
  * TensorStore's row-major f32 array (n = rows*cols).  bf16 matrices are
  * rounded RNE (exact for reference stores, whose values are already on the
- * bf16 grid); norm gains stay f32. */
+ * bf16 grid); norm gains stay f32.  Quantized models (quant_bits 4 or 8,
+ * quant_group 128) pack every streamed matrix (wqkv, waout, wffn1, wffn2t,
+ * lm_head; the embedding stays bf16) into per-row codes + f32 group scales +
+ * zero points, re-deriving the reference's quantize_group grid
+ * (quant.hpp:42-54) so that (code - zero) * scale reproduces reference store
+ * values bit for bit; values off any grid are quantized (lossy, counted in
+ * ffb_info.quant_inexact_groups). */
 ffb_status ffb_upload_tensor(ffb_model *m, const char *name, const float *values, int64_t n);
 
 /* Fills every weight on the device with seeded synthetic values of the right
@@ -158,8 +177,11 @@ typedef struct ffb_info {
     int32_t attn_group;      /* CTAs per (batch row, kv head)              */
     int32_t launches_per_step; /* 1 (fused) or 5*L+1 (baseline)            */
     int32_t mode;
-    uint64_t weight_bytes;   /* streamed weight bytes per step             */
+    uint64_t weight_bytes;   /* streamed weight bytes per step (device format) */
     uint64_t device_bytes;   /* total device allocation                    */
+    uint64_t quant_inexact_groups; /* packer: groups not on a 4/8-bit grid  */
+    int32_t row_bytes;       /* bytes per streamed-matrix row              */
+    int32_t pad_;
 } ffb_info;
 ffb_status ffb_get_info(const ffb_model *m, ffb_info *out);
 

@@ -26,7 +26,7 @@ import numpy as np
 __all__ = [
     "ModelConfig", "RunMode", "DecodeModel", "ValidationError", "DeviceError",
     "UnsupportedConfigError", "UsageError", "PRESETS", "model_preset", "lib", "LIB_PATH",
-    "tensor_names",
+    "tensor_names", "pack_quant_rows", "unpack_quant_rows",
 ]
 
 HERE = os.path.dirname(os.path.abspath(__file__))
@@ -79,6 +79,7 @@ class _Info(C.Structure):
         ("ring_slots", C.c_int32), ("slot_bytes", C.c_int32), ("attn_group", C.c_int32),
         ("launches_per_step", C.c_int32), ("mode", C.c_int32),
         ("weight_bytes", C.c_uint64), ("device_bytes", C.c_uint64),
+        ("quant_inexact_groups", C.c_uint64), ("row_bytes", C.c_int32), ("pad_", C.c_int32),
     ]
 
 
@@ -149,6 +150,40 @@ def model_preset(name: str) -> ModelConfig:
     return PRESETS[name]
 
 
+def pack_quant_rows(values: np.ndarray, quant_bits: int) -> tuple[np.ndarray, int]:
+    """Host weight packer (ffb_pack_quant_rows): f32 [rows][cols] -> device
+    row format bytes [rows][row_bytes], plus the count of groups that lie on
+    no int4/int8 grid (packed lossily)."""
+    v = np.ascontiguousarray(values, np.float32)
+    rows, cols = v.shape
+    rb = lib().ffb_quant_row_bytes(cols, quant_bits)
+    if rb < 0:
+        raise UsageError(f"unsupported quant row: cols={cols} bits={quant_bits}")
+    out = np.zeros((rows, rb), np.uint8)
+    n = lib().ffb_pack_quant_rows(_fp(v), rows, cols, quant_bits,
+                                  out.ctypes.data_as(C.POINTER(C.c_uint8)))
+    if n < 0:
+        raise UsageError(lib().ffb_last_error().decode())
+    return out, int(n)
+
+
+def unpack_quant_rows(packed: np.ndarray, cols: int, quant_bits: int) -> np.ndarray:
+    """Inverse of pack_quant_rows: (code - zero) * scale in f32 (quant.hpp:23-25)."""
+    ng = cols // 128
+    cb = cols // 2 if quant_bits == 4 else cols
+    codes = packed[:, :cb]
+    if quant_bits == 4:
+        c = np.empty((packed.shape[0], cols), np.uint8)
+        c[:, 0::2] = codes & 0xF
+        c[:, 1::2] = codes >> 4
+    else:
+        c = codes.copy()
+    scale = packed[:, cb:cb + 4 * ng].copy().view(np.float32)
+    zero = packed[:, cb + 4 * ng:cb + 5 * ng].astype(np.float32)
+    g = np.arange(cols) // 128
+    return ((c.astype(np.float32) - zero[:, g]) * scale[:, g]).astype(np.float32)
+
+
 def tensor_names(cfg: ModelConfig) -> list[str]:
     """Reference tensor names (tensor_store.hpp:344-363) in upload order."""
     names = []
@@ -197,6 +232,11 @@ def lib():
     L.ffb_get_info.argtypes = [C.c_void_p, P(_Info)]
     L.ffb_logits_device.argtypes = [C.c_void_p]
     L.ffb_logits_device.restype = C.c_void_p
+    L.ffb_quant_row_bytes.argtypes = [C.c_int64, C.c_int32]
+    L.ffb_quant_row_bytes.restype = C.c_int64
+    L.ffb_pack_quant_rows.argtypes = [P(C.c_float), C.c_int64, C.c_int64, C.c_int32,
+                                      P(C.c_uint8)]
+    L.ffb_pack_quant_rows.restype = C.c_int64
     L.ffb_calibrate.argtypes = [C.c_void_p, C.c_int32]
     L.ffb_get_plan_weights.argtypes = [C.c_void_p, P(C.c_double), C.c_int64]
     L.ffb_get_plan_weights.restype = C.c_int64

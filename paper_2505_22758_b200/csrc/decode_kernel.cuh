@@ -69,16 +69,17 @@ struct CtaPlan {
 };
 
 struct DecodeParams {
-    // weights, bf16 row-major [out][in] exactly as the reference's Matrix
-    const __nv_bfloat16* wqkv;    // [L][QKVR][D]
-    const __nv_bfloat16* waout;   // [L][D][D]
-    const __nv_bfloat16* wffn1;   // [L][2*DI][D]   rows interleaved in/gate
-    const __nv_bfloat16* wffn2t;  // [L][DI][D]     W2 stored transposed
+    // streamed weights, rows [out] of weight_row_bytes(D, QB) bytes each, in
+    // the reference's Matrix row order (bf16 or packed int4/int8 rows)
+    const uint8_t* wqkv;    // [L][QKVR] rows
+    const uint8_t* waout;   // [L][D] rows
+    const uint8_t* wffn1;   // [L][2*DI] rows, interleaved in/gate
+    const uint8_t* wffn2t;  // [L][DI] rows, W2 stored transposed
     const float* norm_attn;       // [L][D]  f32 gains (not rounded, tensor_store.hpp:293)
     const float* norm_ffn;        // [L][D]
     const float* final_norm;      // [D]
-    const __nv_bfloat16* embedding;  // [V][D]
-    const __nv_bfloat16* lm_head;    // [V][D]
+    const __nv_bfloat16* embedding;  // [V][D] bf16 (never quantized)
+    const uint8_t* lm_head;          // [V] rows
     __nv_bfloat16* kcache;        // [L][B][NKV][S][DH] position-major per (l, b, head)
     __nv_bfloat16* vcache;
     // activations / scratch (f32)
@@ -122,42 +123,83 @@ struct DecodeParams {
     double rope_theta;
 };
 
-template <int D_, int DI_, int DH_, int NQ_, int NKV_, int B_>
+// Weight storage formats of the streamed matrices (Wqkv, Waout, Wffn1,
+// Wffn2^T, lm_head; the embedding is always bf16, tensor_store.hpp:356-361):
+//   QB = 0   bf16 row-major [out][in]
+//   QB = 4   the reference's weight-only int4 affine scheme (quant.hpp:17-60),
+//            groups of 128 along the row: per row [codes: 2 per byte, little
+//            nibble first][f32 scale x NG][u8 zero point x NG][pad to 16 B]
+//   QB = 8   the same with 8-bit codes (255 levels; the int8 extension)
+// The f32 scale and integer zero point make (c - z) * s bit-identical to the
+// reference's dequantized f32 weights (the packer re-derives them exactly).
+constexpr int kQuantGroup = 128;
+
+template <int D_, int DI_, int DH_, int NQ_, int NKV_, int B_, int QB_ = 0>
 struct Shape {
-    static constexpr int D = D_, DI = DI_, DH = DH_, NQ = NQ_, NKV = NKV_, B = B_;
+    static constexpr int D = D_, DI = DI_, DH = DH_, NQ = NQ_, NKV = NKV_, B = B_, QB = QB_;
     static constexpr int QPG = NQ / NKV;
     static constexpr int QKVR = (NQ + 2 * NKV) * DH;
     static_assert(D == NQ * DH, "d_model must equal n_q_heads * d_head");
     static_assert(NQ % NKV == 0, "GQA grouping");
+    static_assert(QB == 0 || QB == 4 || QB == 8, "weight format");
+    static_assert(QB == 0 || D % kQuantGroup == 0, "quant groups tile the row");
 };
+
+// bytes of one streamed-matrix row of `cols` columns in format qb
+__host__ __device__ constexpr int weight_row_bytes(int cols, int qb) {
+    return qb == 0 ? cols * 2
+                   : ((qb == 4 ? cols / 2 : cols) + 5 * (cols / kQuantGroup) + 15) / 16 * 16;
+}
 
 template <class S>
 struct KTraits {
     static constexpr int NCW = 8;                   // consumer warps
     static constexpr int NCT = NCW * 32;            // consumer threads
-    static constexpr int NTHREADS = NCT + 32;       // + producer warp
-    static constexpr int SLOT_BYTES = 32768;
-    // GEMV mapping: a row of D bf16 = NV 16-byte vectors split over TPR threads
+    // + a producer warpgroup (one active lane): with 12 warps the warpgroups
+    // rebalance registers (setmaxnreg) -- the producer gives its registers to
+    // the two consumer warpgroups (9 warps would cap everyone at 168)
+    static constexpr int NTHREADS = NCT + 128;
+    static constexpr int PRODUCER_REGS = 56;
+    static constexpr int CONSUMER_REGS = 224;  // 4*32*56 + 8*32*224 <= 64K
+    static constexpr int QB = S::QB;
+    static constexpr int NG = S::D / kQuantGroup;   // quant groups per row
+    static constexpr int CODE_BYTES = QB == 4 ? S::D / 2 : S::D;
+    static constexpr int ROW_BYTES = weight_row_bytes(S::D, QB);
+    static constexpr int cmin(int a, int b) { return a < b ? a : b; }
+    static constexpr int cmax(int a, int b) { return a > b ? a : b; }
+    // GEMV mapping.  bf16: a row of D = NV 16-byte vectors, thread lt of a
+    // row takes vectors lt, lt + TPR, ... (CPT = 8 VPT columns, strided).
+    // quant: thread lt takes CPT contiguous columns (one quant group), so
+    // one (scale, zero) per row and thread.
     static constexpr int NV = S::D / 8;
-    static constexpr int TPR = NV < NCT ? NV : NCT;
-    static constexpr int VPT = NV / TPR;            // vectors per thread per row
+    static constexpr int CPT = QB == 0 ? 8 * (NV / cmin(NV, NCT))
+                                       : cmin(cmin(32, S::D / 32), 64 / S::B);
+    static constexpr int NCH = CPT / 8;             // 8-column chunks per thread per row
+    static constexpr int VPT = NCH;
+    static constexpr int TPR = S::D / CPT;          // threads per row
     static constexpr int RG = NCT / TPR;            // row groups working in parallel
     static constexpr int WPR = TPR / 32;            // warps per row
-    static constexpr int ROW_BYTES = S::D * 2;
-    static constexpr int RPS = SLOT_BYTES / ROW_BYTES;  // rows per slot
-    static constexpr int RPT = RPS / RG;            // rows per thread per slot
+    static constexpr int pow2_le(int v) { return v >= 32 ? 32 : v >= 16 ? 16 : v >= 8 ? 8 : v >= 4 ? 4 : v >= 2 ? 2 : 1; }
+    // rows per thread per slot: bf16 fills a 32 KiB slot; quant takes the
+    // largest power of two with RPT * B <= 32 and a slot <= 32 KiB
+    static constexpr int RPT = QB == 0 ? (32768 / ROW_BYTES) / RG
+                                       : cmax(2 / RG, cmin(pow2_le(32 / S::B),
+                                                           pow2_le(cmax(1, 32768 / (RG * ROW_BYTES)))));
+    static constexpr int RPS = RG * RPT;            // rows per slot
+    static constexpr int SLOT_BYTES = QB == 0 ? 32768 : (RPS * ROW_BYTES + 127) / 128 * 128;
     // rows per epilogue batch (whole slots; >= 64/B rows so barriers are rare)
     static constexpr int RB = RPS > 64 / S::B ? RPS : ((64 / S::B) / RPS) * RPS;
     static constexpr int KVC = SLOT_BYTES / (2 * S::DH * 2);  // KV positions per slot
     static constexpr int DPL = S::DH / 32;          // attention dims per lane
     static constexpr int TMAX = 160;                // max GLU pairs per CTA (host-checked)
-    static_assert(TPR % 32 == 0, "a row must span whole warps");
-    static_assert(NV % TPR == 0 && NCT % TPR == 0, "row mapping");
+    static_assert(TPR % 32 == 0 && TPR <= NCT && NCT % TPR == 0, "a row must span whole warps");
+    static_assert(S::D % CPT == 0 && CPT % 8 == 0, "row mapping");
+    static_assert(QB == 0 || kQuantGroup % CPT == 0, "a thread's columns lie in one group");
     static_assert(RPS >= 2 && RPS % 2 == 0 && RPS % RG == 0, "slot rows");
     static_assert(RPS * S::B <= NCT && RB * S::B <= NCT, "epilogue threads");
-    static_assert(RPT * S::B <= 32, "one transposed warp reduction per slot");
+    static_assert(RPT * S::B <= 32 && (RPT & (RPT - 1)) == 0, "one transposed warp reduction per slot");
     static_assert(S::DH % 32 == 0 && DPL <= 8, "attention lane split");
-    static_assert(KVC >= 1, "kv chunk");
+    static_assert(KVC >= 1 && (SLOT_BYTES / 2) % 16 == 0, "kv chunk");
 
     // ---- shared memory carve-up (bytes) ----
     static constexpr int OFF_RED = 0;  // [2][WPR][RPS][B] f32
@@ -172,11 +214,11 @@ struct KTraits {
     // also reused for: attention combine (3*G*QPG), argmax candidates
     // (2*grid*B) and the GLU reduction (NCW*32); grid <= kMaxGrid
     static constexpr int kMaxGrid = 160;
-    static constexpr int cmax(int a, int b) { return a > b ? a : b; }
-    // attention: ring slots consumed together in one softmax pass, positions
-    // per pass (+1 for the current token, rounded to 4) and its scratch:
-    // alpha*q [QPG][DH], scores [QPG][ANP], probabilities [ANP][QPG], stats
-    static constexpr int ATT_SC = 4;
+    // attention: ring slots consumed together in one softmax pass (~128 KiB
+    // of K/V), positions per pass (+1 for the current token, rounded to 4)
+    // and its scratch: alpha*q [QPG][DH], scores [QPG][ANP], probabilities
+    // [ANP][QPG], stats
+    static constexpr int ATT_SC = cmax(1, 131072 / SLOT_BYTES);
     static constexpr int ANP = ((ATT_SC * KVC + 1) + 3) / 4 * 4;
     static constexpr int SZ_ATT = S::QPG * S::DH + 2 * S::QPG * ANP + 4 * S::QPG;
     static constexpr int SZ_WPART =
@@ -190,7 +232,7 @@ struct KTraits {
     static constexpr int FIXED = ((OFF_MISC + SZ_MISC + 1023) / 1024) * 1024;
     static constexpr int MAX_SMEM = 227 * 1024;
     static constexpr int NSLOTS_RAW = (MAX_SMEM - FIXED - 256) / SLOT_BYTES;
-    static constexpr int NSLOTS = NSLOTS_RAW > 8 ? 8 : NSLOTS_RAW;
+    static constexpr int NSLOTS = NSLOTS_RAW > 16 ? 16 : NSLOTS_RAW;
     static_assert(NSLOTS >= 2, "ring too small");
     static_assert(NSLOTS >= ATT_SC + 1, "attention pass must leave a slot for streaming");
     static constexpr int OFF_BARS = FIXED;  // full[NSLOTS], empty[NSLOTS]
@@ -318,7 +360,7 @@ struct DecodeCta {
     // One list of the static per-CTA stream: rows [r0, r1) of a matrix (kv =
     // false) or KV positions [r0, r1) of one (layer, batch row, kv head).
     struct List {
-        const __nv_bfloat16* base;
+        const uint8_t* base;  // matrix rows, or K rows (kv) of one (l, b, head)
         int r0, r1;
         bool kv;
         bool pool;  // the GLU work pool: one marker chunk, claimed dynamically
@@ -335,26 +377,28 @@ struct DecodeCta {
         switch (s) {
             case S_QKV:
                 if (sub > 0) return false;
-                L = {p.wqkv + (size_t)l * S::QKVR * D, pl.qkv_r0, pl.qkv_r1, false, false};
+                L = {p.wqkv + (size_t)l * S::QKVR * T::ROW_BYTES, pl.qkv_r0, pl.qkv_r1, false,
+                     false};
                 return true;
             case S_ATTN: {
                 if (sub > 0 || pl.attn_unit < 0) return false;
                 int p0, p1;
                 attn_range(p0, p1);
                 const int unit = pl.attn_unit;
-                L = {p.kcache + kv_row(l, unit / S::NKV, unit % S::NKV, 0), p0, min(p1, p.pos),
-                     true, false};
+                L = {reinterpret_cast<const uint8_t*>(p.kcache + kv_row(l, unit / S::NKV,
+                                                                        unit % S::NKV, 0)),
+                     p0, min(p1, p.pos), true, false};
                 return true;
             }
             case S_AOUT:
                 if (sub > 0) return false;
-                L = {p.waout + (size_t)l * D * D, pl.aout_r0, pl.aout_r1, false, false};
+                L = {p.waout + (size_t)l * D * T::ROW_BYTES, pl.aout_r0, pl.aout_r1, false, false};
                 return true;
             case S_GLU:
-                if (sub == 0) L = {p.wffn1 + (size_t)l * 2 * S::DI * D, 2 * pl.glu_t0,
+                if (sub == 0) L = {p.wffn1 + (size_t)l * 2 * S::DI * T::ROW_BYTES, 2 * pl.glu_t0,
                                    2 * pl.glu_t1, false, false};
-                else if (sub == 1) L = {p.wffn2t + (size_t)l * S::DI * D, pl.glu_t0, pl.glu_t1,
-                                        false, false};
+                else if (sub == 1) L = {p.wffn2t + (size_t)l * S::DI * T::ROW_BYTES, pl.glu_t0,
+                                        pl.glu_t1, false, false};
                 else if (sub == 2 && p.pool_chunks > 0) L = {nullptr, 0, 1, false, true};
                 else return false;
                 return true;
@@ -403,14 +447,15 @@ struct DecodeCta {
                 c.c0 = c.L.r1;
             } else if (c.L.kv) {
                 const int n = min(T::KVC, c.L.r1 - c.c0);
-                const size_t off = (size_t)c.c0 * DH;
+                const size_t off = (size_t)c.c0 * DH * 2;
                 *src0 = c.L.base + off;
-                *src1 = p.vcache + (c.L.base - p.kcache) + off;
+                *src1 = reinterpret_cast<const uint8_t*>(p.vcache) +
+                        (c.L.base - reinterpret_cast<const uint8_t*>(p.kcache)) + off;
                 *bytes = static_cast<uint32_t>(n) * DH * 2;
                 c.c0 += T::KVC;
             } else {
                 const int n = min(T::RPS, c.L.r1 - c.c0);
-                *src0 = c.L.base + (size_t)c.c0 * D;
+                *src0 = c.L.base + (size_t)c.c0 * T::ROW_BYTES;
                 *src1 = nullptr;
                 *bytes = static_cast<uint32_t>(n) * T::ROW_BYTES;
                 c.c0 += T::RPS;
@@ -433,7 +478,7 @@ struct DecodeCta {
         return (2 * p.pool_ct + T::RPS - 1) / T::RPS + (p.pool_ct + T::RPS - 1) / T::RPS;
     }
 
-    __device__ void pool_stream(uint32_t& it, const __nv_bfloat16* base, int r0, int r1, int ch,
+    __device__ void pool_stream(uint32_t& it, const uint8_t* base, int r0, int r1, int ch,
                                 uint64_t policy) {
         for (int c0 = r0; c0 < r1; c0 += T::RPS) {
             const uint32_t slot = it % T::NSLOTS, ph = (it / T::NSLOTS) & 1;
@@ -441,7 +486,7 @@ struct DecodeCta {
             slot_meta()[slot] = ch;
             const uint32_t bytes = static_cast<uint32_t>(min(T::RPS, r1 - c0)) * T::ROW_BYTES;
             mbar_arrive_expect_tx(&full[slot], bytes);
-            tma_load_1d(ring + slot * T::SLOT_BYTES, base + (size_t)c0 * D, bytes, &full[slot],
+            tma_load_1d(ring + slot * T::SLOT_BYTES, base + (size_t)c0 * T::ROW_BYTES, bytes, &full[slot],
                         policy);
             ++it;
         }
@@ -482,8 +527,9 @@ struct DecodeCta {
             const int ch = static_cast<int>(claim);
             claim = atomicAdd(ctr, 1u) - base;  // next claim in flight while streaming
             const int t0c = p.pool_t0 + ch * p.pool_ct, t1c = t0c + p.pool_ct;
-            pool_stream(it, p.wffn1 + (size_t)l * 2 * S::DI * D, 2 * t0c, 2 * t1c, ch, policy);
-            pool_stream(it, p.wffn2t + (size_t)l * S::DI * D, t0c, t1c, ch, policy);
+            pool_stream(it, p.wffn1 + (size_t)l * 2 * S::DI * T::ROW_BYTES, 2 * t0c, 2 * t1c, ch,
+                        policy);
+            pool_stream(it, p.wffn2t + (size_t)l * S::DI * T::ROW_BYTES, t0c, t1c, ch, policy);
         }
     }
 
@@ -635,19 +681,41 @@ struct DecodeCta {
         trace_ring_wait(stage);
     }
 
-    // Load this thread's activation slice: act[b][j][e] = column (lt + j*TPR)*8 + e.
-    // src_emb: layer-0 input taken straight from the embedding (bf16 row per b).
-    // gain != nullptr -> RMSNorm with that f32 gain (numerics.hpp:14-24).
-    // The gains are constants and are fetched before the dependency wait for
-    // `stage`; only the activations wait.
-    __device__ void load_act(float (&act)[B][T::VPT][8], const float* src, bool from_emb,
-                             const float* gain, int stage) {
+    // This thread's activation slice of one GEMV stage: v[b][ci][e] = column
+    // col_of(lt, ci) + e.  Quant formats also keep sum[b] = the sum of the
+    // thread's (unscaled) activations -- the zero-point term of
+    // s * sum_i (c_i - z) a_i = s * (sum_i c_i a_i - z * sum[b]) -- and, for
+    // int4, pre-scale column e by q4_scale(e), the inverse of the power of
+    // 16 at which the nibble decode (q4_decode) leaves code e.
+    struct Act {
+        float v[B][T::NCH][8];
+        float sum[B];
+    };
+
+    __device__ static int col_of(int lt, int ci) {
+        return T::QB ? lt * T::CPT + ci * 8 : (lt + ci * T::TPR) * 8;
+    }
+
+    // int4 nibble e of a 32-bit code word is decoded in place as c * 16^k(e):
+    // e = 0..4 by masking bits 4e..4e+3, e = 5..7 from the word >> 20
+    __device__ static constexpr float q4_scale(int e) {
+        return e == 0 || e == 5 ? 1.f
+               : e == 1 || e == 6 ? 0.0625f
+               : e == 2 || e == 7 ? 0.00390625f
+               : e == 3 ? 0.000244140625f : 0.0000152587890625f;
+    }
+
+    // Load the activations (RMSNorm'd with `gain` when given,
+    // numerics.hpp:14-24).  src_emb: layer-0 input straight from the bf16
+    // embedding.  Gains are constants, fetched before the dependency wait.
+    __device__ void load_act(Act& act, const float* src, bool from_emb, const float* gain,
+                             int stage) {
         const int ctid = threadIdx.x, lt = ctid % T::TPR, rg = ctid / T::TPR;
-        float g[T::VPT][8];
+        float g[T::NCH][8];
         if (gain != nullptr) {
 #pragma unroll
-            for (int j = 0; j < T::VPT; ++j) {
-                const int col = (lt + j * T::TPR) * 8;
+            for (int j = 0; j < T::NCH; ++j) {
+                const int col = col_of(lt, j);
                 const float4 g0 = __ldg(reinterpret_cast<const float4*>(gain + col));
                 const float4 g1 = __ldg(reinterpret_cast<const float4*>(gain + col + 4));
                 g[j][0] = g0.x; g[j][1] = g0.y; g[j][2] = g0.z; g[j][3] = g0.w;
@@ -658,57 +726,144 @@ struct DecodeCta {
 #pragma unroll
         for (int b = 0; b < B; ++b) {
 #pragma unroll
-            for (int j = 0; j < T::VPT; ++j) {
-                const int col = (lt + j * T::TPR) * 8;
+            for (int j = 0; j < T::NCH; ++j) {
+                const int col = col_of(lt, j);
+                float* a = act.v[b][j];
                 if (from_emb) {
                     const __nv_bfloat16* e = p.embedding + (size_t)p.tokens[b] * D + col;
                     const uint4 w = __ldg(reinterpret_cast<const uint4*>(e));
-                    act[b][j][0] = bf_lo(w.x); act[b][j][1] = bf_hi(w.x);
-                    act[b][j][2] = bf_lo(w.y); act[b][j][3] = bf_hi(w.y);
-                    act[b][j][4] = bf_lo(w.z); act[b][j][5] = bf_hi(w.z);
-                    act[b][j][6] = bf_lo(w.w); act[b][j][7] = bf_hi(w.w);
+                    a[0] = bf_lo(w.x); a[1] = bf_hi(w.x); a[2] = bf_lo(w.y); a[3] = bf_hi(w.y);
+                    a[4] = bf_lo(w.z); a[5] = bf_hi(w.z); a[6] = bf_lo(w.w); a[7] = bf_hi(w.w);
                 } else {
                     const float4 a0 = ldcg_f4(src + (size_t)b * D + col);
                     const float4 a1 = ldcg_f4(src + (size_t)b * D + col + 4);
-                    act[b][j][0] = a0.x; act[b][j][1] = a0.y; act[b][j][2] = a0.z;
-                    act[b][j][3] = a0.w; act[b][j][4] = a1.x; act[b][j][5] = a1.y;
-                    act[b][j][6] = a1.z; act[b][j][7] = a1.w;
+                    a[0] = a0.x; a[1] = a0.y; a[2] = a0.z; a[3] = a0.w;
+                    a[4] = a1.x; a[5] = a1.y; a[6] = a1.z; a[7] = a1.w;
                 }
             }
         }
-        if (gain == nullptr) return;
-        float ss[B];
+        if (gain != nullptr) {
+            float ss[B];
 #pragma unroll
-        for (int b = 0; b < B; ++b) {
-            float s = 0.f;
-            if (rg == 0) {
+            for (int b = 0; b < B; ++b) {
+                float s = 0.f;
+                if (rg == 0) {
 #pragma unroll
-                for (int j = 0; j < T::VPT; ++j)
+                    for (int j = 0; j < T::NCH; ++j)
 #pragma unroll
-                    for (int e = 0; e < 8; ++e) s = fmaf(act[b][j][e], act[b][j][e], s);
+                        for (int e = 0; e < 8; ++e) s = fmaf(act.v[b][j][e], act.v[b][j][e], s);
+                }
+                ss[b] = warp_sum(s);
             }
-            ss[b] = warp_sum(s);
+            float* ns = norm_s();
+            const int warp = ctid / 32, lane = ctid % 32;
+            if (lane == 0)
+#pragma unroll
+                for (int b = 0; b < B; ++b) ns[warp * B + b] = ss[b];
+            consumer_sync(NCT);
+            float inv[B];
+#pragma unroll
+            for (int b = 0; b < B; ++b) {
+                float t = 0.f;
+                for (int w = 0; w < NCW; ++w) t += ns[w * B + b];
+                inv[b] = 1.0f / sqrtf(t / static_cast<float>(D) + p.eps);
+            }
+            consumer_sync(NCT);  // ns reusable afterwards
+#pragma unroll
+            for (int j = 0; j < T::NCH; ++j)
+#pragma unroll
+                for (int b = 0; b < B; ++b)
+#pragma unroll
+                    for (int e = 0; e < 8; ++e) act.v[b][j][e] = g[j][e] * act.v[b][j][e] * inv[b];
         }
-        float* ns = norm_s();
-        const int warp = ctid / 32, lane = ctid % 32;
-        if (lane == 0)
+        if constexpr (T::QB != 0) {
 #pragma unroll
-            for (int b = 0; b < B; ++b) ns[warp * B + b] = ss[b];
-        consumer_sync(NCT);
-        float inv[B];
+            for (int b = 0; b < B; ++b) {
+                float t = 0.f;
 #pragma unroll
-        for (int b = 0; b < B; ++b) {
-            float t = 0.f;
-            for (int w = 0; w < NCW; ++w) t += ns[w * B + b];
-            inv[b] = 1.0f / sqrtf(t / static_cast<float>(D) + p.eps);
+                for (int j = 0; j < T::NCH; ++j)
+#pragma unroll
+                    for (int e = 0; e < 8; ++e) {
+                        t += act.v[b][j][e];
+                        if constexpr (T::QB == 4) act.v[b][j][e] *= q4_scale(e);
+                    }
+                act.sum[b] = t;
+            }
         }
-        consumer_sync(NCT);  // ns reusable afterwards
+    }
+
+    // ---- quantized row decode (fused dequant) -------------------------
+    // Codes become exact f32 integers with the 2^23 magic: OR the code into
+    // the mantissa of 2^23, subtract 2^23 (packed FADD2).  int4: 8 nibbles
+    // of a word -> c * 16^k (see q4_scale); int8: PRMT one byte per value.
+    // (w & mask) | magic in ONE LOP3 (magic in a register; the compiler
+    // otherwise splits the two immediates into two LOP3s)
+    template <uint32_t MASK>
+    __device__ static float q4_nib(uint32_t w, uint32_t magic) {
+        uint32_t r;
+        asm("lop3.b32 %0, %1, %2, %3, 0xEA;" : "=r"(r) : "r"(w), "n"(MASK), "r"(magic));
+        return __uint_as_float(r);
+    }
+
+    __device__ static void q4_decode(uint32_t w, float2 (&d)[4]) {
+        const uint32_t M = 0x4B000000u;
+        const float2 m2 = make_float2(-8388608.f, -8388608.f);
+        const uint32_t h = w >> 20;
+        d[0] = __fadd2_rn(make_float2(q4_nib<0xFu>(w, M), q4_nib<0xF0u>(w, M)), m2);
+        d[1] = __fadd2_rn(make_float2(q4_nib<0xF00u>(w, M), q4_nib<0xF000u>(w, M)), m2);
+        d[2] = __fadd2_rn(make_float2(q4_nib<0xF0000u>(w, M), q4_nib<0xFu>(h, M)), m2);
+        d[3] = __fadd2_rn(make_float2(q4_nib<0xF0u>(h, M), q4_nib<0xF00u>(h, M)), m2);
+    }
+
+    __device__ static void q8_decode(uint32_t w, float2 (&d)[2]) {
+        const float2 m2 = make_float2(-8388608.f, -8388608.f);
+        d[0] = __fadd2_rn(make_float2(__uint_as_float(__byte_perm(w, 0x4B000000u, 0x7440)),
+                                      __uint_as_float(__byte_perm(w, 0x4B000000u, 0x7441))), m2);
+        d[1] = __fadd2_rn(make_float2(__uint_as_float(__byte_perm(w, 0x4B000000u, 0x7442)),
+                                      __uint_as_float(__byte_perm(w, 0x4B000000u, 0x7443))), m2);
+    }
+
+    // This thread's codes of one quantized row (NCH chunks of 8 columns),
+    // its group's scale and zero point.
+    struct QRow {
+        uint32_t w[T::QB == 4 ? T::NCH : 2 * T::NCH];
+        float scale, zero;
+    };
+
+    __device__ static void q_load(const uint8_t* rowp, int lt, QRow& q) {
+        constexpr int NW = T::QB == 4 ? T::NCH : 2 * T::NCH;  // 32-bit code words
+        const uint8_t* cp = rowp + lt * (NW * 4);
+        if constexpr (NW == 4) {
+            const uint4 v = lds_u128(cp);
+            q.w[0] = v.x; q.w[1] = v.y; q.w[2] = v.z; q.w[3] = v.w;
+        } else if constexpr (NW == 2) {
+            const uint2 v = lds_u64(cp);
+            q.w[0] = v.x; q.w[1] = v.y;
+        } else if constexpr (NW == 1) {
+            q.w[0] = lds_u32(cp);
+        } else {
 #pragma unroll
-        for (int j = 0; j < T::VPT; ++j)
-#pragma unroll
-            for (int b = 0; b < B; ++b)
-#pragma unroll
-                for (int e = 0; e < 8; ++e) act[b][j][e] = g[j][e] * act[b][j][e] * inv[b];
+            for (int i = 0; i < NW; i += 4) {
+                const uint4 v = lds_u128(cp + 4 * i);
+                q.w[i] = v.x; q.w[i + 1] = v.y; q.w[i + 2] = v.z; q.w[i + 3] = v.w;
+            }
+        }
+        const int g = (lt * T::CPT) / kQuantGroup;
+        q.scale = *reinterpret_cast<const float*>(rowp + T::CODE_BYTES + 4 * g);
+        q.zero = static_cast<float>(rowp[T::CODE_BYTES + 4 * T::NG + g]);
+    }
+
+    // decoded 8-column chunk ci of a quantized row: d[k] = columns (2k, 2k+1)
+    // as exact f32 integers (int4: times the powers of 16 of q4_scale)
+    __device__ static void q_chunk(const QRow& q, int ci, float2 (&d)[4]) {
+        if constexpr (T::QB == 4) {
+            q4_decode(q.w[ci], d);
+        } else {
+            float2 lo[2], hi[2];
+            q8_decode(q.w[2 * ci], lo);
+            q8_decode(q.w[2 * ci + 1], hi);
+            d[0] = lo[0]; d[1] = lo[1]; d[2] = hi[0]; d[3] = hi[1];
+        }
     }
 
     __device__ static float dot8(const uint4 w, const float (&a)[8], float acc) {
@@ -777,8 +932,7 @@ struct DecodeCta {
     // rows; `epi(c0, nrows, red)` runs once per batch after one named barrier
     // (red is double-buffered across batches).
     template <class Epi>
-    __device__ void gemv(uint32_t& it, const float (&act)[B][T::VPT][8], int r0, int r1,
-                         Epi&& epi) {
+    __device__ void gemv(uint32_t& it, const Act& act, int r0, int r1, Epi&& epi) {
         constexpr int V = T::RPT * B, LV = ilog2(V);
         const int ctid = threadIdx.x, lane = ctid % 32;
         const int rg = ctid / T::TPR, lt = ctid % T::TPR, wr = lt / 32;
@@ -797,6 +951,35 @@ struct DecodeCta {
             for (int r = 0; r < T::RPT; ++r) {
                 // rows past nrows read stale (valid) smem; their sums are dropped
                 const uint8_t* rowp = base + (rg + r * T::RG) * T::ROW_BYTES;
+                if constexpr (T::QB != 0) {  // fused dequant: s * (sum c a - z sum a)
+                    QRow q;
+                    q_load(rowp, lt, q);
+                    float2 acc[B][4];  // 4 independent FFMA2 chains per batch row
+#pragma unroll
+                    for (int b = 0; b < B; ++b)
+#pragma unroll
+                        for (int k = 0; k < 4; ++k) acc[b][k] = make_float2(0.f, 0.f);
+#pragma unroll
+                    for (int j = 0; j < T::NCH; ++j) {
+                        float2 d[4];
+                        q_chunk(q, j, d);
+#pragma unroll
+                        for (int b = 0; b < B; ++b) {
+                            const float* a = act.v[b][j];
+#pragma unroll
+                            for (int k = 0; k < 4; ++k)
+                                acc[b][k] = __ffma2_rn(d[k], make_float2(a[2 * k], a[2 * k + 1]),
+                                                       acc[b][k]);
+                        }
+                    }
+#pragma unroll
+                    for (int b = 0; b < B; ++b) {
+                        const float2 t = __fadd2_rn(__fadd2_rn(acc[b][0], acc[b][1]),
+                                                    __fadd2_rn(acc[b][2], acc[b][3]));
+                        v[r * B + b] = q.scale * ((t.x + t.y) - q.zero * act.sum[b]);
+                    }
+                    continue;
+                }
                 float a0[B], a1[B];
 #pragma unroll
                 for (int b = 0; b < B; ++b) a0[b] = a1[b] = 0.f;
@@ -805,7 +988,7 @@ struct DecodeCta {
                     const uint4 w = lds_u128(rowp + (lt + j * T::TPR) * 16);
 #pragma unroll
                     for (int b = 0; b < B; ++b) {
-                        const float(&a)[8] = act[b][j];
+                        const float(&a)[8] = act.v[b][j];
                         a0[b] = fmaf(bf_lo(w.x), a[0], a0[b]);
                         a1[b] = fmaf(bf_hi(w.x), a[1], a1[b]);
                         a0[b] = fmaf(bf_lo(w.y), a[2], a0[b]);
@@ -844,7 +1027,7 @@ struct DecodeCta {
 
     // ---------------------------------------------------------- S_QKV
     __device__ void stage_qkv(uint32_t& it, int l) {
-        float act[B][T::VPT][8];
+        Act act;
         load_act(act, p.x, l == 0, p.norm_attn + (size_t)l * D, l * kStagesPerLayer + S_QKV);
         trace_mark(l * kStagesPerLayer + S_QKV, 3);
         const float* rp = rope();
@@ -1205,7 +1388,7 @@ struct DecodeCta {
 
     // ---------------------------------------------------------- S_AOUT
     __device__ void stage_aout(uint32_t& it, int l) {
-        float act[B][T::VPT][8];
+        Act act;
         load_act(act, p.attn_out, false, nullptr, l * kStagesPerLayer + S_AOUT);
         const int ctid = threadIdx.x;
         const int r0 = pl.aout_r0, nr = pl.aout_r1 - pl.aout_r0;
@@ -1227,7 +1410,7 @@ struct DecodeCta {
 
     // ---------------------------------------------------------- S_GLU
     // in/gate rows [2 t0, 2 t1) of Wffn1 -> h[t - t0] = silu(gate) * in (smem)
-    __device__ void glu_ffn1(uint32_t& it, const float (&act)[B][T::VPT][8], int t0, int t1) {
+    __device__ void glu_ffn1(uint32_t& it, const Act& act, int t0, int t1) {
         const int ctid = threadIdx.x;
         float* hs = h_s();
         gemv(it, act, 2 * t0, 2 * t1, [&](int c0, int nrows, const float* red) {
@@ -1255,6 +1438,12 @@ struct DecodeCta {
             for (int j = 0; j < T::VPT; ++j)
 #pragma unroll
                 for (int e = 0; e < 8; ++e) acc[b][j][e] = 0.f;
+        // quant: acc[col] = sum_r c_r,col s_r h_r (int4: times 16^k), and the
+        // zero-point term sum_r z_r s_r h_r is the same for all of the
+        // thread's columns (one group per row): one scalar per batch row
+        float zs[B];
+#pragma unroll
+        for (int b = 0; b < B; ++b) zs[b] = 0.f;
         for (int c0 = t0; c0 < t1; c0 += T::RPS) {
             const int nrows = min(T::RPS, t1 - c0);
             const uint32_t slot = it % T::NSLOTS, par = (it / T::NSLOTS) & 1;
@@ -1264,6 +1453,32 @@ struct DecodeCta {
                 float hb[B];
 #pragma unroll
                 for (int b = 0; b < B; ++b) hb[b] = hs[b * T::TMAX + (c0 - t0) + row];
+                if constexpr (T::QB != 0) {
+                    QRow q;
+                    q_load(base + row * T::ROW_BYTES, lt, q);
+#pragma unroll
+                    for (int b = 0; b < B; ++b) {
+                        hb[b] *= q.scale;
+                        zs[b] = fmaf(q.zero, hb[b], zs[b]);
+                    }
+#pragma unroll
+                    for (int j = 0; j < T::NCH; ++j) {
+                        float2 d[4];
+                        q_chunk(q, j, d);
+#pragma unroll
+                        for (int b = 0; b < B; ++b) {
+                            const float2 h2 = make_float2(hb[b], hb[b]);
+#pragma unroll
+                            for (int k = 0; k < 4; ++k) {
+                                float2 a2 = make_float2(acc[b][j][2 * k], acc[b][j][2 * k + 1]);
+                                a2 = __ffma2_rn(d[k], h2, a2);
+                                acc[b][j][2 * k] = a2.x;
+                                acc[b][j][2 * k + 1] = a2.y;
+                            }
+                        }
+                    }
+                    return;
+                }
 #pragma unroll
                 for (int j = 0; j < T::VPT; ++j) {
                     const uint4 w = lds_u128(base + row * T::ROW_BYTES + (lt + j * T::TPR) * 16);
@@ -1287,13 +1502,22 @@ struct DecodeCta {
             if (lane == 0) mbar_arrive(&empty[slot]);
             ++it;
         }
+        if constexpr (T::QB != 0) {  // undo the int4 decode scale, subtract the zero term
+#pragma unroll
+            for (int b = 0; b < B; ++b)
+#pragma unroll
+                for (int j = 0; j < T::NCH; ++j)
+#pragma unroll
+                    for (int e = 0; e < 8; ++e)
+                        acc[b][j][e] = (T::QB == 4 ? acc[b][j][e] * q4_scale(e) : acc[b][j][e]) - zs[b];
+        }
         // per-row-group partial d_model vectors
         float* gp = dst_part + (size_t)rg * B * D;
 #pragma unroll
         for (int b = 0; b < B; ++b)
 #pragma unroll
             for (int j = 0; j < T::VPT; ++j) {
-                const int col = (lt + j * T::TPR) * 8;
+                const int col = col_of(lt, j);
                 float* dst = gp + (size_t)b * D + col;
                 __stcg(reinterpret_cast<float4*>(dst),
                        make_float4(acc[b][j][0], acc[b][j][1], acc[b][j][2], acc[b][j][3]));
@@ -1306,11 +1530,11 @@ struct DecodeCta {
     // Static slice [glu_t0, glu_t1) into glu_part[cta], then pool chunks
     // (claimed by this CTA's producer) each into pool_part[chunk].
     __device__ void stage_glu(uint32_t& it, int l) {
-        float act[B][T::VPT][8];
+        Act act;
         load_act(act, p.x, false, p.norm_ffn + (size_t)l * D, l * kStagesPerLayer + S_GLU);
         glu_ffn1(it, act, pl.glu_t0, pl.glu_t1);
         glu_ffn2(it, pl.glu_t0, pl.glu_t1, p.glu_part + (size_t)cta * T::RG * B * D);
-        if (p.pool_chunks > 0) {
+        if (T::QB == 0 && p.pool_chunks > 0) {  // (pool: bf16 only, host-enforced)
             for (;;) {
                 const uint32_t slot = it % T::NSLOTS, par = (it / T::NSLOTS) & 1;
                 wait_full(slot, par);
@@ -1376,7 +1600,7 @@ struct DecodeCta {
 
     // ---------------------------------------------------------- S_LMHEAD
     __device__ void stage_lmhead(uint32_t& it) {
-        float act[B][T::VPT][8];
+        Act act;
         load_act(act, p.x, p.layers == 0, p.final_norm, p.layers * kStagesPerLayer);
         const int ctid = threadIdx.x;
         float best = -INFINITY;
@@ -1498,8 +1722,12 @@ __global__ void __launch_bounds__(KTraits<S>::NTHREADS, 1)
     }
     __syncthreads();
     if (tid >= T::NCT) {
+        asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(T::PRODUCER_REGS));
         if (tid == T::NCT) cta.template producer<false>();
-    } else if (p.debug & kDebugStreamOnly) {
+        return;
+    }
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(T::CONSUMER_REGS));
+    if (p.debug & kDebugStreamOnly) {
         cta.template producer<true>();  // streaming-only measurement
     } else {
         cta.consumer();

@@ -13,8 +13,8 @@
 namespace ffb200 {
 
 struct KernelOps {
-    int D, DI, DH, NQ, NKV, B;
-    int threads, smem, nslots, slot_bytes, rg, tmax, kvc, rps;
+    int D, DI, DH, NQ, NKV, B, QB;
+    int threads, smem, nslots, slot_bytes, rg, tmax, kvc, rps, row_bytes;
     cudaError_t (*prepare)();
     cudaError_t (*launch)(const DecodeParams&, int grid, cudaStream_t, bool cooperative);
 };
@@ -45,14 +45,16 @@ cudaError_t launch_impl(const DecodeParams& p, int grid, cudaStream_t stream, bo
 template <class S>
 KernelOps make_ops() {
     using T = KTraits<S>;
-    return KernelOps{S::D,       S::DI,        S::DH,  S::NQ,  S::NKV,    S::B,
-                     T::NTHREADS, T::SMEM_BYTES, T::NSLOTS, T::SLOT_BYTES, T::RG, T::TMAX,
-                     T::KVC,      T::RPS,        &prepare_impl<S>, &launch_impl<S>};
+    return KernelOps{S::D,        S::DI,         S::DH,     S::NQ,         S::NKV, S::B,
+                     S::QB,       T::NTHREADS,   T::SMEM_BYTES, T::NSLOTS, T::SLOT_BYTES,
+                     T::RG,       T::TMAX,       T::KVC,    T::RPS,        T::ROW_BYTES,
+                     &prepare_impl<S>, &launch_impl<S>};
 }
 
 // registration hooks, one per kernels_*.cu
 void register_kernels_small(std::vector<KernelOps>& v);
 void register_kernels_1b(std::vector<KernelOps>& v);
 void register_kernels_8b(std::vector<KernelOps>& v);
+void register_kernels_quant(std::vector<KernelOps>& v);
 
 }  // namespace ffb200

@@ -58,15 +58,17 @@ const std::vector<KernelOps>& registry() {
         register_kernels_small(v);
         register_kernels_1b(v);
         register_kernels_8b(v);
+        register_kernels_quant(v);
     });
     return v;
 }
 
 const KernelOps* find_ops(const ffb_model_config& c) {
-    if (c.dtype != 0 || c.quant_bits != 0) return nullptr;
+    if (c.dtype != 0) return nullptr;
+    if (c.quant_bits != 0 && c.quant_group != kQuantGroup) return nullptr;
     for (const auto& k : registry())
         if (k.D == c.d_model && k.DI == c.d_inter && k.DH == c.d_head && k.NQ == c.n_q_heads &&
-            k.NKV == c.n_kv_heads && k.B == c.batch)
+            k.NKV == c.n_kv_heads && k.B == c.batch && k.QB == c.quant_bits)
             return &k;
     return nullptr;
 }
@@ -86,6 +88,8 @@ ffb_status validate_cfg(const ffb_model_config* c) {  // config.hpp:61-83
     if (c->d_model != c->n_q_heads * c->d_head)
         return fail(FFB_VALIDATION, "model: d_model must equal n_q_heads * d_head");
     if (c->vocab_size <= 0) return fail(FFB_VALIDATION, "model: vocab_size must be positive");
+    if (c->quant_bits && c->quant_bits != 4 && c->quant_bits != 8)
+        return fail(FFB_VALIDATION, "quant: only 4-bit (reference) and 8-bit codes are supported");
     if (c->quant_bits && (c->quant_group <= 0 || c->d_model % c->quant_group))
         return fail(FFB_VALIDATION, "quant: group_size must divide every quantized row length");
     return FFB_OK;
@@ -129,6 +133,32 @@ __global__ void synth_bf16_kernel(__nv_bfloat16* dst, int64_t n, uint64_t seed, 
         const uint64_t r = splitmix(seed ^ (static_cast<uint64_t>(i) * 0xd1b54a32d192ed03ull));
         const float u = static_cast<float>(r >> 40) * (1.0f / 16777216.0f);  // [0,1)
         dst[i] = __float2bfloat16_rn((2.0f * u - 1.0f) * a);
+    }
+}
+
+// synthetic packed quant rows (decode_kernel.cuh weight formats): random
+// codes, scale = 2 sqrt(3) stddev / levels (jittered), zero = levels / 2
+__global__ void synth_quant_kernel(uint8_t* dst, int64_t rows, int cols, int qb, int row_bytes,
+                                   uint64_t seed, float stddev) {
+    const int levels = qb == 4 ? 15 : 255;
+    const int code_words = (qb == 4 ? cols / 2 : cols) / 4;
+    const int ng = cols / kQuantGroup;
+    const int code_bytes = code_words * 4;
+    const int64_t n = rows * (code_words + ng);
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const uint64_t r = splitmix(seed ^ (static_cast<uint64_t>(i) * 0xd1b54a32d192ed03ull));
+        if (i < rows * code_words) {
+            const int64_t row = i / code_words, w = i % code_words;
+            *reinterpret_cast<uint32_t*>(dst + row * row_bytes + 4 * w) = static_cast<uint32_t>(r);
+        } else {
+            const int64_t j = i - rows * code_words, row = j / ng, g = j % ng;
+            const float u = static_cast<float>(r >> 40) * (1.0f / 16777216.0f);
+            const float sc = 2.0f * 1.7320508f * stddev / levels * (0.75f + 0.5f * u);
+            uint8_t* rp = dst + row * row_bytes;
+            *reinterpret_cast<float*>(rp + code_bytes + 4 * g) = sc;
+            rp[code_bytes + 4 * ng + g] = static_cast<uint8_t>(levels / 2);
+        }
     }
 }
 
@@ -196,8 +226,11 @@ struct ffb_model {
     std::vector<void*> allocs;
     uint64_t device_bytes = 0;
 
-    __nv_bfloat16 *wqkv = nullptr, *waout = nullptr, *wffn1 = nullptr, *wffn2t = nullptr;
-    __nv_bfloat16 *embedding = nullptr, *lm_head = nullptr, *kcache = nullptr, *vcache = nullptr;
+    // streamed matrices: rows of ops->row_bytes (bf16 or packed int4/int8)
+    uint8_t *wqkv = nullptr, *waout = nullptr, *wffn1 = nullptr, *wffn2t = nullptr,
+            *lm_head = nullptr;
+    __nv_bfloat16 *embedding = nullptr, *kcache = nullptr, *vcache = nullptr;
+    uint64_t quant_inexact_groups = 0;  // packer: groups not on a 4/8-bit grid (lossy)
     float *norm_attn = nullptr, *norm_ffn = nullptr, *final_norm = nullptr;
     float *x = nullptr, *q = nullptr, *attn_out = nullptr, *glu_part = nullptr,
           *attn_part = nullptr, *logits = nullptr, *amax_val = nullptr;
@@ -254,7 +287,7 @@ ffb_status build_plan(ffb_model* m) {
     m->pool_ct = 0;
     m->pool_chunks = 0;
     m->pool_t0 = c.d_inter;
-    if (m->pool_permille > 0 && c.batch <= 2 && c.d_inter / G >= 32) {
+    if (m->pool_permille > 0 && c.batch <= 2 && c.d_inter / G >= 32 && m->ops->QB == 0) {
         const int64_t ct = std::max<int64_t>(m->pool_ct_pref, m->ops->rps);
         const int64_t chunks = (c.d_inter * m->pool_permille) / (1000 * ct);
         if (chunks > 0 && chunks <= m->pool_chunks_max) {
@@ -432,18 +465,22 @@ ffb_status launch_step(ffb_model* m, int64_t pos, const int64_t* d_tokens, float
     return FFB_OK;
 }
 
+// Destination of one reference tensor: kind 0 = streamed matrix (rows of
+// ops->row_bytes, bf16 or packed quant), 1 = f32 vector, 2 = bf16 embedding
 struct TensorDst {
     void* ptr = nullptr;
     int64_t n = 0;
-    bool is_bf16 = true;
+    int kind = 0;
+    int64_t rows = 0;
 };
 
 bool resolve(ffb_model* m, const std::string& name, TensorDst* d) {
     const auto& c = m->cfg;
     const int64_t D = c.d_model;
-    if (name == "embedding") { *d = {m->embedding, c.vocab_size * D, true}; return true; }
-    if (name == "lm_head") { *d = {m->lm_head, c.vocab_size * D, true}; return true; }
-    if (name == "final_norm") { *d = {m->final_norm, D, false}; return true; }
+    const size_t RB = m->ops->row_bytes;
+    if (name == "embedding") { *d = {m->embedding, c.vocab_size * D, 2, c.vocab_size}; return true; }
+    if (name == "lm_head") { *d = {m->lm_head, c.vocab_size * D, 0, c.vocab_size}; return true; }
+    if (name == "final_norm") { *d = {m->final_norm, D, 1, 1}; return true; }
     if (name.rfind("layer.", 0) != 0) return false;
     size_t dot = name.find('.', 6);
     if (dot == std::string::npos) return false;
@@ -456,14 +493,110 @@ bool resolve(ffb_model* m, const std::string& name, TensorDst* d) {
     if (l < 0 || l >= c.layers) return false;
     std::string t = name.substr(dot + 1);
     const int64_t QR = m->qkv_rows();
-    if (t == "wqkv") *d = {m->wqkv + l * QR * D, QR * D, true};
-    else if (t == "waout") *d = {m->waout + l * D * D, D * D, true};
-    else if (t == "wffn1") *d = {m->wffn1 + l * 2 * c.d_inter * D, 2 * c.d_inter * D, true};
-    else if (t == "wffn2t") *d = {m->wffn2t + l * c.d_inter * D, c.d_inter * D, true};
-    else if (t == "norm_attn") *d = {m->norm_attn + l * D, D, false};
-    else if (t == "norm_ffn") *d = {m->norm_ffn + l * D, D, false};
+    if (t == "wqkv") *d = {m->wqkv + l * QR * RB, QR * D, 0, QR};
+    else if (t == "waout") *d = {m->waout + l * D * RB, D * D, 0, D};
+    else if (t == "wffn1") *d = {m->wffn1 + l * 2 * c.d_inter * RB, 2 * c.d_inter * D, 0, 2 * c.d_inter};
+    else if (t == "wffn2t") *d = {m->wffn2t + l * c.d_inter * RB, c.d_inter * D, 0, c.d_inter};
+    else if (t == "norm_attn") *d = {m->norm_attn + l * D, D, 1, 1};
+    else if (t == "norm_ffn") *d = {m->norm_ffn + l * D, D, 1, 1};
     else return false;
     return true;
+}
+
+// ---- weight packer for the quant formats (quant.hpp:17-60) ----------------
+// quantize_group (quant.hpp:42-54) with `levels` = 15 (int4) or 255 (int8):
+// scale = range / levels, zero = clamp(round(-lo / scale)), code =
+// clamp(round(v / scale + zero)).  Reference stores hold weights already
+// snapped to such a grid with the codes discarded (tensor_store.hpp:275-287),
+// so the packer re-derives (codes, scale, zero) and accepts them only if
+// (code - zero) * scale reproduces every value bit for bit; the scale
+// recomputed from the snapped extremes can be off by a few ulps, so nearby
+// scales are tried too.  A group with no exact representation (weights that
+// were never on a grid) keeps quantize_group's lossy result and is counted.
+bool quant_try(const float* v, int n, int levels, float scale, bool exact, uint8_t* codes,
+               float* zero) {
+    float lo = v[0];
+    for (int i = 1; i < n; ++i) lo = std::min(lo, v[i]);
+    float z = std::round(-lo / scale);
+    z = std::min(std::max(z, 0.0f), static_cast<float>(levels));
+    for (int i = 0; i < n; ++i) {
+        float c = std::round(v[i] / scale + z);
+        c = std::min(std::max(c, 0.0f), static_cast<float>(levels));
+        codes[i] = static_cast<uint8_t>(c);
+        if (exact && (c - z) * scale != v[i]) return false;
+    }
+    *zero = z;
+    return true;
+}
+
+bool quant_group(const float* v, int n, int levels, uint8_t* codes, float* scale, float* zero) {
+    float lo = v[0], hi = v[0];
+    for (int i = 1; i < n; ++i) {
+        lo = std::min(lo, v[i]);
+        hi = std::max(hi, v[i]);
+    }
+    const float range = hi - lo;
+    const float s0 = range > 0 ? range / static_cast<float>(levels) : 1.0f;
+    // candidate scale c, tried at +-ulps: the snapped extremes usually sit on
+    // codes 0 and `levels` (s = range / levels), but float rounding can land
+    // the maximum one code lower, and sparse groups need the step itself
+    auto try_near = [&](float c, int ulps) {
+        if (!(c > 0) || !std::isfinite(c)) return false;
+        for (int d = 0; d <= ulps; ++d)
+            for (int sign = -1; sign <= 1; sign += 2) {
+                if (d == 0 && sign > 0) continue;
+                float sc = c;
+                for (int k = 0; k < d; ++k) sc = std::nextafter(sc, sign > 0 ? INFINITY : 0.0f);
+                if (quant_try(v, n, levels, sc, true, codes, zero)) {
+                    *scale = sc;
+                    return true;
+                }
+            }
+        return false;
+    };
+    if (try_near(s0, 8)) return true;
+    if (range > 0) {
+        for (int k = levels - 1; k >= levels - 2; --k)
+            if (try_near(range / static_cast<float>(k), 4)) return true;
+        float step = INFINITY;  // smallest gap between distinct values
+        std::vector<float> u(v, v + n);
+        std::sort(u.begin(), u.end());
+        for (int i = 1; i < n; ++i)
+            if (u[i] > u[i - 1]) step = std::min(step, u[i] - u[i - 1]);
+        if (try_near(step, 4)) return true;
+        if (lo < 0)
+            for (int z = 1; z <= levels; ++z)
+                if (try_near(-lo / static_cast<float>(z), 2)) return true;
+        if (hi > 0)
+            for (int k = 1; k <= levels; ++k)
+                if (try_near(hi / static_cast<float>(k), 2)) return true;
+    }
+    quant_try(v, n, levels, s0, false, codes, zero);
+    *scale = s0;
+    return false;
+}
+
+// One row of `cols` f32 values -> the device row format of decode_kernel.cuh
+// (codes | f32 scales | u8 zeros | pad).  Returns the inexact group count.
+int pack_quant_row(const float* v, int64_t cols, int qb, uint8_t* out, size_t row_bytes) {
+    const int levels = qb == 4 ? 15 : 255;
+    const int64_t ng = cols / kQuantGroup;
+    const int64_t code_bytes = qb == 4 ? cols / 2 : cols;
+    std::memset(out, 0, row_bytes);
+    uint8_t codes[kQuantGroup];
+    int inexact = 0;
+    for (int64_t g = 0; g < ng; ++g) {
+        float sc = 1.f, z = 0.f;
+        if (!quant_group(v + g * kQuantGroup, kQuantGroup, levels, codes, &sc, &z)) ++inexact;
+        for (int i = 0; i < kQuantGroup; ++i) {
+            const int64_t col = g * kQuantGroup + i;
+            if (qb == 4) out[col / 2] |= static_cast<uint8_t>(codes[i] << (4 * (col & 1)));
+            else out[col] = codes[i];
+        }
+        std::memcpy(out + code_bytes + 4 * g, &sc, 4);
+        out[code_bytes + 4 * ng + g] = static_cast<uint8_t>(z);
+    }
+    return inexact;
 }
 
 size_t kv_offset(const ffb_model* m, int64_t b, int64_t l, int64_t h, int64_t pos) {
@@ -486,6 +619,25 @@ extern "C" {
 
 const char* ffb_last_error(void) { return g_err.c_str(); }
 const char* ffb_version(void) { return "ffb200 0.1.0 (sm_100a)"; }
+
+int64_t ffb_quant_row_bytes(int64_t cols, int32_t quant_bits) {
+    if (cols <= 0 || cols % kQuantGroup || (quant_bits != 0 && quant_bits != 4 && quant_bits != 8))
+        return -1;
+    return weight_row_bytes(static_cast<int>(cols), quant_bits);
+}
+
+int64_t ffb_pack_quant_rows(const float* values, int64_t rows, int64_t cols, int32_t quant_bits,
+                            uint8_t* out) {
+    const int64_t rb = ffb_quant_row_bytes(cols, quant_bits);
+    if (!values || !out || rows < 0 || rb < 0 || quant_bits == 0) {
+        fail(FFB_USAGE, "pack_quant_rows: bad arguments");
+        return -1;
+    }
+    int64_t inexact = 0;
+    for (int64_t r = 0; r < rows; ++r)
+        inexact += pack_quant_row(values + r * cols, cols, quant_bits, out + r * rb, rb);
+    return inexact;
+}
 
 int ffb_config_supported(const ffb_model_config* cfg) {
     if (!cfg) return 0;
@@ -551,15 +703,16 @@ ffb_status ffb_create(const ffb_model_config* cfg, int64_t max_seq_len, int devi
         ffb_status s_ = m->alloc(&(ptr), (n)); \
         if (s_) return bail(s_);      \
     } while (0)
-    ALLOC(m->wqkv, (size_t)Lc * m->qkv_rows() * D);
-    ALLOC(m->waout, (size_t)Lc * D * D);
-    ALLOC(m->wffn1, (size_t)Lc * 2 * c.d_inter * D);
-    ALLOC(m->wffn2t, (size_t)Lc * c.d_inter * D);
+    const size_t RB = ops->row_bytes;
+    ALLOC(m->wqkv, (size_t)Lc * m->qkv_rows() * RB);
+    ALLOC(m->waout, (size_t)Lc * D * RB);
+    ALLOC(m->wffn1, (size_t)Lc * 2 * c.d_inter * RB);
+    ALLOC(m->wffn2t, (size_t)Lc * c.d_inter * RB);
     ALLOC(m->norm_attn, (size_t)Lc * D);
     ALLOC(m->norm_ffn, (size_t)Lc * D);
     ALLOC(m->final_norm, (size_t)D);
     ALLOC(m->embedding, (size_t)V * D);
-    ALLOC(m->lm_head, (size_t)V * D);
+    ALLOC(m->lm_head, (size_t)V * RB);
     const size_t kv = (size_t)Lc * B * c.n_kv_heads * max_seq_len * c.d_head;
     ALLOC(m->kcache, kv);
     ALLOC(m->vcache, kv);
@@ -615,8 +768,23 @@ ffb_status ffb_upload_tensor(ffb_model* m, const char* name, const float* values
         return fail(FFB_USAGE, "tensor '%s': expected %lld values, got %lld", name,
                     (long long)d.n, (long long)n);
     CUDA_TRY(cudaSetDevice(m->device));
-    if (!d.is_bf16) {
+    if (d.kind == 1) {
         CUDA_TRY(cudaMemcpy(d.ptr, values, sizeof(float) * n, cudaMemcpyHostToDevice));
+        return FFB_OK;
+    }
+    if (d.kind == 0 && m->ops->QB != 0) {  // quant packer, a block of rows at a time
+        const int64_t cols = m->cfg.d_model;
+        const size_t rb = m->ops->row_bytes;
+        const int64_t rows_per = std::max<int64_t>(1, (4 << 20) / (int64_t)rb);
+        std::vector<uint8_t> buf(rows_per * rb);
+        auto* dst = static_cast<uint8_t*>(d.ptr);
+        for (int64_t r0 = 0; r0 < d.rows; r0 += rows_per) {
+            const int64_t nr = std::min(rows_per, d.rows - r0);
+            for (int64_t r = 0; r < nr; ++r)
+                m->quant_inexact_groups += pack_quant_row(values + (r0 + r) * cols, cols,
+                                                          m->ops->QB, buf.data() + r * rb, rb);
+            CUDA_TRY(cudaMemcpy(dst + r0 * rb, buf.data(), nr * rb, cudaMemcpyHostToDevice));
+        }
         return FFB_OK;
     }
     auto* dst = static_cast<__nv_bfloat16*>(d.ptr);
@@ -644,12 +812,23 @@ ffb_status ffb_init_synthetic(ffb_model* m, uint64_t seed) {
     auto f32 = [&](float* p, int64_t n, uint64_t s) {
         synth_f32_kernel<<<256, 256, 0, m->stream>>>(p, n, seed * 1315423911ull + s, 1.0f, 0.02f);
     };
-    bf(m->wqkv, L * m->qkv_rows() * D, 1, sd);
-    bf(m->waout, L * D * D, 2, sd);
-    bf(m->wffn1, L * 2 * c.d_inter * D, 3, sd);
-    bf(m->wffn2t, L * c.d_inter * D, 4, sdi);
+    // streamed matrices: bf16 values, or random codes with per-group scales
+    // spanning the same +-sqrt(3) stddev range and a mid-range zero point
+    auto mat = [&](uint8_t* p, int64_t rows, uint64_t s, float stddev) {
+        if (m->ops->QB == 0) {
+            bf(reinterpret_cast<__nv_bfloat16*>(p), rows * D, s, stddev);
+        } else {
+            synth_quant_kernel<<<4096, 256, 0, m->stream>>>(
+                p, rows, static_cast<int>(D), m->ops->QB, m->ops->row_bytes,
+                seed * 1315423911ull + s, stddev);
+        }
+    };
+    mat(m->wqkv, L * m->qkv_rows(), 1, sd);
+    mat(m->waout, L * D, 2, sd);
+    mat(m->wffn1, L * 2 * c.d_inter, 3, sd);
+    mat(m->wffn2t, L * c.d_inter, 4, sdi);
     bf(m->embedding, c.vocab_size * D, 5, sd);
-    bf(m->lm_head, c.vocab_size * D, 6, sd);
+    mat(m->lm_head, c.vocab_size, 6, sd);
     f32(m->norm_attn, L * D, 7);
     f32(m->norm_ffn, L * D, 8);
     f32(m->final_norm, D, 9);
@@ -888,10 +1067,12 @@ ffb_status ffb_get_info(const ffb_model* m, ffb_info* out) {
     out->launches_per_step =
         m->mode == FFB_MODE_BASELINE ? static_cast<int32_t>(c.layers * kStagesPerLayer + 1) : 1;
     out->mode = m->mode;
-    const uint64_t row = static_cast<uint64_t>(c.d_model) * 2;
+    const uint64_t row = static_cast<uint64_t>(m->ops->row_bytes);
     out->weight_bytes = row * (static_cast<uint64_t>(c.layers) *
                                    (m->qkv_rows() + c.d_model + 3 * c.d_inter) +
                                c.vocab_size);
+    out->quant_inexact_groups = m->quant_inexact_groups;
+    out->row_bytes = m->ops->row_bytes;
     out->device_bytes = m->device_bytes;
     return FFB_OK;
 }

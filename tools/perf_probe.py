@@ -10,6 +10,7 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--model", default="llama31_8b")
 ap.add_argument("--ctx", type=int, default=4096)
 ap.add_argument("--batch", type=int, default=1)
+ap.add_argument("--quant", type=int, default=0, help="weight bits: 0 (bf16), 4, 8")
 ap.add_argument("--steps", type=int, default=100)
 ap.add_argument("--sweep", default="", help="comma list of l2_prefetch_bytes")
 ap.add_argument("--ncu", action="store_true", help="few launches, for profiling")
@@ -17,7 +18,7 @@ ap.add_argument("--calibrate", type=int, default=0, help="ffb_calibrate iteratio
 ap.add_argument("--pf-stages", type=int, default=0x3f, help="l2_prefetch_stages mask for --sweep")
 a = ap.parse_args()
 
-cfg = model_preset(a.model).replace(batch=a.batch)
+cfg = model_preset(a.model).replace(batch=a.batch, quant_bits=a.quant)
 m = DecodeModel(cfg, a.ctx + 8)
 m.init_synthetic(1)
 if a.calibrate:

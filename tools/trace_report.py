@@ -16,11 +16,12 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--model", default="llama31_8b")
 ap.add_argument("--ctx", type=int, default=4096)
 ap.add_argument("--batch", type=int, default=1)
+ap.add_argument("--quant", type=int, default=0, help="weight bits: 0 (bf16), 4, 8")
 ap.add_argument("--mode", default="fused_overlap")
 ap.add_argument("--reverse", action="store_true", help="plan_reverse option")
 ap.add_argument("--calibrate", type=int, default=0, help="ffb_calibrate iterations first")
 a = ap.parse_args()
-cfg = model_preset(a.model).replace(batch=a.batch)
+cfg = model_preset(a.model).replace(batch=a.batch, quant_bits=a.quant)
 m = DecodeModel(cfg, a.ctx + 8, mode={"fused_overlap": RunMode.FUSED_OVERLAP, "fused": RunMode.FUSED,
                                       "baseline": RunMode.BASELINE}[a.mode])
 m.init_synthetic(1)

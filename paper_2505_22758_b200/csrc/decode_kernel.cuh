@@ -65,7 +65,9 @@ struct CtaPlan {
     int32_t red_c0, red_c1;    // residual columns this CTA reduces / initialises
     int32_t attn_unit;         // b * NKV + kv_head, or -1 when idle in S_ATTN
     int32_t attn_g;            // slot of this CTA inside its unit's split-K group
-    int32_t pad[4];
+    int32_t qkv_heads;         // bit h: this CTA's Wqkv rows include q/k/v rows of kv head h
+    int32_t attn_dep;          // CTAs whose Wqkv rows touch this CTA's kv head (S_ATTN dependency)
+    int32_t pad[2];
 };
 
 struct DecodeParams {
@@ -94,6 +96,7 @@ struct DecodeParams {
     int64_t* greedy;   // [B]
     uint32_t* counters;       // [L*5 + 1] stage counters
     uint32_t* head_counters;  // [L][units]
+    uint32_t* qkv_head_counters;  // [L][NKV]: arrivals of CTAs holding that head's Wqkv rows
     uint32_t* amax_counter;   // [1]
     const CtaPlan* plan;      // [grid]
     const int64_t* tokens;    // [B]
@@ -298,9 +301,10 @@ struct DecodeCta {
                 *ctr = p.counters + (l - 1) * kStagesPerLayer + S_RED;
                 *target = full_grid;
                 return true;
-            case S_ATTN:
-                *ctr = p.counters + l * kStagesPerLayer + S_QKV;
-                *target = full_grid;
+            case S_ATTN:  // only the CTAs that computed this kv head's q/k/v rows
+                if (pl.attn_unit < 0) return false;
+                *ctr = p.qkv_head_counters + l * S::NKV + pl.attn_unit % S::NKV;
+                *target = p.epoch * static_cast<uint32_t>(pl.attn_dep);
                 return true;
             case S_AOUT:
                 *ctr = p.counters + l * kStagesPerLayer + S_ATTN;
@@ -1067,7 +1071,13 @@ struct DecodeCta {
                 }
             }
         });
-        arrive(p.counters + l * kStagesPerLayer + S_QKV, l * kStagesPerLayer + S_QKV);
+        // fine-grained release: one arrival per kv head whose rows this CTA
+        // holds (S_ATTN of that head waits for exactly those CTAs)
+        consumer_sync(NCT);
+        if (threadIdx.x < S::NKV && ((pl.qkv_heads >> threadIdx.x) & 1))
+            red_release_gpu(p.qkv_head_counters + l * S::NKV + threadIdx.x, 1);
+        trace_mark(l * kStagesPerLayer + S_QKV, 2);
+        trace_ring_wait(l * kStagesPerLayer + S_QKV);
     }
 
     // ---------------------------------------------------------- S_ATTN

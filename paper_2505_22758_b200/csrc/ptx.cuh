@@ -67,20 +67,33 @@ __device__ __forceinline__ bool mbar_test_wait(uint64_t* bar, uint32_t parity) {
     return ok != 0;
 }
 
-// Spin watchdog: a wait that outlives ~10 s of polling traps, turning a
-// schedule bug into a launch error instead of a hung GPU.
-#ifndef FFB_SPIN_LIMIT
-#define FFB_SPIN_LIMIT (1ull << 31)
+// Spin watchdog: a wait that outlives FFB_SPIN_NS of wall time (%globaltimer,
+// sampled every 1024 polls) traps, turning a schedule bug into a launch
+// error instead of a hung GPU.
+#ifndef FFB_SPIN_NS
+#define FFB_SPIN_NS 4000000000ull
 #endif
 
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-    unsigned long long n = 0;
-    while (!mbar_try_wait(bar, parity)) {
-        if (++n > FFB_SPIN_LIMIT) __trap();
+__device__ __forceinline__ uint64_t spin_clock_ns() {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
+__device__ __forceinline__ void spin_watchdog(uint32_t& n, uint64_t& t0) {
+    if ((++n & 1023u) == 0) {
+        const uint64_t t = spin_clock_ns();
+        if (t0 == 0) t0 = t;
+        else if (t - t0 > FFB_SPIN_NS) __trap();
     }
 }
 
-// ---------------------------------------------------------------- TMA bulk
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    uint32_t n = 0;
+    uint64_t t0 = 0;
+    while (!mbar_try_wait(bar, parity)) spin_watchdog(n, t0);
+}
+
 __device__ __forceinline__ uint64_t policy_evict_first() {
     uint64_t p;
     asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
@@ -125,10 +138,9 @@ __device__ __forceinline__ uint32_t atom_add_acq_rel_gpu(uint32_t* p, uint32_t v
 
 __device__ __forceinline__ void spin_until_geq(const uint32_t* p, uint32_t target) {
     // Monotone epoch counters: the value only grows, so >= is exact.
-    unsigned long long n = 0;
-    while (static_cast<int32_t>(ld_acquire_gpu(p) - target) < 0) {
-        if (++n > FFB_SPIN_LIMIT) __trap();
-    }
+    uint32_t n = 0;
+    uint64_t t0 = 0;
+    while (static_cast<int32_t>(ld_acquire_gpu(p) - target) < 0) spin_watchdog(n, t0);
 }
 
 // named barrier over the consumer warps only (id 1; id 0 is __syncthreads)

@@ -214,6 +214,7 @@ struct ffb_model {
     std::vector<double> sm_weight;
     std::vector<CtaPlan> plan_host;
     int16_t* sm_rank = nullptr;       // device [max smid + 1] -> dense rank, or null
+    int calib_mask = 0xf;             // option "calib_mask": matrices using the weights
     int use_sm_rank = 1;              // option "sm_rank": plans follow SM ids
     int64_t pool_permille = 0;        // share of d_inter in the dynamic GLU pool (off)
     int64_t pool_ct_pref = 4;         // preferred pairs per pool chunk
@@ -236,7 +237,8 @@ struct ffb_model {
           *attn_part = nullptr, *logits = nullptr, *amax_val = nullptr;
     int32_t* amax_idx = nullptr;
     int64_t *greedy = nullptr, *tokens_dev = nullptr;
-    uint32_t *counters = nullptr, *head_counters = nullptr, *amax_counter = nullptr;
+    uint32_t *counters = nullptr, *head_counters = nullptr, *amax_counter = nullptr,
+             *qkv_head_counters = nullptr;
     CtaPlan* plan = nullptr;
     int64_t* tokens_pinned = nullptr;
     int64_t* greedy_pinned = nullptr;
@@ -303,22 +305,25 @@ ffb_status build_plan(ffb_model* m) {
     std::vector<double> cum(G + 1, 0.0);
     for (int64_t k = 0; k < G; ++k)
         cum[k + 1] = cum[k] + m->sm_weight[m->plan_reverse ? G - 1 - k : k];
-    auto wsplit = [&](int64_t units, int64_t k) {
+    // calib_mask bit 0/1/2/3: QKV / AOUT / GLU / LM head rows follow the
+    // weights (the others split uniformly)
+    auto wsplit_m = [&](int64_t units, int64_t k, int bit) {
         if (k >= G) return units;
+        if (!((m->calib_mask >> bit) & 1)) return (units * k) / G;
         return std::min<int64_t>(units, std::llround(units * cum[k] / cum[G]));
     };
     for (int64_t i = 0; i < G; ++i) {
         CtaPlan& p = plan[i];
         std::memset(&p, 0, sizeof(p));
         const int64_t k = m->plan_reverse ? G - 1 - i : i;  // weight-slice order
-        p.qkv_r0 = static_cast<int32_t>(2 * wsplit(qkv_pairs, k));
-        p.qkv_r1 = static_cast<int32_t>(2 * wsplit(qkv_pairs, k + 1));
-        p.aout_r0 = static_cast<int32_t>(wsplit(c.d_model, k));
-        p.aout_r1 = static_cast<int32_t>(wsplit(c.d_model, k + 1));
-        p.glu_t0 = static_cast<int32_t>(wsplit(glu_static, k));
-        p.glu_t1 = static_cast<int32_t>(wsplit(glu_static, k + 1));
-        p.lm_r0 = static_cast<int32_t>(wsplit(c.vocab_size, k));
-        p.lm_r1 = static_cast<int32_t>(wsplit(c.vocab_size, k + 1));
+        p.qkv_r0 = static_cast<int32_t>(2 * wsplit_m(qkv_pairs, k, 0));
+        p.qkv_r1 = static_cast<int32_t>(2 * wsplit_m(qkv_pairs, k + 1, 0));
+        p.aout_r0 = static_cast<int32_t>(wsplit_m(c.d_model, k, 1));
+        p.aout_r1 = static_cast<int32_t>(wsplit_m(c.d_model, k + 1, 1));
+        p.glu_t0 = static_cast<int32_t>(wsplit_m(glu_static, k, 2));
+        p.glu_t1 = static_cast<int32_t>(wsplit_m(glu_static, k + 1, 2));
+        p.lm_r0 = static_cast<int32_t>(wsplit_m(c.vocab_size, k, 3));
+        p.lm_r1 = static_cast<int32_t>(wsplit_m(c.vocab_size, k + 1, 3));
         p.red_c0 = static_cast<int32_t>(split_at(c.d_model, i, G));
         p.red_c1 = static_cast<int32_t>(split_at(c.d_model, i + 1, G));
         if (i < static_cast<int64_t>(m->n_units) * m->attn_group) {
@@ -328,8 +333,28 @@ ffb_status build_plan(ffb_model* m) {
             p.attn_unit = -1;
             p.attn_g = 0;
         }
+        // kv heads whose q / k / v rows intersect [qkv_r0, qkv_r1)
+        {
+            const int64_t QR = c.n_q_heads * c.d_head, KR = c.n_kv_heads * c.d_head;
+            const int64_t qpg = c.n_q_heads / c.n_kv_heads;
+            p.qkv_heads = 0;
+            for (int64_t r = p.qkv_r0; r < p.qkv_r1; ++r) {
+                const int64_t h = r < QR ? r / (qpg * c.d_head)
+                                         : (r < QR + KR ? (r - QR) / c.d_head
+                                                        : (r - QR - KR) / c.d_head);
+                p.qkv_heads |= 1 << h;
+            }
+        }
         if (p.glu_t1 - p.glu_t0 > m->ops->tmax || p.aout_r1 - p.aout_r0 > m->ops->tmax)
             return fail(FFB_UNSUPPORTED, "d_inter too large for the per-CTA GLU buffer");
+    }
+    if (c.n_kv_heads > 31) return fail(FFB_UNSUPPORTED, "more than 31 kv heads");
+    for (int64_t i = 0; i < G; ++i) {  // S_ATTN dependency counts per kv head
+        CtaPlan& p = plan[i];
+        p.attn_dep = 0;
+        if (p.attn_unit < 0) continue;
+        const int h = p.attn_unit % static_cast<int>(c.n_kv_heads);
+        for (int64_t j = 0; j < G; ++j) p.attn_dep += (plan[j].qkv_heads >> h) & 1;
     }
     CUDA_TRY(cudaMemcpy(m->plan, plan.data(), sizeof(CtaPlan) * G, cudaMemcpyHostToDevice));
     m->plan_host = plan;
@@ -402,6 +427,7 @@ DecodeParams make_params(const ffb_model* m, int64_t pos, const int64_t* d_token
     p.greedy = d_greedy ? d_greedy : m->greedy;
     p.counters = m->counters;
     p.head_counters = m->head_counters;
+    p.qkv_head_counters = m->qkv_head_counters;
     p.amax_counter = m->amax_counter;
     p.plan = m->plan;
     p.tokens = d_tokens;
@@ -436,6 +462,8 @@ DecodeParams make_params(const ffb_model* m, int64_t pos, const int64_t* d_token
 ffb_status reset_sync_state(ffb_model* m, cudaStream_t stream) {
     const int64_t Lc = std::max<int64_t>(1, m->cfg.layers);
     CUDA_TRY(cudaMemsetAsync(m->counters, 0, sizeof(uint32_t) * (Lc * 5 + 1), stream));
+    CUDA_TRY(cudaMemsetAsync(m->qkv_head_counters, 0,
+                             sizeof(uint32_t) * Lc * m->cfg.n_kv_heads, stream));
     CUDA_TRY(cudaMemsetAsync(m->head_counters, 0,
                              sizeof(uint32_t) * std::max<int64_t>(1, Lc * m->n_units), stream));
     CUDA_TRY(cudaMemsetAsync(m->amax_counter, 0, sizeof(uint32_t), stream));
@@ -730,6 +758,7 @@ ffb_status ffb_create(const ffb_model_config* cfg, int64_t max_seq_len, int devi
     ALLOC(m->tokens_dev, (size_t)B);
     ALLOC(m->counters, (size_t)Lc * 5 + 1);
     ALLOC(m->head_counters, (size_t)Lc * units);
+    ALLOC(m->qkv_head_counters, (size_t)Lc * c.n_kv_heads);
     ALLOC(m->amax_counter, 1);
     ALLOC(m->plan, (size_t)m->grid);
     ALLOC(m->staging, (size_t)ffb_model::kStagingElems);
@@ -742,6 +771,7 @@ ffb_status ffb_create(const ffb_model_config* cfg, int64_t max_seq_len, int devi
 #undef ALLOC
     if (cudaMemset(m->counters, 0, sizeof(uint32_t) * (Lc * 5 + 1)) != cudaSuccess ||
         cudaMemset(m->head_counters, 0, sizeof(uint32_t) * Lc * units) != cudaSuccess ||
+        cudaMemset(m->qkv_head_counters, 0, sizeof(uint32_t) * Lc * c.n_kv_heads) != cudaSuccess ||
         cudaMemset(m->amax_counter, 0, sizeof(uint32_t)) != cudaSuccess ||
         cudaMemset(m->kcache, 0, kv * 2) != cudaSuccess ||
         cudaMemset(m->vcache, 0, kv * 2) != cudaSuccess)
@@ -752,6 +782,8 @@ ffb_status ffb_create(const ffb_model_config* cfg, int64_t max_seq_len, int devi
         return bail(fail(FFB_DEVICE, "cudaMallocHost failed"));
     st = build_plan(m);
     if (st) return bail(st);
+    // quant stages are dequant-compute bound: L2 prefetch measured slower
+    if (ops->QB != 0) m->l2_prefetch = 0;
     st = probe_sm_ranks(m);
     if (st) return bail(st);
     *out = m;
@@ -937,6 +969,19 @@ ffb_status ffb_set_option(ffb_model* m, const char* key, int64_t value) {
         if (value < 0 || value > (64ll << 20))
             return fail(FFB_USAGE, "l2_prefetch_bytes out of range [0, 64 MiB]");
         m->l2_prefetch = value;
+        return FFB_OK;
+    }
+    if (std::strcmp(key, "calib_mask") == 0) {
+        if (value < 0 || value > 0xf) return fail(FFB_USAGE, "calib_mask is a 4-bit mask");
+        m->calib_mask = static_cast<int>(value);
+        CUDA_TRY(cudaSetDevice(m->device));
+        CUDA_TRY(cudaDeviceSynchronize());
+        ffb_status s = build_plan(m);
+        if (s) return s;
+        s = reset_sync_state(m, m->stream);
+        if (s) return s;
+        CUDA_TRY(cudaStreamSynchronize(m->stream));
+        m->epoch = 0;
         return FFB_OK;
     }
     if (std::strcmp(key, "sm_rank") == 0) {
@@ -1137,7 +1182,10 @@ ffb_status ffb_calibrate(ffb_model* m, int32_t iterations) {
             }
             for (int i = 0; i < G; ++i)
                 m->sm_weight[i] = std::min(1.3, std::max(0.7, m->sm_weight[i] * G / sum));
+            // a new plan changes per-head arrival counts: restart the epochs
             st = build_plan(m);
+            if (!st) st = reset_sync_state(m, m->stream);
+            m->epoch = 0;
         }
         m->mode = saved_mode;
         m->trace = saved_trace;

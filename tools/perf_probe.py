@@ -15,6 +15,7 @@ ap.add_argument("--steps", type=int, default=100)
 ap.add_argument("--sweep", default="", help="comma list of l2_prefetch_bytes")
 ap.add_argument("--ncu", action="store_true", help="few launches, for profiling")
 ap.add_argument("--calibrate", type=int, default=0, help="ffb_calibrate iterations first")
+ap.add_argument("--masks", default="", help="comma list of calib_mask values to compare")
 ap.add_argument("--pf-stages", type=int, default=0x3f, help="l2_prefetch_stages mask for --sweep")
 a = ap.parse_args()
 
@@ -50,6 +51,13 @@ def timeit(name):
     ms = e0.elapsed_time(e1) / a.steps
     print(f"{a.model} b{a.batch} ctx{a.ctx} {name:22s} {ms:.4f} ms/step {nbytes / ms / 1e9:6.2f} TB/s", flush=True)
 
+if a.masks:
+    m.set_mode(RunMode.FUSED_OVERLAP)
+    for rep in range(2):
+        for mk in [int(x, 0) for x in a.masks.split(",")]:
+            m.set_option("calib_mask", mk)
+            timeit(f"calib_mask={mk:#x}")
+    sys.exit(0)
 if a.sweep:
     m.set_mode(RunMode.FUSED_OVERLAP)
     m.set_option("l2_prefetch_stages", a.pf_stages)

@@ -91,9 +91,29 @@ int64_t ffb_pack_quant_rows(const float *values, int64_t rows, int64_t cols,
 int ffb_config_supported(const ffb_model_config *cfg);
 
 /* Allocates weights, KV cache [L][B][Hkv][max_seq_len][d_head] bf16 and
- * scratch on `device`.  tp_rank/tp_size: tensor-parallel shard (tp_size 1 = whole model). */
+ * scratch on `device`.  tp_rank/tp_size: tensor-parallel shard (tp_size 1 =
+ * whole model): rank r holds kv heads [r Hkv/tp, (r+1)
+ * Hkv/tp) with their q heads (Wqkv rows, KV cache), the matching input
+ * columns of Waout, d_inter slice r of Wffn1 / Wffn2^T and vocab slice r of
+ * lm_head; embedding and norms are replicated.  Per layer the residual
+ * deltas of the O-projection and the FFN are summed across ranks inside the
+ * persistent kernel over peer memory (NVLink P2P), plus one argmax exchange
+ * per step.  A TP rank must be connected (ffb_tp_connect) before stepping. */
 ffb_status ffb_create(const ffb_model_config *cfg, int64_t max_seq_len, int device,
                       int tp_rank, int tp_size, ffb_model **out);
+/* Same, with the persistent grid limited to `grid` CTAs (0 = one per SM),
+ * e.g. to co-locate the ranks of a TP group on one GPU for testing. */
+ffb_status ffb_create_ex(const ffb_model_config *cfg, int64_t max_seq_len, int device,
+                         int tp_rank, int tp_size, int grid, ffb_model **out);
+
+/* Tensor-parallel wiring: every rank exports a blob (ffb_tp_blob_bytes
+ * bytes: its exchange buffers as raw pointers + CUDA IPC handles), the blobs
+ * are all-gathered by the caller (e.g. torch.distributed), and every rank
+ * connects to the array of tp_size blobs ordered by rank.  Same-process
+ * ranks use the raw pointers, other processes open the IPC handles. */
+int64_t ffb_tp_blob_bytes(void);
+ffb_status ffb_tp_export(ffb_model *m, void *blob);
+ffb_status ffb_tp_connect(ffb_model *m, const void *blobs, int32_t n);
 void ffb_destroy(ffb_model *m);
 
 /* Weight packer.  `name` uses the reference's tensor names
@@ -151,7 +171,9 @@ ffb_status ffb_set_debug(ffb_model *m, int32_t flags);
 ffb_status ffb_set_trace(ffb_model *m, int enable);
 int64_t ffb_get_trace(ffb_model *m, uint64_t *out, int64_t n);
 
-/* One decode step for every batch row (reference.hpp:37-139 contract):
+/* One decode step for every batch row (reference.hpp:37-139 contract).
+ * With tensor parallelism every rank calls it with the same tokens; logits
+ * are this rank's vocab slice [batch][vocab/tp], greedy is the global argmax.
  * tokens[batch] (host), pos == kv length of every layer, appends one KV
  * position per layer.  logits_out: batch x vocab f32 (host, may be NULL);
  * greedy_out: batch int64 argmax with lowest-index tie break (host, may be

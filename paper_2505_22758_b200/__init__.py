@@ -26,7 +26,8 @@ import numpy as np
 __all__ = [
     "ModelConfig", "RunMode", "DecodeModel", "ValidationError", "DeviceError",
     "UnsupportedConfigError", "UsageError", "PRESETS", "model_preset", "lib", "LIB_PATH",
-    "tensor_names", "pack_quant_rows", "unpack_quant_rows",
+    "tensor_names", "pack_quant_rows", "unpack_quant_rows", "tp_shard", "tp_unshard",
+    "TPGroup", "all_gather_tp_blobs",
 ]
 
 HERE = os.path.dirname(os.path.abspath(__file__))
@@ -184,6 +185,62 @@ def unpack_quant_rows(packed: np.ndarray, cols: int, quant_bits: int) -> np.ndar
     return ((c.astype(np.float32) - zero[:, g]) * scale[:, g]).astype(np.float32)
 
 
+def tp_shard(cfg: ModelConfig, name: str, full: np.ndarray, rank: int, tp: int) -> np.ndarray:
+    """Host restatement of the TP shard of one reference tensor (what
+    ffb_upload_tensor keeps on rank `rank`, runtime.cu: resolve): Wqkv rows
+    of the rank's q heads, then k heads, then v heads; Waout all rows x the
+    rank's q-head columns; Wffn1 / Wffn2^T rows of d_inter slice r; lm_head
+    vocab rows of slice r; everything else replicated."""
+    if tp == 1:
+        return full
+    dh = cfg.d_head
+    nq, nkv = cfg.n_q_heads // tp, cfg.n_kv_heads // tp
+    ad, kv = nq * dh, nkv * dh
+    gq, gk = cfg.n_q_heads * dh, cfg.n_kv_heads * dh
+    di, v = cfg.d_inter // tp, cfg.vocab_size // tp
+    t = name.split(".")[-1]
+    if t == "wqkv":
+        return np.concatenate([full[rank * ad:(rank + 1) * ad],
+                               full[gq + rank * kv:gq + (rank + 1) * kv],
+                               full[gq + gk + rank * kv:gq + gk + (rank + 1) * kv]])
+    if t == "waout":
+        return full[:, rank * ad:(rank + 1) * ad]
+    if t == "wffn1":
+        return full[2 * rank * di:2 * (rank + 1) * di]
+    if t == "wffn2t":
+        return full[rank * di:(rank + 1) * di]
+    if name == "lm_head":
+        return full[rank * v:(rank + 1) * v]
+    return full
+
+
+def tp_unshard(cfg: ModelConfig, name: str, shards: list[np.ndarray]) -> np.ndarray:
+    """Inverse of tp_shard (replicated tensors: rank 0's copy)."""
+    tp = len(shards)
+    if tp == 1:
+        return shards[0]
+    t = name.split(".")[-1]
+    if t == "wqkv":
+        dh = cfg.d_head
+        ad, kv = cfg.n_q_heads // tp * dh, cfg.n_kv_heads // tp * dh
+        return np.concatenate([s[:ad] for s in shards] + [s[ad:ad + kv] for s in shards] +
+                              [s[ad + kv:] for s in shards])
+    if t == "waout":
+        return np.concatenate(shards, axis=1)
+    if t in ("wffn1", "wffn2t") or name == "lm_head":
+        return np.concatenate(shards)
+    return shards[0]
+
+
+def all_gather_tp_blobs(blob: bytes, group=None) -> list[bytes]:
+    """Multi-process TP wiring: all-gather every rank's ffb_tp_export blob
+    over torch.distributed (any backend), ordered by rank."""
+    import torch.distributed as dist
+    out = [None] * dist.get_world_size(group)
+    dist.all_gather_object(out, bytes(blob), group=group)
+    return out
+
+
 def tensor_names(cfg: ModelConfig) -> list[str]:
     """Reference tensor names (tensor_store.hpp:344-363) in upload order."""
     names = []
@@ -209,6 +266,11 @@ def lib():
     L.ffb_version.restype = C.c_char_p
     L.ffb_config_supported.argtypes = [P(_Cfg)]
     L.ffb_create.argtypes = [P(_Cfg), C.c_int64, C.c_int, C.c_int, C.c_int, P(C.c_void_p)]
+    L.ffb_create_ex.argtypes = [P(_Cfg), C.c_int64, C.c_int, C.c_int, C.c_int, C.c_int,
+                                P(C.c_void_p)]
+    L.ffb_tp_blob_bytes.restype = C.c_int64
+    L.ffb_tp_export.argtypes = [C.c_void_p, C.c_void_p]
+    L.ffb_tp_connect.argtypes = [C.c_void_p, C.c_void_p, C.c_int32]
     L.ffb_destroy.argtypes = [C.c_void_p]
     L.ffb_destroy.restype = None
     L.ffb_upload_tensor.argtypes = [C.c_void_p, C.c_char_p, P(C.c_float), C.c_int64]
@@ -265,16 +327,34 @@ class DecodeModel:
     """
 
     def __init__(self, cfg: ModelConfig, max_seq_len: int, device: int = 0,
-                 mode: RunMode = RunMode.FUSED_OVERLAP, tp_rank: int = 0, tp_size: int = 1):
+                 mode: RunMode = RunMode.FUSED_OVERLAP, tp_rank: int = 0, tp_size: int = 1,
+                 grid: int = 0):
+        """cfg is the WHOLE model; with tp_size > 1 this handle is shard
+        tp_rank (ffb_create_ex) and must be connected to its
+        peers (tp_connect) before stepping."""
         L = lib()
         self.cfg = cfg
+        self.tp_rank, self.tp_size = tp_rank, tp_size
+        self.device = device
         self.max_seq_len = max_seq_len
         self._c = cfg._c()
         h = C.c_void_p()
-        _check(L.ffb_create(C.byref(self._c), max_seq_len, device, tp_rank, tp_size,
-                            C.byref(h)))
+        _check(L.ffb_create_ex(C.byref(self._c), max_seq_len, device, tp_rank, tp_size, grid,
+                               C.byref(h)))
         self._h = h
         self.set_mode(mode)
+
+    # ------------------------------------------------------------ TP wiring
+    def tp_blob(self) -> bytes:
+        """This rank's exchange-buffer descriptor (ffb_tp_export)."""
+        buf = C.create_string_buffer(lib().ffb_tp_blob_bytes())
+        _check(lib().ffb_tp_export(self._h, buf))
+        return buf.raw
+
+    def tp_connect(self, blobs: list[bytes]):
+        """Connect to every rank's blob, ordered by rank (ffb_tp_connect)."""
+        raw = b"".join(blobs)
+        _check(lib().ffb_tp_connect(self._h, C.create_string_buffer(raw, len(raw)), len(blobs)))
 
     @staticmethod
     def supported(cfg: ModelConfig) -> bool:
@@ -417,3 +497,89 @@ class DecodeModel:
 
     def logits_device_ptr(self) -> int:
         return lib().ffb_logits_device(self._h) or 0
+
+
+class TPGroup:
+    """The ranks of one tensor-parallel group driven from ONE process: on
+    several GPUs, or co-located on one GPU with the SMs split between the
+    ranks (grid = SMs / tp each) -- the single-GPU test harness of the TP
+    path.  Steps launch every rank asynchronously on its own stream (the
+    ranks wait for each other inside the kernel), then synchronise.  Logits
+    are gathered across ranks (each rank holds a vocab slice)."""
+
+    def __init__(self, cfg: ModelConfig, max_seq_len: int, tp: int, devices=None, grid: int = 0,
+                 mode: RunMode = RunMode.FUSED_OVERLAP):
+        import torch
+        self.torch = torch
+        self.cfg, self.tp = cfg, tp
+        devices = devices or [0] * tp
+        if grid == 0 and len(set(devices)) < tp:
+            sms = torch.cuda.get_device_properties(devices[0]).multi_processor_count
+            grid = sms // tp
+        self.ranks = [DecodeModel(cfg, max_seq_len, device=d, mode=mode, tp_rank=r, tp_size=tp,
+                                  grid=grid) for r, d in enumerate(devices)]
+        blobs = [m.tp_blob() for m in self.ranks]
+        for m in self.ranks:
+            m.tp_connect(blobs)
+        self.streams = [torch.cuda.Stream(device=d) for d in devices]
+        self.devices = devices
+
+    def close(self):
+        for m in self.ranks:
+            m.close()
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    def upload_store(self, store):
+        for m in self.ranks:
+            m.upload_store(store)
+
+    def init_synthetic(self, seed: int = 1234):
+        for m in self.ranks:
+            m.init_synthetic(seed)
+
+    def kv_import(self, k, v, n_pos):
+        for m in self.ranks:
+            m.kv_import(k, v, n_pos)
+
+    def set_length(self, layer, n):
+        for m in self.ranks:
+            m.set_length(layer, n)
+
+    def set_mode(self, mode):
+        for m in self.ranks:
+            m.set_mode(mode)
+
+    def length(self, layer):
+        return self.ranks[0].length(layer)
+
+    def step(self, tokens, pos: int):
+        """One decode step on every rank: (logits [B][V] gathered, greedy [B])."""
+        torch = self.torch
+        c = self.cfg
+        tok = np.ascontiguousarray(np.asarray(tokens, dtype=np.int64).reshape(-1))
+        if tok.size != c.batch:
+            raise ValidationError("execute_program: one token per batch row required")
+        vl = c.vocab_size // self.tp
+        dts = [torch.from_numpy(tok).to(f"cuda:{d}") for d in self.devices]
+        lgs = [torch.empty((c.batch, vl), dtype=torch.float32, device=f"cuda:{d}")
+               for d in self.devices]
+        grs = [torch.empty(c.batch, dtype=torch.int64, device=f"cuda:{d}") for d in self.devices]
+        for d, s in zip(self.devices, self.streams):
+            s.wait_stream(torch.cuda.current_stream(d))
+        for m, t, lg, gr, s in zip(self.ranks, dts, lgs, grs, self.streams):
+            m.step_device(t.data_ptr(), pos, lg.data_ptr(), gr.data_ptr(), s.cuda_stream)
+        for s in self.streams:
+            s.synchronize()
+        greedy = [g.cpu().numpy() for g in grs]
+        for g in greedy[1:]:  # every rank agrees on the global argmax
+            if not np.array_equal(g, greedy[0]):
+                raise DeviceError(f"TP ranks disagree on the greedy token: {greedy}")
+        return np.concatenate([lg.cpu().numpy() for lg in lgs], axis=1), greedy[0]
+
+    def forward(self, tokens, pos: int) -> np.ndarray:
+        return self.step(tokens, pos)[0]

@@ -122,6 +122,15 @@ struct DecodeParams {
     // that a per-SM weighted plan (ffb_calibrate) follows the SM whatever
     // block index the launch put there; nullptr -> blockIdx.x
     const int16_t* sm_rank;
+    // tensor parallelism (tp_size > 1): the residual deltas of S_AOUT and
+    // S_RED and the LM-head argmax are exchanged with the other ranks over
+    // peer memory (NVLink P2P / same device).  xch[r]: rank r's exchange
+    // buffer [2 stage][2 layer parity][B][D] f32 + [kMaxTP][B] argmax slots;
+    // xflag[r]: rank r's arrival flags [L][2][grid] + [1] (argmax).
+    int32_t tp_size, tp_rank;
+    int32_t vocab_base;   // first global vocab row of this rank's lm_head slice
+    float* xch[8];
+    uint32_t* xflag[8];
     float eps;
     double rope_theta;
 };
@@ -137,15 +146,20 @@ struct DecodeParams {
 // reference's dequantized f32 weights (the packer re-derives them exactly).
 constexpr int kQuantGroup = 128;
 
+// Shape of one tensor-parallel shard (TP = 1: the whole model): the residual
+// width D and the norms/embedding are replicated; NQ / NKV are this shard's
+// query / kv heads (attention width AD = NQ * DH, = D when TP = 1) and DI its
+// slice of d_inter.
 template <int D_, int DI_, int DH_, int NQ_, int NKV_, int B_, int QB_ = 0>
 struct Shape {
     static constexpr int D = D_, DI = DI_, DH = DH_, NQ = NQ_, NKV = NKV_, B = B_, QB = QB_;
+    static constexpr int AD = NQ * DH;
     static constexpr int QPG = NQ / NKV;
     static constexpr int QKVR = (NQ + 2 * NKV) * DH;
-    static_assert(D == NQ * DH, "d_model must equal n_q_heads * d_head");
+    static_assert(AD <= D && D % AD == 0, "attention width divides d_model");
     static_assert(NQ % NKV == 0, "GQA grouping");
     static_assert(QB == 0 || QB == 4 || QB == 8, "weight format");
-    static_assert(QB == 0 || D % kQuantGroup == 0, "quant groups tile the row");
+    static_assert(QB == 0 || AD % kQuantGroup == 0, "quant groups tile the row");
 };
 
 // bytes of one streamed-matrix row of `cols` columns in format qb
@@ -154,59 +168,79 @@ __host__ __device__ constexpr int weight_row_bytes(int cols, int qb) {
                    : ((qb == 4 ? cols / 2 : cols) + 5 * (cols / kQuantGroup) + 15) / 16 * 16;
 }
 
+constexpr int kNCW = 8;              // consumer warps
+constexpr int kNCT = kNCW * 32;      // consumer threads
+constexpr int cmin_(int a, int b) { return a < b ? a : b; }
+constexpr int cmax_(int a, int b) { return a > b ? a : b; }
+constexpr int pow2_le_(int v) {
+    return v >= 32 ? 32 : v >= 16 ? 16 : v >= 8 ? 8 : v >= 4 ? 4 : v >= 2 ? 2 : 1;
+}
+
+// GEMV mapping of streamed rows with K columns (K = D for Wqkv / Wffn1 /
+// Wffn2^T / lm_head, K = AD for the Waout shard).  bf16: a row = NV 16-byte
+// vectors, thread lt of a row takes vectors lt, lt + TPR, ... (CPT = 8 VPT
+// columns, strided).  quant: thread lt takes CPT contiguous columns (one
+// quant group), so one (scale, zero) per row and thread.
+template <class S, int K_>
+struct RowMap {
+    static constexpr int K = K_;
+    static constexpr int QB = S::QB;
+    static constexpr int NG = K / kQuantGroup;      // quant groups per row
+    static constexpr int CODE_BYTES = QB == 4 ? K / 2 : K;
+    static constexpr int ROW_BYTES = weight_row_bytes(K, QB);
+    static constexpr int NV = K / 8;
+    static constexpr int CPT = QB == 0 ? 8 * (NV / cmin_(NV, kNCT))
+                                       : cmin_(cmin_(32, K / 32), 64 / S::B);
+    static constexpr int NCH = CPT / 8;             // 8-column chunks per thread per row
+    static constexpr int VPT = NCH;
+    static constexpr int TPR = K / CPT;             // threads per row
+    static constexpr int RG = kNCT / TPR;           // row groups working in parallel
+    static constexpr int WPR = TPR / 32;            // warps per row
+    // rows per thread per slot: bf16 fills a 32 KiB slot; quant takes the
+    // largest power of two with RPT * B <= 32 and a slot <= 32 KiB
+    static constexpr int RPT = QB == 0 ? cmin_((32768 / ROW_BYTES) / RG, 32 / S::B)
+                                       : cmax_(2 / RG, cmin_(pow2_le_(32 / S::B),
+                                                             pow2_le_(cmax_(1, 32768 / (RG * ROW_BYTES)))));
+    static constexpr int RPS = RG * RPT;            // rows per slot
+    static constexpr int SLOT = (RPS * ROW_BYTES + 127) / 128 * 128;
+    // rows per epilogue batch (whole slots; >= 64/B rows so barriers are rare)
+    static constexpr int RB = RPS > 64 / S::B ? RPS : ((64 / S::B) / RPS) * RPS;
+    static_assert(TPR % 32 == 0 && TPR <= kNCT && kNCT % TPR == 0, "a row must span whole warps");
+    static_assert(K % CPT == 0 && CPT % 8 == 0, "row mapping");
+    static_assert(QB == 0 || kQuantGroup % CPT == 0, "a thread's columns lie in one group");
+    static_assert(RPS >= 2 && RPS % 2 == 0 && RPS % RG == 0, "slot rows");
+    static_assert(RPS * S::B <= kNCT && RB * S::B <= kNCT, "epilogue threads");
+    static_assert(RPT * S::B <= 32 && (RPT & (RPT - 1)) == 0, "one transposed warp reduction per slot");
+};
+
 template <class S>
-struct KTraits {
-    static constexpr int NCW = 8;                   // consumer warps
-    static constexpr int NCT = NCW * 32;            // consumer threads
+struct KTraits : RowMap<S, S::D> {
+    using MD = RowMap<S, S::D>;   // rows of d_model columns
+    using MA = RowMap<S, S::AD>;  // Waout shard rows (attention width)
+    static constexpr int NCW = kNCW;
+    static constexpr int NCT = kNCT;
     // + a producer warpgroup (one active lane): with 12 warps the warpgroups
     // rebalance registers (setmaxnreg) -- the producer gives its registers to
     // the two consumer warpgroups (9 warps would cap everyone at 168)
     static constexpr int NTHREADS = NCT + 128;
     static constexpr int PRODUCER_REGS = 56;
     static constexpr int CONSUMER_REGS = 224;  // 4*32*56 + 8*32*224 <= 64K
-    static constexpr int QB = S::QB;
-    static constexpr int NG = S::D / kQuantGroup;   // quant groups per row
-    static constexpr int CODE_BYTES = QB == 4 ? S::D / 2 : S::D;
-    static constexpr int ROW_BYTES = weight_row_bytes(S::D, QB);
     static constexpr int cmin(int a, int b) { return a < b ? a : b; }
     static constexpr int cmax(int a, int b) { return a > b ? a : b; }
-    // GEMV mapping.  bf16: a row of D = NV 16-byte vectors, thread lt of a
-    // row takes vectors lt, lt + TPR, ... (CPT = 8 VPT columns, strided).
-    // quant: thread lt takes CPT contiguous columns (one quant group), so
-    // one (scale, zero) per row and thread.
-    static constexpr int NV = S::D / 8;
-    static constexpr int CPT = QB == 0 ? 8 * (NV / cmin(NV, NCT))
-                                       : cmin(cmin(32, S::D / 32), 64 / S::B);
-    static constexpr int NCH = CPT / 8;             // 8-column chunks per thread per row
-    static constexpr int VPT = NCH;
-    static constexpr int TPR = S::D / CPT;          // threads per row
-    static constexpr int RG = NCT / TPR;            // row groups working in parallel
-    static constexpr int WPR = TPR / 32;            // warps per row
-    static constexpr int pow2_le(int v) { return v >= 32 ? 32 : v >= 16 ? 16 : v >= 8 ? 8 : v >= 4 ? 4 : v >= 2 ? 2 : 1; }
-    // rows per thread per slot: bf16 fills a 32 KiB slot; quant takes the
-    // largest power of two with RPT * B <= 32 and a slot <= 32 KiB
-    static constexpr int RPT = QB == 0 ? (32768 / ROW_BYTES) / RG
-                                       : cmax(2 / RG, cmin(pow2_le(32 / S::B),
-                                                           pow2_le(cmax(1, 32768 / (RG * ROW_BYTES)))));
-    static constexpr int RPS = RG * RPT;            // rows per slot
-    static constexpr int SLOT_BYTES = QB == 0 ? 32768 : (RPS * ROW_BYTES + 127) / 128 * 128;
-    // rows per epilogue batch (whole slots; >= 64/B rows so barriers are rare)
-    static constexpr int RB = RPS > 64 / S::B ? RPS : ((64 / S::B) / RPS) * RPS;
+    static constexpr int SLOT_BYTES = S::QB == 0 ? 32768 : cmax(MD::SLOT, MA::SLOT);
+    static constexpr int RED_FLOATS = cmax(MD::WPR * MD::RB, MA::WPR * MA::RB) * S::B;
     static constexpr int KVC = SLOT_BYTES / (2 * S::DH * 2);  // KV positions per slot
     static constexpr int DPL = S::DH / 32;          // attention dims per lane
-    static constexpr int TMAX = 160;                // max GLU pairs per CTA (host-checked)
-    static_assert(TPR % 32 == 0 && TPR <= NCT && NCT % TPR == 0, "a row must span whole warps");
-    static_assert(S::D % CPT == 0 && CPT % 8 == 0, "row mapping");
-    static_assert(QB == 0 || kQuantGroup % CPT == 0, "a thread's columns lie in one group");
-    static_assert(RPS >= 2 && RPS % 2 == 0 && RPS % RG == 0, "slot rows");
-    static_assert(RPS * S::B <= NCT && RB * S::B <= NCT, "epilogue threads");
-    static_assert(RPT * S::B <= 32 && (RPT & (RPT - 1)) == 0, "one transposed warp reduction per slot");
+    // max GLU pairs / Waout rows per CTA (host-checked): the d_inter share of
+    // one SM with calibration headroom (weights up to 1.3x the mean)
+    static constexpr int TMAX = cmax(160, ((S::DI * 135) / (100 * 148) + 15) / 16 * 16);
+    static_assert(MD::SLOT <= SLOT_BYTES && MA::SLOT <= SLOT_BYTES, "slot fits both row maps");
     static_assert(S::DH % 32 == 0 && DPL <= 8, "attention lane split");
     static_assert(KVC >= 1 && (SLOT_BYTES / 2) % 16 == 0, "kv chunk");
 
     // ---- shared memory carve-up (bytes) ----
-    static constexpr int OFF_RED = 0;  // [2][WPR][RPS][B] f32
-    static constexpr int SZ_RED = 2 * WPR * RB * S::B * 4;
+    static constexpr int OFF_RED = 0;  // [2][WPR][RB][B] f32 (largest row map)
+    static constexpr int SZ_RED = 2 * RED_FLOATS * 4;
     static constexpr int OFF_H = OFF_RED + SZ_RED;  // [B][TMAX] f32
     static constexpr int SZ_H = S::B * TMAX * 4;
     static constexpr int OFF_ROPE = OFF_H + SZ_H;  // [DH/2][2] f32
@@ -274,7 +308,7 @@ struct DecodeCta {
     }
 
     __device__ float* red_buf(uint32_t it) {
-        return reinterpret_cast<float*>(smem + T::OFF_RED) + (it & 1) * (T::WPR * T::RB * B);
+        return reinterpret_cast<float*>(smem + T::OFF_RED) + (it & 1) * T::RED_FLOATS;
     }
     __device__ float* h_s() { return reinterpret_cast<float*>(smem + T::OFF_H); }
     __device__ float* rope() { return reinterpret_cast<float*>(smem + T::OFF_ROPE); }
@@ -368,6 +402,7 @@ struct DecodeCta {
         int r0, r1;
         bool kv;
         bool pool;  // the GLU work pool: one marker chunk, claimed dynamically
+        int row_bytes = T::ROW_BYTES, rps = T::RPS;  // matrix row geometry
     };
 
     // The lists of (stage, sub) in consumption order; false past the end.
@@ -396,7 +431,8 @@ struct DecodeCta {
             }
             case S_AOUT:
                 if (sub > 0) return false;
-                L = {p.waout + (size_t)l * D * T::ROW_BYTES, pl.aout_r0, pl.aout_r1, false, false};
+                L = {p.waout + (size_t)l * D * MA::ROW_BYTES, pl.aout_r0, pl.aout_r1, false, false,
+                     MA::ROW_BYTES, MA::RPS};
                 return true;
             case S_GLU:
                 if (sub == 0) L = {p.wffn1 + (size_t)l * 2 * S::DI * T::ROW_BYTES, 2 * pl.glu_t0,
@@ -458,11 +494,11 @@ struct DecodeCta {
                 *bytes = static_cast<uint32_t>(n) * DH * 2;
                 c.c0 += T::KVC;
             } else {
-                const int n = min(T::RPS, c.L.r1 - c.c0);
-                *src0 = c.L.base + (size_t)c.c0 * T::ROW_BYTES;
+                const int n = min(c.L.rps, c.L.r1 - c.c0);
+                *src0 = c.L.base + (size_t)c.c0 * c.L.row_bytes;
                 *src1 = nullptr;
-                *bytes = static_cast<uint32_t>(n) * T::ROW_BYTES;
-                c.c0 += T::RPS;
+                *bytes = static_cast<uint32_t>(n) * c.L.row_bytes;
+                c.c0 += c.L.rps;
             }
             return true;
         }
@@ -691,13 +727,18 @@ struct DecodeCta {
     // s * sum_i (c_i - z) a_i = s * (sum_i c_i a_i - z * sum[b]) -- and, for
     // int4, pre-scale column e by q4_scale(e), the inverse of the power of
     // 16 at which the nibble decode (q4_decode) leaves code e.
+    using MD = typename T::MD;
+    using MA = typename T::MA;
+
+    template <class M = MD>
     struct Act {
-        float v[B][T::NCH][8];
+        float v[B][M::NCH][8];
         float sum[B];
     };
 
+    template <class M = MD>
     __device__ static int col_of(int lt, int ci) {
-        return T::QB ? lt * T::CPT + ci * 8 : (lt + ci * T::TPR) * 8;
+        return M::QB ? lt * M::CPT + ci * 8 : (lt + ci * M::TPR) * 8;
     }
 
     // int4 nibble e of a 32-bit code word is decoded in place as c * 16^k(e):
@@ -712,14 +753,15 @@ struct DecodeCta {
     // Load the activations (RMSNorm'd with `gain` when given,
     // numerics.hpp:14-24).  src_emb: layer-0 input straight from the bf16
     // embedding.  Gains are constants, fetched before the dependency wait.
-    __device__ void load_act(Act& act, const float* src, bool from_emb, const float* gain,
+    template <class M = MD>
+    __device__ void load_act(Act<M>& act, const float* src, bool from_emb, const float* gain,
                              int stage) {
-        const int ctid = threadIdx.x, lt = ctid % T::TPR, rg = ctid / T::TPR;
-        float g[T::NCH][8];
+        const int ctid = threadIdx.x, lt = ctid % M::TPR, rg = ctid / M::TPR;
+        float g[M::NCH][8];
         if (gain != nullptr) {
 #pragma unroll
-            for (int j = 0; j < T::NCH; ++j) {
-                const int col = col_of(lt, j);
+            for (int j = 0; j < M::NCH; ++j) {
+                const int col = col_of<M>(lt, j);
                 const float4 g0 = __ldg(reinterpret_cast<const float4*>(gain + col));
                 const float4 g1 = __ldg(reinterpret_cast<const float4*>(gain + col + 4));
                 g[j][0] = g0.x; g[j][1] = g0.y; g[j][2] = g0.z; g[j][3] = g0.w;
@@ -730,8 +772,8 @@ struct DecodeCta {
 #pragma unroll
         for (int b = 0; b < B; ++b) {
 #pragma unroll
-            for (int j = 0; j < T::NCH; ++j) {
-                const int col = col_of(lt, j);
+            for (int j = 0; j < M::NCH; ++j) {
+                const int col = col_of<M>(lt, j);
                 float* a = act.v[b][j];
                 if (from_emb) {
                     const __nv_bfloat16* e = p.embedding + (size_t)p.tokens[b] * D + col;
@@ -739,8 +781,8 @@ struct DecodeCta {
                     a[0] = bf_lo(w.x); a[1] = bf_hi(w.x); a[2] = bf_lo(w.y); a[3] = bf_hi(w.y);
                     a[4] = bf_lo(w.z); a[5] = bf_hi(w.z); a[6] = bf_lo(w.w); a[7] = bf_hi(w.w);
                 } else {
-                    const float4 a0 = ldcg_f4(src + (size_t)b * D + col);
-                    const float4 a1 = ldcg_f4(src + (size_t)b * D + col + 4);
+                    const float4 a0 = ldcg_f4(src + (size_t)b * M::K + col);
+                    const float4 a1 = ldcg_f4(src + (size_t)b * M::K + col + 4);
                     a[0] = a0.x; a[1] = a0.y; a[2] = a0.z; a[3] = a0.w;
                     a[4] = a1.x; a[5] = a1.y; a[6] = a1.z; a[7] = a1.w;
                 }
@@ -753,7 +795,7 @@ struct DecodeCta {
                 float s = 0.f;
                 if (rg == 0) {
 #pragma unroll
-                    for (int j = 0; j < T::NCH; ++j)
+                    for (int j = 0; j < M::NCH; ++j)
 #pragma unroll
                         for (int e = 0; e < 8; ++e) s = fmaf(act.v[b][j][e], act.v[b][j][e], s);
                 }
@@ -770,26 +812,26 @@ struct DecodeCta {
             for (int b = 0; b < B; ++b) {
                 float t = 0.f;
                 for (int w = 0; w < NCW; ++w) t += ns[w * B + b];
-                inv[b] = 1.0f / sqrtf(t / static_cast<float>(D) + p.eps);
+                inv[b] = 1.0f / sqrtf(t / static_cast<float>(M::K) + p.eps);
             }
             consumer_sync(NCT);  // ns reusable afterwards
 #pragma unroll
-            for (int j = 0; j < T::NCH; ++j)
+            for (int j = 0; j < M::NCH; ++j)
 #pragma unroll
                 for (int b = 0; b < B; ++b)
 #pragma unroll
                     for (int e = 0; e < 8; ++e) act.v[b][j][e] = g[j][e] * act.v[b][j][e] * inv[b];
         }
-        if constexpr (T::QB != 0) {
+        if constexpr (M::QB != 0) {
 #pragma unroll
             for (int b = 0; b < B; ++b) {
                 float t = 0.f;
 #pragma unroll
-                for (int j = 0; j < T::NCH; ++j)
+                for (int j = 0; j < M::NCH; ++j)
 #pragma unroll
                     for (int e = 0; e < 8; ++e) {
                         t += act.v[b][j][e];
-                        if constexpr (T::QB == 4) act.v[b][j][e] *= q4_scale(e);
+                        if constexpr (M::QB == 4) act.v[b][j][e] *= q4_scale(e);
                     }
                 act.sum[b] = t;
             }
@@ -829,13 +871,15 @@ struct DecodeCta {
 
     // This thread's codes of one quantized row (NCH chunks of 8 columns),
     // its group's scale and zero point.
+    template <class M = MD>
     struct QRow {
-        uint32_t w[T::QB == 4 ? T::NCH : 2 * T::NCH];
+        uint32_t w[M::QB == 4 ? M::NCH : 2 * M::NCH];
         float scale, zero;
     };
 
-    __device__ static void q_load(const uint8_t* rowp, int lt, QRow& q) {
-        constexpr int NW = T::QB == 4 ? T::NCH : 2 * T::NCH;  // 32-bit code words
+    template <class M = MD>
+    __device__ static void q_load(const uint8_t* rowp, int lt, QRow<M>& q) {
+        constexpr int NW = M::QB == 4 ? M::NCH : 2 * M::NCH;  // 32-bit code words
         const uint8_t* cp = rowp + lt * (NW * 4);
         if constexpr (NW == 4) {
             const uint4 v = lds_u128(cp);
@@ -852,14 +896,15 @@ struct DecodeCta {
                 q.w[i] = v.x; q.w[i + 1] = v.y; q.w[i + 2] = v.z; q.w[i + 3] = v.w;
             }
         }
-        const int g = (lt * T::CPT) / kQuantGroup;
-        q.scale = *reinterpret_cast<const float*>(rowp + T::CODE_BYTES + 4 * g);
-        q.zero = static_cast<float>(rowp[T::CODE_BYTES + 4 * T::NG + g]);
+        const int g = (lt * M::CPT) / kQuantGroup;
+        q.scale = *reinterpret_cast<const float*>(rowp + M::CODE_BYTES + 4 * g);
+        q.zero = static_cast<float>(rowp[M::CODE_BYTES + 4 * M::NG + g]);
     }
 
     // decoded 8-column chunk ci of a quantized row: d[k] = columns (2k, 2k+1)
     // as exact f32 integers (int4: times the powers of 16 of q4_scale)
-    __device__ static void q_chunk(const QRow& q, int ci, float2 (&d)[4]) {
+    template <class M>
+    __device__ static void q_chunk(const QRow<M>& q, int ci, float2 (&d)[4]) {
         if constexpr (T::QB == 4) {
             q4_decode(q.w[ci], d);
         } else {
@@ -935,28 +980,28 @@ struct DecodeCta {
     // red[wr][row][b].  Warps never wait for each other inside a batch of RB
     // rows; `epi(c0, nrows, red)` runs once per batch after one named barrier
     // (red is double-buffered across batches).
-    template <class Epi>
-    __device__ void gemv(uint32_t& it, const Act& act, int r0, int r1, Epi&& epi) {
-        constexpr int V = T::RPT * B, LV = ilog2(V);
+    template <class M = MD, class Epi>
+    __device__ void gemv(uint32_t& it, const Act<M>& act, int r0, int r1, Epi&& epi) {
+        constexpr int V = M::RPT * B, LV = ilog2(V);
         const int ctid = threadIdx.x, lane = ctid % 32;
-        const int rg = ctid / T::TPR, lt = ctid % T::TPR, wr = lt / 32;
+        const int rg = ctid / M::TPR, lt = ctid % M::TPR, wr = lt / 32;
         const int vidx = lane >> (5 - LV), vr = vidx / B, vb = vidx % B;
         const bool writer = (lane & ((32 >> LV) - 1)) == 0;
         int batch_c0 = r0;
         uint32_t nbatch = 0;
         float* red = red_buf(0);
-        for (int c0 = r0; c0 < r1; c0 += T::RPS) {
-            const int nrows = min(T::RPS, r1 - c0);
+        for (int c0 = r0; c0 < r1; c0 += M::RPS) {
+            const int nrows = min(M::RPS, r1 - c0);
             const uint32_t slot = it % T::NSLOTS, par = (it / T::NSLOTS) & 1;
             wait_full(slot, par);
             const uint8_t* base = ring + slot * T::SLOT_BYTES;
             float v[V];
 #pragma unroll
-            for (int r = 0; r < T::RPT; ++r) {
+            for (int r = 0; r < M::RPT; ++r) {
                 // rows past nrows read stale (valid) smem; their sums are dropped
-                const uint8_t* rowp = base + (rg + r * T::RG) * T::ROW_BYTES;
-                if constexpr (T::QB != 0) {  // fused dequant: s * (sum c a - z sum a)
-                    QRow q;
+                const uint8_t* rowp = base + (rg + r * M::RG) * M::ROW_BYTES;
+                if constexpr (M::QB != 0) {  // fused dequant: s * (sum c a - z sum a)
+                    QRow<M> q;
                     q_load(rowp, lt, q);
                     float2 acc[B][4];  // 4 independent FFMA2 chains per batch row
 #pragma unroll
@@ -964,7 +1009,7 @@ struct DecodeCta {
 #pragma unroll
                         for (int k = 0; k < 4; ++k) acc[b][k] = make_float2(0.f, 0.f);
 #pragma unroll
-                    for (int j = 0; j < T::NCH; ++j) {
+                    for (int j = 0; j < M::NCH; ++j) {
                         float2 d[4];
                         q_chunk(q, j, d);
 #pragma unroll
@@ -988,8 +1033,8 @@ struct DecodeCta {
 #pragma unroll
                 for (int b = 0; b < B; ++b) a0[b] = a1[b] = 0.f;
 #pragma unroll
-                for (int j = 0; j < T::VPT; ++j) {
-                    const uint4 w = lds_u128(rowp + (lt + j * T::TPR) * 16);
+                for (int j = 0; j < M::VPT; ++j) {
+                    const uint4 w = lds_u128(rowp + (lt + j * M::TPR) * 16);
 #pragma unroll
                     for (int b = 0; b < B; ++b) {
                         const float(&a)[8] = act.v[b][j];
@@ -1009,29 +1054,30 @@ struct DecodeCta {
             __syncwarp();
             if (lane == 0) mbar_arrive(&empty[slot]);
             const float s = reduce_multi<V>(v, lane);
-            const int row = rg + vr * T::RG;
-            if (writer && row < nrows) red[(wr * T::RB + (c0 - batch_c0) + row) * B + vb] = s;
+            const int row = rg + vr * M::RG;
+            if (writer && row < nrows) red[(wr * M::RB + (c0 - batch_c0) + row) * B + vb] = s;
             ++it;
             const int batch_rows = c0 + nrows - batch_c0;
-            if (c0 + T::RPS >= r1 || batch_rows + T::RPS > T::RB) {
+            if (c0 + M::RPS >= r1 || batch_rows + M::RPS > M::RB) {
                 consumer_sync(NCT);
                 epi(batch_c0, batch_rows, red);
-                batch_c0 = c0 + T::RPS;
+                batch_c0 = c0 + M::RPS;
                 red = red_buf(++nbatch);
             }
         }
     }
 
+    template <class M = MD>
     __device__ static float row_total(const float* red, int row, int b) {
         float t = 0.f;
 #pragma unroll
-        for (int w = 0; w < T::WPR; ++w) t += red[(w * T::RB + row) * B + b];
+        for (int w = 0; w < M::WPR; ++w) t += red[(w * M::RB + row) * B + b];
         return t;
     }
 
     // ---------------------------------------------------------- S_QKV
     __device__ void stage_qkv(uint32_t& it, int l) {
-        Act act;
+        Act<> act;
         load_act(act, p.x, l == 0, p.norm_attn + (size_t)l * D, l * kStagesPerLayer + S_QKV);
         trace_mark(l * kStagesPerLayer + S_QKV, 3);
         const float* rp = rope();
@@ -1396,31 +1442,77 @@ struct DecodeCta {
         }
     }
 
+    // ---------------------------------------------------------- TP exchange
+    // Cross-rank sum of a residual delta: every rank's CTA i owns the same
+    // slice [c0, c1) of d_model (identical plans), writes its delta into its
+    // own exchange buffer, releases one arrival on CTA i's flag of every rank
+    // (system scope: peers on other GPUs), waits for TP arrivals on its own
+    // flag, then adds sum_r delta_r (fixed rank order: bit-identical x on
+    // every rank).  delta: [B][cnt] in smem, slot 0 (S_AOUT) or 1 (S_RED).
+    __device__ float* xch_slot(int r, int slot, int l) const {
+        return p.xch[r] + ((size_t)(slot * 2 + (l & 1)) * B) * D;
+    }
+
+    __device__ void tp_exchange_add(const float* delta, int c0, int cnt, int slot, int l) {
+        const int ctid = threadIdx.x;
+        float* mine = xch_slot(p.tp_rank, slot, l);
+        for (int i = ctid; i < cnt * B; i += NCT) {
+            const int b = i / cnt, c = i % cnt;
+            __stcg(mine + (size_t)b * D + c0 + c, delta[b * cnt + c]);
+        }
+        consumer_sync(NCT);
+        const size_t fi = ((size_t)l * 2 + slot) * grid + cta;
+        if (ctid < p.tp_size) red_release_sys(p.xflag[ctid] + fi, 1);
+        if (ctid == 0) spin_until_geq_sys(p.xflag[p.tp_rank] + fi, p.epoch * p.tp_size);
+        consumer_sync(NCT);
+        for (int i = ctid; i < cnt * B; i += NCT) {
+            const int b = i / cnt, c = i % cnt;
+            float t = 0.f;
+            for (int r = 0; r < p.tp_size; ++r)
+                t += ldcg_f(xch_slot(r, slot, l) + (size_t)b * D + c0 + c);
+            float* xp = p.x + (size_t)b * D + c0 + c;
+            __stcg(xp, ldcg_f(xp) + t);
+        }
+    }
+
     // ---------------------------------------------------------- S_AOUT
+    // x[rows] += Waout[rows] . attn_out.  TP: Waout is split by input
+    // columns (this rank's q heads, AD = NQ * DH of them), each rank holds a
+    // partial of every row, summed across ranks (tp_exchange_add).
     __device__ void stage_aout(uint32_t& it, int l) {
-        Act act;
-        load_act(act, p.attn_out, false, nullptr, l * kStagesPerLayer + S_AOUT);
+        Act<MA> act;
+        load_act<MA>(act, p.attn_out, false, nullptr, l * kStagesPerLayer + S_AOUT);
         const int ctid = threadIdx.x;
         const int r0 = pl.aout_r0, nr = pl.aout_r1 - pl.aout_r0;
         float* acc = h_s();  // [B][TMAX] row results; x updated once at the end
-        gemv(it, act, r0, pl.aout_r1, [&](int c0, int nrows, const float* red) {
+        gemv<MA>(it, act, r0, pl.aout_r1, [&](int c0, int nrows, const float* red) {
             if (ctid < nrows * B) {
                 const int r = ctid / B, b = ctid % B;
-                acc[b * T::TMAX + c0 - r0 + r] = row_total(red, r, b);
+                acc[b * T::TMAX + c0 - r0 + r] = row_total<MA>(red, r, b);
             }
         });
         consumer_sync(NCT);
-        for (int i = ctid; i < nr * B; i += NCT) {  // one L2 round trip for all rows
-            const int r = i / B, b = i % B;
-            float* xp = p.x + (size_t)b * D + r0 + r;
-            __stcg(xp, ldcg_f(xp) + acc[b * T::TMAX + r]);
+        if (p.tp_size > 1) {
+            float* d = wpart();  // [B][nr] compact copy for the exchange
+            for (int i = ctid; i < nr * B; i += NCT) {
+                const int b = i / nr, r = i % nr;
+                d[b * nr + r] = acc[b * T::TMAX + r];
+            }
+            consumer_sync(NCT);
+            tp_exchange_add(d, r0, nr, 0, l);
+        } else {
+            for (int i = ctid; i < nr * B; i += NCT) {  // one L2 round trip for all rows
+                const int r = i / B, b = i % B;
+                float* xp = p.x + (size_t)b * D + r0 + r;
+                __stcg(xp, ldcg_f(xp) + acc[b * T::TMAX + r]);
+            }
         }
         arrive(p.counters + l * kStagesPerLayer + S_AOUT, l * kStagesPerLayer + S_AOUT);
     }
 
     // ---------------------------------------------------------- S_GLU
     // in/gate rows [2 t0, 2 t1) of Wffn1 -> h[t - t0] = silu(gate) * in (smem)
-    __device__ void glu_ffn1(uint32_t& it, const Act& act, int t0, int t1) {
+    __device__ void glu_ffn1(uint32_t& it, const Act<>& act, int t0, int t1) {
         const int ctid = threadIdx.x;
         float* hs = h_s();
         gemv(it, act, 2 * t0, 2 * t1, [&](int c0, int nrows, const float* red) {
@@ -1464,7 +1556,7 @@ struct DecodeCta {
 #pragma unroll
                 for (int b = 0; b < B; ++b) hb[b] = hs[b * T::TMAX + (c0 - t0) + row];
                 if constexpr (T::QB != 0) {
-                    QRow q;
+                    QRow<> q;
                     q_load(base + row * T::ROW_BYTES, lt, q);
 #pragma unroll
                     for (int b = 0; b < B; ++b) {
@@ -1540,7 +1632,7 @@ struct DecodeCta {
     // Static slice [glu_t0, glu_t1) into glu_part[cta], then pool chunks
     // (claimed by this CTA's producer) each into pool_part[chunk].
     __device__ void stage_glu(uint32_t& it, int l) {
-        Act act;
+        Act<> act;
         load_act(act, p.x, false, p.norm_ffn + (size_t)l * D, l * kStagesPerLayer + S_GLU);
         glu_ffn1(it, act, pl.glu_t0, pl.glu_t1);
         glu_ffn2(it, pl.glu_t0, pl.glu_t1, p.glu_part + (size_t)cta * T::RG * B * D);
@@ -1572,7 +1664,8 @@ struct DecodeCta {
         // which CTA computed which pool chunk -> deterministic sums
         const int nstatic = grid * T::RG;
         const int nparts = nstatic + p.pool_chunks * T::RG;
-        float* scratch = wpart();  // [NCW][32]
+        float* scratch = wpart();          // [NCW][32]
+        float* delta = wpart() + NCW * 32;  // [B][c1 - c0] (TP)
         for (int b = 0; b < B; ++b) {
             for (int cb = c0; cb < c1; cb += 32) {
                 const int col = cb + lane;
@@ -1599,18 +1692,23 @@ struct DecodeCta {
                 if (warp == 0 && col < c1) {
                     float t = 0.f;
                     for (int w = 0; w < NCW; ++w) t += scratch[w * 32 + lane];
-                    float* xp = p.x + (size_t)b * D + col;
-                    __stcg(xp, ldcg_f(xp) + t);
+                    if (p.tp_size > 1) {
+                        delta[b * (c1 - c0) + col - c0] = t;  // exchanged below
+                    } else {
+                        float* xp = p.x + (size_t)b * D + col;
+                        __stcg(xp, ldcg_f(xp) + t);
+                    }
                 }
                 consumer_sync(NCT);
             }
         }
+        if (p.tp_size > 1) tp_exchange_add(delta, c0, c1 - c0, 1, l);
         arrive(p.counters + l * kStagesPerLayer + S_RED, l * kStagesPerLayer + S_RED);
     }
 
     // ---------------------------------------------------------- S_LMHEAD
     __device__ void stage_lmhead(uint32_t& it) {
-        Act act;
+        Act<> act;
         load_act(act, p.x, p.layers == 0, p.final_norm, p.layers * kStagesPerLayer);
         const int ctid = threadIdx.x;
         float best = -INFINITY;
@@ -1675,7 +1773,44 @@ struct DecodeCta {
                         any = true;
                     }
                 }
-                p.greedy[ctid] = bi;
+                if (p.tp_size == 1) {
+                    p.greedy[ctid] = bi;
+                } else {  // this rank's candidate, as a global vocab index
+                    cv[ctid] = any ? bv : -INFINITY;
+                    ci[ctid] = bi + p.vocab_base;
+                }
+            }
+            if (p.tp_size > 1) {
+                // exchange (value, index) with every rank; ranks own ascending
+                // vocab slices, so scanning ranks in order keeps the lowest
+                // index on ties (numerics.hpp:169-175)
+                consumer_sync(NCT);
+                const size_t amax_off = (size_t)4 * B * D;
+                const size_t fi = (size_t)p.layers * 2 * grid;
+                if (ctid < B * p.tp_size) {
+                    const int r = ctid / B, b = ctid % B;
+                    float* dst = p.xch[r] + amax_off + ((size_t)p.tp_rank * B + b) * 2;
+                    __stcg(dst, cv[b]);
+                    __stcg(dst + 1, __int_as_float(ci[b]));
+                }
+                consumer_sync(NCT);
+                if (ctid < p.tp_size) red_release_sys(p.xflag[ctid] + fi, 1);
+                if (ctid == 0) spin_until_geq_sys(p.xflag[p.tp_rank] + fi, p.epoch * p.tp_size);
+                consumer_sync(NCT);
+                if (ctid < B) {
+                    float bv = -INFINITY;
+                    int bi = 0;
+                    for (int r = 0; r < p.tp_size; ++r) {
+                        const float* src = p.xch[p.tp_rank] + amax_off + ((size_t)r * B + ctid) * 2;
+                        const float v = ldcg_f(src);
+                        const int i = __float_as_int(ldcg_f(src + 1));
+                        if (r == 0 || v > bv) {
+                            bv = v;
+                            bi = i;
+                        }
+                    }
+                    p.greedy[ctid] = bi;
+                }
             }
         }
     }

@@ -14,7 +14,7 @@ namespace ffb200 {
 
 struct KernelOps {
     int D, DI, DH, NQ, NKV, B, QB;
-    int threads, smem, nslots, slot_bytes, rg, tmax, kvc, rps, row_bytes;
+    int threads, smem, nslots, slot_bytes, rg, tmax, kvc, rps, row_bytes, row_bytes_a;
     cudaError_t (*prepare)();
     cudaError_t (*launch)(const DecodeParams&, int grid, cudaStream_t, bool cooperative);
 };
@@ -48,7 +48,7 @@ KernelOps make_ops() {
     return KernelOps{S::D,        S::DI,         S::DH,     S::NQ,         S::NKV, S::B,
                      S::QB,       T::NTHREADS,   T::SMEM_BYTES, T::NSLOTS, T::SLOT_BYTES,
                      T::RG,       T::TMAX,       T::KVC,    T::RPS,        T::ROW_BYTES,
-                     &prepare_impl<S>, &launch_impl<S>};
+                     T::MA::ROW_BYTES, &prepare_impl<S>, &launch_impl<S>};
 }
 
 // registration hooks, one per kernels_*.cu
@@ -56,5 +56,6 @@ void register_kernels_small(std::vector<KernelOps>& v);
 void register_kernels_1b(std::vector<KernelOps>& v);
 void register_kernels_8b(std::vector<KernelOps>& v);
 void register_kernels_quant(std::vector<KernelOps>& v);
+void register_kernels_70b(std::vector<KernelOps>& v);
 
 }  // namespace ffb200

@@ -136,6 +136,23 @@ __device__ __forceinline__ uint32_t atom_add_acq_rel_gpu(uint32_t* p, uint32_t v
     return old;
 }
 
+// system scope (peer GPUs over NVLink): tensor-parallel exchange flags
+__device__ __forceinline__ void red_release_sys(uint32_t* p, uint32_t v) {
+    asm volatile("red.release.sys.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+__device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
+    uint32_t v;
+    asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+__device__ __forceinline__ void spin_until_geq_sys(const uint32_t* p, uint32_t target) {
+    uint32_t n = 0;
+    uint64_t t0 = 0;
+    while (static_cast<int32_t>(ld_acquire_sys(p) - target) < 0) spin_watchdog(n, t0);
+}
+
 __device__ __forceinline__ void spin_until_geq(const uint32_t* p, uint32_t target) {
     // Monotone epoch counters: the value only grows, so >= is exact.
     uint32_t n = 0;

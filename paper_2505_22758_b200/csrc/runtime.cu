@@ -24,6 +24,8 @@
 #include <string>
 #include <vector>
 
+#include <unistd.h>
+
 #include "../../include/flashformer_b200.h"
 #include "kernel_ops.cuh"
 
@@ -59,6 +61,7 @@ const std::vector<KernelOps>& registry() {
         register_kernels_1b(v);
         register_kernels_8b(v);
         register_kernels_quant(v);
+        register_kernels_70b(v);
     });
     return v;
 }
@@ -192,8 +195,20 @@ int64_t kv_swz(int64_t d, int64_t pos) { return (((d >> 3) ^ (pos & 7)) << 3) | 
 
 }  // namespace
 
+constexpr int kMaxTP = 8;
+
 struct ffb_model {
-    ffb_model_config cfg{};
+    ffb_model_config cfg{};   // this shard's config (== gcfg when tp_size == 1)
+    ffb_model_config gcfg{};  // the whole model
+    int64_t vocab_base = 0;   // first global vocab row of this shard's lm_head
+    // tensor-parallel exchange (decode_kernel.cuh: tp_exchange_add)
+    float* xch = nullptr;           // [2][2][B][D] + [kMaxTP][B][2]
+    uint32_t* xflag = nullptr;      // [L][2][grid] + 1
+    size_t xch_bytes = 0, xflag_bytes = 0;
+    float* peer_xch[kMaxTP] = {};
+    uint32_t* peer_xflag[kMaxTP] = {};
+    bool tp_connected = false;
+    std::vector<void*> ipc_opened;
     const KernelOps* ops = nullptr;
     int device = 0, grid = 0, tp_rank = 0, tp_size = 1;
     int64_t max_seq = 0;
@@ -263,6 +278,7 @@ struct ffb_model {
 
     ~ffb_model() {
         if (device >= 0) cudaSetDevice(device);
+        for (void* q : ipc_opened) cudaIpcCloseMemHandle(q);
         for (void* p : allocs) cudaFree(p);
         if (tokens_pinned) cudaFreeHost(tokens_pinned);
         if (greedy_pinned) cudaFreeHost(greedy_pinned);
@@ -366,6 +382,9 @@ ffb_status build_plan(ffb_model* m) {
 // not see `grid` distinct SMs.
 ffb_status probe_sm_ranks(ffb_model* m) {
     const int G = m->grid;
+    int sms = 0;
+    CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, m->device));
+    if (G < std::min(sms, 160)) return FFB_OK;  // partial grid: SM set varies per launch
     int32_t* d_ids = nullptr;
     CUDA_TRY(cudaMalloc(&d_ids, sizeof(int32_t) * G));
     cudaError_t e = cudaFuncSetAttribute(smid_probe_kernel,
@@ -453,6 +472,13 @@ DecodeParams make_params(const ffb_model* m, int64_t pos, const int64_t* d_token
     p.pool_ct = m->pool_ct;
     p.pool_chunks = m->pool_chunks;
     p.sm_rank = (m->mode == FFB_MODE_BASELINE || !m->use_sm_rank) ? nullptr : m->sm_rank;
+    p.tp_size = m->tp_size;
+    p.tp_rank = m->tp_rank;
+    p.vocab_base = static_cast<int32_t>(m->vocab_base);
+    for (int r = 0; r < kMaxTP; ++r) {
+        p.xch[r] = m->peer_xch[r];
+        p.xflag[r] = m->peer_xflag[r];
+    }
     return p;
 }
 
@@ -462,6 +488,7 @@ DecodeParams make_params(const ffb_model* m, int64_t pos, const int64_t* d_token
 ffb_status reset_sync_state(ffb_model* m, cudaStream_t stream) {
     const int64_t Lc = std::max<int64_t>(1, m->cfg.layers);
     CUDA_TRY(cudaMemsetAsync(m->counters, 0, sizeof(uint32_t) * (Lc * 5 + 1), stream));
+    if (m->xflag) CUDA_TRY(cudaMemsetAsync(m->xflag, 0, m->xflag_bytes, stream));
     CUDA_TRY(cudaMemsetAsync(m->qkv_head_counters, 0,
                              sizeof(uint32_t) * Lc * m->cfg.n_kv_heads, stream));
     CUDA_TRY(cudaMemsetAsync(m->head_counters, 0,
@@ -494,21 +521,57 @@ ffb_status launch_step(ffb_model* m, int64_t pos, const int64_t* d_tokens, float
 }
 
 // Destination of one reference tensor: kind 0 = streamed matrix (rows of
-// ops->row_bytes, bf16 or packed quant), 1 = f32 vector, 2 = bf16 embedding
+// `row_bytes`, bf16 or packed quant), 1 = f32 vector, 2 = bf16 embedding.
+// The caller passes the WHOLE reference tensor (gcols columns); a TP shard
+// keeps the rows listed in `rows` (global row ranges, concatenated) and the
+// columns [col0, col0 + cols).
 struct TensorDst {
     void* ptr = nullptr;
-    int64_t n = 0;
     int kind = 0;
-    int64_t rows = 0;
+    int64_t gn = 0;          // expected element count of the reference tensor
+    int64_t gcols = 0;
+    int64_t col0 = 0, cols = 0;
+    std::vector<std::pair<int64_t, int64_t>> rows;  // [r0, r1) ranges
+    size_t row_bytes = 0;
+    int64_t local_rows() const {
+        int64_t n = 0;
+        for (auto& r : rows) n += r.second - r.first;
+        return n;
+    }
 };
 
 bool resolve(ffb_model* m, const std::string& name, TensorDst* d) {
-    const auto& c = m->cfg;
-    const int64_t D = c.d_model;
+    const auto& c = m->cfg;   // shard
+    const auto& g = m->gcfg;  // whole model
+    const int64_t D = c.d_model, r = m->tp_rank;
     const size_t RB = m->ops->row_bytes;
-    if (name == "embedding") { *d = {m->embedding, c.vocab_size * D, 2, c.vocab_size}; return true; }
-    if (name == "lm_head") { *d = {m->lm_head, c.vocab_size * D, 0, c.vocab_size}; return true; }
-    if (name == "final_norm") { *d = {m->final_norm, D, 1, 1}; return true; }
+    auto mat = [&](void* ptr, int64_t grows, std::vector<std::pair<int64_t, int64_t>> rows,
+                   int64_t col0, int64_t cols, size_t rb) {
+        d->ptr = ptr;
+        d->kind = 0;
+        d->gn = grows * D;
+        d->gcols = D;
+        d->col0 = col0;
+        d->cols = cols;
+        d->rows = std::move(rows);
+        d->row_bytes = rb;
+    };
+    auto vec = [&](void* ptr, int64_t n, int kind) {
+        d->ptr = ptr;
+        d->kind = kind;
+        d->gn = n;
+        d->gcols = kind == 2 ? D : n;
+        d->col0 = 0;
+        d->cols = d->gcols;
+        d->rows = {{0, n / d->gcols}};
+        d->row_bytes = kind == 2 ? D * 2 : n * 4;
+    };
+    if (name == "embedding") { vec(m->embedding, g.vocab_size * D, 2); return true; }
+    if (name == "lm_head") {
+        mat(m->lm_head, g.vocab_size, {{m->vocab_base, m->vocab_base + c.vocab_size}}, 0, D, RB);
+        return true;
+    }
+    if (name == "final_norm") { vec(m->final_norm, D, 1); return true; }
     if (name.rfind("layer.", 0) != 0) return false;
     size_t dot = name.find('.', 6);
     if (dot == std::string::npos) return false;
@@ -520,13 +583,24 @@ bool resolve(ffb_model* m, const std::string& name, TensorDst* d) {
     }
     if (l < 0 || l >= c.layers) return false;
     std::string t = name.substr(dot + 1);
-    const int64_t QR = m->qkv_rows();
-    if (t == "wqkv") *d = {m->wqkv + l * QR * RB, QR * D, 0, QR};
-    else if (t == "waout") *d = {m->waout + l * D * RB, D * D, 0, D};
-    else if (t == "wffn1") *d = {m->wffn1 + l * 2 * c.d_inter * RB, 2 * c.d_inter * D, 0, 2 * c.d_inter};
-    else if (t == "wffn2t") *d = {m->wffn2t + l * c.d_inter * RB, c.d_inter * D, 0, c.d_inter};
-    else if (t == "norm_attn") *d = {m->norm_attn + l * D, D, 1, 1};
-    else if (t == "norm_ffn") *d = {m->norm_ffn + l * D, D, 1, 1};
+    const int64_t QR = m->qkv_rows(), dh = c.d_head;
+    const int64_t AD = c.n_q_heads * dh;  // shard attention width
+    const int64_t gQ = g.n_q_heads * dh, gK = g.n_kv_heads * dh, KVl = c.n_kv_heads * dh;
+    if (t == "wqkv")  // this shard's q heads, then its k heads, then its v heads
+        mat(m->wqkv + l * QR * RB, (g.n_q_heads + 2 * g.n_kv_heads) * dh,
+            {{r * AD, (r + 1) * AD}, {gQ + r * KVl, gQ + (r + 1) * KVl},
+             {gQ + gK + r * KVl, gQ + gK + (r + 1) * KVl}},
+            0, D, RB);
+    else if (t == "waout")  // every output row, the input columns of this shard's q heads
+        mat(m->waout + l * D * m->ops->row_bytes_a, D, {{0, D}}, r * AD, AD, m->ops->row_bytes_a);
+    else if (t == "wffn1")  // interleaved (in, gate) row pairs of this d_inter slice
+        mat(m->wffn1 + l * 2 * c.d_inter * RB, 2 * g.d_inter,
+            {{2 * r * c.d_inter, 2 * (r + 1) * c.d_inter}}, 0, D, RB);
+    else if (t == "wffn2t")
+        mat(m->wffn2t + l * c.d_inter * RB, g.d_inter, {{r * c.d_inter, (r + 1) * c.d_inter}}, 0,
+            D, RB);
+    else if (t == "norm_attn") vec(m->norm_attn + l * D, D, 1);
+    else if (t == "norm_ffn") vec(m->norm_ffn + l * D, D, 1);
     else return false;
     return true;
 }
@@ -674,12 +748,35 @@ int ffb_config_supported(const ffb_model_config* cfg) {
 
 ffb_status ffb_create(const ffb_model_config* cfg, int64_t max_seq_len, int device, int tp_rank,
                       int tp_size, ffb_model** out) {
+    return ffb_create_ex(cfg, max_seq_len, device, tp_rank, tp_size, 0, out);
+}
+
+// The shard of rank `r` of `tp`: kv heads
+// [r NKV/tp, (r+1) NKV/tp) with their q heads, d_inter slice r, vocab slice r.
+static ffb_status shard_config(const ffb_model_config& g, int r, int tp, ffb_model_config* out) {
+    if (tp < 1 || tp > kMaxTP) return fail(FFB_USAGE, "tp_size must be in [1, %d]", kMaxTP);
+    if (r < 0 || r >= tp) return fail(FFB_USAGE, "tp_rank %d out of range", r);
+    if (g.n_kv_heads % tp || g.d_inter % tp || g.vocab_size % tp)
+        return fail(FFB_UNSUPPORTED,
+                    "tensor parallelism needs n_kv_heads, d_inter and vocab_size divisible by tp");
+    *out = g;
+    out->n_q_heads = g.n_q_heads / tp;
+    out->n_kv_heads = g.n_kv_heads / tp;
+    out->d_inter = g.d_inter / tp;
+    out->vocab_size = g.vocab_size / tp;
+    return FFB_OK;
+}
+
+ffb_status ffb_create_ex(const ffb_model_config* gcfg, int64_t max_seq_len, int device,
+                         int tp_rank, int tp_size, int grid, ffb_model** out) {
     if (!out) return fail(FFB_USAGE, "out is NULL");
     *out = nullptr;
-    ffb_status st = validate_cfg(cfg);
+    ffb_status st = validate_cfg(gcfg);
     if (st) return st;
-    if (tp_size != 1 || tp_rank != 0)
-        return fail(FFB_UNSUPPORTED, "tensor-parallel shards are not built in this version");
+    ffb_model_config local;
+    st = shard_config(*gcfg, tp_rank, tp_size, &local);
+    if (st) return st;
+    const ffb_model_config* cfg = &local;
     if (max_seq_len < 1) return fail(FFB_VALIDATION, "max_seq_len must be >= 1");
     const KernelOps* ops = find_ops(*cfg);
     if (!ops)
@@ -707,9 +804,15 @@ ffb_status ffb_create(const ffb_model_config* cfg, int64_t max_seq_len, int devi
 
     auto m = new ffb_model();
     m->cfg = *cfg;
+    m->gcfg = *gcfg;
+    m->tp_rank = tp_rank;
+    m->tp_size = tp_size;
+    m->vocab_base = cfg->vocab_size * tp_rank;
     m->ops = ops;
     m->device = device;
     m->grid = std::min(prop.multiProcessorCount, 160);  // KTraits::kMaxGrid
+    if (grid > 0) m->grid = std::min(m->grid, grid);    // e.g. TP ranks sharing one GPU
+    if (tp_size > 1) m->calib_mask = 0xf & ~0x2;        // S_AOUT rows must match across ranks
     m->max_seq = max_seq_len;
     m->kv_len.assign(cfg->layers, 0);
     auto bail = [&](ffb_status s) {
@@ -733,14 +836,14 @@ ffb_status ffb_create(const ffb_model_config* cfg, int64_t max_seq_len, int devi
     } while (0)
     const size_t RB = ops->row_bytes;
     ALLOC(m->wqkv, (size_t)Lc * m->qkv_rows() * RB);
-    ALLOC(m->waout, (size_t)Lc * D * RB);
+    ALLOC(m->waout, (size_t)Lc * D * ops->row_bytes_a);  // rows of AD = NQ_local * dh columns
     ALLOC(m->wffn1, (size_t)Lc * 2 * c.d_inter * RB);
     ALLOC(m->wffn2t, (size_t)Lc * c.d_inter * RB);
     ALLOC(m->norm_attn, (size_t)Lc * D);
     ALLOC(m->norm_ffn, (size_t)Lc * D);
     ALLOC(m->final_norm, (size_t)D);
-    ALLOC(m->embedding, (size_t)V * D);
-    ALLOC(m->lm_head, (size_t)V * RB);
+    ALLOC(m->embedding, (size_t)gcfg->vocab_size * D);  // replicated, full vocabulary
+    ALLOC(m->lm_head, (size_t)V * RB);                   // this shard's vocab rows
     const size_t kv = (size_t)Lc * B * c.n_kv_heads * max_seq_len * c.d_head;
     ALLOC(m->kcache, kv);
     ALLOC(m->vcache, kv);
@@ -768,6 +871,17 @@ ffb_status ffb_create(const ffb_model_config* cfg, int64_t max_seq_len, int devi
     ALLOC(m->pool_counters, (size_t)Lc);
     if (cudaMemset(m->pool_counters, 0, sizeof(uint32_t) * Lc) != cudaSuccess)
         return bail(fail(FFB_DEVICE, "cudaMemset failed"));
+    // TP exchange buffer + flags (also allocated at tp_size 1: harmless, 16 KB)
+    m->xch_bytes = sizeof(float) * ((size_t)4 * B * D + (size_t)kMaxTP * B * 2);
+    m->xflag_bytes = sizeof(uint32_t) * ((size_t)Lc * 2 * m->grid + 1);
+    ALLOC(m->xch, m->xch_bytes / sizeof(float));
+    ALLOC(m->xflag, m->xflag_bytes / sizeof(uint32_t));
+    if (cudaMemset(m->xflag, 0, m->xflag_bytes) != cudaSuccess ||
+        cudaMemset(m->xch, 0, m->xch_bytes) != cudaSuccess)
+        return bail(fail(FFB_DEVICE, "cudaMemset failed"));
+    m->peer_xch[tp_rank] = m->xch;
+    m->peer_xflag[tp_rank] = m->xflag;
+    m->tp_connected = tp_size == 1;
 #undef ALLOC
     if (cudaMemset(m->counters, 0, sizeof(uint32_t) * (Lc * 5 + 1)) != cudaSuccess ||
         cudaMemset(m->head_counters, 0, sizeof(uint32_t) * Lc * units) != cudaSuccess ||
@@ -796,38 +910,51 @@ ffb_status ffb_upload_tensor(ffb_model* m, const char* name, const float* values
     if (!m || !name || !values) return fail(FFB_USAGE, "NULL argument");
     TensorDst d;
     if (!resolve(m, name, &d)) return fail(FFB_USAGE, "unknown tensor name '%s'", name);
-    if (n != d.n)
+    if (n != d.gn)
         return fail(FFB_USAGE, "tensor '%s': expected %lld values, got %lld", name,
-                    (long long)d.n, (long long)n);
+                    (long long)d.gn, (long long)n);
     CUDA_TRY(cudaSetDevice(m->device));
     if (d.kind == 1) {
         CUDA_TRY(cudaMemcpy(d.ptr, values, sizeof(float) * n, cudaMemcpyHostToDevice));
         return FFB_OK;
     }
+    // the shard's rows / columns as one contiguous f32 block (no copy at TP 1)
+    const int64_t lrows = d.local_rows(), cols = d.cols;
+    std::vector<float> shard;
+    const float* src = values;
+    if (d.rows.size() != 1 || d.rows[0].first != 0 || d.cols != d.gcols) {
+        shard.resize((size_t)lrows * cols);
+        int64_t o = 0;
+        for (auto& rr : d.rows)
+            for (int64_t r = rr.first; r < rr.second; ++r, ++o)
+                std::memcpy(shard.data() + o * cols, values + r * d.gcols + d.col0,
+                            sizeof(float) * cols);
+        src = shard.data();
+    }
     if (d.kind == 0 && m->ops->QB != 0) {  // quant packer, a block of rows at a time
-        const int64_t cols = m->cfg.d_model;
-        const size_t rb = m->ops->row_bytes;
+        const size_t rb = d.row_bytes;
         const int64_t rows_per = std::max<int64_t>(1, (4 << 20) / (int64_t)rb);
         std::vector<uint8_t> buf(rows_per * rb);
         auto* dst = static_cast<uint8_t*>(d.ptr);
-        for (int64_t r0 = 0; r0 < d.rows; r0 += rows_per) {
-            const int64_t nr = std::min(rows_per, d.rows - r0);
+        for (int64_t r0 = 0; r0 < lrows; r0 += rows_per) {
+            const int64_t nr = std::min(rows_per, lrows - r0);
             for (int64_t r = 0; r < nr; ++r)
-                m->quant_inexact_groups += pack_quant_row(values + (r0 + r) * cols, cols,
+                m->quant_inexact_groups += pack_quant_row(src + (r0 + r) * cols, cols,
                                                           m->ops->QB, buf.data() + r * rb, rb);
             CUDA_TRY(cudaMemcpy(dst + r0 * rb, buf.data(), nr * rb, cudaMemcpyHostToDevice));
         }
         return FFB_OK;
     }
+    const int64_t ln = lrows * cols;
     auto* dst = static_cast<__nv_bfloat16*>(d.ptr);
-    for (int64_t off = 0; off < n; off += ffb_model::kStagingElems) {
-        const int64_t cnt = std::min<int64_t>(ffb_model::kStagingElems, n - off);
-        CUDA_TRY(cudaMemcpyAsync(m->staging, values + off, sizeof(float) * cnt,
+    for (int64_t off = 0; off < ln; off += ffb_model::kStagingElems) {
+        const int64_t cnt = std::min<int64_t>(ffb_model::kStagingElems, ln - off);
+        CUDA_TRY(cudaMemcpyAsync(m->staging, src + off, sizeof(float) * cnt,
                                  cudaMemcpyHostToDevice, m->stream));
         f32_to_bf16_kernel<<<1184, 256, 0, m->stream>>>(m->staging, dst + off, cnt);
         CUDA_TRY(cudaGetLastError());
+        CUDA_TRY(cudaStreamSynchronize(m->stream));  // staging reused
     }
-    CUDA_TRY(cudaStreamSynchronize(m->stream));
     return FFB_OK;
 }
 
@@ -846,21 +973,25 @@ ffb_status ffb_init_synthetic(ffb_model* m, uint64_t seed) {
     };
     // streamed matrices: bf16 values, or random codes with per-group scales
     // spanning the same +-sqrt(3) stddev range and a mid-range zero point
-    auto mat = [&](uint8_t* p, int64_t rows, uint64_t s, float stddev) {
+    // (TP shards draw their own matrices; embedding and norms are replicated)
+    const uint64_t rs = 0x9e37ull * static_cast<uint64_t>(m->tp_rank);
+    auto mat = [&](uint8_t* p, int64_t rows, int64_t cols, size_t rb, uint64_t s, float stddev) {
         if (m->ops->QB == 0) {
-            bf(reinterpret_cast<__nv_bfloat16*>(p), rows * D, s, stddev);
+            bf(reinterpret_cast<__nv_bfloat16*>(p), rows * cols, s + rs, stddev);
         } else {
             synth_quant_kernel<<<4096, 256, 0, m->stream>>>(
-                p, rows, static_cast<int>(D), m->ops->QB, m->ops->row_bytes,
-                seed * 1315423911ull + s, stddev);
+                p, rows, static_cast<int>(cols), m->ops->QB, static_cast<int>(rb),
+                seed * 1315423911ull + s + rs, stddev);
         }
     };
-    mat(m->wqkv, L * m->qkv_rows(), 1, sd);
-    mat(m->waout, L * D, 2, sd);
-    mat(m->wffn1, L * 2 * c.d_inter, 3, sd);
-    mat(m->wffn2t, L * c.d_inter, 4, sdi);
-    bf(m->embedding, c.vocab_size * D, 5, sd);
-    mat(m->lm_head, c.vocab_size, 6, sd);
+    const size_t RB = m->ops->row_bytes, RBA = m->ops->row_bytes_a;
+    const int64_t AD = c.n_q_heads * c.d_head;
+    mat(m->wqkv, L * m->qkv_rows(), D, RB, 1, sd);
+    mat(m->waout, L * D, AD, RBA, 2, sd);
+    mat(m->wffn1, L * 2 * c.d_inter, D, RB, 3, sd);
+    mat(m->wffn2t, L * c.d_inter, D, RB, 4, sdi);
+    bf(m->embedding, m->gcfg.vocab_size * D, 5, sd);
+    mat(m->lm_head, c.vocab_size, D, RB, 6, sd);
     f32(m->norm_attn, L * D, 7);
     f32(m->norm_ffn, L * D, 8);
     f32(m->final_norm, D, 9);
@@ -919,7 +1050,10 @@ ffb_status ffb_kv_import(ffb_model* m, const float* k, const float* v, int64_t s
     for (int64_t b = 0; b < c.batch; ++b)
         for (int64_t l = 0; l < c.layers; ++l)
             for (int64_t h = 0; h < c.n_kv_heads; ++h) {
-                const size_t src = (((size_t)b * c.layers + l) * c.n_kv_heads + h) * src_max_seq * c.d_head;
+                // the reference layout holds every kv head; take this shard's
+                const int64_t gh = m->tp_rank * c.n_kv_heads + h;
+                const size_t src =
+                    (((size_t)b * c.layers + l) * m->gcfg.n_kv_heads + gh) * src_max_seq * c.d_head;
                 for (int64_t ps = 0; ps < n_pos; ++ps)
                     for (int64_t d = 0; d < c.d_head; ++d) {
                         const int64_t i = ps * c.d_head + d;
@@ -971,6 +1105,10 @@ ffb_status ffb_set_option(ffb_model* m, const char* key, int64_t value) {
         m->l2_prefetch = value;
         return FFB_OK;
     }
+    const bool plan_key = !std::strcmp(key, "calib_mask") || !std::strcmp(key, "plan_reverse") ||
+                          !std::strcmp(key, "glu_pool_permille") || !std::strcmp(key, "glu_pool_chunk");
+    if (plan_key && m->tp_size > 1)
+        return fail(FFB_UNSUPPORTED, "option '%s' changes the plan; not with tensor parallelism", key);
     if (std::strcmp(key, "calib_mask") == 0) {
         if (value < 0 || value > 0xf) return fail(FFB_USAGE, "calib_mask is a 4-bit mask");
         m->calib_mask = static_cast<int>(value);
@@ -1047,9 +1185,11 @@ int64_t ffb_get_trace(ffb_model* m, uint64_t* out, int64_t n) {
 
 static ffb_status check_step(ffb_model* m, const int64_t* tokens, int64_t pos) {
     const auto& c = m->cfg;
+    if (!m->tp_connected)
+        return fail(FFB_USAGE, "tensor-parallel rank not connected (ffb_tp_connect)");
     if (tokens)
         for (int64_t b = 0; b < c.batch; ++b)
-            if (tokens[b] < 0 || tokens[b] >= c.vocab_size)
+            if (tokens[b] < 0 || tokens[b] >= m->gcfg.vocab_size)
                 return fail(FFB_VALIDATION, "decode_step: token id out of range");
     for (int64_t l = 0; l < c.layers; ++l)
         if (m->kv_len[l] != pos)
@@ -1113,9 +1253,9 @@ ffb_status ffb_get_info(const ffb_model* m, ffb_info* out) {
         m->mode == FFB_MODE_BASELINE ? static_cast<int32_t>(c.layers * kStagesPerLayer + 1) : 1;
     out->mode = m->mode;
     const uint64_t row = static_cast<uint64_t>(m->ops->row_bytes);
-    out->weight_bytes = row * (static_cast<uint64_t>(c.layers) *
-                                   (m->qkv_rows() + c.d_model + 3 * c.d_inter) +
-                               c.vocab_size);
+    out->weight_bytes = row * (static_cast<uint64_t>(c.layers) * (m->qkv_rows() + 3 * c.d_inter) +
+                               c.vocab_size) +
+                        static_cast<uint64_t>(m->ops->row_bytes_a) * c.layers * c.d_model;
     out->quant_inexact_groups = m->quant_inexact_groups;
     out->row_bytes = m->ops->row_bytes;
     out->device_bytes = m->device_bytes;
@@ -1126,6 +1266,8 @@ const float* ffb_logits_device(const ffb_model* m) { return m ? m->logits : null
 
 ffb_status ffb_calibrate(ffb_model* m, int32_t iterations) {
     if (!m) return fail(FFB_USAGE, "NULL handle");
+    if (m->tp_size > 1)
+        return fail(FFB_UNSUPPORTED, "calibrate: per-rank plans would desynchronise TP epochs");
     if (iterations < 0 || iterations > 16) return fail(FFB_USAGE, "iterations in [0, 16]");
     const auto& c = m->cfg;
     const int G = m->grid;
@@ -1199,6 +1341,70 @@ ffb_status ffb_calibrate(ffb_model* m, int32_t iterations) {
     if (st) return st;
     CUDA_TRY(cudaStreamSynchronize(m->stream));
     m->epoch = 0;
+    return FFB_OK;
+}
+
+// ---- tensor parallelism: peer exchange buffers ------------------------------
+struct TpBlob {
+    uint32_t magic, rank, tp, device;
+    uint64_t pid;
+    uint64_t xch_ptr, xflag_ptr;  // raw pointers (same process)
+    cudaIpcMemHandle_t xch_ipc, xflag_ipc;
+};
+
+int64_t ffb_tp_blob_bytes(void) { return sizeof(TpBlob); }
+
+ffb_status ffb_tp_export(ffb_model* m, void* blob) {
+    if (!m || !blob) return fail(FFB_USAGE, "NULL argument");
+    CUDA_TRY(cudaSetDevice(m->device));
+    TpBlob b{};
+    b.magic = 0xFFB200u;
+    b.rank = static_cast<uint32_t>(m->tp_rank);
+    b.tp = static_cast<uint32_t>(m->tp_size);
+    b.device = static_cast<uint32_t>(m->device);
+    b.pid = static_cast<uint64_t>(getpid());
+    b.xch_ptr = reinterpret_cast<uint64_t>(m->xch);
+    b.xflag_ptr = reinterpret_cast<uint64_t>(m->xflag);
+    // IPC handles (multi-process ranks); may fail in restricted sandboxes,
+    // in which case only same-process peers can connect
+    if (cudaIpcGetMemHandle(&b.xch_ipc, m->xch) != cudaSuccess ||
+        cudaIpcGetMemHandle(&b.xflag_ipc, m->xflag) != cudaSuccess)
+        cudaGetLastError();
+    std::memcpy(blob, &b, sizeof(b));
+    return FFB_OK;
+}
+
+ffb_status ffb_tp_connect(ffb_model* m, const void* blobs, int32_t n) {
+    if (!m || !blobs) return fail(FFB_USAGE, "NULL argument");
+    if (n != m->tp_size) return fail(FFB_USAGE, "tp_connect: expected %d blobs", m->tp_size);
+    CUDA_TRY(cudaSetDevice(m->device));
+    const auto* bl = static_cast<const TpBlob*>(blobs);
+    for (int i = 0; i < n; ++i) {
+        const TpBlob& b = bl[i];
+        if (b.magic != 0xFFB200u || (int)b.tp != m->tp_size || (int)b.rank != i)
+            return fail(FFB_USAGE, "tp_connect: blob %d is not rank %d of %d", i, i, m->tp_size);
+        if (i == m->tp_rank) continue;
+        if (b.pid == static_cast<uint64_t>(getpid())) {  // same process: one address space
+            if ((int)b.device != m->device) {
+                cudaError_t e = cudaDeviceEnablePeerAccess(static_cast<int>(b.device), 0);
+                if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled)
+                    return fail(FFB_DEVICE, "peer access to device %u: %s", b.device,
+                                cudaGetErrorString(e));
+                cudaGetLastError();
+            }
+            m->peer_xch[i] = reinterpret_cast<float*>(b.xch_ptr);
+            m->peer_xflag[i] = reinterpret_cast<uint32_t*>(b.xflag_ptr);
+        } else {
+            void *px = nullptr, *pf = nullptr;
+            CUDA_TRY(cudaIpcOpenMemHandle(&px, b.xch_ipc, cudaIpcMemLazyEnablePeerAccess));
+            m->ipc_opened.push_back(px);
+            CUDA_TRY(cudaIpcOpenMemHandle(&pf, b.xflag_ipc, cudaIpcMemLazyEnablePeerAccess));
+            m->ipc_opened.push_back(pf);
+            m->peer_xch[i] = static_cast<float*>(px);
+            m->peer_xflag[i] = static_cast<uint32_t*>(pf);
+        }
+    }
+    m->tp_connected = true;
     return FFB_OK;
 }
 

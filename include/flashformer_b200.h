@@ -86,6 +86,13 @@ int64_t ffb_quant_row_bytes(int64_t cols, int32_t quant_bits);
  * number of groups whose values lie on no such grid (packed lossily), or -1. */
 int64_t ffb_pack_quant_rows(const float *values, int64_t rows, int64_t cols,
                             int32_t quant_bits, uint8_t *out);
+/* Same with an explicit code order: layout 0 = plain (column order, used by
+ * Wffn2^T and the CUDA-core GEMV), 1 = tensor-core order (each lane quad of
+ * the mma.sync A fragment reads its 32 codes of a 128-column group as one
+ * 16-byte (int4) / 32-byte (int8) block; used by Wqkv / Wffn1 / lm_head /
+ * Waout rows whose width is a multiple of 1024). */
+int64_t ffb_pack_quant_rows_ex(const float *values, int64_t rows, int64_t cols,
+                               int32_t quant_bits, int32_t layout, uint8_t *out);
 
 /* 1 if a kernel specialisation exists for this shape (no device needed). */
 int ffb_config_supported(const ffb_model_config *cfg);

@@ -151,24 +151,39 @@ def model_preset(name: str) -> ModelConfig:
     return PRESETS[name]
 
 
-def pack_quant_rows(values: np.ndarray, quant_bits: int) -> tuple[np.ndarray, int]:
-    """Host weight packer (ffb_pack_quant_rows): f32 [rows][cols] -> device
+def pack_quant_rows(values: np.ndarray, quant_bits: int, layout: int = 0) -> tuple[np.ndarray, int]:
+    """Host weight packer (ffb_pack_quant_rows_ex): f32 [rows][cols] -> device
     row format bytes [rows][row_bytes], plus the count of groups that lie on
-    no int4/int8 grid (packed lossily)."""
+    no int4/int8 grid (packed lossily).  layout 1 = tensor-core code order."""
     v = np.ascontiguousarray(values, np.float32)
     rows, cols = v.shape
     rb = lib().ffb_quant_row_bytes(cols, quant_bits)
     if rb < 0:
         raise UsageError(f"unsupported quant row: cols={cols} bits={quant_bits}")
     out = np.zeros((rows, rb), np.uint8)
-    n = lib().ffb_pack_quant_rows(_fp(v), rows, cols, quant_bits,
-                                  out.ctypes.data_as(C.POINTER(C.c_uint8)))
+    n = lib().ffb_pack_quant_rows_ex(_fp(v), rows, cols, quant_bits, layout,
+                                     out.ctypes.data_as(C.POINTER(C.c_uint8)))
     if n < 0:
         raise UsageError(lib().ffb_last_error().decode())
     return out, int(n)
 
 
-def unpack_quant_rows(packed: np.ndarray, cols: int, quant_bits: int) -> np.ndarray:
+def tc_code_positions(quant_bits: int) -> np.ndarray:
+    """Column i of a 128-column group -> nibble (int4) / byte (int8)
+    position in the tensor-core code order (runtime.cu: tc_nibble_index,
+    tc_byte_index; decode_kernel.cuh: tc_slot)."""
+    i = np.arange(128)
+    s, r = i // 16, i % 16
+    q, hi, plus8 = (r % 8) // 2, r % 2, (r >= 8).astype(int)
+    if quant_bits == 4:
+        t, u = s // 2, s % 2
+        bit = hi * 16 + plus8 * 4 + u * 8
+        return (q * 4 + t) * 8 + bit // 4
+    return q * 32 + s * 4 + plus8 * 2 + hi
+
+
+def unpack_quant_rows(packed: np.ndarray, cols: int, quant_bits: int,
+                      layout: int = 0) -> np.ndarray:
     """Inverse of pack_quant_rows: (code - zero) * scale in f32 (quant.hpp:23-25)."""
     ng = cols // 128
     cb = cols // 2 if quant_bits == 4 else cols
@@ -179,6 +194,9 @@ def unpack_quant_rows(packed: np.ndarray, cols: int, quant_bits: int) -> np.ndar
         c[:, 1::2] = codes >> 4
     else:
         c = codes.copy()
+    if layout == 1:  # stored position -> column
+        pos = (np.arange(ng)[:, None] * 128 + tc_code_positions(quant_bits)[None, :]).ravel()
+        c = c[:, pos]
     scale = packed[:, cb:cb + 4 * ng].copy().view(np.float32)
     zero = packed[:, cb + 4 * ng:cb + 5 * ng].astype(np.float32)
     g = np.arange(cols) // 128

@@ -37,6 +37,7 @@
 #pragma once
 #include <cstdint>
 #include <cuda_bf16.h>
+#include <cuda_fp16.h>
 
 #include "ptx.cuh"
 
@@ -201,7 +202,19 @@ struct RowMap {
     static constexpr int RPT = QB == 0 ? cmin_((32768 / ROW_BYTES) / RG, 32 / S::B)
                                        : cmax_(2 / RG, cmin_(pow2_le_(32 / S::B),
                                                              pow2_le_(cmax_(1, 32768 / (RG * ROW_BYTES)))));
-    static constexpr int RPS = RG * RPT;            // rows per slot
+    // Tensor-core GEMV (quant formats, K a multiple of 8 x 128): the 8 warps
+    // split K, each holds its K range of the activations as fp16 hi/lo MMA
+    // B fragments in registers and decodes 16-row x 16-column weight tiles
+    // straight into mma.sync A fragments (gemv_tc).  Rows of such matrices
+    // use the MMA code order (weight_layout_tc); Wffn2^T (CUDA-core AXPY)
+    // keeps the plain order.
+    static constexpr bool TC = QB != 0 && S::B == 1 && K % (kNCW * kQuantGroup) == 0;
+    static constexpr int KW = K / kNCW;             // TC: columns per warp
+    static constexpr int KS = TC ? KW / 16 : 1;     // TC: k16 steps per warp
+    static constexpr int TC_ROWS = QB == 4 ? 16 : 8;  // TC: rows per M tile (int8: 8 + 8 zero)
+    static constexpr int RPS = TC ? TC_ROWS : RG * RPT;  // rows per slot
+    static constexpr int EWPR = TC ? kNCW : WPR;    // per-row partials in the epilogue
+    static constexpr int APT = RPS / RG;            // rows per thread per slot (CUDA-core AXPY)
     static constexpr int SLOT = (RPS * ROW_BYTES + 127) / 128 * 128;
     // rows per epilogue batch (whole slots; >= 64/B rows so barriers are rare)
     static constexpr int RB = RPS > 64 / S::B ? RPS : ((64 / S::B) / RPS) * RPS;
@@ -210,7 +223,9 @@ struct RowMap {
     static_assert(QB == 0 || kQuantGroup % CPT == 0, "a thread's columns lie in one group");
     static_assert(RPS >= 2 && RPS % 2 == 0 && RPS % RG == 0, "slot rows");
     static_assert(RPS * S::B <= kNCT && RB * S::B <= kNCT, "epilogue threads");
-    static_assert(RPT * S::B <= 32 && (RPT & (RPT - 1)) == 0, "one transposed warp reduction per slot");
+    static_assert(TC || (RPT * S::B <= 32 && (RPT & (RPT - 1)) == 0),
+                  "one transposed warp reduction per slot");
+    static_assert(!TC || (2 * S::B <= 8 && KW % kQuantGroup == 0), "TC: hi/lo columns fit n8");
 };
 
 template <class S>
@@ -228,7 +243,7 @@ struct KTraits : RowMap<S, S::D> {
     static constexpr int cmin(int a, int b) { return a < b ? a : b; }
     static constexpr int cmax(int a, int b) { return a > b ? a : b; }
     static constexpr int SLOT_BYTES = S::QB == 0 ? 32768 : cmax(MD::SLOT, MA::SLOT);
-    static constexpr int RED_FLOATS = cmax(MD::WPR * MD::RB, MA::WPR * MA::RB) * S::B;
+    static constexpr int RED_FLOATS = cmax(MD::EWPR * MD::RB, MA::EWPR * MA::RB) * S::B;
     static constexpr int KVC = SLOT_BYTES / (2 * S::DH * 2);  // KV positions per slot
     static constexpr int DPL = S::DH / 32;          // attention dims per lane
     // max GLU pairs / Waout rows per CTA (host-checked): the d_inter share of
@@ -260,9 +275,10 @@ struct KTraits : RowMap<S, S::D> {
     static constexpr int ANP = ((ATT_SC * KVC + 1) + 3) / 4 * 4;
     static constexpr int SZ_ATT = S::QPG * S::DH + 2 * S::QPG * ANP + 4 * S::QPG;
     static constexpr int SZ_WPART =
-        4 * cmax(cmax(cmax(NCW * S::QPG * (S::DH + 2), 3 * kMaxGrid * S::QPG),
-                      cmax(2 * kMaxGrid * S::B, NCW * 32)),
-                 SZ_ATT);
+        4 * cmax(cmax(cmax(cmax(NCW * S::QPG * (S::DH + 2), 3 * kMaxGrid * S::QPG),
+                           cmax(2 * kMaxGrid * S::B, NCW * 32)),
+                      SZ_ATT),
+                 cmax(MD::TC ? S::D : 0, MA::TC ? S::AD : 0));  // TC activation strips
     static constexpr int OFF_AMAX = OFF_WPART + SZ_WPART;  // [NCT] (f32, i32)
     static constexpr int SZ_AMAX = NCT * 8;
     static constexpr int OFF_MISC = OFF_AMAX + SZ_AMAX;  // flags
@@ -733,7 +749,7 @@ struct DecodeCta {
 
     template <class M = MD>
     struct Act {
-        float v[B][M::NCH][8];
+        float v[B][M::TC ? 1 : M::NCH][8];
         float sum[B];
     };
 
@@ -751,12 +767,223 @@ struct DecodeCta {
                : e == 3 ? 0.000244140625f : 0.0000152587890625f;
     }
 
+    // ---- tensor-core GEMV (quant formats) -----------------------------
+    // Activation column k of batch row b (layer-0 input from the embedding).
+    template <class M>
+    __device__ __forceinline__ float2 act_pair(const float* src, bool from_emb, int b, int k) const {
+        if (from_emb) {
+            const uint32_t w = __ldg(reinterpret_cast<const uint32_t*>(
+                p.embedding + (size_t)p.tokens[b] * D + k));
+            return make_float2(bf_lo(w), bf_hi(w));
+        }
+        return __ldcg(reinterpret_cast<const float2*>(src + (size_t)b * M::K + k));
+    }
+
+    // MMA B fragments (m16n8k16, "col"): lane (g, q) holds column n = g
+    // = batch row g % B as fp16 hi (g < B) or lo (B <= g < 2B) part, rows
+    // k = 2q, 2q+1 (bf[j][0]) and 2q+8, 2q+9 (bf[j][1]) of k-step j of the
+    // warp's K range.  hi + lo carries 22 bits of each f32 activation; int4
+    // pre-scales the second register by 1/16 (see gemv_tc's decode).
+    template <class M>
+    __device__ __forceinline__ void load_act_tc(Act<M>& act, const float* src, bool from_emb, const float* gain,
+                                int stage) {
+        const int ctid = threadIdx.x, warp = ctid / 32, lane = ctid % 32, g = lane / 4, q = lane % 4;
+        constexpr int PL = M::KW / 32;  // columns per lane of the warp's K range (16 at d 4096)
+        static_assert(PL % 4 == 0, "float4 staging");
+        const int col0 = warp * M::KW + lane * PL;
+        float gl[PL];
+        if (gain != nullptr) {
+#pragma unroll
+            for (int i = 0; i < PL; i += 4) {
+                const float4 g4 = __ldg(reinterpret_cast<const float4*>(gain + col0 + i));
+                gl[i] = g4.x; gl[i + 1] = g4.y; gl[i + 2] = g4.z; gl[i + 3] = g4.w;
+            }
+        }
+        wait_stage(stage);
+        // coalesced load of the warp's K range (lane: PL consecutive columns)
+        float v[B][PL];
+#pragma unroll
+        for (int b = 0; b < B; ++b) {
+            if (from_emb) {
+                const __nv_bfloat16* e = p.embedding + (size_t)p.tokens[b] * D + col0;
+#pragma unroll
+                for (int i = 0; i < PL; i += 8) {
+                    const uint4 w = __ldg(reinterpret_cast<const uint4*>(e + i));
+                    v[b][i] = bf_lo(w.x); v[b][i + 1] = bf_hi(w.x);
+                    v[b][i + 2] = bf_lo(w.y); v[b][i + 3] = bf_hi(w.y);
+                    v[b][i + 4] = bf_lo(w.z); v[b][i + 5] = bf_hi(w.z);
+                    v[b][i + 6] = bf_lo(w.w); v[b][i + 7] = bf_hi(w.w);
+                }
+            } else {
+#pragma unroll
+                for (int i = 0; i < PL; i += 4) {
+                    const float4 a4 = ldcg_f4(src + (size_t)b * M::K + col0 + i);
+                    v[b][i] = a4.x; v[b][i + 1] = a4.y; v[b][i + 2] = a4.z; v[b][i + 3] = a4.w;
+                }
+            }
+        }
+        float inv[B];
+#pragma unroll
+        for (int b = 0; b < B; ++b) inv[b] = 1.f;
+        if (gain != nullptr) {  // RMSNorm statistics over the whole row, numerics.hpp:14-24
+            float* ns = norm_s();
+#pragma unroll
+            for (int b = 0; b < B; ++b) {
+                float sq = 0.f;
+#pragma unroll
+                for (int i = 0; i < PL; ++i) sq = fmaf(v[b][i], v[b][i], sq);
+                sq = warp_sum(sq);
+                if (lane == 0) ns[warp * B + b] = sq;
+            }
+            consumer_sync(NCT);
+#pragma unroll
+            for (int b = 0; b < B; ++b) {
+                float t = 0.f;
+                for (int w = 0; w < NCW; ++w) t += ns[w * B + b];
+                inv[b] = 1.0f / sqrtf(t / static_cast<float>(M::K) + p.eps);
+            }
+            consumer_sync(NCT);  // ns reusable afterwards
+        }
+        // MMA B fragments (m16n8k16 "col", batch 1): column n = 0 carries the
+        // fp16 hi part, n = 1 the lo part of each activation (hi + lo keeps
+        // 22 bits), n >= 2 zero.  Lane (g, q) of k-step j needs rows 2q, 2q+1
+        // (reg 0) and 2q+8, 2q+9 (reg 1) of column g; int4 pre-scales reg 1 by
+        // 1/16 (the decode leaves those codes times 16).  Each lane builds
+        // the table of its own k-steps (PL / 16 of them) into this warp's
+        // smem strip [j][n][q][reg]; tc_slot reads it per k-step.
+        uint32_t* tab = reinterpret_cast<uint32_t*>(wpart()) + warp * M::KS * 16;
+        const float sc1 = M::QB == 4 ? 0.0625f : 1.f;
+#pragma unroll
+        for (int jj = 0; jj < PL / 16; ++jj) {
+            const int j = lane * (PL / 16) + jj;
+            uint32_t e[16];
+#pragma unroll
+            for (int qq = 0; qq < 4; ++qq)
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const int c = jj * 16 + 2 * qq + 8 * h;
+                    float x0 = gain ? gl[c] * v[0][c] * inv[0] : v[0][c];
+                    float x1 = gain ? gl[c + 1] * v[0][c + 1] * inv[0] : v[0][c + 1];
+                    if (h == 1) {
+                        x0 *= sc1;
+                        x1 *= sc1;
+                    }
+                    const __half h0 = __float2half_rn(x0), h1 = __float2half_rn(x1);
+                    __half2 hi = __halves2half2(h0, h1);
+                    __half2 lo = __halves2half2(__float2half_rn(x0 - __half2float(h0)),
+                                                __float2half_rn(x1 - __half2float(h1)));
+                    e[qq * 2 + h] = *reinterpret_cast<uint32_t*>(&hi);       // n = 0
+                    e[8 + qq * 2 + h] = *reinterpret_cast<uint32_t*>(&lo);   // n = 1
+                }
+#pragma unroll
+            for (int i = 0; i < 16; i += 4)
+                *reinterpret_cast<uint4*>(tab + j * 16 + i) = make_uint4(e[i], e[i + 1], e[i + 2], e[i + 3]);
+        }
+        consumer_sync(NCT);  // tables complete before any warp's first MMA
+    }
+
+    __device__ static void mma_f16(float (&c)[4], uint32_t a0, uint32_t a1, uint32_t a2,
+                                   uint32_t a3, uint32_t b0, uint32_t b1) {
+        asm volatile(
+            "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
+            "{%8,%9}, {%0,%1,%2,%3};"
+            : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+            : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+    }
+
+    // fp16 magic decode: (w & mask) | 0x6400 per half = 1024 + code (int4
+    // nibbles at bits 4..7 / 20..23 come out as 1024 + 16 code), then one
+    // HSUB2 of (1024 + zero) leaves (code - zero) exactly.
+    template <uint32_t MASK>
+    __device__ static uint32_t f16_nib(uint32_t w) {
+        uint32_t r;
+        asm("lop3.b32 %0, %1, %2, %3, 0xEA;" : "=r"(r) : "r"(w), "n"(MASK), "r"(0x64006400u));
+        return r;
+    }
+
+    __device__ static uint32_t hsub2_u(uint32_t a, uint32_t b) {
+        __half2 r = __hsub2(*reinterpret_cast<__half2*>(&a), *reinterpret_cast<__half2*>(&b));
+        return *reinterpret_cast<uint32_t*>(&r);
+    }
+
+    // One 16-row (int4) / 8-row (int8) slot of a TC matrix against this
+    // warp's K range: per 128-column group, decode the A fragments of rows
+    // g and g + 8 (MMA code order, weight_layout_tc), 8 MMAs into a group
+    // accumulator, scale by the rows' group scales.  out[0..3] = C fragment
+    // (rows g / g+8, columns 2q, 2q+1) summed over the warp's groups.
+    template <class M>
+    __device__ __forceinline__ void tc_slot(const uint8_t* base, float (&out)[4]) {
+        const int ctid = threadIdx.x, warp = ctid / 32, lane = ctid % 32, g = lane / 4, q = lane % 4;
+        const uint32_t* tab = reinterpret_cast<const uint32_t*>(wpart()) + warp * M::KS * 16;
+        auto frag = [&](int j) {  // (reg 0, reg 1) of k-step j for column g
+            return g < 2 ? *reinterpret_cast<const uint2*>(tab + j * 16 + g * 8 + q * 2)
+                         : make_uint2(0u, 0u);
+        };
+        const uint8_t* rA = base + g * M::ROW_BYTES;
+        const uint8_t* rB = base + (g + 8) * M::ROW_BYTES;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) out[e] = 0.f;
+#pragma unroll 1
+        for (int gi = 0; gi < M::KW / kQuantGroup; ++gi) {
+            const int G = warp * (M::KW / kQuantGroup) + gi;  // group index in the row
+            const float sA = *reinterpret_cast<const float*>(rA + M::CODE_BYTES + 4 * G);
+            const uint32_t zA = rA[M::CODE_BYTES + 4 * M::NG + G];
+            float acc[4] = {0.f, 0.f, 0.f, 0.f};
+            if constexpr (M::QB == 4) {
+                const float sB = *reinterpret_cast<const float*>(rB + M::CODE_BYTES + 4 * G);
+                const uint32_t zB = rB[M::CODE_BYTES + 4 * M::NG + G];
+                // (1024 + z) and (1024 + 16 z) per half, both exact in fp16
+                const uint32_t zA1 = (0x6400u | zA) * 0x10001u, zA16 = (0x6400u | (zA << 4)) * 0x10001u;
+                const uint32_t zB1 = (0x6400u | zB) * 0x10001u, zB16 = (0x6400u | (zB << 4)) * 0x10001u;
+                const uint4 wa = lds_u128(rA + G * 64 + q * 16);
+                const uint4 wb = lds_u128(rB + G * 64 + q * 16);
+                const uint32_t wA[4] = {wa.x, wa.y, wa.z, wa.w}, wB[4] = {wb.x, wb.y, wb.z, wb.w};
+#pragma unroll
+                for (int t = 0; t < 4; ++t) {
+                    const uint32_t a8 = wA[t] >> 8, b8 = wB[t] >> 8;
+#pragma unroll
+                    for (int u = 0; u < 2; ++u) {  // k-steps 2t, 2t+1
+                        const uint32_t xa = u ? a8 : wA[t], xb = u ? b8 : wB[t];
+                        const uint32_t a0 = hsub2_u(f16_nib<0x000F000Fu>(xa), zA1);
+                        const uint32_t a2 = hsub2_u(f16_nib<0x00F000F0u>(xa), zA16);
+                        const uint32_t a1 = hsub2_u(f16_nib<0x000F000Fu>(xb), zB1);
+                        const uint32_t a3 = hsub2_u(f16_nib<0x00F000F0u>(xb), zB16);
+                        const uint2 bf = frag(gi * 8 + 2 * t + u);
+                        mma_f16(acc, a0, a1, a2, a3, bf.x, bf.y);
+                    }
+                }
+                out[0] = fmaf(sA, acc[0], out[0]);
+                out[1] = fmaf(sA, acc[1], out[1]);
+                out[2] = fmaf(sB, acc[2], out[2]);
+                out[3] = fmaf(sB, acc[3], out[3]);
+            } else {  // int8: 8 real rows (g), rows g + 8 zero
+                const uint32_t z1 = (0x6400u | zA) * 0x10001u;
+                const uint4 w0 = lds_u128(rA + G * 128 + q * 32);
+                const uint4 w1 = lds_u128(rA + G * 128 + q * 32 + 16);
+                const uint32_t wA[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
+#pragma unroll
+                for (int st = 0; st < 8; ++st) {
+                    const uint32_t a0 = hsub2_u(__byte_perm(wA[st], 0x64646464u, 0x4140), z1);
+                    const uint32_t a2 = hsub2_u(__byte_perm(wA[st], 0x64646464u, 0x4342), z1);
+                    const uint2 bf = frag(gi * 8 + st);
+                    mma_f16(acc, a0, 0u, a2, 0u, bf.x, bf.y);
+                }
+                out[0] = fmaf(sA, acc[0], out[0]);
+                out[1] = fmaf(sA, acc[1], out[1]);
+            }
+        }
+    }
+
     // Load the activations (RMSNorm'd with `gain` when given,
     // numerics.hpp:14-24).  src_emb: layer-0 input straight from the bf16
     // embedding.  Gains are constants, fetched before the dependency wait.
     template <class M = MD>
-    __device__ void load_act(Act<M>& act, const float* src, bool from_emb, const float* gain,
+    __device__ __forceinline__ void load_act(Act<M>& act, const float* src, bool from_emb, const float* gain,
                              int stage) {
+        if constexpr (M::TC) {
+            load_act_tc<M>(act, src, from_emb, gain, stage);
+            return;
+        }
         const int ctid = threadIdx.x, lt = ctid % M::TPR, rg = ctid / M::TPR;
         float g[M::NCH][8];
         if (gain != nullptr) {
@@ -974,6 +1201,61 @@ struct DecodeCta {
         return r;
     }
 
+    // Tensor-core GEMV over rows [r0, r1): per slot every warp runs tc_slot
+    // on its K range, the hi/lo columns of each batch row are added (lane
+    // pairs), and the per-warp row partials go to red[warp][row][b]; the
+    // epilogue (same contract as gemv) sums the 8 warps (row_total).
+    template <class M, class Epi>
+    __device__ __forceinline__ void gemv_tc(uint32_t& it, const Act<M>& act, int r0, int r1, Epi&& epi) {
+        const int ctid = threadIdx.x, warp = ctid / 32, lane = ctid % 32, g = lane / 4, q = lane % 4;
+        int batch_c0 = r0;
+        uint32_t nbatch = 0;
+        float* red = red_buf(0);
+        for (int c0 = r0; c0 < r1; c0 += M::RPS) {
+            const int nrows = min(M::RPS, r1 - c0);
+            const uint32_t slot = it % T::NSLOTS, par = (it / T::NSLOTS) & 1;
+            wait_full(slot, par);
+            float c[4];
+            tc_slot<M>(ring + slot * T::SLOT_BYTES, c);
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[slot]);
+            ++it;
+            // columns 2q, 2q+1: batch rows (hi) or their lo parts; fold lo
+            // into hi (partner lane q ^ B/2), B = 1 keeps both in one lane
+            float v[4];
+            if constexpr (B == 1) {
+                v[0] = c[0] + c[1];
+                v[2] = c[2] + c[3];
+            } else {
+#pragma unroll
+                for (int e = 0; e < 4; ++e) v[e] = c[e] + __shfl_xor_sync(0xffffffffu, c[e], B / 2);
+            }
+            const int base_row = c0 - batch_c0;
+            if constexpr (B == 1) {
+                if (q == 0) {
+                    if (g < nrows) red[(warp * M::RB + base_row + g) * B] = v[0];
+                    if (g + 8 < nrows) red[(warp * M::RB + base_row + g + 8) * B] = v[2];
+                }
+            } else {
+                if (q < B / 2) {
+#pragma unroll
+                    for (int e = 0; e < 2; ++e) {
+                        const int b = 2 * q + e;
+                        if (g < nrows) red[(warp * M::RB + base_row + g) * B + b] = v[e];
+                        if (g + 8 < nrows) red[(warp * M::RB + base_row + g + 8) * B + b] = v[2 + e];
+                    }
+                }
+            }
+            const int batch_rows = c0 + nrows - batch_c0;
+            if (c0 + M::RPS >= r1 || batch_rows + M::RPS > M::RB) {
+                consumer_sync(NCT);
+                epi(batch_c0, batch_rows, red);
+                batch_c0 = c0 + M::RPS;
+                red = red_buf(++nbatch);
+            }
+        }
+    }
+
     // GEMV over rows [r0, r1) streamed by the producer.  Per slot every warp
     // forms its column-slice partial dots for all RPT x B (row, batch) values
     // (two accumulators per row, no per-row branches), releases the slot, and
@@ -982,7 +1264,11 @@ struct DecodeCta {
     // rows; `epi(c0, nrows, red)` runs once per batch after one named barrier
     // (red is double-buffered across batches).
     template <class M = MD, class Epi>
-    __device__ void gemv(uint32_t& it, const Act<M>& act, int r0, int r1, Epi&& epi) {
+    __device__ __forceinline__ void gemv(uint32_t& it, const Act<M>& act, int r0, int r1, Epi&& epi) {
+        if constexpr (M::TC) {
+            gemv_tc<M>(it, act, r0, r1, epi);
+            return;
+        }
         constexpr int V = M::RPT * B, LV = ilog2(V);
         const int ctid = threadIdx.x, lane = ctid % 32;
         const int rg = ctid / M::TPR, lt = ctid % M::TPR, wr = lt / 32;
@@ -1072,7 +1358,7 @@ struct DecodeCta {
     __device__ static float row_total(const float* red, int row, int b) {
         float t = 0.f;
 #pragma unroll
-        for (int w = 0; w < M::WPR; ++w) t += red[(w * M::RB + row) * B + b];
+        for (int w = 0; w < M::EWPR; ++w) t += red[(w * M::RB + row) * B + b];
         return t;
     }
 
@@ -1595,10 +1881,10 @@ struct DecodeCta {
             };
             if (nrows == T::RPS) {  // full slot: straight-line, no per-row branches
 #pragma unroll
-                for (int r = 0; r < T::RPT; ++r) axpy_row(rg + r * T::RG);
+                for (int r = 0; r < T::APT; ++r) axpy_row(rg + r * T::RG);
             } else {
 #pragma unroll
-                for (int r = 0; r < T::RPT; ++r)
+                for (int r = 0; r < T::APT; ++r)
                     if (rg + r * T::RG < nrows) axpy_row(rg + r * T::RG);
             }
             __syncwarp();

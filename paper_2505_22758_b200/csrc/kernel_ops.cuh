@@ -15,6 +15,7 @@ namespace ffb200 {
 struct KernelOps {
     int D, DI, DH, NQ, NKV, B, QB;
     int threads, smem, nslots, slot_bytes, rg, tmax, kvc, rps, row_bytes, row_bytes_a;
+    int tc_d, tc_a;  // d_model-column / Waout rows use the tensor-core code order
     cudaError_t (*prepare)();
     cudaError_t (*launch)(const DecodeParams&, int grid, cudaStream_t, bool cooperative);
 };
@@ -48,7 +49,8 @@ KernelOps make_ops() {
     return KernelOps{S::D,        S::DI,         S::DH,     S::NQ,         S::NKV, S::B,
                      S::QB,       T::NTHREADS,   T::SMEM_BYTES, T::NSLOTS, T::SLOT_BYTES,
                      T::RG,       T::TMAX,       T::KVC,    T::RPS,        T::ROW_BYTES,
-                     T::MA::ROW_BYTES, &prepare_impl<S>, &launch_impl<S>};
+                     T::MA::ROW_BYTES, T::MD::TC ? 1 : 0, T::MA::TC ? 1 : 0,
+                     &prepare_impl<S>, &launch_impl<S>};
 }
 
 // registration hooks, one per kernels_*.cu

@@ -533,6 +533,7 @@ struct TensorDst {
     int64_t col0 = 0, cols = 0;
     std::vector<std::pair<int64_t, int64_t>> rows;  // [r0, r1) ranges
     size_t row_bytes = 0;
+    int layout = 0;  // quant code order: 1 = tensor-core (decode_kernel.cuh: tc_slot)
     int64_t local_rows() const {
         int64_t n = 0;
         for (auto& r : rows) n += r.second - r.first;
@@ -569,6 +570,7 @@ bool resolve(ffb_model* m, const std::string& name, TensorDst* d) {
     if (name == "embedding") { vec(m->embedding, g.vocab_size * D, 2); return true; }
     if (name == "lm_head") {
         mat(m->lm_head, g.vocab_size, {{m->vocab_base, m->vocab_base + c.vocab_size}}, 0, D, RB);
+        d->layout = m->ops->tc_d;
         return true;
     }
     if (name == "final_norm") { vec(m->final_norm, D, 1); return true; }
@@ -586,6 +588,7 @@ bool resolve(ffb_model* m, const std::string& name, TensorDst* d) {
     const int64_t QR = m->qkv_rows(), dh = c.d_head;
     const int64_t AD = c.n_q_heads * dh;  // shard attention width
     const int64_t gQ = g.n_q_heads * dh, gK = g.n_kv_heads * dh, KVl = c.n_kv_heads * dh;
+    d->layout = 0;
     if (t == "wqkv")  // this shard's q heads, then its k heads, then its v heads
         mat(m->wqkv + l * QR * RB, (g.n_q_heads + 2 * g.n_kv_heads) * dh,
             {{r * AD, (r + 1) * AD}, {gQ + r * KVl, gQ + (r + 1) * KVl},
@@ -602,6 +605,8 @@ bool resolve(ffb_model* m, const std::string& name, TensorDst* d) {
     else if (t == "norm_attn") vec(m->norm_attn + l * D, D, 1);
     else if (t == "norm_ffn") vec(m->norm_ffn + l * D, D, 1);
     else return false;
+    if (t == "wqkv" || t == "wffn1") d->layout = m->ops->tc_d;
+    if (t == "waout") d->layout = m->ops->tc_a;
     return true;
 }
 
@@ -678,9 +683,34 @@ bool quant_group(const float* v, int n, int levels, uint8_t* codes, float* scale
     return false;
 }
 
+// Byte / nibble position of column i (0..127) of a 128-column group in the
+// tensor-core code order (decode_kernel.cuh: tc_slot): lane quad q of the
+// mma.sync A fragment owns columns 16s + 2q + {0, 1, 8, 9} of k-step s.
+//   int4: 64 bytes = q-major 16-byte blocks of 4 words; word t holds k-steps
+//         2t, 2t+1: nibble 0/4/1/5 = step 2t columns +0/+1/+8/+9... laid out
+//         so one LOP3 yields the (c, c+1) fp16 pair: bits 0-3 = +0, 16-19 = +1,
+//         4-7 = +8, 20-23 = +9 of step 2t; bits 8-11, 24-27, 12-15, 28-31 the
+//         same of step 2t+1.
+//   int8: 128 bytes = q-major 32-byte blocks, 4 bytes (+0, +1, +8, +9) per step.
+static int tc_nibble_index(int i) {  // int4: nibble index (byte * 2 + high) in the group
+    const int s = i / 16, r = i % 16;
+    const int q = (r % 8) / 2, hi = r % 2, plus8 = r >= 8;
+    const int t = s / 2, u = s % 2;
+    const int bit = (hi ? 16 : 0) + (plus8 ? 4 : 0) + (u ? 8 : 0);  // bit offset in the word
+    return (q * 4 + t) * 8 + bit / 4;
+}
+
+static int tc_byte_index(int i) {  // int8: byte index in the group
+    const int s = i / 16, r = i % 16;
+    const int q = (r % 8) / 2, hi = r % 2, plus8 = r >= 8;
+    return q * 32 + s * 4 + (plus8 ? 2 : 0) + hi;
+}
+
 // One row of `cols` f32 values -> the device row format of decode_kernel.cuh
-// (codes | f32 scales | u8 zeros | pad).  Returns the inexact group count.
-int pack_quant_row(const float* v, int64_t cols, int qb, uint8_t* out, size_t row_bytes) {
+// (codes | f32 scales | u8 zeros | pad); layout 1 = tensor-core code order.
+// Returns the inexact group count.
+int pack_quant_row(const float* v, int64_t cols, int qb, uint8_t* out, size_t row_bytes,
+                   int layout = 0) {
     const int levels = qb == 4 ? 15 : 255;
     const int64_t ng = cols / kQuantGroup;
     const int64_t code_bytes = qb == 4 ? cols / 2 : cols;
@@ -691,9 +721,10 @@ int pack_quant_row(const float* v, int64_t cols, int qb, uint8_t* out, size_t ro
         float sc = 1.f, z = 0.f;
         if (!quant_group(v + g * kQuantGroup, kQuantGroup, levels, codes, &sc, &z)) ++inexact;
         for (int i = 0; i < kQuantGroup; ++i) {
-            const int64_t col = g * kQuantGroup + i;
-            if (qb == 4) out[col / 2] |= static_cast<uint8_t>(codes[i] << (4 * (col & 1)));
-            else out[col] = codes[i];
+            int64_t pos = g * kQuantGroup + i;  // nibble (int4) / byte (int8) position
+            if (layout == 1) pos = g * kQuantGroup + (qb == 4 ? tc_nibble_index(i) : tc_byte_index(i));
+            if (qb == 4) out[pos / 2] |= static_cast<uint8_t>(codes[i] << (4 * (pos & 1)));
+            else out[pos] = codes[i];
         }
         std::memcpy(out + code_bytes + 4 * g, &sc, 4);
         out[code_bytes + 4 * ng + g] = static_cast<uint8_t>(z);
@@ -730,6 +761,11 @@ int64_t ffb_quant_row_bytes(int64_t cols, int32_t quant_bits) {
 
 int64_t ffb_pack_quant_rows(const float* values, int64_t rows, int64_t cols, int32_t quant_bits,
                             uint8_t* out) {
+    return ffb_pack_quant_rows_ex(values, rows, cols, quant_bits, 0, out);
+}
+
+int64_t ffb_pack_quant_rows_ex(const float* values, int64_t rows, int64_t cols,
+                               int32_t quant_bits, int32_t layout, uint8_t* out) {
     const int64_t rb = ffb_quant_row_bytes(cols, quant_bits);
     if (!values || !out || rows < 0 || rb < 0 || quant_bits == 0) {
         fail(FFB_USAGE, "pack_quant_rows: bad arguments");
@@ -737,7 +773,7 @@ int64_t ffb_pack_quant_rows(const float* values, int64_t rows, int64_t cols, int
     }
     int64_t inexact = 0;
     for (int64_t r = 0; r < rows; ++r)
-        inexact += pack_quant_row(values + r * cols, cols, quant_bits, out + r * rb, rb);
+        inexact += pack_quant_row(values + r * cols, cols, quant_bits, out + r * rb, rb, layout);
     return inexact;
 }
 
@@ -940,7 +976,8 @@ ffb_status ffb_upload_tensor(ffb_model* m, const char* name, const float* values
             const int64_t nr = std::min(rows_per, lrows - r0);
             for (int64_t r = 0; r < nr; ++r)
                 m->quant_inexact_groups += pack_quant_row(src + (r0 + r) * cols, cols,
-                                                          m->ops->QB, buf.data() + r * rb, rb);
+                                                          m->ops->QB, buf.data() + r * rb, rb,
+                                                          d.layout);
             CUDA_TRY(cudaMemcpy(dst + r0 * rb, buf.data(), nr * rb, cudaMemcpyHostToDevice));
         }
         return FFB_OK;

@@ -28,6 +28,24 @@ def test_packer_reproduces_reference_grid_bit_exact(preset, qb):
         np.testing.assert_array_equal(P.unpack_quant_rows(packed, w.shape[1], qb), w)
 
 
+@pytest.mark.parametrize("qb", [4, 8])
+def test_tensor_core_code_order_round_trip(qb):
+    """Layout 1 (the mma.sync A-fragment order) stores every code exactly once
+    and reproduces the same f32 weights as the plain order."""
+    pos = P.tc_code_positions(qb)
+    assert sorted(pos.tolist()) == list(range(128))
+    cfg = O.preset("llama31_8b").replace(quant_bits=qb, layers=1, d_inter=256, vocab_size=64)
+    st = O.OracleStore(cfg, 42, 8)
+    w = st.tensor("lm_head")
+    plain, ie0 = P.pack_quant_rows(w, qb, 0)
+    tc, ie1 = P.pack_quant_rows(w, qb, 1)
+    assert ie0 == ie1 == 0
+    assert not np.array_equal(plain, tc)
+    np.testing.assert_array_equal(P.unpack_quant_rows(tc, w.shape[1], qb, 1), w)
+    np.testing.assert_array_equal(plain[:, w.shape[1] // (2 if qb == 4 else 1):],
+                                  tc[:, w.shape[1] // (2 if qb == 4 else 1):])
+
+
 def test_row_bytes_match_the_device_format():
     # codes + f32 scale + u8 zero per group of 128, padded to 16 bytes
     assert P.lib().ffb_quant_row_bytes(4096, 4) == 2048 + 32 * 5

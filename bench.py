@@ -43,6 +43,10 @@ def parse():
     ap.add_argument("--model", default="llama31_8b")
     ap.add_argument("--ctx", type=int, default=4096)
     ap.add_argument("--batch", type=int, default=1)
+    ap.add_argument("--quant", type=int, default=0, choices=[0, 4, 8],
+                    help="weight-only quantization bits (BASELINE config Q)")
+    ap.add_argument("--tp", type=int, default=1,
+                    help="tensor-parallel ranks (torchrun, one process per GPU); 1 = replicas")
     ap.add_argument("--mode", default="fused_overlap",
                     choices=["fused_overlap", "fused", "baseline"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -225,13 +229,20 @@ def run_ours(args):
         dist.init_process_group("nccl")
     dev = local
     torch.cuda.set_device(dev)
-    cfg = model_preset(args.model).replace(batch=args.batch)
+    cfg = model_preset(args.model).replace(batch=args.batch, quant_bits=args.quant)
     ctx = args.ctx
+    tp = args.tp if world > 1 else 1
+    if tp > 1 and tp != world:
+        raise SystemExit("--tp must equal the number of ranks")
     mode = {"fused_overlap": RunMode.FUSED_OVERLAP, "fused": RunMode.FUSED,
             "baseline": RunMode.BASELINE}[args.mode]
-    m = DecodeModel(cfg, ctx + 8, device=dev, mode=mode)
+    m = DecodeModel(cfg, ctx + 8, device=dev, mode=mode, tp_rank=rank if tp > 1 else 0,
+                    tp_size=tp)
+    if tp > 1:  # wire the TP group: all-gather every rank's exchange-buffer blob
+        from paper_2505_22758_b200 import all_gather_tp_blobs
+        m.tp_connect(all_gather_tp_blobs(m.tp_blob()))
     m.init_synthetic(1234)
-    if args.calibrate:  # per-SM load balance (setup, outside the timed region)
+    if args.calibrate and tp == 1:  # per-SM load balance (setup, outside the timed region)
         for l in range(cfg.layers):
             m.set_length(l, ctx)
         m.calibrate(args.calibrate)
@@ -310,6 +321,31 @@ def run_ours(args):
             k = max(10, args.steps // 4)
             variants[name + "_ms_per_step"] = round(max_over_ranks(timed(rm, k)), 5)
         m.set_mode(mode)
+        # device-resident greedy generation (ffb_decode_loop): 32 tokens per
+        # call, no host round trip between tokens; cache reset per call
+        n_gen = 32
+        start = torch.full((cfg.batch,), 17, dtype=torch.int64, device=f"cuda:{dev}")
+        gen = torch.empty((n_gen, cfg.batch), dtype=torch.int64, device=f"cuda:{dev}")
+
+        def gen_loop(k):
+            for _ in range(k):
+                for l in range(cfg.layers):  # generation starts n_gen positions back
+                    m.set_length(l, ctx - n_gen)
+                m.decode_loop(start.data_ptr(), ctx - n_gen, n_gen, gen.data_ptr(), False,
+                              stream.cuda_stream)
+        torch.cuda.synchronize(dev)  # start / gen were written on the default stream
+        gen_loop(2)
+        torch.cuda.synchronize(dev)
+        barrier()
+        g0 = torch.cuda.Event(enable_timing=True)
+        g1 = torch.cuda.Event(enable_timing=True)
+        k = max(2, args.steps // 32)
+        g0.record(stream)
+        gen_loop(k)
+        g1.record(stream)
+        torch.cuda.synchronize(dev)
+        variants["decode_loop_ms_per_token"] = round(
+            max_over_ranks(g0.elapsed_time(g1) / (k * n_gen)) / cfg.batch, 5)
 
     algo = algorithmic_bytes(cfg, ctx)
     peak, peak_kind = measured_peak()
@@ -328,13 +364,16 @@ def run_ours(args):
             "metric": METRIC, "value": round(ms / args.batch, 5), "unit": UNIT,
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": round(ms, 5), "higher_is_better": False,
-            "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+            "scaling": "strong" if tp > 1 else "weak", "vs_baseline": None,
+            "dtype": f"int{args.quant} weights, f32 math" if args.quant else "bf16",
             "data": "synthetic (seeded device-side init of the model shape)",
             "config": {
-                "workload": f"{args.model} bf16 decode step, batch {args.batch}, "
-                            f"{ctx}-token KV cache",
+                "workload": f"{args.model} {'int%d' % args.quant if args.quant else 'bf16'} "
+                            f"decode step, batch {args.batch}, {ctx}-token KV cache"
+                            + (f", tensor-parallel {tp}" if tp > 1 else ""),
                 "model": args.model, "global_batch": args.batch * world, "seq_len": ctx,
-                "parallelism": f"replicas{world}" if world > 1 else "single",
+                "parallelism": (f"tp{tp}" if tp > 1 else f"replicas{world}") if world > 1
+                else "single",
                 "mode": args.mode, "l2": "inputs (15.5 GB) larger than L2; no flush",
             },
             "tokens_per_s": round(1e3 * args.batch * world / ms, 2),

@@ -196,6 +196,17 @@ ffb_status ffb_decode_step(ffb_model *m, const int64_t *tokens, int64_t pos, flo
 ffb_status ffb_decode_step_device(ffb_model *m, const int64_t *d_tokens, int64_t pos,
                                   float *d_logits, int64_t *d_greedy, void *stream);
 
+/* Device-resident multi-token decode: n_steps
+ * decode steps enqueued back to back on `stream` with no host round trip.
+ * teacher_forced = 0 (generation): step 0 reads d_tokens[batch], step i > 0
+ * the greedy tokens of step i-1; teacher_forced = 1 (prompt ingestion,
+ * decode-as-prefill like the reference): step i reads d_tokens[i][batch].
+ * d_out[n_steps][batch] receives every step's greedy tokens; the device
+ * logits (ffb_logits_device) hold the last step's.  pos == cache length;
+ * the length advances by n_steps on enqueue. */
+ffb_status ffb_decode_loop(ffb_model *m, const int64_t *d_tokens, int64_t pos, int32_t n_steps,
+                           int32_t teacher_forced, int64_t *d_out, void *stream);
+
 /* Introspection for roofline accounting and tests. */
 typedef struct ffb_info {
     int32_t grid;            /* CTAs per launch (one per SM)               */

@@ -310,6 +310,8 @@ def lib():
     L.ffb_decode_step_device.argtypes = [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p,
                                          C.c_void_p, C.c_void_p]
     L.ffb_get_info.argtypes = [C.c_void_p, P(_Info)]
+    L.ffb_decode_loop.argtypes = [C.c_void_p, C.c_void_p, C.c_int64, C.c_int32, C.c_int32,
+                                  C.c_void_p, C.c_void_p]
     L.ffb_logits_device.argtypes = [C.c_void_p]
     L.ffb_logits_device.restype = C.c_void_p
     L.ffb_quant_row_bytes.argtypes = [C.c_int64, C.c_int32]
@@ -507,6 +509,43 @@ class DecodeModel:
                                             C.c_void_p(d_logits or None),
                                             C.c_void_p(d_greedy or None),
                                             C.c_void_p(stream or None)))
+
+    def decode_loop(self, d_tokens: int, pos: int, n_steps: int, d_out: int,
+                    teacher_forced: bool = False, stream: int = 0):
+        """Device-resident multi-token decode (ffb_decode_loop): raw device
+        pointers, asynchronous on `stream`."""
+        _check(lib().ffb_decode_loop(self._h, C.c_void_p(d_tokens), pos, n_steps,
+                                     1 if teacher_forced else 0, C.c_void_p(d_out),
+                                     C.c_void_p(stream or None)))
+
+    def generate(self, tokens, pos: int, n_steps: int, prompt=None) -> np.ndarray:
+        """Greedy generation on the device (decode_loop): returns the n_steps
+        produced tokens int64 [n_steps][batch].  With `prompt` ([n][batch],
+        teacher-forced from `pos`), token 0 is the prediction after the
+        prompt; otherwise `tokens` ([batch]) is consumed at `pos` first.  The
+        cache ends holding every consumed token."""
+        import torch
+        dev = f"cuda:{self.device}"
+        B = self.cfg.batch
+        stream = torch.cuda.Stream(device=self.device)  # (0 would mean the handle's own stream)
+        with torch.cuda.stream(stream):
+            return self._generate(torch, dev, B, stream.cuda_stream, tokens, pos, n_steps, prompt)
+
+    def _generate(self, torch, dev, B, st, tokens, pos, n_steps, prompt):
+        out = torch.empty((n_steps, B), dtype=torch.int64, device=dev)
+        if prompt is not None:
+            pr = torch.as_tensor(np.asarray(prompt, np.int64).reshape(-1, B), device=dev)
+            po = torch.empty_like(pr)
+            self.decode_loop(pr.data_ptr(), pos, pr.shape[0], po.data_ptr(), True, st)
+            out[0] = po[-1]
+            if n_steps > 1:
+                self.decode_loop(po[-1].data_ptr(), pos + pr.shape[0], n_steps - 1,
+                                 out[1:].data_ptr(), False, st)
+        else:
+            start = torch.as_tensor(np.asarray(tokens, np.int64).reshape(B), device=dev)
+            self.decode_loop(start.data_ptr(), pos, n_steps, out.data_ptr(), False, st)
+        torch.cuda.synchronize(self.device)
+        return out.cpu().numpy()
 
     def info(self) -> dict:
         i = _Info()

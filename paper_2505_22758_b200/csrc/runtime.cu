@@ -1277,6 +1277,29 @@ ffb_status ffb_decode_step_device(ffb_model* m, const int64_t* d_tokens, int64_t
     return FFB_OK;
 }
 
+ffb_status ffb_decode_loop(ffb_model* m, const int64_t* d_tokens, int64_t pos, int32_t n_steps,
+                           int32_t teacher_forced, int64_t* d_out, void* stream) {
+    if (!m || !d_tokens || !d_out) return fail(FFB_USAGE, "NULL argument");
+    if (n_steps < 1) return fail(FFB_USAGE, "decode_loop: n_steps must be >= 1");
+    ffb_status st = check_step(m, nullptr, pos);
+    if (st) return st;
+    if (pos + n_steps > m->max_seq)
+        return fail(FFB_VALIDATION, "kv_append: cache capacity reached (max_seq_len)");
+    CUDA_TRY(cudaSetDevice(m->device));
+    cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : m->stream;
+    const int64_t B = m->cfg.batch;
+    for (int32_t i = 0; i < n_steps; ++i) {
+        // step i reads its tokens from the prompt (teacher forcing) or from
+        // the previous step's greedy output, all on the device
+        const int64_t* tok = teacher_forced ? d_tokens + (int64_t)i * B
+                                            : (i == 0 ? d_tokens : d_out + (int64_t)(i - 1) * B);
+        st = launch_step(m, pos + i, tok, nullptr, d_out + (int64_t)i * B, s);
+        if (st) return st;
+        for (auto& n : m->kv_len) n += 1;
+    }
+    return FFB_OK;
+}
+
 ffb_status ffb_get_info(const ffb_model* m, ffb_info* out) {
     if (!m || !out) return fail(FFB_USAGE, "NULL argument");
     const auto& c = m->cfg;

@@ -243,3 +243,30 @@ def test_calibrated_plan_keeps_parity_and_mode_identity():
               f"same-KV {e_strict:.2e}")
         m.calibrate(0)
         assert np.all(m.plan_weights() == 1.0)
+
+
+def test_device_resident_decode_loop_matches_stepwise_and_oracle():
+    """ffb_decode_loop: a teacher-forced prompt then
+    greedy generation, all on the device, gives the same tokens as the
+    host-driven step loop and as the oracle's argmax chain."""
+    cfg = O.preset("tiny").replace(layers=2)
+    prompt = O.tiny_prompt(12, cfg.vocab_size)
+    n = 10
+    st = O.OracleStore(cfg, 42, 40)
+    with device_from_store(st, 40) as m:
+        gen = [int(t) for t in m.generate(None, 0, n, prompt=prompt)[:, 0]]
+        assert m.length(0) == len(prompt) + n - 1
+    st2 = O.OracleStore(cfg, 42, 40)
+    with device_from_store(st2, 40) as m2:  # host-driven steps
+        for pos, t in enumerate(prompt):
+            _, g = m2.step([t], pos, logits=False)
+        ref = [int(g[0])]
+        for i in range(1, n):
+            _, g = m2.step([ref[-1]], len(prompt) + i - 1, logits=False)
+            ref.append(int(g[0]))
+    for pos, t in enumerate(prompt):  # oracle argmax chain
+        lg = st.forward([t], pos)
+    want = [int(np.argmax(lg[0]))]
+    for i in range(1, n):
+        want.append(int(np.argmax(st.forward([want[-1]], len(prompt) + i - 1)[0])))
+    assert gen == ref == want, (gen, ref, want)

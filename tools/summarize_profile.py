@@ -140,7 +140,7 @@ def main():
         if bench:
             f.write(f"bench: {bench['value']} ms/token (device), e2e {bench['e2e']['value']} "
                     f"ms/token; roofline achieved {bench['roofline']['achieved']} GB/s = "
-                    f"{bench['roofline']['frac']:.3f} of measured {bench['roofline']['peak']} "
+                    f"{bench['roofline']['frac']:.3f} of {bench['roofline'].get('peak_kind', 'measured')} {bench['roofline']['peak']} "
                     f"GB/s; variants {bench.get('variants')}; clocks {bench.get('clocks')}\n\n")
         f.write(f"ncu --set full (one launch, replayed; serialised/cold, compare shares not "
                 f"absolutes): duration {m.get('duration', 0) * 1e3:.3f} ms, DRAM read "

@@ -111,6 +111,7 @@ struct DecodeParams {
     int32_t debug;       // kDebug* bits; 0 in production
     uint64_t* trace;     // optional [grid][n_stages][8] trace records
     int64_t l2_prefetch; // bytes the L2 prefetch cursor runs ahead of the ring
+    int32_t kv_prefetch;  // 1: prefetch the next layer's K/V range into L2 (prefetch_kv)
     int32_t l2_pf_stages; // stage types (bit s % 5, bit 5 = LM head) where the
                           // producer may prefetch while its ring is full
     // GLU work pool (dynamic load balance, deterministic): pairs [pool_t0, DI)
@@ -590,6 +591,21 @@ struct DecodeCta {
         }
     }
 
+    // L2 prefetch of this CTA's past K/V positions of layer l (its ring
+    // chunks of S_ATTN), in KVC-position pieces
+    __device__ void prefetch_kv(int l) const {
+        if (pl.attn_unit < 0) return;
+        int p0, p1;
+        attn_range(p0, p1);
+        const int e = min(p1, p.pos);
+        const size_t row = kv_row(l, pl.attn_unit / S::NKV, pl.attn_unit % S::NKV, 0);
+        for (int c0 = p0; c0 < e; c0 += T::KVC) {
+            const uint32_t bytes = static_cast<uint32_t>(min(T::KVC, e - c0)) * DH * 2;
+            prefetch_l2(p.kcache + row + (size_t)c0 * DH, bytes);
+            prefetch_l2(p.vcache + row + (size_t)c0 * DH, bytes);
+        }
+    }
+
     // Producer: issues every chunk of the stream into the ring (TMA bulk).
     // FusedOverlap: gated only by free slots, plus an L2 prefetch cursor
     // (cp.async.bulk.prefetch.L2) running up to p.l2_prefetch bytes ahead of
@@ -608,6 +624,7 @@ struct DecodeCta {
         int64_t pf_bytes = 0;
         bool pf_live = window > 0;
         int cur_stage = p.stage_begin;
+        int kv_pf_stage = -1;
         const void *s0, *s1;
         uint32_t bytes;
         int stage;
@@ -620,6 +637,18 @@ struct DecodeCta {
                 }
             }
             cur_stage = stage;
+            // KV warm-up: the past positions this CTA's attention reads in
+            // layer l' are prefetched into L2 when the stream reaches layer
+            // l' - 1's GLU (layer 0: its QKV), so the ring's KV loads at the
+            // end of QKV hit L2 instead of waiting on HBM latency
+            if (!DRAIN && p.kv_prefetch && stage != kv_pf_stage) {
+                const int sl = stage / kStagesPerLayer, sk = stage % kStagesPerLayer;
+                int target = -1;
+                if (stage == 0) target = 0;
+                else if (sk == S_GLU && sl + 1 < p.layers) target = sl + 1;
+                if (target >= 0) prefetch_kv(target);
+                kv_pf_stage = stage;
+            }
             if (s0 == nullptr) {  // GLU work-pool marker
                 pool_run<DRAIN>(it, stage / kStagesPerLayer, policy);
                 continue;
@@ -1652,17 +1681,22 @@ struct DecodeCta {
                 __stcg(dst + 1, mlc[2 * h + 1]);
             }
         }
-        // last arriver of the group combines (numerics.hpp:123-145)
+        // The group's first CTA (attn_g == 0) combines (numerics.hpp:123-145):
+        // the others publish their partial with one release arrival and move
+        // on (no round trip); the combiner polls for the G - 1 arrivals
+        // instead of a last-arriver acq_rel atomic, saving one L2 round trip
+        // on the chain to S_AOUT.
         consumer_sync(NCT);
         trace_mark(l * kStagesPerLayer + S_ATTN, 7);
-        int* flag = misc();
-        if (ctid == 0) {
-            const uint32_t old =
-                atom_add_acq_rel_gpu(p.head_counters + (size_t)l * p.n_units + unit, 1);
-            flag[0] = (old + 1 == p.epoch * static_cast<uint32_t>(p.attn_group)) ? 1 : 0;
+        uint32_t* hc = p.head_counters + (size_t)l * p.n_units + unit;
+        if (pl.attn_g != 0) {
+            if (ctid == 0) red_release_gpu(hc, 1);
+            return;
         }
+        if (ctid == 0)
+            spin_until_geq(hc, p.epoch * static_cast<uint32_t>(p.attn_group - 1));
         consumer_sync(NCT);
-        if (flag[0]) {
+        {
             // One L2 round trip: every thread first issues the G o-values of
             // its (first two) outputs into registers, then the (m, l) of the
             // whole group go to smem; per head (one warp): M = max m,

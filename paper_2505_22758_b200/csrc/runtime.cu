@@ -223,6 +223,7 @@ struct ffb_model {
     // stage costs up to +8% (profiles/summary_r01.md)
     int64_t l2_prefetch = 512 << 10;
     int32_t l2_pf_stages = (1 << S_ATTN) | (1 << S_AOUT);
+    int32_t kv_prefetch = 0;          // option "kv_prefetch" (measured +1.5 %: off)
     int plan_reverse = 0;             // weight slices assigned in reverse CTA order
     // per-SM plan weights (ffb_calibrate): streamed-row shares of QKV / AOUT /
     // GLU / LM head proportional to each SM's measured streaming rate
@@ -466,6 +467,7 @@ DecodeParams make_params(const ffb_model* m, int64_t pos, const int64_t* d_token
     p.trace = m->trace;
     p.l2_prefetch = m->l2_prefetch;
     p.l2_pf_stages = m->l2_pf_stages;
+    p.kv_prefetch = m->kv_prefetch;
     p.pool_part = m->pool_part;
     p.pool_counters = m->pool_counters;
     p.pool_t0 = m->pool_t0;
@@ -1157,6 +1159,10 @@ ffb_status ffb_set_option(ffb_model* m, const char* key, int64_t value) {
         if (s) return s;
         CUDA_TRY(cudaStreamSynchronize(m->stream));
         m->epoch = 0;
+        return FFB_OK;
+    }
+    if (std::strcmp(key, "kv_prefetch") == 0) {
+        m->kv_prefetch = value ? 1 : 0;
         return FFB_OK;
     }
     if (std::strcmp(key, "sm_rank") == 0) {

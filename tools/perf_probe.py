@@ -16,6 +16,7 @@ ap.add_argument("--sweep", default="", help="comma list of l2_prefetch_bytes")
 ap.add_argument("--ncu", action="store_true", help="few launches, for profiling")
 ap.add_argument("--calibrate", type=int, default=0, help="ffb_calibrate iterations first")
 ap.add_argument("--masks", default="", help="comma list of calib_mask values to compare")
+ap.add_argument("--ab", default="", help="option=v0,v1: interleaved A/B of one option")
 ap.add_argument("--pf-stages", type=int, default=0x3f, help="l2_prefetch_stages mask for --sweep")
 a = ap.parse_args()
 
@@ -51,6 +52,14 @@ def timeit(name):
     ms = e0.elapsed_time(e1) / a.steps
     print(f"{a.model} b{a.batch} ctx{a.ctx} {name:22s} {ms:.4f} ms/step {nbytes / ms / 1e9:6.2f} TB/s", flush=True)
 
+if a.ab:
+    key, vals = a.ab.split("=")
+    m.set_mode(RunMode.FUSED_OVERLAP)
+    for rep in range(3):
+        for v in [int(x, 0) for x in vals.split(",")]:
+            m.set_option(key, v)
+            timeit(f"{key}={v}")
+    sys.exit(0)
 if a.masks:
     m.set_mode(RunMode.FUSED_OVERLAP)
     for rep in range(2):

@@ -100,3 +100,6 @@ print(f"attn: dep->q {seg(1, 5):.2f}  q->ring {seg(5, 6):.2f}  pass {seg(6, 3):.
       f"partial {seg(3, 7):.2f}  combine(last) {seg(7, 2):.2f} us")
 if os.environ.get("PHASES"):
     print(f"attn phases: ring->A {seg(6, 5):.2f}  A->B {seg(5, 7):.2f}  B->C/end {seg(7, 3):.2f} us")
+
+if os.environ.get("COMBINE"):
+    print(f"combine: partial->atomic-done {seg(7, 5):.2f}  ->ml-loaded {seg(5, 6):.2f}  ->done {seg(6, 2):.2f} us")

@@ -56,6 +56,7 @@ inline ffb_model_config to_c(const ModelConfig& m) {
     c.quant_bits = m.quant ? m.quant->bits : 0;
     c.quant_group = m.quant ? m.quant->group_size : 0;
     c.batch = m.batch;
+    c.kind = m.kind == ModelKind::StackedLinear ? 1 : 0;
     return c;
 }
 

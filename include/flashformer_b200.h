@@ -57,7 +57,9 @@ typedef enum ffb_mode {
     FFB_MODE_FUSED_OVERLAP = 2
 } ffb_mode;
 
-/* fusesim::ModelConfig (config.hpp:45-86), decoder kind.
+/* fusesim::ModelConfig (config.hpp:45-86).
+ * kind: 0 = llama_decoder, 1 = stacked_linear (config.hpp:18; only layers,
+ *       d_model and batch are used; square d_model x d_model layers).
  * dtype: 0 = bf16 (the only compiled storage type).
  * quant_bits: 0 (bf16 weights), 4 (reference int4 g128), 8 (int8 extension). */
 typedef struct ffb_model_config {
@@ -67,6 +69,8 @@ typedef struct ffb_model_config {
     int32_t quant_bits;
     int32_t quant_group;
     int64_t batch;
+    int32_t kind;
+    int32_t reserved_;
 } ffb_model_config;
 
 typedef struct ffb_model ffb_model;
@@ -206,6 +210,17 @@ ffb_status ffb_decode_step_device(ffb_model *m, const int64_t *d_tokens, int64_t
  * the length advances by n_steps on enqueue. */
 ffb_status ffb_decode_loop(ffb_model *m, const int64_t *d_tokens, int64_t pos, int32_t n_steps,
                            int32_t teacher_forced, int64_t *d_out, void *stream);
+
+/* Stacked-linear kind (reference_linear_forward, reference.hpp:141-152; the
+ * paper's cross-layer fusion ablation): tensors
+ * "linear.<l>" (d_model x d_model, bf16-rounded) and "residual" (batch x
+ * d_model input) via ffb_upload_tensor; x_in (host [batch][d_model], NULL =
+ * the uploaded residual) -> x_out = W_{L-1} ... W_0 x_in (host, may be
+ * NULL).  Run modes apply (baseline = one launch per layer).  Synchronous. */
+ffb_status ffb_linear_forward(ffb_model *m, const float *x_in, float *x_out, void *stream);
+/* Same, device pointers (either may be NULL), asynchronous on `stream`. */
+ffb_status ffb_linear_forward_device(ffb_model *m, const float *d_x_in, float *d_x_out,
+                                     void *stream);
 
 /* Introspection for roofline accounting and tests. */
 typedef struct ffb_info {

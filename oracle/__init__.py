@@ -271,6 +271,9 @@ def ref_lib():
         R.ref_streamed_weight_bytes.argtypes = [C.POINTER(FoConfig)]
         R.ref_total_weight_bytes.restype = C.c_uint64
         R.ref_total_weight_bytes.argtypes = [C.POINTER(FoConfig)]
+        R.ref_linear_init.restype = C.c_void_p
+        R.ref_linear_init.argtypes = [C.c_int64, C.c_int64, C.c_int64, C.c_uint64]
+        R.ref_linear_forward.argtypes = [C.c_void_p, C.POINTER(C.c_float), C.POINTER(C.c_double)]
         R.ref_time_forward.restype = C.c_double
         R.ref_time_forward.argtypes = [C.c_void_p, C.POINTER(C.c_int64), C.c_int64, C.c_int]
         _ref = R
@@ -374,3 +377,64 @@ def tiny_prompt(n: int = 128, vocab: int = 32000) -> list[int]:
     g = MT32()
     L.fo_mt32_seed(C.byref(g), C.c_uint32(5))
     return [int(L.fo_mt32_next(C.byref(g)) % vocab) for _ in range(n)]
+
+
+class LinearOracle:
+    """Stacked-linear kind (test infrastructure): the C restatement of
+    init_weights' "linear.<l>" tensors and of reference_linear_forward
+    (reference.hpp:141-152), f64."""
+
+    def __init__(self, layers: int, d_model: int, batch: int = 1, seed: int = 1234, dtype: int = 0):
+        self.layers, self.d_model, self.batch = layers, d_model, batch
+        L = lib()
+        L.fo_fill_linear.argtypes = [C.c_char_p, C.c_int64, C.c_int64, C.c_uint64, C.c_int32,
+                                     C.POINTER(C.c_float)]
+        L.fo_linear_forward.argtypes = [C.POINTER(C.c_float), C.c_int64, C.c_int64, C.c_int64,
+                                        C.POINTER(C.c_float), C.POINTER(C.c_double)]
+        self.w = np.empty((layers, d_model, d_model), np.float32)
+        for l in range(layers):
+            L.fo_fill_linear(f"linear.{l}".encode(), d_model, d_model, seed, dtype,
+                             _p(self.w[l]))
+
+    def tensor(self, name: str) -> np.ndarray:
+        return self.w[int(name.split(".")[1])]
+
+    def forward(self, x0: np.ndarray) -> np.ndarray:
+        x0 = np.ascontiguousarray(x0, np.float32).reshape(self.batch, self.d_model)
+        out = np.empty((self.batch, self.d_model), np.float64)
+        lib().fo_linear_forward(_p(self.w), self.layers, self.d_model, self.batch, _p(x0),
+                                _p(out, C.c_double))
+        return out
+
+
+class RefLinear:
+    """The same from the unmodified reference (oracle/_ref)."""
+
+    def __init__(self, layers: int, d_model: int, batch: int = 1, seed: int = 1234):
+        R = ref_lib()
+        self.layers, self.d_model, self.batch = layers, d_model, batch
+        self._h = R.ref_linear_init(layers, d_model, batch, seed)
+        if not self._h:
+            raise ValueError(R.ref_last_error().decode())
+
+    def tensor(self, name: str) -> np.ndarray:
+        R = ref_lib()
+        out = np.empty((self.d_model, self.d_model), np.float32)
+        if R.ref_get_tensor(self._h, name.encode(), _p(out)) < 0:
+            raise KeyError(name)
+        return out
+
+    def forward(self, x0: np.ndarray) -> np.ndarray:
+        x0 = np.ascontiguousarray(x0, np.float32).reshape(self.batch, self.d_model)
+        out = np.empty((self.batch, self.d_model), np.float64)
+        if ref_lib().ref_linear_forward(self._h, _p(x0), _p(out, C.c_double)):
+            raise ValueError(ref_lib().ref_last_error().decode())
+        return out
+
+    def close(self):
+        if getattr(self, "_h", None):
+            ref_lib().ref_free(self._h)
+            self._h = None
+
+    def __del__(self):
+        self.close()

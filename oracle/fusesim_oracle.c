@@ -697,3 +697,50 @@ done:
     free(attn); free(aout); free(sc);
     return rc;
 }
+
+/* ------------------------------------------------------------------ */
+/* Stacked-linear kind                                                  */
+/* ------------------------------------------------------------------ */
+/* fill_matrix of one named tensor (tensor_store.hpp:270-290) with the
+ * stacked-linear rules: fan-in = cols, never quantized (weight_meta,
+ * tensor_store.hpp:199-210), bf16-rounded when dtype == 0. */
+void fo_fill_linear(const char *name, int64_t rows, int64_t cols, uint64_t seed, int32_t dtype,
+                    float *dst) {
+    fo_config c;
+    memset(&c, 0, sizeof(c));
+    c.dtype = dtype;
+    fill_job j;
+    memset(&j, 0, sizeof(j));
+    snprintf(j.name, sizeof(j.name), "%s", name);
+    j.dst = dst;
+    j.rows = rows;
+    j.cols = cols;
+    j.fan_in_scale = 1.0 / sqrt((double)cols);
+    j.kind = 2;
+    run_fill(&c, seed, &j);
+}
+
+/* reference_linear_forward (reference.hpp:141-152): x <- W_l x for every
+ * layer, f64 accumulation of f32 weights; w = [layers][d][d] row-major. */
+void fo_linear_forward(const float *w, int64_t layers, int64_t d, int64_t batch, const float *x0,
+                       double *out) {
+    double *x = (double *)malloc(sizeof(double) * d), *y = (double *)malloc(sizeof(double) * d);
+    for (int64_t b = 0; b < batch; ++b) {
+        for (int64_t i = 0; i < d; ++i) x[i] = (double)x0[b * d + i];
+        for (int64_t l = 0; l < layers; ++l) {
+            const float *wl = w + (size_t)l * d * d;
+            for (int64_t r = 0; r < d; ++r) {
+                double acc = 0.0;
+                const float *row = wl + (size_t)r * d;
+                for (int64_t c2 = 0; c2 < d; ++c2) acc += (double)row[c2] * x[c2];
+                y[r] = acc;
+            }
+            double *t = x;
+            x = y;
+            y = t;
+        }
+        for (int64_t i = 0; i < d; ++i) out[b * d + i] = x[i];
+    }
+    free(x);
+    free(y);
+}

@@ -128,6 +128,14 @@ void fo_attn_partial_update(double *m, double *l, double *o, int64_t d, const do
 int fo_attn_reduce(const double *m, const double *l, const double *o, int64_t n_partials,
                    int64_t d, double *out);
 
+/* Stacked-linear kind: fill_matrix of "linear.<l>" (tensor_store.hpp:270-290,
+ * fan-in = cols, never quantized) and reference_linear_forward
+ * (reference.hpp:141-152) in f64. */
+void fo_fill_linear(const char *name, int64_t rows, int64_t cols, uint64_t seed, int32_t dtype,
+                    float *dst);
+void fo_linear_forward(const float *w, int64_t layers, int64_t d, int64_t batch, const float *x0,
+                       double *out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -132,7 +132,8 @@ int64_t ref_get_tensor(void* h, const char* name, float* out) {
     auto* st = static_cast<TensorStore*>(h);
     std::string n(name);
     const std::vector<float>* v = nullptr;
-    if (n == "final_norm") v = &st->final_norm;
+    if (n.rfind("linear.", 0) == 0) v = &st->linear_layers.at(std::stoi(n.substr(7))).values;
+    else if (n == "final_norm") v = &st->final_norm;
     else if (n == "embedding") v = &st->embedding.values;
     else if (n == "lm_head") v = &st->lm_head.values;
     else if (n.rfind("layer.", 0) == 0) {
@@ -249,6 +250,32 @@ double ref_time_forward(void* h, const int64_t* tokens, int64_t pos, int steps) 
     }
     std::sort(ts.begin(), ts.end());
     return ts.empty() ? 0.0 : ts[ts.size() / 2];
+}
+
+// Stacked-linear kind (presets.hpp:48-55, reference.hpp:141-152).
+void* ref_linear_init(int64_t layers, int64_t d_model, int64_t batch, uint64_t seed) {
+    TensorStore* st = nullptr;
+    int rc = guarded([&] {
+        ModelConfig m;
+        m.kind = ModelKind::StackedLinear;
+        m.layers = layers;
+        m.d_model = d_model;
+        m.batch = batch;
+        st = new TensorStore(init_weights(m, seed, 1));
+    });
+    return rc == 0 ? st : nullptr;
+}
+
+int ref_linear_forward(void* h, const float* x0, double* out) {
+    auto* st = static_cast<TensorStore*>(h);
+    return guarded([&] {
+        const ModelConfig& m = st->model;
+        for (int64_t b = 0; b < m.batch; ++b)
+            std::memcpy(st->residual[b].data(), x0 + b * m.d_model, sizeof(float) * m.d_model);
+        auto y = reference_linear_forward(*st);
+        for (int64_t b = 0; b < m.batch; ++b)
+            std::memcpy(out + b * m.d_model, y[b].data(), sizeof(double) * m.d_model);
+    });
 }
 
 }  // extern "C"

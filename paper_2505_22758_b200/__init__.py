@@ -70,7 +70,7 @@ class _Cfg(C.Structure):
         ("d_head", C.c_int64), ("n_q_heads", C.c_int64), ("n_kv_heads", C.c_int64),
         ("vocab_size", C.c_int64), ("rope_theta", C.c_double), ("rmsnorm_eps", C.c_double),
         ("dtype", C.c_int32), ("quant_bits", C.c_int32), ("quant_group", C.c_int32),
-        ("batch", C.c_int64),
+        ("batch", C.c_int64), ("kind", C.c_int32), ("reserved_", C.c_int32),
     ]
 
 
@@ -100,6 +100,7 @@ class ModelConfig:
     quant_bits: int = 0
     quant_group: int = 128
     batch: int = 1
+    kind: int = 0           # 0 llama_decoder, 1 stacked_linear (config.hpp:18)
 
     @property
     def qkv_rows(self) -> int:
@@ -115,10 +116,12 @@ class ModelConfig:
     def _c(self) -> _Cfg:
         return _Cfg(self.layers, self.d_model, self.d_inter, self.d_head, self.n_q_heads,
                     self.n_kv_heads, self.vocab_size, self.rope_theta, self.rmsnorm_eps,
-                    self.dtype, self.quant_bits, self.quant_group, self.batch)
+                    self.dtype, self.quant_bits, self.quant_group, self.batch, self.kind, 0)
 
     def streamed_weight_bytes(self) -> int:
         """StoreLayout::streamed_weight_bytes (tensor_store.hpp:170-174)."""
+        if self.kind == 1:  # linear layers are never quantized (tensor_store.hpp:199)
+            return self.layers * self.d_model * self.d_model * 2
         if self.quant_bits == 4:
             row = self.d_model // 2 + (self.d_model // self.quant_group) * 4
         elif self.quant_bits == 8:
@@ -141,6 +144,10 @@ PRESETS = {
     # BASELINE.json configs (SURVEY.md §8 tags T, S)
     "tiny": ModelConfig(4, 512, 1792, 64, 8, 2, 32000),
     "llama32_1b": ModelConfig(16, 2048, 8192, 64, 32, 8, 128256),
+    # stacked-linear presets (presets.hpp:48-55): 32 square layers
+    "stacked_linear_2k": ModelConfig(32, 2048, 0, 0, 0, 0, 0, kind=1),
+    "stacked_linear_4k": ModelConfig(32, 4096, 0, 0, 0, 0, 0, kind=1),
+    "stacked_linear_8k": ModelConfig(32, 8192, 0, 0, 0, 0, 0, kind=1),
 }
 
 
@@ -260,7 +267,9 @@ def all_gather_tp_blobs(blob: bytes, group=None) -> list[bytes]:
 
 
 def tensor_names(cfg: ModelConfig) -> list[str]:
-    """Reference tensor names (tensor_store.hpp:344-363) in upload order."""
+    """Reference tensor names (tensor_store.hpp:339-363) in upload order."""
+    if cfg.kind == 1:
+        return [f"linear.{l}" for l in range(cfg.layers)]
     names = []
     for l in range(cfg.layers):
         names += [f"layer.{l}.{t}" for t in
@@ -312,6 +321,8 @@ def lib():
     L.ffb_get_info.argtypes = [C.c_void_p, P(_Info)]
     L.ffb_decode_loop.argtypes = [C.c_void_p, C.c_void_p, C.c_int64, C.c_int32, C.c_int32,
                                   C.c_void_p, C.c_void_p]
+    L.ffb_linear_forward.argtypes = [C.c_void_p, P(C.c_float), P(C.c_float), C.c_void_p]
+    L.ffb_linear_forward_device.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
     L.ffb_logits_device.argtypes = [C.c_void_p]
     L.ffb_logits_device.restype = C.c_void_p
     L.ffb_quant_row_bytes.argtypes = [C.c_int64, C.c_int32]
@@ -546,6 +557,21 @@ class DecodeModel:
             self.decode_loop(start.data_ptr(), pos, n_steps, out.data_ptr(), False, st)
         torch.cuda.synchronize(self.device)
         return out.cpu().numpy()
+
+    def linear_forward(self, x=None) -> np.ndarray:
+        """Stacked-linear kind (reference_linear_forward, reference.hpp:141-152):
+        x [batch][d_model] (None: the uploaded "residual") -> W_{L-1}...W_0 x."""
+        c = self.cfg
+        out = np.empty((c.batch, c.d_model), np.float32)
+        xi = None if x is None else np.ascontiguousarray(x, np.float32).reshape(c.batch, c.d_model)
+        _check(lib().ffb_linear_forward(self._h, _fp(xi) if xi is not None else None, _fp(out),
+                                        None))
+        return out
+
+    def linear_forward_device(self, d_x_in: int = 0, d_x_out: int = 0, stream: int = 0):
+        _check(lib().ffb_linear_forward_device(self._h, C.c_void_p(d_x_in or None),
+                                               C.c_void_p(d_x_out or None),
+                                               C.c_void_p(stream or None)))
 
     def info(self) -> dict:
         i = _Info()

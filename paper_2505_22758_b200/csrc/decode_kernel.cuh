@@ -133,6 +133,11 @@ struct DecodeParams {
     int32_t vocab_base;   // first global vocab row of this rank's lm_head slice
     float* xch[8];
     uint32_t* xflag[8];
+    // stacked-linear model kind (reference.hpp:141-152, interpreter.hpp:
+    // 227-238): x_{l+1} = W_l x_l, square d_model layers, one stage per layer
+    int32_t kind;           // 0 = llama decoder, 1 = stacked linear
+    const uint8_t* wlin;    // [L][D] rows
+    float* xbuf;            // [2][B][D] ping-pong activations
     float eps;
     double rope_theta;
 };
@@ -335,12 +340,20 @@ struct DecodeCta {
     __device__ int* misc() { return reinterpret_cast<int*>(smem + T::OFF_MISC); }
 
     // ------------------------------------------------------------ schedule
-    __device__ int n_stages() const { return p.layers * kStagesPerLayer + 1; }
+    __device__ int n_stages() const {
+        return p.kind == 1 ? p.layers : p.layers * kStagesPerLayer + 1;
+    }
 
     // counter a stage's consumers wait on before starting, and its target
     __device__ bool dependency(int stage, const uint32_t** ctr, uint32_t* target) const {
         const int l = stage / kStagesPerLayer, s = stage % kStagesPerLayer;
         const uint32_t full_grid = p.epoch * static_cast<uint32_t>(grid);
+        if (p.kind == 1) {  // stacked linear: layer l needs every row of layer l - 1
+            if (stage == 0) return false;
+            *ctr = p.counters + stage - 1;
+            *target = full_grid;
+            return true;
+        }
         if (stage == p.layers * kStagesPerLayer) {  // LM head
             if (p.layers == 0) return false;
             *ctr = p.counters + (p.layers - 1) * kStagesPerLayer + S_RED;
@@ -426,6 +439,11 @@ struct DecodeCta {
     // The lists of (stage, sub) in consumption order; false past the end.
     __device__ bool list_of(int stage, int sub, List& L) const {
         const int l = stage / kStagesPerLayer, s = stage % kStagesPerLayer;
+        if (p.kind == 1) {
+            if (sub > 0) return false;
+            L = {p.wlin + (size_t)stage * D * T::ROW_BYTES, pl.aout_r0, pl.aout_r1, false, false};
+            return true;
+        }
         if (stage == p.layers * kStagesPerLayer) {
             if (sub > 0) return false;
             L = {p.lm_head, pl.lm_r0, pl.lm_r1, false, false};
@@ -2136,11 +2154,33 @@ struct DecodeCta {
         }
     }
 
+    // ---------------------------------------------------------- linear
+    // x_out[rows] = W_l[rows] . x_in (no residual, no norm; f32 accumulation,
+    // interpreter.hpp:227-238)
+    __device__ void stage_linear(uint32_t& it, int l) {
+        Act<> act;
+        const float* xin = p.xbuf + (size_t)(l & 1) * B * D;
+        float* xout = p.xbuf + (size_t)((l + 1) & 1) * B * D;
+        load_act(act, xin, false, nullptr, l);
+        const int ctid = threadIdx.x;
+        gemv(it, act, pl.aout_r0, pl.aout_r1, [&](int c0, int nrows, const float* red) {
+            if (ctid < nrows * B) {
+                const int r = ctid / B, b = ctid % B;
+                __stcg(xout + (size_t)b * D + c0 + r, row_total(red, r, b));
+            }
+        });
+        arrive(p.counters + l, l);
+    }
+
     __device__ void consumer() {
         uint32_t it = 0;
         const int last = min(p.stage_end, n_stages());
         for (int stage = p.stage_begin; stage < last; ++stage) {
             trace_mark(stage, 0);
+            if (p.kind == 1) {
+                stage_linear(it, stage);
+                continue;
+            }
             const int l = stage / kStagesPerLayer, s = stage % kStagesPerLayer;
             if (stage == p.layers * kStagesPerLayer) {
                 stage_lmhead(it);
@@ -2179,7 +2219,7 @@ __global__ void __launch_bounds__(KTraits<S>::NTHREADS, 1)
         cta.rope()[2 * tid + 1] = static_cast<float>(sin(ang));
     }
     // residual init from the embedding: each CTA owns its reduce columns
-    if (p.stage_begin == 0 && tid < T::NCT) {
+    if (p.kind == 0 && p.stage_begin == 0 && tid < T::NCT) {
         for (int b = 0; b < S::B; ++b) {
             const __nv_bfloat16* e = p.embedding + (size_t)p.tokens[b] * S::D;
             for (int c = cta.pl.red_c0 + tid; c < cta.pl.red_c1; c += T::NCT)

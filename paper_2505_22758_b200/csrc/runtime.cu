@@ -68,6 +68,11 @@ const std::vector<KernelOps>& registry() {
 
 const KernelOps* find_ops(const ffb_model_config& c) {
     if (c.dtype != 0) return nullptr;
+    if (c.kind == 1) {  // stacked linear: only the d_model-column GEMV is used
+        for (const auto& k : registry())
+            if (k.D == c.d_model && k.B == c.batch && k.QB == 0 && k.D == k.NQ * k.DH) return &k;
+        return nullptr;
+    }
     if (c.quant_bits != 0 && c.quant_group != kQuantGroup) return nullptr;
     for (const auto& k : registry())
         if (k.D == c.d_model && k.DI == c.d_inter && k.DH == c.d_head && k.NQ == c.n_q_heads &&
@@ -81,6 +86,8 @@ ffb_status validate_cfg(const ffb_model_config* c) {  // config.hpp:61-83
     if (c->layers < 0) return fail(FFB_VALIDATION, "model: layers must be >= 0");
     if (c->d_model <= 0) return fail(FFB_VALIDATION, "model: d_model must be positive");
     if (c->batch < 1 || c->batch > 16) return fail(FFB_VALIDATION, "model: batch must be in [1,16]");
+    if (c->kind != 0 && c->kind != 1) return fail(FFB_VALIDATION, "model: unknown kind");
+    if (c->kind == 1) return FFB_OK;  // stacked_linear: other fields ignored-but-valid
     if (c->d_inter <= 0) return fail(FFB_VALIDATION, "model: d_inter must be positive");
     if (c->d_head <= 0 || c->d_head % 2)
         return fail(FFB_VALIDATION, "model: d_head must be positive and even");
@@ -248,6 +255,8 @@ struct ffb_model {
             *lm_head = nullptr;
     __nv_bfloat16 *embedding = nullptr, *kcache = nullptr, *vcache = nullptr;
     uint64_t quant_inexact_groups = 0;  // packer: groups not on a 4/8-bit grid (lossy)
+    uint8_t* wlin = nullptr;            // stacked linear: [L][D] bf16 rows
+    float* xbuf = nullptr;              // stacked linear: [2][B][D]
     float *norm_attn = nullptr, *norm_ffn = nullptr, *final_norm = nullptr;
     float *x = nullptr, *q = nullptr, *attn_out = nullptr, *glu_part = nullptr,
           *attn_part = nullptr, *logits = nullptr, *amax_val = nullptr;
@@ -293,6 +302,25 @@ namespace {
 ffb_status build_plan(ffb_model* m) {
     const auto& c = m->cfg;
     const int64_t G = m->grid;
+    if (c.kind == 1) {  // stacked linear: rows of every layer split over the CTAs
+        if ((int64_t)m->sm_weight.size() != G) m->sm_weight.assign(G, 1.0);
+        std::vector<double> cum(G + 1, 0.0);
+        for (int64_t k = 0; k < G; ++k) cum[k + 1] = cum[k] + m->sm_weight[k];
+        std::vector<CtaPlan> plan(G);
+        for (int64_t i = 0; i < G; ++i) {
+            CtaPlan& p = plan[i];
+            std::memset(&p, 0, sizeof(p));
+            p.aout_r0 = static_cast<int32_t>(i == 0 ? 0 : std::llround(c.d_model * cum[i] / cum[G]));
+            p.aout_r1 = static_cast<int32_t>(i + 1 == G ? c.d_model
+                                                          : std::llround(c.d_model * cum[i + 1] / cum[G]));
+            p.attn_unit = -1;
+        }
+        m->n_units = 0;
+        m->attn_group = 0;
+        CUDA_TRY(cudaMemcpy(m->plan, plan.data(), sizeof(CtaPlan) * G, cudaMemcpyHostToDevice));
+        m->plan_host = plan;
+        return FFB_OK;
+    }
     m->n_units = static_cast<int>(c.batch * c.n_kv_heads);
     if (m->n_units > G) return fail(FFB_UNSUPPORTED, "batch * n_kv_heads exceeds the SM count");
     // split-K group per (batch row, kv head): as many SMs as fit, at most
@@ -474,6 +502,10 @@ DecodeParams make_params(const ffb_model* m, int64_t pos, const int64_t* d_token
     p.pool_ct = m->pool_ct;
     p.pool_chunks = m->pool_chunks;
     p.sm_rank = (m->mode == FFB_MODE_BASELINE || !m->use_sm_rank) ? nullptr : m->sm_rank;
+    p.kind = m->cfg.kind;
+    p.wlin = m->wlin;
+    p.xbuf = m->xbuf;
+    if (m->cfg.kind == 1) p.stage_end = static_cast<int32_t>(m->cfg.layers);
     p.tp_size = m->tp_size;
     p.tp_rank = m->tp_rank;
     p.vocab_base = static_cast<int32_t>(m->vocab_base);
@@ -489,6 +521,10 @@ DecodeParams make_params(const ffb_model* m, int64_t pos, const int64_t* d_token
 // the plan changes (the pool counter base depends on pool_chunks).
 ffb_status reset_sync_state(ffb_model* m, cudaStream_t stream) {
     const int64_t Lc = std::max<int64_t>(1, m->cfg.layers);
+    if (m->cfg.kind == 1) {
+        CUDA_TRY(cudaMemsetAsync(m->counters, 0, sizeof(uint32_t) * (Lc + 1), stream));
+        return FFB_OK;
+    }
     CUDA_TRY(cudaMemsetAsync(m->counters, 0, sizeof(uint32_t) * (Lc * 5 + 1), stream));
     if (m->xflag) CUDA_TRY(cudaMemsetAsync(m->xflag, 0, m->xflag_bytes, stream));
     CUDA_TRY(cudaMemsetAsync(m->qkv_head_counters, 0,
@@ -510,7 +546,8 @@ ffb_status launch_step(ffb_model* m, int64_t pos, const int64_t* d_tokens, float
     }
     DecodeParams p = make_params(m, pos, d_tokens, d_logits, d_greedy);
     if (m->mode == FFB_MODE_BASELINE) {
-        const int n = static_cast<int>(m->cfg.layers * kStagesPerLayer + 1);
+        const int n = m->cfg.kind == 1 ? static_cast<int>(m->cfg.layers)
+                                       : static_cast<int>(m->cfg.layers * kStagesPerLayer + 1);
         for (int s = 0; s < n; ++s) {
             p.stage_begin = s;
             p.stage_end = s + 1;
@@ -569,6 +606,22 @@ bool resolve(ffb_model* m, const std::string& name, TensorDst* d) {
         d->rows = {{0, n / d->gcols}};
         d->row_bytes = kind == 2 ? D * 2 : n * 4;
     };
+    if (c.kind == 1) {  // stacked linear: "linear.<l>" (d x d), "residual" (batch x d)
+        if (name == "residual") {
+            vec(m->xbuf, c.batch * D, 1);
+            return true;
+        }
+        if (name.rfind("linear.", 0) != 0) return false;
+        int64_t l = -1;
+        try {
+            l = std::stoll(name.substr(7));
+        } catch (...) {
+            return false;
+        }
+        if (l < 0 || l >= c.layers) return false;
+        mat(m->wlin + l * D * RB, D, {{0, D}}, 0, D, RB);
+        return true;
+    }
     if (name == "embedding") { vec(m->embedding, g.vocab_size * D, 2); return true; }
     if (name == "lm_head") {
         mat(m->lm_head, g.vocab_size, {{m->vocab_base, m->vocab_base + c.vocab_size}}, 0, D, RB);
@@ -811,9 +864,13 @@ ffb_status ffb_create_ex(const ffb_model_config* gcfg, int64_t max_seq_len, int 
     *out = nullptr;
     ffb_status st = validate_cfg(gcfg);
     if (st) return st;
-    ffb_model_config local;
-    st = shard_config(*gcfg, tp_rank, tp_size, &local);
-    if (st) return st;
+    ffb_model_config local = *gcfg;
+    if (gcfg->kind == 1) {
+        if (tp_size != 1) return fail(FFB_UNSUPPORTED, "stacked_linear: tensor parallelism not built");
+    } else {
+        st = shard_config(*gcfg, tp_rank, tp_size, &local);
+        if (st) return st;
+    }
     const ffb_model_config* cfg = &local;
     if (max_seq_len < 1) return fail(FFB_VALIDATION, "max_seq_len must be >= 1");
     const KernelOps* ops = find_ops(*cfg);
@@ -867,6 +924,28 @@ ffb_status ffb_create_ex(const ffb_model_config* gcfg, int64_t max_seq_len, int 
     const auto& c = *cfg;
     const int64_t L = c.layers, D = c.d_model, B = c.batch, V = c.vocab_size;
     const int64_t Lc = std::max<int64_t>(L, 1);
+    if (c.kind == 1) {  // stacked linear: weights, ping-pong activations, counters, plan
+        m->kv_len.assign(cfg->layers, 0);
+        m->l2_prefetch = 0;
+        m->kv_prefetch = 0;
+        m->tp_connected = true;
+        ffb_status s2 = FFB_OK;
+        if (!s2) s2 = m->alloc(&m->wlin, (size_t)Lc * D * ops->row_bytes);
+        if (!s2) s2 = m->alloc(&m->xbuf, (size_t)2 * B * D);
+        if (!s2) s2 = m->alloc(&m->counters, (size_t)Lc + 1);
+        if (!s2) s2 = m->alloc(&m->plan, (size_t)m->grid);
+        if (!s2) s2 = m->alloc(&m->staging, (size_t)ffb_model::kStagingElems);
+        if (s2) return bail(s2);
+        if (cudaMemset(m->counters, 0, sizeof(uint32_t) * (Lc + 1)) != cudaSuccess ||
+            cudaMemset(m->xbuf, 0, sizeof(float) * 2 * B * D) != cudaSuccess)
+            return bail(fail(FFB_DEVICE, "cudaMemset failed"));
+        st = build_plan(m);
+        if (st) return bail(st);
+        st = probe_sm_ranks(m);
+        if (st) return bail(st);
+        *out = m;
+        return FFB_OK;
+    }
 #define ALLOC(ptr, n)                 \
     do {                              \
         ffb_status s_ = m->alloc(&(ptr), (n)); \
@@ -1000,6 +1079,17 @@ ffb_status ffb_upload_tensor(ffb_model* m, const char* name, const float* values
 ffb_status ffb_init_synthetic(ffb_model* m, uint64_t seed) {
     if (!m) return fail(FFB_USAGE, "NULL handle");
     CUDA_TRY(cudaSetDevice(m->device));
+    if (m->cfg.kind == 1) {
+        const int64_t D = m->cfg.d_model;
+        synth_bf16_kernel<<<4096, 256, 0, m->stream>>>(reinterpret_cast<__nv_bfloat16*>(m->wlin),
+                                                       m->cfg.layers * D * D, seed * 31 + 1,
+                                                       1.0f / std::sqrt(static_cast<float>(D)));
+        synth_f32_kernel<<<64, 256, 0, m->stream>>>(m->xbuf, m->cfg.batch * D, seed * 31 + 2,
+                                                    0.0f, 1.0f);
+        CUDA_TRY(cudaGetLastError());
+        CUDA_TRY(cudaStreamSynchronize(m->stream));
+        return FFB_OK;
+    }
     const auto& c = m->cfg;
     const int64_t L = c.layers, D = c.d_model;
     const float sd = 1.0f / std::sqrt(static_cast<float>(D));
@@ -1228,6 +1318,9 @@ int64_t ffb_get_trace(ffb_model* m, uint64_t* out, int64_t n) {
 
 static ffb_status check_step(ffb_model* m, const int64_t* tokens, int64_t pos) {
     const auto& c = m->cfg;
+    if (m->cfg.kind != 0)
+        return fail(FFB_VALIDATION, "decode_step: llama_decoder models only (stacked_linear: "
+                                    "ffb_linear_forward)");
     if (!m->tp_connected)
         return fail(FFB_USAGE, "tensor-parallel rank not connected (ffb_tp_connect)");
     if (tokens)
@@ -1306,6 +1399,38 @@ ffb_status ffb_decode_loop(ffb_model* m, const int64_t* d_tokens, int64_t pos, i
     return FFB_OK;
 }
 
+ffb_status ffb_linear_forward_device(ffb_model* m, const float* d_x_in, float* d_x_out,
+                                     void* stream) {
+    if (!m) return fail(FFB_USAGE, "NULL handle");
+    if (m->cfg.kind != 1) return fail(FFB_VALIDATION, "linear_forward: stacked_linear models only");
+    CUDA_TRY(cudaSetDevice(m->device));
+    cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : m->stream;
+    const size_t bytes = sizeof(float) * m->cfg.batch * m->cfg.d_model;
+    if (d_x_in) CUDA_TRY(cudaMemcpyAsync(m->xbuf, d_x_in, bytes, cudaMemcpyDeviceToDevice, s));
+    ffb_status st = launch_step(m, 0, nullptr, nullptr, nullptr, s);
+    if (st) return st;
+    if (d_x_out)
+        CUDA_TRY(cudaMemcpyAsync(d_x_out, m->xbuf + (m->cfg.layers & 1) * m->cfg.batch * m->cfg.d_model,
+                                 bytes, cudaMemcpyDeviceToDevice, s));
+    return FFB_OK;
+}
+
+ffb_status ffb_linear_forward(ffb_model* m, const float* x_in, float* x_out, void* stream) {
+    if (!m) return fail(FFB_USAGE, "NULL handle");
+    if (m->cfg.kind != 1) return fail(FFB_VALIDATION, "linear_forward: stacked_linear models only");
+    CUDA_TRY(cudaSetDevice(m->device));
+    cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : m->stream;
+    const size_t bytes = sizeof(float) * m->cfg.batch * m->cfg.d_model;
+    if (x_in) CUDA_TRY(cudaMemcpyAsync(m->xbuf, x_in, bytes, cudaMemcpyHostToDevice, s));
+    ffb_status st = launch_step(m, 0, nullptr, nullptr, nullptr, s);
+    if (st) return st;
+    if (x_out)
+        CUDA_TRY(cudaMemcpyAsync(x_out, m->xbuf + (m->cfg.layers & 1) * m->cfg.batch * m->cfg.d_model,
+                                 bytes, cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaStreamSynchronize(s));
+    return FFB_OK;
+}
+
 ffb_status ffb_get_info(const ffb_model* m, ffb_info* out) {
     if (!m || !out) return fail(FFB_USAGE, "NULL argument");
     const auto& c = m->cfg;
@@ -1319,7 +1444,8 @@ ffb_status ffb_get_info(const ffb_model* m, ffb_info* out) {
         m->mode == FFB_MODE_BASELINE ? static_cast<int32_t>(c.layers * kStagesPerLayer + 1) : 1;
     out->mode = m->mode;
     const uint64_t row = static_cast<uint64_t>(m->ops->row_bytes);
-    out->weight_bytes = row * (static_cast<uint64_t>(c.layers) * (m->qkv_rows() + 3 * c.d_inter) +
+    if (c.kind == 1) out->weight_bytes = row * static_cast<uint64_t>(c.layers) * c.d_model;
+    else out->weight_bytes = row * (static_cast<uint64_t>(c.layers) * (m->qkv_rows() + 3 * c.d_inter) +
                                c.vocab_size) +
                         static_cast<uint64_t>(m->ops->row_bytes_a) * c.layers * c.d_model;
     out->quant_inexact_groups = m->quant_inexact_groups;
@@ -1334,6 +1460,7 @@ ffb_status ffb_calibrate(ffb_model* m, int32_t iterations) {
     if (!m) return fail(FFB_USAGE, "NULL handle");
     if (m->tp_size > 1)
         return fail(FFB_UNSUPPORTED, "calibrate: per-rank plans would desynchronise TP epochs");
+    if (m->cfg.kind != 0) return fail(FFB_UNSUPPORTED, "calibrate: llama_decoder models only");
     if (iterations < 0 || iterations > 16) return fail(FFB_USAGE, "iterations in [0, 16]");
     const auto& c = m->cfg;
     const int G = m->grid;

@@ -270,3 +270,29 @@ def test_device_resident_decode_loop_matches_stepwise_and_oracle():
     for i in range(1, n):
         want.append(int(np.argmax(st.forward([want[-1]], len(prompt) + i - 1)[0])))
     assert gen == ref == want, (gen, ref, want)
+
+
+@pytest.mark.parametrize("d,layers,batch", [(2048, 4, 1), (4096, 3, 1), (4096, 2, 4)])
+def test_stacked_linear_matches_oracle_all_modes(d, layers, batch):
+    """Stacked-linear kind (reference_linear_forward, reference.hpp:141-152;
+    the paper's fusion ablation): x <- W_l x through `layers` square bf16
+    layers in one persistent launch (or one launch per layer in BASELINE),
+    against the f64 oracle; the three modes agree bit for bit."""
+    from paper_2505_22758_b200 import ModelConfig
+    lo = O.LinearOracle(layers, d, batch, 1234)
+    x = np.random.default_rng(1).standard_normal((batch, d)).astype(np.float32)
+    want = lo.forward(x)
+    cfg = ModelConfig(layers, d, 0, 0, 0, 0, 0, batch=batch, kind=1)
+    outs = []
+    with DecodeModel(cfg, 1) as m:
+        for l in range(layers):
+            m.upload_tensor(f"linear.{l}", lo.tensor(f"linear.{l}"))
+        for mode in MODES:
+            m.set_mode(mode)
+            outs.append(m.linear_forward(x))
+        m.upload_tensor("residual", x)
+        np.testing.assert_array_equal(m.linear_forward(None), outs[-1])
+    for b in range(batch):
+        assert rel_err(outs[-1][b], want[b]) < 1e-5
+    np.testing.assert_array_equal(outs[0], outs[1])
+    np.testing.assert_array_equal(outs[1], outs[2])

@@ -270,3 +270,16 @@ def test_capacity_error():
     st.forward([1], 1)
     with pytest.raises(ValueError, match="capacity"):
         st.forward([1], 2)
+
+
+def test_stacked_linear_oracle_bit_exact_vs_reference():
+    """Stacked-linear kind: the restated linear.<l>
+    tensors and reference_linear_forward equal the reference's bit for bit."""
+    if not O.ref_available():
+        pytest.skip("oracle/_ref not built")
+    lo = O.LinearOracle(3, 256, 2, 1234)
+    rl = O.RefLinear(3, 256, 2, 1234)
+    for l in range(3):
+        np.testing.assert_array_equal(lo.tensor(f"linear.{l}"), rl.tensor(f"linear.{l}"))
+    x = np.random.default_rng(0).standard_normal((2, 256)).astype(np.float32)
+    np.testing.assert_array_equal(lo.forward(x), rl.forward(x))

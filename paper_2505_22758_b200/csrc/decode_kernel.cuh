@@ -278,8 +278,10 @@ struct KTraits : RowMap<S, S::D> {
     // and its scratch: alpha*q [QPG][DH], scores [QPG][ANP], probabilities
     // [ANP][QPG], stats
     static constexpr int ATT_SC = cmax(1, 131072 / SLOT_BYTES);
-    static constexpr int ANP = ((ATT_SC * KVC + 1) + 3) / 4 * 4;
-    static constexpr int SZ_ATT = S::QPG * S::DH + 2 * S::QPG * ANP + 4 * S::QPG;
+    static constexpr int ANP = ((ATT_SC * KVC + 1) + 15) / 16 * 16;
+    // alpha*q f32 [QPG][DH], scores f32 [QPG][ANP], probabilities as bf16
+    // hi/lo MMA rows [16][ANP] (tensor-core P.V), stats [QPG][4]
+    static constexpr int SZ_ATT = S::QPG * S::DH + S::QPG * ANP + cmax(S::QPG, 8) * ANP + 4 * S::QPG;
     static constexpr int SZ_WPART =
         4 * cmax(cmax(cmax(cmax(NCW * S::QPG * (S::DH + 2), 3 * kMaxGrid * S::QPG),
                            cmax(2 * kMaxGrid * S::B, NCW * 32)),
@@ -1363,27 +1365,29 @@ struct DecodeCta {
                     }
                     continue;
                 }
-                float a0[B], a1[B];
+                // packed f32x2 FMAs on (even, odd) column pairs: one FFMA2
+                // per two weights and batch row; two chains per batch row
+                float2 a0[B], a1[B];
 #pragma unroll
-                for (int b = 0; b < B; ++b) a0[b] = a1[b] = 0.f;
+                for (int b = 0; b < B; ++b) a0[b] = a1[b] = make_float2(0.f, 0.f);
 #pragma unroll
                 for (int j = 0; j < M::VPT; ++j) {
                     const uint4 w = lds_u128(rowp + (lt + j * M::TPR) * 16);
+                    const float2 w0 = make_float2(bf_lo(w.x), bf_hi(w.x));
+                    const float2 w1 = make_float2(bf_lo(w.y), bf_hi(w.y));
+                    const float2 w2 = make_float2(bf_lo(w.z), bf_hi(w.z));
+                    const float2 w3 = make_float2(bf_lo(w.w), bf_hi(w.w));
 #pragma unroll
                     for (int b = 0; b < B; ++b) {
                         const float(&a)[8] = act.v[b][j];
-                        a0[b] = fmaf(bf_lo(w.x), a[0], a0[b]);
-                        a1[b] = fmaf(bf_hi(w.x), a[1], a1[b]);
-                        a0[b] = fmaf(bf_lo(w.y), a[2], a0[b]);
-                        a1[b] = fmaf(bf_hi(w.y), a[3], a1[b]);
-                        a0[b] = fmaf(bf_lo(w.z), a[4], a0[b]);
-                        a1[b] = fmaf(bf_hi(w.z), a[5], a1[b]);
-                        a0[b] = fmaf(bf_lo(w.w), a[6], a0[b]);
-                        a1[b] = fmaf(bf_hi(w.w), a[7], a1[b]);
+                        a0[b] = __ffma2_rn(w0, make_float2(a[0], a[1]), a0[b]);
+                        a1[b] = __ffma2_rn(w1, make_float2(a[2], a[3]), a1[b]);
+                        a0[b] = __ffma2_rn(w2, make_float2(a[4], a[5]), a0[b]);
+                        a1[b] = __ffma2_rn(w3, make_float2(a[6], a[7]), a1[b]);
                     }
                 }
 #pragma unroll
-                for (int b = 0; b < B; ++b) v[r * B + b] = a0[b] + a1[b];
+                for (int b = 0; b < B; ++b) v[r * B + b] = (a0[b].x + a1[b].x) + (a0[b].y + a1[b].y);
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(&empty[slot]);
@@ -1482,7 +1486,8 @@ struct DecodeCta {
     __device__ float* att_q() { return wpart(); }                 // [QPG][DH]
     __device__ float* att_sc() { return att_q() + QPG * DH; }     // [QPG][ANP]
     __device__ float* att_p() { return att_sc() + QPG * ANP; }    // [ANP][QPG]
-    __device__ float* att_st() { return att_p() + ANP * QPG; }    // [QPG][4] m l scale
+    __device__ float* att_st() { return att_p() + ANP * (QPG > 8 ? QPG : 8); }  // [QPG][4] m l scale
+    __device__ __nv_bfloat16* att_pt() { return reinterpret_cast<__nv_bfloat16*>(att_p()); }  // [16][ANP]
 
     // K (kv = 0) or V (kv = 1) row of pass position j: ring slot (it0 + j /
     // KVC) for j < nring, else the current token staged in h_s
@@ -1597,6 +1602,186 @@ struct DecodeCta {
         consumer_sync(NCT);  // sc / p / stats reusable by the next pass
     }
 
+    // ---- tensor-core attention pass (mma.sync m16n8k16 bf16, f32 accumulate)
+    // GQA groups QPG query heads on one kv head, so the decode step is two
+    // small contractions per pass: S[pos][h] = K[pos][:] . (alpha q_h) with
+    // K tiles as A (ldmatrix from the swizzled ring rows) and q as B, and
+    // O[h][dim] = P[h][pos] V[pos][dim] with P as A and V tiles as B
+    // (ldmatrix.trans).  q and P enter as bf16 hi + lo (two MMA columns /
+    // rows per head: 16 bits of mantissa), K and V are bf16 already.
+    static constexpr int NTS = (2 * QPG + 7) / 8;  // score n-tiles (hi/lo columns)
+    static constexpr int DPW = DH / NCW;           // P.V output dims per warp
+    static constexpr int NTW = DPW / 8;            // P.V n-tiles per warp
+    static_assert(2 * QPG <= 16 && DPW % 8 == 0 && (NTW == 1 || NTW == 2), "TC attention shape");
+
+    __device__ static uint32_t bf2_pack(float lo_elem, float hi_elem) {
+        __nv_bfloat162 v = __floats2bfloat162_rn(lo_elem, hi_elem);
+        return *reinterpret_cast<uint32_t*>(&v);
+    }
+
+    __device__ static void mma_bf16(float (&c)[4], uint32_t a0, uint32_t a1, uint32_t a2,
+                                    uint32_t a3, uint32_t b0, uint32_t b1) {
+        asm volatile(
+            "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
+            "{%8,%9}, {%0,%1,%2,%3};"
+            : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+            : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+    }
+
+    __device__ static void ldsm_x4(const void* p, uint32_t& r0, uint32_t& r1, uint32_t& r2,
+                                   uint32_t& r3) {
+        asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+                     : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+                     : "r"(smem_u32(p)));
+    }
+
+    __device__ static void ldsm_x4_t(const void* p, uint32_t& r0, uint32_t& r1, uint32_t& r2,
+                                     uint32_t& r3) {
+        asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
+                     : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+                     : "r"(smem_u32(p)));
+    }
+
+    __device__ static void ldsm_x2_t(const void* p, uint32_t& r0, uint32_t& r1) {
+        asm volatile("ldmatrix.sync.aligned.m8n8.x2.trans.shared.b16 {%0,%1}, [%2];"
+                     : "=r"(r0), "=r"(r1)
+                     : "r"(smem_u32(p)));
+    }
+
+    // o[NTW][4]: this warp's P.V accumulator (rows = heads hi/lo, columns =
+    // its dims), carried across passes (online softmax rescale per row).
+    __device__ void attn_pass_tc(uint32_t it0, int nring, int n, int pos0, float (&o)[NTW][4]) {
+        const int ctid = threadIdx.x, warp = ctid / 32, lane = ctid % 32, g = lane / 4, q4 = lane % 4;
+        float* sc = att_sc();
+        const float* qs = att_q();
+        float* st = att_st();
+        __nv_bfloat16* pt = att_pt();
+        const int ntiles = (n + 15) / 16;
+        {  // A: scores, warps over 16-position tiles
+            uint32_t qb[DH / 16][NTS][2];  // q B fragments (column = head hi / lo)
+#pragma unroll
+            for (int kk = 0; kk < DH / 16; ++kk)
+#pragma unroll
+                for (int nt = 0; nt < NTS; ++nt) {
+                    const int col = nt * 8 + g;
+                    const int h = col % QPG;
+                    const bool live = col < 2 * QPG, lo = col >= QPG;
+#pragma unroll
+                    for (int r = 0; r < 2; ++r) {
+                        const int d = kk * 16 + 2 * q4 + 8 * r;
+                        uint32_t v = 0u;
+                        if (live) {
+                            const float x0 = qs[h * DH + d], x1 = qs[h * DH + d + 1];
+                            if (lo) {
+                                const float h0 = __bfloat162float(__float2bfloat16_rn(x0));
+                                const float h1 = __bfloat162float(__float2bfloat16_rn(x1));
+                                v = bf2_pack(x0 - h0, x1 - h1);
+                            } else {
+                                v = bf2_pack(x0, x1);
+                            }
+                        }
+                        qb[kk][nt][r] = v;
+                    }
+                }
+            for (int t = warp; t < ntiles; t += NCW) {
+                // this lane's ldmatrix row: position t*16 + (lane & 7) + 8 * ((lane >> 3) & 1)
+                const int jr = min(t * 16 + (lane & 7) + 8 * ((lane >> 3) & 1), n - 1);
+                const uint8_t* row = att_row(it0, jr, nring, 0);
+                const int key = (pos0 + jr) & 7;
+                float c[NTS][4];
+#pragma unroll
+                for (int nt = 0; nt < NTS; ++nt)
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) c[nt][e] = 0.f;
+#pragma unroll
+                for (int kk = 0; kk < DH / 16; ++kk) {
+                    uint32_t a0, a1, a2, a3;
+                    ldsm_x4(row + (((2 * kk + (lane >> 4)) ^ key) << 4), a0, a1, a2, a3);
+#pragma unroll
+                    for (int nt = 0; nt < NTS; ++nt)
+                        mma_bf16(c[nt], a0, a1, a2, a3, qb[kk][nt][0], qb[kk][nt][1]);
+                }
+                // C[pos][col]: fold the lo column into the hi one
+#pragma unroll
+                for (int nt = 0; nt < NTS; ++nt)
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        const int col = nt * 8 + 2 * q4 + (e & 1);
+                        const int j = t * 16 + g + 8 * (e >> 1);
+                        if (QPG >= 4) {
+                            // lo of column col sits at col + QPG: same n-tile for QPG = 4
+                            // (lane q4 + 2), next n-tile for QPG = 8 (same lane)
+                            float partner;
+                            if constexpr (QPG == 8) partner = nt == 0 ? c[NTS - 1][e] : 0.f;
+                            else partner = __shfl_xor_sync(0xffffffffu, c[nt][e], QPG / 2);
+                            if (col < QPG && j < n) sc[col * ANP + j] = c[nt][e] + partner;
+                        } else {  // QPG 2: lo columns 2, 3 at lane q4 + 1
+                            const float partner = __shfl_xor_sync(0xffffffffu, c[nt][e], 1);
+                            if (col < QPG && j < n) sc[col * ANP + j] = c[nt][e] + partner;
+                        }
+                    }
+            }
+        }
+        consumer_sync(NCT);
+        for (int h = warp; h < QPG; h += NCW) {  // B: online softmax of head h -> P hi/lo rows
+            float cmax = -INFINITY;
+            for (int j = lane; j < n; j += 32) cmax = fmaxf(cmax, sc[h * ANP + j]);
+            cmax = warp_max(cmax);
+            const float m_old = st[h * 4 + 0];
+            const float m_new = fmaxf(m_old, cmax);
+            const float scale = exp2f(m_old - m_new);  // 0 for the first pass
+            float psum = 0.f;
+            for (int j = lane; j < ntiles * 16; j += 32) {
+                const float pj = j < n ? exp2f(sc[h * ANP + j] - m_new) : 0.f;
+                const __nv_bfloat16 hi = __float2bfloat16_rn(pj);
+                pt[h * ANP + j] = hi;
+                pt[(QPG + h) * ANP + j] = __float2bfloat16_rn(pj - __bfloat162float(hi));
+                psum += pj;
+            }
+            psum = warp_sum(psum);
+            if (lane == 0) {
+                st[h * 4 + 0] = m_new;
+                st[h * 4 + 1] = st[h * 4 + 1] * scale + psum;
+                st[h * 4 + 2] = scale;
+            }
+        }
+        consumer_sync(NCT);
+        {  // C: P.V, warp w owns dims [w DPW, (w+1) DPW) over every position
+            const int r0 = g, r1 = g + 8;  // A rows (heads hi/lo) of this lane
+            const float s0 = r0 < 2 * QPG ? st[(r0 % QPG) * 4 + 2] : 0.f;
+            const float s1 = r1 < 2 * QPG ? st[(r1 % QPG) * 4 + 2] : 0.f;
+#pragma unroll
+            for (int nt = 0; nt < NTW; ++nt) {
+                o[nt][0] *= s0;
+                o[nt][1] *= s0;
+                o[nt][2] *= s1;
+                o[nt][3] *= s1;
+            }
+            const int c0 = warp * (DPW / 8);  // first 16-byte dim chunk of this warp
+            for (int t = 0; t < ntiles; ++t) {
+                const uint32_t a0 = r0 < 2 * QPG ? *reinterpret_cast<const uint32_t*>(pt + r0 * ANP + t * 16 + 2 * q4) : 0u;
+                const uint32_t a2 = r0 < 2 * QPG ? *reinterpret_cast<const uint32_t*>(pt + r0 * ANP + t * 16 + 2 * q4 + 8) : 0u;
+                const uint32_t a1 = r1 < 2 * QPG ? *reinterpret_cast<const uint32_t*>(pt + r1 * ANP + t * 16 + 2 * q4) : 0u;
+                const uint32_t a3 = r1 < 2 * QPG ? *reinterpret_cast<const uint32_t*>(pt + r1 * ANP + t * 16 + 2 * q4 + 8) : 0u;
+                // ldmatrix.trans rows: position t*16 + (lane & 7) + 8*((lane>>3)&1), chunk c0 + (lane>>4)
+                const int jr = min(t * 16 + (lane & 7) + 8 * ((lane >> 3) & 1), n - 1);
+                const uint8_t* row = att_row(it0, jr, nring, 1);
+                const int key = (pos0 + jr) & 7;
+                if constexpr (NTW == 2) {
+                    uint32_t b00, b01, b10, b11;
+                    ldsm_x4_t(row + (((c0 + (lane >> 4)) ^ key) << 4), b00, b01, b10, b11);
+                    mma_bf16(o[0], a0, a1, a2, a3, b00, b01);
+                    mma_bf16(o[NTW - 1], a0, a1, a2, a3, b10, b11);
+                } else {
+                    uint32_t b00, b01;
+                    ldsm_x2_t(row + ((c0 ^ key) << 4), b00, b01);
+                    mma_bf16(o[0], a0, a1, a2, a3, b00, b01);
+                }
+            }
+        }
+        consumer_sync(NCT);  // sc / pt / stats reusable by the next pass
+    }
+
     __device__ void stage_attn(uint32_t& it, int l) {
         if (pl.attn_unit < 0) return;  // idle CTA: no chunks were streamed
         const int ctid = threadIdx.x, warp = ctid / 32, lane = ctid % 32;
@@ -1631,11 +1816,11 @@ struct DecodeCta {
                 }
             }
         }
-        float2 o[QPG][4];
+        float o[NTW][4];
 #pragma unroll
-        for (int h = 0; h < QPG; ++h)
+        for (int nt = 0; nt < NTW; ++nt)
 #pragma unroll
-            for (int e = 0; e < 4; ++e) o[h][e] = make_float2(0.f, 0.f);
+            for (int e = 0; e < 4; ++e) o[nt][e] = 0.f;
         consumer_sync(NCT);
         trace_mark(l * kStagesPerLayer + S_ATTN, 5);
 
@@ -1649,7 +1834,7 @@ struct DecodeCta {
             for (int s = 0; s < nslots; ++s, ++it)
                 wait_full(it % T::NSLOTS, (it / T::NSLOTS) & 1);
             trace_mark(l * kStagesPerLayer + S_ATTN, 6);
-            attn_pass(it0, nring, n, c0, o);
+            attn_pass_tc(it0, nring, n, c0, o);
             if (lane == 0)
                 for (uint32_t i = it0; i < it; ++i) mbar_arrive(&empty[i % T::NSLOTS]);
             if (last) break;
@@ -1662,36 +1847,35 @@ struct DecodeCta {
             mlc[2 * ctid] = st[ctid * 4 + 0];
             mlc[2 * ctid + 1] = st[ctid * 4 + 1];
         }
-        // groups sharing a warp first (lanes dc, dc + DC, ...), then warps
-#pragma unroll
-        for (int h = 0; h < QPG; ++h)
-#pragma unroll
-            for (int e = 0; e < 4; ++e)
-#pragma unroll
-                for (int off = DC; off < 32; off <<= 1) {
-                    o[h][e].x += __shfl_xor_sync(0xffffffffu, o[h][e].x, off);
-                    o[h][e].y += __shfl_xor_sync(0xffffffffu, o[h][e].y, off);
-                }
-        consumer_sync(NCT);  // st/sc/p/q dead from here: wpart reused for o
-        float* ro = wpart();  // [NCW][QPG][DH]
+        // O[h][dim] = C[row h][dim] + C[row QPG + h][dim] (hi + lo of P):
+        // QPG = 8: rows g / g + 8 of the same lane; QPG < 8: row g + QPG is
+        // lane + 4 QPG.  Each (h, d) is owned by one lane: no cross-warp sum.
+        float ov[NTW][2];
         {
-            const int dc = ctid % DC;
-            if (lane < DC || DC >= 32) {
 #pragma unroll
-                for (int h = 0; h < QPG; ++h)
+            for (int nt = 0; nt < NTW; ++nt)
 #pragma unroll
-                    for (int e = 0; e < 4; ++e)
-                        *reinterpret_cast<float2*>(ro + (warp * QPG + h) * DH + dc * 8 + 2 * e) =
-                            o[h][e];
-            }
+                for (int e = 0; e < 2; ++e) {
+                    if constexpr (QPG == 8) ov[nt][e] = o[nt][e] + o[nt][e + 2];
+                    else ov[nt][e] = o[nt][e] + __shfl_xor_sync(0xffffffffu, o[nt][e], 4 * QPG);
+                }
+        }
+        consumer_sync(NCT);  // q / scores / P / stats dead from here: wpart reused for O
+        float* ro = wpart();  // [QPG][DH]
+        {
+            const int g = lane / 4, q4 = lane % 4;
+            if (g < QPG)
+#pragma unroll
+                for (int nt = 0; nt < NTW; ++nt)
+#pragma unroll
+                    for (int e = 0; e < 2; ++e)
+                        ro[g * DH + warp * DPW + nt * 8 + 2 * q4 + e] = ov[nt][e];
         }
         consumer_sync(NCT);
         float* part = p.attn_part + ((size_t)unit * grid + pl.attn_g) * QPG * STR;
         for (int idx = ctid; idx < QPG * DH; idx += NCT) {
             const int h = idx / DH, d = idx % DH;
-            float O = 0.f;
-            for (int w = 0; w < NCW; ++w)
-                if ((w * 32) % DC == 0 || DC >= 32) O += ro[(w * QPG + h) * DH + d];
+            const float O = ro[h * DH + d];
             float* dst = part + h * STR;
             __stcg(dst + 2 + d, O);
             if (d == 0) {
@@ -1923,12 +2107,21 @@ struct DecodeCta {
 #pragma unroll
                 for (int j = 0; j < T::VPT; ++j) {
                     const uint4 w = lds_u128(base + row * T::ROW_BYTES + (lt + j * T::TPR) * 16);
-                    const float wf[8] = {bf_lo(w.x), bf_hi(w.x), bf_lo(w.y), bf_hi(w.y),
-                                         bf_lo(w.z), bf_hi(w.z), bf_lo(w.w), bf_hi(w.w)};
+                    const float2 wf[4] = {make_float2(bf_lo(w.x), bf_hi(w.x)),
+                                          make_float2(bf_lo(w.y), bf_hi(w.y)),
+                                          make_float2(bf_lo(w.z), bf_hi(w.z)),
+                                          make_float2(bf_lo(w.w), bf_hi(w.w))};
 #pragma unroll
-                    for (int b = 0; b < B; ++b)
+                    for (int b = 0; b < B; ++b) {
+                        const float2 h2 = make_float2(hb[b], hb[b]);
 #pragma unroll
-                        for (int e = 0; e < 8; ++e) acc[b][j][e] = fmaf(hb[b], wf[e], acc[b][j][e]);
+                        for (int k = 0; k < 4; ++k) {
+                            float2 a2 = make_float2(acc[b][j][2 * k], acc[b][j][2 * k + 1]);
+                            a2 = __ffma2_rn(wf[k], h2, a2);
+                            acc[b][j][2 * k] = a2.x;
+                            acc[b][j][2 * k + 1] = a2.y;
+                        }
+                    }
                 }
             };
             if (nrows == T::RPS) {  // full slot: straight-line, no per-row branches

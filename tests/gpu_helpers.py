@@ -94,10 +94,16 @@ def check_step(store: "O.OracleStore", m: DecodeModel, tokens, pos: int,
     K, V = store.kv()
     k_or = K[:, :, :, pos].copy()
     v_or = V[:, :, :, pos].copy()
+    # rows of layer l are comparable while no earlier layer's row flipped (a
+    # flip changes the next layer's input, the oracle's rows then legitimately
+    # drift by more than one rounding step); the hooked run below checks
+    # the arithmetic of every layer regardless
     flips = 0
-    for dev, ora in ((k_dev, k_or), (v_dev, v_or)):
-        assert kv_rows_match(dev, ora)
-        flips += int((dev != ora).sum())
+    for l in range(store.cfg.layers):
+        if flips == 0:
+            for dev, ora in ((k_dev, k_or), (v_dev, v_or)):
+                assert kv_rows_match(dev[:, l], ora[:, l]), f"layer {l}"
+        flips += int((k_dev[:, l] != k_or[:, l]).sum() + (v_dev[:, l] != v_or[:, l]).sum())
     # rewind the oracle cache and redo the step with the device's rows
     for l in range(store.cfg.layers):
         store.set_length(l, pos)

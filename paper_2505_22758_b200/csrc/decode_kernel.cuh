@@ -277,7 +277,9 @@ struct KTraits : RowMap<S, S::D> {
     // of K/V), positions per pass (+1 for the current token, rounded to 4)
     // and its scratch: alpha*q [QPG][DH], scores [QPG][ANP], probabilities
     // [ANP][QPG], stats
-    static constexpr int ATT_SC = cmax(1, 131072 / SLOT_BYTES);
+    // (batch > 1: 3 slots, so the producer fills the next pass's slots while
+    // this pass computes; batch 1 at 4k context fits one pass of 4)
+    static constexpr int ATT_SC = S::B == 1 ? cmax(1, 131072 / SLOT_BYTES) : 3;
     static constexpr int ANP = ((ATT_SC * KVC + 1) + 15) / 16 * 16;
     // alpha*q f32 [QPG][DH], scores f32 [QPG][ANP], probabilities as bf16
     // hi/lo MMA rows [16][ANP] (tensor-core P.V), stats [QPG][4]
@@ -1227,28 +1229,6 @@ struct DecodeCta {
 
     static constexpr int ilog2(int v) { return v <= 1 ? 0 : 1 + ilog2(v / 2); }
 
-    // Sums V values over each group of G consecutive lanes (G, V powers of
-    // two, V <= G <= 32): afterwards lane l of a group holds the group sum of
-    // value index (l % G) / (G / V).  V - 1 + log2(G / V) shuffles.
-    template <int V, int G>
-    __device__ static float reduce_group(float (&v)[V], int lane) {
-        static_assert(V >= 1 && V <= G && G <= 32 && (V & (V - 1)) == 0 && (G & (G - 1)) == 0,
-                      "powers of two, V <= G <= 32");
-#pragma unroll
-        for (int s = V / 2, o = G / 2; s >= 1; s >>= 1, o >>= 1) {
-            const bool upper = (lane & o) != 0;
-#pragma unroll
-            for (int i = 0; i < s; ++i) {
-                const float send = upper ? v[i] : v[i + s];
-                const float keep = upper ? v[i + s] : v[i];
-                v[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
-            }
-        }
-        float r = v[0];
-#pragma unroll
-        for (int o = G / V / 2; o >= 1; o >>= 1) r += __shfl_xor_sync(0xffffffffu, r, o);
-        return r;
-    }
 
     // Tensor-core GEMV over rows [r0, r1): per slot every warp runs tc_slot
     // on its K range, the hi/lo columns of each batch row are added (lane
@@ -1465,17 +1445,16 @@ struct DecodeCta {
     }
 
     // ---------------------------------------------------------- S_ATTN
-    // Split-K flash-decoding (numerics.hpp:64-145) on CUDA cores.  A CTA's
-    // positions [p0, p1) are consumed in passes of up to ATT_SC ring slots
-    // (plus the current token in the last pass), three barriers per pass:
-    //   A  scores: thread j dots position j's K row (16-byte chunks XOR-
-    //      swizzled by pos & 7 -> conflict-free) with alpha*q of all QPG heads
-    //      (smem broadcasts) -> sc[h][j]
+    // Split-K flash-decoding (numerics.hpp:64-145).  A CTA's positions
+    // [p0, p1) are consumed in passes of up to ATT_SC ring slots (plus the
+    // current token in the last pass), three barriers per pass:
+    //   A  scores: tensor-core K . (alpha log2e q) over 16-position tiles
     //   B  softmax: warp h takes the pass max, rescales its running (m, l)
-    //      (online softmax across passes) and writes p[j][h] = e^{s - m}
-    //   C  P.V: thread (pg, dc) accumulates o[h][8 dims of chunk dc] for all
-    //      heads over positions pg, pg + PG, ...
-    // At ctx 4096 on the 8B shape a CTA owns ~228 positions: one pass.
+    //      (online softmax across passes) and writes P (bf16 hi/lo rows)
+    //   C  P.V on tensor cores, warp w owning dims [w DH/8, (w+1) DH/8)
+    // K/V rows keep their 16-byte chunks XOR-swizzled by pos & 7, so the
+    // per-lane ldmatrix row addresses are bank-conflict free.  At ctx 4096 on
+    // the 8B shape a CTA owns ~228 positions: one pass.
     static constexpr int DC = DH / 8;   // 16-byte chunks per K/V row
     static constexpr int PG = NCT / DC;  // position groups in phase C
     static constexpr int ANP = T::ANP;
@@ -1497,109 +1476,6 @@ struct DecodeCta {
             return ring + slot * T::SLOT_BYTES + kv * (T::SLOT_BYTES / 2) + (j % T::KVC) * DH * 2;
         }
         return reinterpret_cast<const uint8_t*>(h_s()) + kv * DH * 2;
-    }
-
-    // One pass over n positions [pos0, pos0 + n), the first nring of them in
-    // ring slots it0, it0 + 1, ... (already waited for).  Scores are kept in
-    // log2 units (q is pre-scaled by alpha * log2 e), so p = 2^{s - m}: the
-    // same softmax, one MUFU.EX2 per probability.  Dot products use packed
-    // f32x2 FMAs (FFMA2) on (even, odd) dimension pairs.
-    // (A (position-group, chunk) mapping of phase A with q in registers and a
-    // shuffle fold was tried: no faster, and it showed an unexplained
-    // overlap-mode corruption at batch 4 on the toy shape; not used.)
-    __device__ void attn_pass(uint32_t it0, int nring, int n, int pos0, float2 (&o)[QPG][4]) {
-        const int ctid = threadIdx.x, warp = ctid / 32, lane = ctid % 32;
-        float* sc = att_sc();
-        float* pr = att_p();
-        const float* qs = att_q();
-        float* st = att_st();
-        for (int j = ctid; j < n; j += NCT) {  // A: scores, thread = position
-            const uint8_t* row = att_row(it0, j, nring, 0);
-            const int key = (pos0 + j) & 7;
-            float2 acc[QPG];
-#pragma unroll
-            for (int h = 0; h < QPG; ++h) acc[h] = make_float2(0.f, 0.f);
-#pragma unroll 2
-            for (int ch = 0; ch < DC; ++ch) {
-                float4 q4[QPG][2];  // all heads' q for this chunk first (LDS in flight)
-#pragma unroll
-                for (int h = 0; h < QPG; ++h) {
-                    q4[h][0] = *reinterpret_cast<const float4*>(qs + h * DH + ch * 8);
-                    q4[h][1] = *reinterpret_cast<const float4*>(qs + h * DH + ch * 8 + 4);
-                }
-                const uint4 w = lds_u128(row + ((ch ^ key) << 4));
-                const float2 k0 = make_float2(bf_lo(w.x), bf_hi(w.x));
-                const float2 k1 = make_float2(bf_lo(w.y), bf_hi(w.y));
-                const float2 k2 = make_float2(bf_lo(w.z), bf_hi(w.z));
-                const float2 k3 = make_float2(bf_lo(w.w), bf_hi(w.w));
-#pragma unroll
-                for (int h = 0; h < QPG; ++h) {
-                    acc[h] = __ffma2_rn(make_float2(q4[h][0].x, q4[h][0].y), k0, acc[h]);
-                    acc[h] = __ffma2_rn(make_float2(q4[h][0].z, q4[h][0].w), k1, acc[h]);
-                    acc[h] = __ffma2_rn(make_float2(q4[h][1].x, q4[h][1].y), k2, acc[h]);
-                    acc[h] = __ffma2_rn(make_float2(q4[h][1].z, q4[h][1].w), k3, acc[h]);
-                }
-            }
-#pragma unroll
-            for (int h = 0; h < QPG; ++h) sc[h * ANP + j] = acc[h].x + acc[h].y;
-        }
-        consumer_sync(NCT);
-        for (int h = warp; h < QPG; h += NCW) {  // B: online softmax of head h
-            float cmax = -INFINITY;
-            for (int j = lane; j < n; j += 32) cmax = fmaxf(cmax, sc[h * ANP + j]);
-            cmax = warp_max(cmax);
-            const float m_old = st[h * 4 + 0];
-            const float m_new = fmaxf(m_old, cmax);
-            const float scale = exp2f(m_old - m_new);  // 0 for the first pass
-            float psum = 0.f;
-            for (int j = lane; j < n; j += 32) {
-                const float pj = exp2f(sc[h * ANP + j] - m_new);
-                pr[j * QPG + h] = pj;
-                psum += pj;
-            }
-            psum = warp_sum(psum);
-            if (lane == 0) {
-                st[h * 4 + 0] = m_new;
-                st[h * 4 + 1] = st[h * 4 + 1] * scale + psum;
-                st[h * 4 + 2] = scale;
-            }
-        }
-        consumer_sync(NCT);
-        {  // C: P.V
-            const int dc = ctid % DC, pg = ctid / DC;
-#pragma unroll
-            for (int h = 0; h < QPG; ++h) {
-                const float2 s2 = make_float2(st[h * 4 + 2], st[h * 4 + 2]);
-#pragma unroll
-                for (int e = 0; e < 4; ++e) o[h][e] = __fmul2_rn(o[h][e], s2);
-            }
-#pragma unroll 2
-            for (int j = pg; j < n; j += PG) {
-                const uint4 w = lds_u128(att_row(it0, j, nring, 1) + ((dc ^ ((pos0 + j) & 7)) << 4));
-                const float2 v2[4] = {make_float2(bf_lo(w.x), bf_hi(w.x)),
-                                      make_float2(bf_lo(w.y), bf_hi(w.y)),
-                                      make_float2(bf_lo(w.z), bf_hi(w.z)),
-                                      make_float2(bf_lo(w.w), bf_hi(w.w))};
-                float pj[QPG];
-                if constexpr (QPG % 4 == 0) {
-#pragma unroll
-                    for (int h = 0; h < QPG; h += 4) {
-                        const float4 p4 = *reinterpret_cast<const float4*>(pr + j * QPG + h);
-                        pj[h] = p4.x; pj[h + 1] = p4.y; pj[h + 2] = p4.z; pj[h + 3] = p4.w;
-                    }
-                } else {
-#pragma unroll
-                    for (int h = 0; h < QPG; ++h) pj[h] = pr[j * QPG + h];
-                }
-#pragma unroll
-                for (int h = 0; h < QPG; ++h) {
-                    const float2 p2 = make_float2(pj[h], pj[h]);
-#pragma unroll
-                    for (int e = 0; e < 4; ++e) o[h][e] = __ffma2_rn(p2, v2[e], o[h][e]);
-                }
-            }
-        }
-        consumer_sync(NCT);  // sc / p / stats reusable by the next pass
     }
 
     // ---- tensor-core attention pass (mma.sync m16n8k16 bf16, f32 accumulate)

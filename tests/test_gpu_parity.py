@@ -296,3 +296,23 @@ def test_stacked_linear_matches_oracle_all_modes(d, layers, batch):
         assert rel_err(outs[-1][b], want[b]) < 1e-5
     np.testing.assert_array_equal(outs[0], outs[1])
     np.testing.assert_array_equal(outs[1], outs[2])
+
+
+def test_tiny_reference_stream_through_device_loop():
+    """The same T-config reference run (128-token prompt + 64 steps, golden
+    from the reference itself) fed through ffb_decode_loop in ONE
+    teacher-forced call: every step's greedy token equals the reference's
+    argmax, with no host round trip between tokens."""
+    import torch
+    g = np.load(os.path.join(GOLDEN, "tiny_decode.npz"))
+    fed, argmax = g["fed"].astype(np.int64), g["argmax"].astype(np.int64)
+    st = O.OracleStore(O.preset("tiny"), 1234, len(fed) + 1)
+    with device_from_store(st) as m:
+        s = torch.cuda.Stream()
+        with torch.cuda.stream(s):
+            d_in = torch.as_tensor(fed.reshape(-1, 1), device="cuda")
+            d_out = torch.empty_like(d_in)
+            m.decode_loop(d_in.data_ptr(), 0, len(fed), d_out.data_ptr(), True, s.cuda_stream)
+        s.synchronize()
+        np.testing.assert_array_equal(d_out.cpu().numpy()[:, 0], argmax)
+        assert m.length(0) == len(fed)

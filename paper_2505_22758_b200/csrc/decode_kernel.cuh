@@ -252,10 +252,11 @@ struct KTraits : RowMap<S, S::D> {
     static constexpr int RED_FLOATS = cmax(MD::EWPR * MD::RB, MA::EWPR * MA::RB) * S::B;
     static constexpr int KVC = SLOT_BYTES / (2 * S::DH * 2);  // KV positions per slot
     static constexpr int DPL = S::DH / 32;          // attention dims per lane
-    // max GLU pairs / Waout rows per CTA (host-checked): the d_inter share of
-    // one CTA with calibration headroom (weights up to 1.3x the mean), for
-    // grids down to 72 CTAs (TP ranks co-located on one GPU)
-    static constexpr int TMAX = cmax(160, ((S::DI * 135) / (100 * 72) + 15) / 16 * 16);
+    // max GLU pairs / Waout rows per CTA (host-checked): a CTA's share with
+    // calibration headroom (weights up to 1.3x the mean), for grids down to
+    // 148 / TP CTAs (a TP group co-located on one GPU, TP = D / AD)
+    static constexpr int GMIN = 148 / (S::D / S::AD);
+    static constexpr int TMAX = cmax(160, (cmax(S::DI, S::D) * 135 / (100 * GMIN) + 15) / 16 * 16);
     static_assert(MD::SLOT <= SLOT_BYTES && MA::SLOT <= SLOT_BYTES, "slot fits both row maps");
     static_assert(S::DH % 32 == 0 && DPL <= 8, "attention lane split");
     static_assert(KVC >= 1 && (SLOT_BYTES / 2) % 16 == 0, "kv chunk");

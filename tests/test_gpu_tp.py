@@ -77,3 +77,24 @@ def test_8b_width_tp2_single_step():
     print(f"8B width TP2: rel_err {e:.2e}")
     assert e < 1e-4
     assert int(greedy[0]) == int(np.argmax(want))
+
+
+@pytest.mark.parametrize("tp", [1, 2, 4, 8])
+def test_70b_width_shards_match_oracle(tp):
+    """Llama-3-70B width (d_model 8192, 64 q / 8 kv heads, d_inter 28672):
+    the TP 1/2/4/8 shard kernels (kernels_70b.cu) of one layer, reduced
+    vocabulary, 256-position context, co-located on one GPU (148 / TP SMs
+    per rank), against the f64 oracle of the whole layer."""
+    cfg = O.preset("llama31_70b").replace(layers=1, vocab_size=4096)
+    st = O.OracleStore(cfg, 1234, 258)
+    st.synthetic_prefill(256, 7)
+    want = None
+    with _group(st, tp) as g:
+        logits, greedy = g.step([17], 256)
+    for l in range(cfg.layers):
+        st.set_length(l, 256)
+    want = st.forward([17], 256)[0]
+    e = rel_err(logits[0], want)
+    print(f"70B width TP{tp}: rel_err {e:.2e}")
+    assert e < 1e-4
+    assert int(greedy[0]) == int(np.argmax(want))

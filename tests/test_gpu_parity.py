@@ -316,3 +316,27 @@ def test_tiny_reference_stream_through_device_loop():
         s.synchronize()
         np.testing.assert_array_equal(d_out.cpu().numpy()[:, 0], argmax)
         assert m.length(0) == len(fed)
+
+
+@pytest.mark.parametrize("batch,prefill", [(1, 1500), (4, 700)])
+def test_multi_pass_attention_matches_oracle(batch, prefill):
+    """Long contexts: a CTA's positions span several attention passes (the
+    online softmax rescale across passes, batch > 1 double-buffered passes)."""
+    cfg = TOY.replace(batch=batch)
+    st = O.OracleStore(cfg, 3, prefill + 2)
+    st.synthetic_prefill(prefill, 11)
+    toks = [11, 400, 7, 99][:batch]
+    with device_from_store(st) as m:
+        e_plain, e_strict, flips = check_step(st, m, toks, prefill)
+    print(f"b{batch} prefill {prefill}: rel_err {e_plain:.2e}, same-KV {e_strict:.2e}, flips {flips}")
+
+
+def test_8b_width_long_context_multi_pass():
+    """8B width, one layer, 9000-position context: ~500 positions per CTA, two
+    attention passes per CTA."""
+    cfg = O.preset("llama31_8b").replace(layers=1, vocab_size=4096)
+    st = O.OracleStore(cfg, 1234, 9002)
+    st.synthetic_prefill(9000, 7)
+    with device_from_store(st) as m:
+        e_plain, e_strict, flips = check_step(st, m, [17], 9000)
+    print(f"8B ctx 9000: rel_err {e_plain:.2e}, same-KV {e_strict:.2e}, flips {flips}")

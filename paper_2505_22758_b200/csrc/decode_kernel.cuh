@@ -975,12 +975,14 @@ struct DecodeCta {
         const uint8_t* rB = base + (g + 8) * M::ROW_BYTES;
 #pragma unroll
         for (int e = 0; e < 4; ++e) out[e] = 0.f;
-#pragma unroll 1
+        // two groups per iteration and two accumulators per group (even /
+        // odd k-steps): four independent MMA chains instead of one
+#pragma unroll 2
         for (int gi = 0; gi < M::KW / kQuantGroup; ++gi) {
             const int G = warp * (M::KW / kQuantGroup) + gi;  // group index in the row
             const float sA = *reinterpret_cast<const float*>(rA + M::CODE_BYTES + 4 * G);
             const uint32_t zA = rA[M::CODE_BYTES + 4 * M::NG + G];
-            float acc[4] = {0.f, 0.f, 0.f, 0.f};
+            float acc[4] = {0.f, 0.f, 0.f, 0.f}, acc2[4] = {0.f, 0.f, 0.f, 0.f};
             if constexpr (M::QB == 4) {
                 const float sB = *reinterpret_cast<const float*>(rB + M::CODE_BYTES + 4 * G);
                 const uint32_t zB = rB[M::CODE_BYTES + 4 * M::NG + G];
@@ -1001,13 +1003,13 @@ struct DecodeCta {
                         const uint32_t a1 = hsub2_u(f16_nib<0x000F000Fu>(xb), zB1);
                         const uint32_t a3 = hsub2_u(f16_nib<0x00F000F0u>(xb), zB16);
                         const uint2 bf = frag(gi * 8 + 2 * t + u);
-                        mma_f16(acc, a0, a1, a2, a3, bf.x, bf.y);
+                        mma_f16(u ? acc2 : acc, a0, a1, a2, a3, bf.x, bf.y);
                     }
                 }
-                out[0] = fmaf(sA, acc[0], out[0]);
-                out[1] = fmaf(sA, acc[1], out[1]);
-                out[2] = fmaf(sB, acc[2], out[2]);
-                out[3] = fmaf(sB, acc[3], out[3]);
+                out[0] = fmaf(sA, acc[0] + acc2[0], out[0]);
+                out[1] = fmaf(sA, acc[1] + acc2[1], out[1]);
+                out[2] = fmaf(sB, acc[2] + acc2[2], out[2]);
+                out[3] = fmaf(sB, acc[3] + acc2[3], out[3]);
             } else {  // int8: 8 real rows (g), rows g + 8 zero
                 const uint32_t z1 = (0x6400u | zA) * 0x10001u;
                 const uint4 w0 = lds_u128(rA + G * 128 + q * 32);
@@ -1018,10 +1020,10 @@ struct DecodeCta {
                     const uint32_t a0 = hsub2_u(__byte_perm(wA[st], 0x64646464u, 0x4140), z1);
                     const uint32_t a2 = hsub2_u(__byte_perm(wA[st], 0x64646464u, 0x4342), z1);
                     const uint2 bf = frag(gi * 8 + st);
-                    mma_f16(acc, a0, 0u, a2, 0u, bf.x, bf.y);
+                    mma_f16((st & 1) ? acc2 : acc, a0, 0u, a2, 0u, bf.x, bf.y);
                 }
-                out[0] = fmaf(sA, acc[0], out[0]);
-                out[1] = fmaf(sA, acc[1], out[1]);
+                out[0] = fmaf(sA, acc[0] + acc2[0], out[0]);
+                out[1] = fmaf(sA, acc[1] + acc2[1], out[1]);
             }
         }
     }

@@ -103,3 +103,14 @@ if os.environ.get("PHASES"):
 
 if os.environ.get("COMBINE"):
     print(f"combine: partial->atomic-done {seg(7, 5):.2f}  ->ml-loaded {seg(5, 6):.2f}  ->done {seg(6, 2):.2f} us")
+
+if os.environ.get("GLUSPLIT"):
+    g = [s for s in range(S - 1) if s % 5 == 3]
+    def seg2(a, b):
+        v = []
+        for s in g:
+            x = tr[:, s, a].astype(np.int64); y = tr[:, s, b].astype(np.int64)
+            ok = (x > 0) & (y > x)
+            if ok.any(): v.append(np.median((y - x)[ok]) / 1e3)
+        return np.mean(v) if v else float("nan")
+    print(f"glu: dep->ffn1 done {seg2(1, 3):.2f}  ffn1->done {seg2(3, 2):.2f} us")

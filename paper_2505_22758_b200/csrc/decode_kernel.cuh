@@ -33,9 +33,12 @@
 //            the matching Wffn2^T rows into a per-CTA d_model accumulator
 //             -> written as a partial
 //   S_RED    x[cols] += sum over CTAs of the GLU partials (fixed order)
+// (bf16 at batch <= 2, KTraits::F2R: S_GLU stops at h, written to global
+// memory, and S_RED is the second GEMV x[rows] += W2[rows] . h.)
 // and a tail S_LMHEAD: RMSNorm -> lm_head rows -> logits + fused argmax.
 #pragma once
 #include <cstdint>
+#include <type_traits>
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
 
@@ -227,7 +230,7 @@ struct RowMap {
     static_assert(TPR % 32 == 0 && TPR <= kNCT && kNCT % TPR == 0, "a row must span whole warps");
     static_assert(K % CPT == 0 && CPT % 8 == 0, "row mapping");
     static_assert(QB == 0 || kQuantGroup % CPT == 0, "a thread's columns lie in one group");
-    static_assert(RPS >= 2 && RPS % 2 == 0 && RPS % RG == 0, "slot rows");
+    static_assert(RPS >= 1 && (RPS == 1 || RPS % 2 == 0) && RPS % RG == 0, "slot rows");
     static_assert(RPS * S::B <= kNCT && RB * S::B <= kNCT, "epilogue threads");
     static_assert(TC || (RPT * S::B <= 32 && (RPT & (RPT - 1)) == 0),
                   "one transposed warp reduction per slot");
@@ -238,6 +241,17 @@ template <class S>
 struct KTraits : RowMap<S, S::D> {
     using MD = RowMap<S, S::D>;   // rows of d_model columns
     using MA = RowMap<S, S::AD>;  // Waout shard rows (attention width)
+    // Two-phase FFN (bf16, batch <= 2, d_model >= 4096, d_inter a multiple
+    // of 8 x 256 whose bf16 row fits a slot): S_GLU writes h = silu(g) * a
+    // to global memory and S_RED streams W2 rows ([D][DI], row-owned like
+    // Waout) against it -- no per-CTA d_model partials and no reduction
+    // pass, one more full-grid barrier inside the FFN.  Otherwise Wffn2^T
+    // rows are AXPYed into per-CTA partials that S_RED sums.  Same-box A/B:
+    // 8B b1 2.725 -> 2.700 ms, b2 3.204 -> 3.176; 1B b1 0.638 -> 0.650
+    // (the reduction of 2048-wide partials is cheaper than the barrier).
+    static constexpr bool F2R = S::QB == 0 && S::B <= 2 && S::D >= 4096 &&
+                                S::DI % (8 * kNCT) == 0 && S::DI * 2 <= 32768;
+    using MF = std::conditional_t<F2R, RowMap<S, S::DI>, MD>;
     static constexpr int NCW = kNCW;
     static constexpr int NCT = kNCT;
     // + a producer warpgroup (one active lane): with 12 warps the warpgroups
@@ -249,7 +263,8 @@ struct KTraits : RowMap<S, S::D> {
     static constexpr int cmin(int a, int b) { return a < b ? a : b; }
     static constexpr int cmax(int a, int b) { return a > b ? a : b; }
     static constexpr int SLOT_BYTES = S::QB == 0 ? 32768 : cmax(MD::SLOT, MA::SLOT);
-    static constexpr int RED_FLOATS = cmax(MD::EWPR * MD::RB, MA::EWPR * MA::RB) * S::B;
+    static constexpr int RED_FLOATS =
+        cmax(cmax(MD::EWPR * MD::RB, MA::EWPR * MA::RB), MF::EWPR * MF::RB) * S::B;
     static constexpr int KVC = SLOT_BYTES / (2 * S::DH * 2);  // KV positions per slot
     static constexpr int DPL = S::DH / 32;          // attention dims per lane
     // max GLU pairs / Waout rows per CTA (host-checked): a CTA's share with
@@ -257,7 +272,8 @@ struct KTraits : RowMap<S, S::D> {
     // 148 / TP CTAs (a TP group co-located on one GPU, TP = D / AD)
     static constexpr int GMIN = 148 / (S::D / S::AD);
     static constexpr int TMAX = cmax(160, (cmax(S::DI, S::D) * 135 / (100 * GMIN) + 15) / 16 * 16);
-    static_assert(MD::SLOT <= SLOT_BYTES && MA::SLOT <= SLOT_BYTES, "slot fits both row maps");
+    static_assert(MD::SLOT <= SLOT_BYTES && MA::SLOT <= SLOT_BYTES && MF::SLOT <= SLOT_BYTES,
+                  "slot fits every row map");
     static_assert(S::DH % 32 == 0 && DPL <= 8, "attention lane split");
     static_assert(KVC >= 1 && (SLOT_BYTES / 2) % 16 == 0, "kv chunk");
 
@@ -478,10 +494,16 @@ struct DecodeCta {
             case S_GLU:
                 if (sub == 0) L = {p.wffn1 + (size_t)l * 2 * S::DI * T::ROW_BYTES, 2 * pl.glu_t0,
                                    2 * pl.glu_t1, false, false};
-                else if (sub == 1) L = {p.wffn2t + (size_t)l * S::DI * T::ROW_BYTES, pl.glu_t0,
-                                        pl.glu_t1, false, false};
+                else if (sub == 1 && !T::F2R)
+                    L = {p.wffn2t + (size_t)l * S::DI * T::ROW_BYTES, pl.glu_t0, pl.glu_t1, false,
+                         false};
                 else if (sub == 2 && p.pool_chunks > 0) L = {nullptr, 0, 1, false, true};
                 else return false;
+                return true;
+            case S_RED:  // two-phase FFN: W2 rows, the CTA's d_model rows (as Waout)
+                if (!T::F2R || sub > 0) return false;
+                L = {p.wffn2t + (size_t)l * D * MF::ROW_BYTES, pl.aout_r0, pl.aout_r1, false,
+                     false, MF::ROW_BYTES, MF::RPS};
                 return true;
             default:
                 return false;
@@ -798,6 +820,7 @@ struct DecodeCta {
     // 16 at which the nibble decode (q4_decode) leaves code e.
     using MD = typename T::MD;
     using MA = typename T::MA;
+    using MF = typename T::MF;
 
     template <class M = MD>
     struct Act {
@@ -1923,7 +1946,10 @@ struct DecodeCta {
                 const int pr = ctid / B, b = ctid % B;
                 const float a = row_total(red, 2 * pr, b), g = row_total(red, 2 * pr + 1, b);
                 const float silu = g / (1.0f + expf(-g));
-                hs[b * T::TMAX + (c0 / 2 - t0) + pr] = silu * a;
+                if constexpr (T::F2R)
+                    __stcg(p.glu_part + (size_t)b * S::DI + c0 / 2 + pr, silu * a);
+                else
+                    hs[b * T::TMAX + (c0 / 2 - t0) + pr] = silu * a;
             }
         });
         consumer_sync(NCT);  // h complete
@@ -2046,6 +2072,10 @@ struct DecodeCta {
         Act<> act;
         load_act(act, p.x, false, p.norm_ffn + (size_t)l * D, l * kStagesPerLayer + S_GLU);
         glu_ffn1(it, act, pl.glu_t0, pl.glu_t1);
+        if constexpr (T::F2R) {  // h is in glu_part; S_RED applies W2
+            arrive(p.counters + l * kStagesPerLayer + S_GLU, l * kStagesPerLayer + S_GLU);
+            return;
+        }
         glu_ffn2(it, pl.glu_t0, pl.glu_t1, p.glu_part + (size_t)cta * T::RG * B * D);
         if (T::QB == 0 && p.pool_chunks > 0) {  // (pool: bf16 only, host-enforced)
             for (;;) {
@@ -2067,6 +2097,41 @@ struct DecodeCta {
     }
 
     // ---------------------------------------------------------- S_RED
+    // Two-phase FFN: x[rows] += W2[rows] . h (h = [B][DI] in glu_part, written
+    // by every CTA's S_GLU); rows are this CTA's Waout rows.  TP: W2 is split
+    // by input columns (this rank's d_inter slice), partials summed across
+    // ranks in exchange slot 1.
+    __device__ void stage_ffn2(uint32_t& it, int l) {
+        Act<MF> act;
+        load_act<MF>(act, p.glu_part, false, nullptr, l * kStagesPerLayer + S_RED);
+        const int ctid = threadIdx.x;
+        const int r0 = pl.aout_r0, nr = pl.aout_r1 - pl.aout_r0;
+        float* acc = h_s();  // [B][TMAX]
+        gemv<MF>(it, act, r0, pl.aout_r1, [&](int c0, int nrows, const float* red) {
+            if (ctid < nrows * B) {
+                const int r = ctid / B, b = ctid % B;
+                acc[b * T::TMAX + c0 - r0 + r] = row_total<MF>(red, r, b);
+            }
+        });
+        consumer_sync(NCT);
+        if (p.tp_size > 1) {
+            float* d = wpart();
+            for (int i = ctid; i < nr * B; i += NCT) {
+                const int b = i / nr, r = i % nr;
+                d[b * nr + r] = acc[b * T::TMAX + r];
+            }
+            consumer_sync(NCT);
+            tp_exchange_add(d, r0, nr, 1, l);
+        } else {
+            for (int i = ctid; i < nr * B; i += NCT) {
+                const int r = i / B, b = i % B;
+                float* xp = p.x + (size_t)b * D + r0 + r;
+                __stcg(xp, ldcg_f(xp) + acc[b * T::TMAX + r]);
+            }
+        }
+        arrive(p.counters + l * kStagesPerLayer + S_RED, l * kStagesPerLayer + S_RED);
+    }
+
     __device__ void stage_red(int l) {
         wait_stage(l * kStagesPerLayer + S_RED);
         const int ctid = threadIdx.x, warp = ctid / 32, lane = ctid % 32;
@@ -2263,7 +2328,10 @@ struct DecodeCta {
                 case S_ATTN: stage_attn(it, l); break;
                 case S_AOUT: stage_aout(it, l); break;
                 case S_GLU: stage_glu(it, l); break;
-                default: stage_red(l); break;
+                default:
+                    if constexpr (T::F2R) stage_ffn2(it, l);
+                    else stage_red(l);
+                    break;
             }
         }
     }

@@ -16,6 +16,7 @@ struct KernelOps {
     int D, DI, DH, NQ, NKV, B, QB;
     int threads, smem, nslots, slot_bytes, rg, tmax, kvc, rps, row_bytes, row_bytes_a;
     int tc_d, tc_a;  // d_model-column / Waout rows use the tensor-core code order
+    int ffn2_rows;   // W2 stored [D][DI] (two-phase FFN, KTraits::F2R), else Wffn2^T
     cudaError_t (*prepare)();
     cudaError_t (*launch)(const DecodeParams&, int grid, cudaStream_t, bool cooperative);
 };
@@ -49,7 +50,7 @@ KernelOps make_ops() {
     return KernelOps{S::D,        S::DI,         S::DH,     S::NQ,         S::NKV, S::B,
                      S::QB,       T::NTHREADS,   T::SMEM_BYTES, T::NSLOTS, T::SLOT_BYTES,
                      T::RG,       T::TMAX,       T::KVC,    T::RPS,        T::ROW_BYTES,
-                     T::MA::ROW_BYTES, T::MD::TC ? 1 : 0, T::MA::TC ? 1 : 0,
+                     T::MA::ROW_BYTES, T::MD::TC ? 1 : 0, T::MA::TC ? 1 : 0, T::F2R ? 1 : 0,
                      &prepare_impl<S>, &launch_impl<S>};
 }
 

@@ -334,7 +334,8 @@ ffb_status build_plan(ffb_model* m) {
     m->pool_ct = 0;
     m->pool_chunks = 0;
     m->pool_t0 = c.d_inter;
-    if (m->pool_permille > 0 && c.batch <= 2 && c.d_inter / G >= 32 && m->ops->QB == 0) {
+    if (m->pool_permille > 0 && c.batch <= 2 && c.d_inter / G >= 32 && m->ops->QB == 0 &&
+        !m->ops->ffn2_rows) {
         const int64_t ct = std::max<int64_t>(m->pool_ct_pref, m->ops->rps);
         const int64_t chunks = (c.d_inter * m->pool_permille) / (1000 * ct);
         if (chunks > 0 && chunks <= m->pool_chunks_max) {
@@ -573,6 +574,7 @@ struct TensorDst {
     std::vector<std::pair<int64_t, int64_t>> rows;  // [r0, r1) ranges
     size_t row_bytes = 0;
     int layout = 0;  // quant code order: 1 = tensor-core (decode_kernel.cuh: tc_slot)
+    bool transpose = false;  // store the shard block transposed (W2 as [D][DI], KTraits::F2R)
     int64_t local_rows() const {
         int64_t n = 0;
         for (auto& r : rows) n += r.second - r.first;
@@ -654,9 +656,11 @@ bool resolve(ffb_model* m, const std::string& name, TensorDst* d) {
     else if (t == "wffn1")  // interleaved (in, gate) row pairs of this d_inter slice
         mat(m->wffn1 + l * 2 * c.d_inter * RB, 2 * g.d_inter,
             {{2 * r * c.d_inter, 2 * (r + 1) * c.d_inter}}, 0, D, RB);
-    else if (t == "wffn2t")
+    else if (t == "wffn2t") {
         mat(m->wffn2t + l * c.d_inter * RB, g.d_inter, {{r * c.d_inter, (r + 1) * c.d_inter}}, 0,
             D, RB);
+        d->transpose = m->ops->ffn2_rows != 0;
+    }
     else if (t == "norm_attn") vec(m->norm_attn + l * D, D, 1);
     else if (t == "norm_ffn") vec(m->norm_ffn + l * D, D, 1);
     else return false;
@@ -967,7 +971,8 @@ ffb_status ffb_create_ex(const ffb_model_config* gcfg, int64_t max_seq_len, int 
     ALLOC(m->x, (size_t)B * D);
     ALLOC(m->q, (size_t)B * D);
     ALLOC(m->attn_out, (size_t)B * D);
-    ALLOC(m->glu_part, (size_t)m->grid * ops->rg * B * D);
+    // per-CTA partials, or h = [B][DI] for the two-phase FFN
+    ALLOC(m->glu_part, std::max<size_t>((size_t)m->grid * ops->rg * B * D, (size_t)B * c.d_inter));
     const int64_t units = B * c.n_kv_heads;
     const int64_t qpg = c.n_q_heads / c.n_kv_heads;
     ALLOC(m->attn_part, (size_t)units * m->grid * qpg * (c.d_head + 2));
@@ -1048,6 +1053,17 @@ ffb_status ffb_upload_tensor(ffb_model* m, const char* name, const float* values
             for (int64_t r = rr.first; r < rr.second; ++r, ++o)
                 std::memcpy(shard.data() + o * cols, values + r * d.gcols + d.col0,
                             sizeof(float) * cols);
+        src = shard.data();
+    }
+    if (d.transpose) {  // [lrows][cols] -> [cols][lrows]
+        std::vector<float> tr((size_t)lrows * cols);
+        constexpr int64_t TB = 64;  // cache-blocked
+        for (int64_t r0 = 0; r0 < lrows; r0 += TB)
+            for (int64_t k0 = 0; k0 < cols; k0 += TB)
+                for (int64_t r = r0; r < std::min(lrows, r0 + TB); ++r)
+                    for (int64_t k = k0; k < std::min(cols, k0 + TB); ++k)
+                        tr[(size_t)k * lrows + r] = src[(size_t)r * cols + k];
+        shard.swap(tr);
         src = shard.data();
     }
     if (d.kind == 0 && m->ops->QB != 0) {  // quant packer, a block of rows at a time

@@ -166,16 +166,18 @@ def test_tiny_greedy_decode_matches_reference():
         print("tiny decode worst rel err at kept steps:", worst)
 
 
-@pytest.mark.parametrize("name,ctx", [("llama32_1b", 1024), ("llama31_8b", 4096)])
-def test_full_width_single_step_matches_oracle(name, ctx):
+@pytest.mark.parametrize("name,ctx,batch", [("llama32_1b", 1024, 1), ("llama31_8b", 4096, 1),
+                                            ("llama31_8b", 1024, 2), ("llama31_8b", 512, 4)])
+def test_full_width_single_step_matches_oracle(name, ctx, batch):
     """S/E width (real d_model, heads, d_inter) with reduced depth/vocab so the
-    f64 oracle stays cheap; full context length."""
-    cfg = O.preset(name).replace(layers=1, vocab_size=4096)
+    f64 oracle stays cheap; full context length.  Batch 1/2 run the two-phase
+    FFN (W2 rows, KTraits::F2R), batch 4 the Wffn2^T AXPY + reduction."""
+    cfg = O.preset(name).replace(layers=1, vocab_size=4096, batch=batch)
     st = O.OracleStore(cfg, 1234, ctx + 2)
     st.synthetic_prefill(ctx, 7)
     with device_from_store(st) as m:
-        e_plain, e_strict, flips = check_step(st, m, [17], ctx)
-    print(f"{name} ctx {ctx}: rel_err {e_plain:.2e}, same-KV {e_strict:.2e}, flips {flips}")
+        e_plain, e_strict, flips = check_step(st, m, [17, 3, 99, 4000][:batch], ctx)
+    print(f"{name} b{batch} ctx {ctx}: rel_err {e_plain:.2e}, same-KV {e_strict:.2e}, flips {flips}")
 
 
 @pytest.mark.parametrize("name", ["llama31_8b"])

@@ -294,9 +294,12 @@ struct KTraits : RowMap<S, S::D> {
     // of K/V), positions per pass (+1 for the current token, rounded to 4)
     // and its scratch: alpha*q [QPG][DH], scores [QPG][ANP], probabilities
     // [ANP][QPG], stats
-    // (batch > 1: 3 slots, so the producer fills the next pass's slots while
-    // this pass computes; batch 1 at 4k context fits one pass of 4)
-    static constexpr int ATT_SC = S::B == 1 ? cmax(1, 131072 / SLOT_BYTES) : 3;
+    // (batch 1 at 4k context fits one pass of 4 slots; batch > 1 runs
+    // several passes, the producer filling the next pass's slots while this
+    // one computes: 4-slot passes at batch 2 (2 passes at 4k), 3 at batch 4
+    // -- same-box A/B at 8B, 4k context: b2 3.17 / 3.14 ms for 3 / 4 slots,
+    // b4 3.99 / 4.08 / 4.08 / 4.50 ms for 3 / 2 / 4 / 1 slots)
+    static constexpr int ATT_SC = S::B == 1 ? cmax(1, 131072 / SLOT_BYTES) : S::B == 2 ? 4 : 3;
     static constexpr int ANP = ((ATT_SC * KVC + 1) + 15) / 16 * 16;
     // alpha*q f32 [QPG][DH], scores f32 [QPG][ANP], probabilities as bf16
     // hi/lo MMA rows [16][ANP] (tensor-core P.V), stats [QPG][4]
@@ -1626,19 +1629,49 @@ struct DecodeCta {
         }
         consumer_sync(NCT);
         for (int h = warp; h < QPG; h += NCW) {  // B: online softmax of head h -> P hi/lo rows
+            // 8 consecutive positions per lane (16-byte smem accesses), held
+            // in registers between the max and the exp pass
+            constexpr int PIT = (ANP + 255) / 256;
+            float v[PIT][8];
             float cmax = -INFINITY;
-            for (int j = lane; j < n; j += 32) cmax = fmaxf(cmax, sc[h * ANP + j]);
+#pragma unroll
+            for (int i = 0; i < PIT; ++i) {
+                const int j0 = i * 256 + lane * 8;
+#pragma unroll
+                for (int e = 0; e < 8; ++e) v[i][e] = -INFINITY;
+                if (j0 < n) {
+                    const float4 x0 = *reinterpret_cast<const float4*>(sc + h * ANP + j0);
+                    const float4 x1 = *reinterpret_cast<const float4*>(sc + h * ANP + j0 + 4);
+                    const float xs[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
+#pragma unroll
+                    for (int e = 0; e < 8; ++e) v[i][e] = j0 + e < n ? xs[e] : -INFINITY;
+                }
+#pragma unroll
+                for (int e = 0; e < 8; ++e) cmax = fmaxf(cmax, v[i][e]);
+            }
             cmax = warp_max(cmax);
             const float m_old = st[h * 4 + 0];
             const float m_new = fmaxf(m_old, cmax);
             const float scale = exp2f(m_old - m_new);  // 0 for the first pass
             float psum = 0.f;
-            for (int j = lane; j < ntiles * 16; j += 32) {
-                const float pj = j < n ? exp2f(sc[h * ANP + j] - m_new) : 0.f;
-                const __nv_bfloat16 hi = __float2bfloat16_rn(pj);
-                pt[h * ANP + j] = hi;
-                pt[(QPG + h) * ANP + j] = __float2bfloat16_rn(pj - __bfloat162float(hi));
-                psum += pj;
+#pragma unroll
+            for (int i = 0; i < PIT; ++i) {
+                const int j0 = i * 256 + lane * 8;
+                if (j0 < ntiles * 16) {
+                    uint32_t hw[4], lw[4];
+#pragma unroll
+                    for (int e = 0; e < 8; e += 2) {
+                        const float p0 = j0 + e < n ? exp2f(v[i][e] - m_new) : 0.f;
+                        const float p1 = j0 + e + 1 < n ? exp2f(v[i][e + 1] - m_new) : 0.f;
+                        const __nv_bfloat16 h0 = __float2bfloat16_rn(p0), h1 = __float2bfloat16_rn(p1);
+                        hw[e / 2] = bf2_pack(__bfloat162float(h0), __bfloat162float(h1));
+                        lw[e / 2] = bf2_pack(p0 - __bfloat162float(h0), p1 - __bfloat162float(h1));
+                        psum += p0 + p1;
+                    }
+                    *reinterpret_cast<uint4*>(pt + h * ANP + j0) = make_uint4(hw[0], hw[1], hw[2], hw[3]);
+                    *reinterpret_cast<uint4*>(pt + (QPG + h) * ANP + j0) =
+                        make_uint4(lw[0], lw[1], lw[2], lw[3]);
+                }
             }
             psum = warp_sum(psum);
             if (lane == 0) {
@@ -1660,26 +1693,55 @@ struct DecodeCta {
                 o[nt][3] *= s1;
             }
             const int c0 = warp * (DPW / 8);  // first 16-byte dim chunk of this warp
-            for (int t = 0; t < ntiles; ++t) {
-                const uint32_t a0 = r0 < 2 * QPG ? *reinterpret_cast<const uint32_t*>(pt + r0 * ANP + t * 16 + 2 * q4) : 0u;
-                const uint32_t a2 = r0 < 2 * QPG ? *reinterpret_cast<const uint32_t*>(pt + r0 * ANP + t * 16 + 2 * q4 + 8) : 0u;
-                const uint32_t a1 = r1 < 2 * QPG ? *reinterpret_cast<const uint32_t*>(pt + r1 * ANP + t * 16 + 2 * q4) : 0u;
-                const uint32_t a3 = r1 < 2 * QPG ? *reinterpret_cast<const uint32_t*>(pt + r1 * ANP + t * 16 + 2 * q4 + 8) : 0u;
+            // software-pipelined: tile t + 1's fragments are loaded before
+            // tile t's MMAs; even / odd tiles accumulate into two sets (two
+            // independent MMA chains)
+            float o2[NTW][4];
+#pragma unroll
+            for (int nt = 0; nt < NTW; ++nt)
+#pragma unroll
+                for (int e = 0; e < 4; ++e) o2[nt][e] = 0.f;
+            struct Frag {
+                uint32_t a[4], b[2 * NTW];
+            };
+            const uint8_t* cur_v = reinterpret_cast<const uint8_t*>(h_s()) + DH * 2;
+            auto load = [&](int t, Frag& f) {
+                const __nv_bfloat16* p0 = pt + r0 * ANP + t * 16 + 2 * q4;
+                const __nv_bfloat16* p1 = pt + r1 * ANP + t * 16 + 2 * q4;
+                f.a[0] = r0 < 2 * QPG ? *reinterpret_cast<const uint32_t*>(p0) : 0u;
+                f.a[2] = r0 < 2 * QPG ? *reinterpret_cast<const uint32_t*>(p0 + 8) : 0u;
+                f.a[1] = r1 < 2 * QPG ? *reinterpret_cast<const uint32_t*>(p1) : 0u;
+                f.a[3] = r1 < 2 * QPG ? *reinterpret_cast<const uint32_t*>(p1 + 8) : 0u;
                 // ldmatrix.trans rows: position t*16 + (lane & 7) + 8*((lane>>3)&1), chunk c0 + (lane>>4)
                 const int jr = min(t * 16 + (lane & 7) + 8 * ((lane >> 3) & 1), n - 1);
-                const uint8_t* row = att_row(it0, jr, nring, 1);
+                const uint32_t slot = (it0 + jr / T::KVC) % T::NSLOTS;
+                const uint8_t* rr = ring + slot * T::SLOT_BYTES + T::SLOT_BYTES / 2 + (jr % T::KVC) * DH * 2;
+                const uint8_t* row = jr < nring ? rr : cur_v;  // (att_row, branch-free)
                 const int key = (pos0 + jr) & 7;
-                if constexpr (NTW == 2) {
-                    uint32_t b00, b01, b10, b11;
-                    ldsm_x4_t(row + (((c0 + (lane >> 4)) ^ key) << 4), b00, b01, b10, b11);
-                    mma_bf16(o[0], a0, a1, a2, a3, b00, b01);
-                    mma_bf16(o[NTW - 1], a0, a1, a2, a3, b10, b11);
-                } else {
-                    uint32_t b00, b01;
-                    ldsm_x2_t(row + ((c0 ^ key) << 4), b00, b01);
-                    mma_bf16(o[0], a0, a1, a2, a3, b00, b01);
-                }
+                if constexpr (NTW == 2)
+                    ldsm_x4_t(row + (((c0 + (lane >> 4)) ^ key) << 4), f.b[0], f.b[1], f.b[2], f.b[3]);
+                else
+                    ldsm_x2_t(row + ((c0 ^ key) << 4), f.b[0], f.b[1]);
+            };
+            auto mma_f = [&](const Frag& f, float (&acc)[NTW][4]) {
+#pragma unroll
+                for (int nt = 0; nt < NTW; ++nt)
+                    mma_bf16(acc[nt], f.a[0], f.a[1], f.a[2], f.a[3], f.b[2 * nt], f.b[2 * nt + 1]);
+            };
+            Frag f0, f1;
+            load(0, f0);
+            int t = 0;
+            for (; t + 2 <= ntiles; t += 2) {
+                load(t + 1, f1);
+                mma_f(f0, o);
+                if (t + 2 < ntiles) load(t + 2, f0);
+                mma_f(f1, o2);
             }
+            if (t < ntiles) mma_f(f0, o);
+#pragma unroll
+            for (int nt = 0; nt < NTW; ++nt)
+#pragma unroll
+                for (int e = 0; e < 4; ++e) o[nt][e] += o2[nt][e];
         }
         consumer_sync(NCT);  // sc / pt / stats reusable by the next pass
     }

@@ -143,6 +143,17 @@ struct DecodeParams {
     float* xbuf;            // [2][B][D] ping-pong activations
     float eps;
     double rope_theta;
+    // batch >= 8 (Shape::KCP): every GEMV input as MMA A-fragment tables,
+    // [K/16 k-steps][32 lanes][4 x f16x2 hi | 4 x f16x2 lo] (1 KiB per
+    // k-step; frag_off), written by the producing stage's epilogue and
+    // streamed into the ring by TMA one K chunk at a time.  The RMSNorm
+    // scale is factored out: tables hold x * gain, the GEMV result is
+    // multiplied by 1 / rms from the per-CTA sums of squares.
+    uint8_t* xfrag_a;  // x * norm_ffn[l]: S_GLU input (written by S_AOUT)
+    uint8_t* xfrag_f;  // x * norm_attn[l] / final_norm: S_QKV / LM-head input
+    uint8_t* afrag;    // attn_out: S_AOUT input (attention combine)
+    uint8_t* hfrag;    // h = silu(g) * a: S_RED input (S_GLU)
+    float* ssq;        // [2][grid][B] sum of squares of each CTA's x rows (0 after S_AOUT, 1 after S_RED)
 };
 
 // Weight storage formats of the streamed matrices (Wqkv, Waout, Wffn1,
@@ -160,12 +171,20 @@ constexpr int kQuantGroup = 128;
 // width D and the norms/embedding are replicated; NQ / NKV are this shard's
 // query / kv heads (attention width AD = NQ * DH, = D when TP = 1) and DI its
 // slice of d_inter.
+constexpr int gcd_(int a, int b) { return b == 0 ? a : gcd_(b, a % b); }
+constexpr int pow2_div_(int v, int cap) { return (v % 2 == 0 && cap > 1) ? 2 * pow2_div_(v / 2, cap / 2) : 1; }
+
 template <int D_, int DI_, int DH_, int NQ_, int NKV_, int B_, int QB_ = 0>
 struct Shape {
     static constexpr int D = D_, DI = DI_, DH = DH_, NQ = NQ_, NKV = NKV_, B = B_, QB = QB_;
     static constexpr int AD = NQ * DH;
     static constexpr int QPG = NQ / NKV;
     static constexpr int QKVR = (NQ + 2 * NKV) * DH;
+    // batch >= 8: every projection is a dense contraction on tensor cores,
+    // streamed in K chunks of KC columns (RowMap::KCP, DecodeCta::gemv_kc)
+    static constexpr bool KCP = B >= 8;
+    static constexpr int KC = pow2_div_(gcd_(D, gcd_(AD, DI)), 512);
+    static_assert(!KCP || (QB == 0 && B <= 16 && KC >= 128), "batch >= 8: bf16, K chunks >= 128");
     static_assert(AD <= D && D % AD == 0, "attention width divides d_model");
     static_assert(NQ % NKV == 0, "GQA grouping");
     static_assert(QB == 0 || QB == 4 || QB == 8, "weight format");
@@ -222,19 +241,35 @@ struct RowMap {
     static constexpr int KS = TC ? KW / 16 : 1;     // TC: k16 steps per warp
     static constexpr int TC_ROWS = QB == 4 ? 16 : 8;  // TC: rows per M tile (int8: 8 + 8 zero)
     static constexpr int RPS = TC ? TC_ROWS : RG * RPT;  // rows per slot
-    static constexpr int EWPR = TC ? kNCW : WPR;    // per-row partials in the epilogue
+    static constexpr int EWPR = S::KCP ? 1 : TC ? kNCW : WPR;  // per-row partials in the epilogue
     static constexpr int APT = RPS / RG;            // rows per thread per slot (CUDA-core AXPY)
-    static constexpr int SLOT = (RPS * ROW_BYTES + 127) / 128 * 128;
+    // batch >= 8 (KCP): a weight slot holds RW rows x KC columns (row stride
+    // padded by 16 bytes: conflict-free ldmatrix), the activations of a
+    // chunk arrive as one slot of MMA A fragments (ATAB bytes); warps split
+    // the slot as RP row parts (two n8 tiles each) x KP k parts (8 k16 steps)
+    static constexpr bool KCP = S::KCP;
+    static constexpr int KC = S::KC;
+    static constexpr int RW = KCP ? 16384 / KC : 1;
+    static constexpr int NKC = KCP ? K / KC : 1;
+    static constexpr int SEG = KC * 2;
+    static constexpr int WSTRIDE = SEG + 16;
+    static constexpr int ATAB = KC / 16 * 1024;
+    static constexpr int RP = KCP ? RW / 16 : 1;
+    static constexpr int KP = kNCW / RP;
+    static constexpr int SLOT = KCP ? RW * WSTRIDE : (RPS * ROW_BYTES + 127) / 128 * 128;
     // rows per epilogue batch (whole slots; >= 64/B rows so barriers are rare)
-    static constexpr int RB = RPS > 64 / S::B ? RPS : ((64 / S::B) / RPS) * RPS;
-    static_assert(TPR % 32 == 0 && TPR <= kNCT && kNCT % TPR == 0, "a row must span whole warps");
-    static_assert(K % CPT == 0 && CPT % 8 == 0, "row mapping");
+    static constexpr int RB = KCP ? 16 : RPS > 64 / S::B ? RPS : ((64 / S::B) / RPS) * RPS;
+    // (CUDA-core / quant row mapping; unused at batch >= 8)
+    static_assert(KCP || (TPR % 32 == 0 && TPR <= kNCT && kNCT % TPR == 0), "a row must span whole warps");
+    static_assert(KCP || (K % CPT == 0 && CPT % 8 == 0), "row mapping");
     static_assert(QB == 0 || kQuantGroup % CPT == 0, "a thread's columns lie in one group");
-    static_assert(RPS >= 1 && (RPS == 1 || RPS % 2 == 0) && RPS % RG == 0, "slot rows");
-    static_assert(RPS * S::B <= kNCT && RB * S::B <= kNCT, "epilogue threads");
-    static_assert(TC || (RPT * S::B <= 32 && (RPT & (RPT - 1)) == 0),
+    static_assert(KCP || (RPS >= 1 && (RPS == 1 || RPS % 2 == 0) && RPS % RG == 0), "slot rows");
+    static_assert(RB * S::B <= kNCT && (KCP || RPS * S::B <= kNCT), "epilogue threads");
+    static_assert(KCP || TC || (RPT * S::B <= 32 && (RPT & (RPT - 1)) == 0),
                   "one transposed warp reduction per slot");
     static_assert(!TC || (2 * S::B <= 8 && KW % kQuantGroup == 0), "TC: hi/lo columns fit n8");
+    static_assert(!KCP || (K % KC == 0 && RP * KP == kNCW && KC / 16 == 8 * KP && ATAB <= SLOT),
+                  "K-chunked tensor-core GEMV geometry");
 };
 
 template <class S>
@@ -249,8 +284,8 @@ struct KTraits : RowMap<S, S::D> {
     // rows are AXPYed into per-CTA partials that S_RED sums.  Same-box A/B:
     // 8B b1 2.725 -> 2.700 ms, b2 3.204 -> 3.176; 1B b1 0.638 -> 0.650
     // (the reduction of 2048-wide partials is cheaper than the barrier).
-    static constexpr bool F2R = S::QB == 0 && S::B <= 2 && S::D >= 4096 &&
-                                S::DI % (8 * kNCT) == 0 && S::DI * 2 <= 32768;
+    static constexpr bool F2R = S::KCP || (S::QB == 0 && S::B <= 2 && S::D >= 4096 &&
+                                           S::DI % (8 * kNCT) == 0 && S::DI * 2 <= 32768);
     using MF = std::conditional_t<F2R, RowMap<S, S::DI>, MD>;
     static constexpr int NCW = kNCW;
     static constexpr int NCT = kNCT;
@@ -262,9 +297,11 @@ struct KTraits : RowMap<S, S::D> {
     static constexpr int CONSUMER_REGS = 224;  // 4*32*56 + 8*32*224 <= 64K
     static constexpr int cmin(int a, int b) { return a < b ? a : b; }
     static constexpr int cmax(int a, int b) { return a > b ? a : b; }
-    static constexpr int SLOT_BYTES = S::QB == 0 ? 32768 : cmax(MD::SLOT, MA::SLOT);
+    static constexpr int SLOT_BYTES = S::KCP ? MD::SLOT : S::QB == 0 ? 32768 : cmax(MD::SLOT, MA::SLOT);
+    // KCP: [KP][RW][B] k-part partials + [RW][B] finished rows (gemv_kc)
     static constexpr int RED_FLOATS =
-        cmax(cmax(MD::EWPR * MD::RB, MA::EWPR * MA::RB), MF::EWPR * MF::RB) * S::B;
+        S::KCP ? (MD::KP * MD::RW * S::B + MD::RW * S::B + 1) / 2
+               : cmax(cmax(MD::EWPR * MD::RB, MA::EWPR * MA::RB), MF::EWPR * MF::RB) * S::B;
     static constexpr int KVC = SLOT_BYTES / (2 * S::DH * 2);  // KV positions per slot
     static constexpr int DPL = S::DH / 32;          // attention dims per lane
     // max GLU pairs / Waout rows per CTA (host-checked): a CTA's share with
@@ -285,7 +322,7 @@ struct KTraits : RowMap<S, S::D> {
     static constexpr int OFF_ROPE = OFF_H + SZ_H;  // [DH/2][2] f32
     static constexpr int SZ_ROPE = S::DH * 4;
     static constexpr int OFF_NORM = OFF_ROPE + SZ_ROPE;  // [NCW][B] f32
-    static constexpr int SZ_NORM = NCW * S::B * 4 + 16;
+    static constexpr int SZ_NORM = (NCW + 1) * S::B * 4 + 16;  // [NCW][B] partials + [B] (KCP inv)
     static constexpr int OFF_WPART = OFF_NORM + SZ_NORM;  // [NCW][QPG][DH+2] f32
     // also reused for: attention combine (3*G*QPG), argmax candidates
     // (2*grid*B) and the GLU reduction (NCW*32); grid <= kMaxGrid
@@ -379,14 +416,25 @@ struct DecodeCta {
             return true;
         }
         if (stage == p.layers * kStagesPerLayer) {  // LM head
-            if (p.layers == 0) return false;
+            if (p.layers == 0) {
+                if constexpr (!S::KCP) return false;
+                *ctr = p.counters + p.layers * kStagesPerLayer + 1;  // init counter
+                *target = full_grid;
+                return true;
+            }
             *ctr = p.counters + (p.layers - 1) * kStagesPerLayer + S_RED;
             *target = full_grid;
             return true;
         }
         switch (s) {
             case S_QKV:
-                if (l == 0) return false;
+                if (l == 0) {
+                    if constexpr (!S::KCP) return false;
+                    // KCP: every CTA's initial x rows and A table (kc_publish)
+                    *ctr = p.counters + p.layers * kStagesPerLayer + 1;
+                    *target = full_grid;
+                    return true;
+                }
                 *ctr = p.counters + (l - 1) * kStagesPerLayer + S_RED;
                 *target = full_grid;
                 return true;
@@ -450,6 +498,26 @@ struct DecodeCta {
         ++it;
     }
 
+    // KCP weight slot: n row segments of seg bytes (source stride sstride)
+    // at the padded slot stride MD::WSTRIDE
+    template <bool DRAIN>
+    __device__ void chunk_rows(uint32_t& it, const uint8_t* src, int n, uint32_t seg, size_t sstride,
+                               uint64_t policy) {
+        const uint32_t slot = it % T::NSLOTS, ph = (it / T::NSLOTS) & 1;
+        if (DRAIN) {
+            mbar_wait(&full[slot], ph);
+            __syncwarp();
+            if ((threadIdx.x & 31) == 0) mbar_arrive(&empty[slot]);
+        } else {
+            mbar_wait(&empty[slot], ph ^ 1);
+            mbar_arrive_expect_tx(&full[slot], n * seg);
+            uint8_t* dst = ring + slot * T::SLOT_BYTES;
+            for (int r = 0; r < n; ++r)
+                tma_load_1d(dst + r * MD::WSTRIDE, src + r * sstride, seg, &full[slot], policy);
+        }
+        ++it;
+    }
+
     // One list of the static per-CTA stream: rows [r0, r1) of a matrix (kv =
     // false) or KV positions [r0, r1) of one (layer, batch row, kv head).
     struct List {
@@ -458,7 +526,15 @@ struct DecodeCta {
         bool kv;
         bool pool;  // the GLU work pool: one marker chunk, claimed dynamically
         int row_bytes = T::ROW_BYTES, rps = T::RPS;  // matrix row geometry
+        // KCP: per row block, per K chunk: the chunk's A-fragment table (one
+        // slot, dependency-gated) then RW-row weight slots of the chunk
+        const uint8_t* atab = nullptr;
+        int nkc = 0;
     };
+    // KCP rows per accumulator block: the chunk's A table stays in its slot
+    // while the block's weight slots stream past it, so a block spans at
+    // most NSLOTS - 1 weight slots (and at most 256 rows of accumulators)
+    static constexpr int KC_BLOCK = cmin_(256, (T::NSLOTS - 1) * T::MD::RW);
 
     // The lists of (stage, sub) in consumption order; false past the end.
     __device__ bool list_of(int stage, int sub, List& L) const {
@@ -471,6 +547,7 @@ struct DecodeCta {
         if (stage == p.layers * kStagesPerLayer) {
             if (sub > 0) return false;
             L = {p.lm_head, pl.lm_r0, pl.lm_r1, false, false};
+            if constexpr (S::KCP) { L.atab = p.xfrag_f; L.nkc = MD::NKC; }
             return true;
         }
         switch (s) {
@@ -478,6 +555,7 @@ struct DecodeCta {
                 if (sub > 0) return false;
                 L = {p.wqkv + (size_t)l * S::QKVR * T::ROW_BYTES, pl.qkv_r0, pl.qkv_r1, false,
                      false};
+                if constexpr (S::KCP) { L.atab = p.xfrag_f; L.nkc = MD::NKC; }
                 return true;
             case S_ATTN: {
                 if (sub > 0 || pl.attn_unit < 0) return false;
@@ -493,10 +571,14 @@ struct DecodeCta {
                 if (sub > 0) return false;
                 L = {p.waout + (size_t)l * D * MA::ROW_BYTES, pl.aout_r0, pl.aout_r1, false, false,
                      MA::ROW_BYTES, MA::RPS};
+                if constexpr (S::KCP) { L.atab = p.afrag; L.nkc = MA::NKC; }
                 return true;
             case S_GLU:
-                if (sub == 0) L = {p.wffn1 + (size_t)l * 2 * S::DI * T::ROW_BYTES, 2 * pl.glu_t0,
-                                   2 * pl.glu_t1, false, false};
+                if (sub == 0) {
+                    L = {p.wffn1 + (size_t)l * 2 * S::DI * T::ROW_BYTES, 2 * pl.glu_t0,
+                         2 * pl.glu_t1, false, false};
+                    if constexpr (S::KCP) { L.atab = p.xfrag_a; L.nkc = MD::NKC; }
+                }
                 else if (sub == 1 && !T::F2R)
                     L = {p.wffn2t + (size_t)l * S::DI * T::ROW_BYTES, pl.glu_t0, pl.glu_t1, false,
                          false};
@@ -507,6 +589,7 @@ struct DecodeCta {
                 if (!T::F2R || sub > 0) return false;
                 L = {p.wffn2t + (size_t)l * D * MF::ROW_BYTES, pl.aout_r0, pl.aout_r1, false,
                      false, MF::ROW_BYTES, MF::RPS};
+                if constexpr (S::KCP) { L.atab = p.hfrag; L.nkc = MF::NKC; }
                 return true;
             default:
                 return false;
@@ -518,6 +601,9 @@ struct DecodeCta {
         int stage, sub, c0;
         bool valid;
         List L;
+        int kcc, kcj;  // KCP: chunk, slot within the chunk (-1: A table)
+        int out_rows;  // KCP: the emitted chunk is out_rows row segments (0: one copy)
+        bool out_dep;  // the emitted chunk reads data of this stage's dependency
     };
 
     __device__ void cursor_init(Cursor& c) const {
@@ -539,6 +625,8 @@ struct DecodeCta {
                 }
                 c.valid = true;
                 c.c0 = c.L.r0;
+                c.kcc = 0;
+                c.kcj = -1;
             }
             if (c.c0 >= c.L.r1) {
                 c.valid = false;
@@ -546,6 +634,34 @@ struct DecodeCta {
                 continue;
             }
             *stage = c.stage;
+            c.out_rows = 0;
+            c.out_dep = false;
+            if (c.L.nkc > 0) {  // KCP
+                const int blk_end = min(c.c0 + KC_BLOCK, c.L.r1);
+                if (c.kcj < 0) {
+                    *src0 = c.L.atab + (size_t)c.kcc * MD::ATAB;
+                    *src1 = nullptr;
+                    *bytes = MD::ATAB;
+                    c.out_dep = true;
+                    c.kcj = 0;
+                    return true;
+                }
+                const int row0 = c.c0 + c.kcj * MD::RW;
+                if (row0 < blk_end) {
+                    *src0 = c.L.base + (size_t)row0 * c.L.row_bytes + (size_t)c.kcc * MD::SEG;
+                    *src1 = nullptr;
+                    *bytes = MD::SEG;
+                    c.out_rows = min(MD::RW, blk_end - row0);
+                    ++c.kcj;
+                    return true;
+                }
+                c.kcj = -1;
+                if (++c.kcc == c.L.nkc) {
+                    c.kcc = 0;
+                    c.c0 = blk_end;
+                }
+                continue;
+            }
             if (c.L.pool) {  // marker: the caller runs the dynamic pool protocol
                 *src0 = nullptr;
                 *src1 = nullptr;
@@ -673,6 +789,7 @@ struct DecodeCta {
         bool pf_live = window > 0;
         int cur_stage = p.stage_begin;
         int kv_pf_stage = -1;
+        int dep_stage = -1;  // KCP: last stage whose dependency the producer waited for
         const void *s0, *s1;
         uint32_t bytes;
         int stage;
@@ -700,6 +817,23 @@ struct DecodeCta {
             if (s0 == nullptr) {  // GLU work-pool marker
                 pool_run<DRAIN>(it, stage / kStagesPerLayer, policy);
                 continue;
+            }
+            if constexpr (S::KCP) {
+                if (c.out_dep && !DRAIN && stage != dep_stage && !(p.debug & kDebugStreamOnly)) {
+                    // the A table is written by the previous stage's epilogues
+                    // (every mode: the stage-change wait of the non-overlap
+                    // modes skips a launch's first stage)
+                    const uint32_t* ctr;
+                    uint32_t target;
+                    if (dependency(stage, &ctr, &target)) spin_until_geq(ctr, target);
+                    fence_proxy_async_global();
+                    dep_stage = stage;
+                }
+                if (c.out_rows > 0) {
+                    chunk_rows<DRAIN>(it, static_cast<const uint8_t*>(s0), c.out_rows, bytes,
+                                      c.L.row_bytes, policy);
+                    continue;
+                }
             }
             const int64_t need = s1 ? 2 * (int64_t)bytes : bytes;
             if (!DRAIN) {
@@ -1422,14 +1556,190 @@ struct DecodeCta {
         return t;
     }
 
+    // ================================================ batch >= 8 (KCP)
+    // A-fragment table offset of activation column k, batch row b (m16n8k16
+    // row-major A: lane (g, q) holds rows g / g + 8, columns 2q, 2q + 1 and
+    // 2q + 8, 2q + 9 of each k16 step; registers a0..a3 = (g, lo k), (g + 8,
+    // lo k), (g, hi k), (g + 8, hi k)); the lo part is 16 bytes further.
+    __device__ static size_t frag_off(int k, int b) {
+        const int kst = k >> 4, kk = k & 15;
+        const int lane = (b & 7) * 4 + ((kk & 7) >> 1);
+        const int reg = (kk >> 3) * 2 + (b >> 3);
+        return (size_t)kst * 1024 + lane * 32 + reg * 4 + (kk & 1) * 2;
+    }
+    // v as fp16 hi + lo (22 bits of mantissa, as the quant tensor-core
+    // GEMV's activations; bf16 hi + lo would carry 16 and measurably move
+    // the logits); the bf16 weights are widened to fp16 exactly in gemv_kc
+    __device__ static void frag_put(uint8_t* tab, int k, int b, float v) {
+        const __half hi = __float2half_rn(v);
+        const __half lo = __float2half_rn(v - __half2float(hi));
+        uint8_t* d = tab + frag_off(k, b);
+        *reinterpret_cast<__half*>(d) = hi;
+        *reinterpret_cast<__half*>(d + 16) = lo;
+    }
+    // bf16x2 -> fp16x2 (exact for |w| in the fp16 normal range; bf16
+    // weights below 2^-14 keep 2^-24 absolute precision)
+    __device__ static uint32_t bf2_to_h2(uint32_t w) {
+        const __half2 h = __floats2half2_rn(__uint_as_float(w << 16), __uint_as_float(w & 0xffff0000u));
+        return *reinterpret_cast<const uint32_t*>(&h);
+    }
+
+    // After this CTA updated x rows [c0, c1): their A-table entries x * gain
+    // and this CTA's per-batch-row sum of squares (ssq_out[cta][b]).  Ends
+    // with a proxy fence: the tables are read by TMA (async proxy).
+    __device__ void kc_publish(int c0, int c1, const float* gain, uint8_t* tab, float* ssq_out) {
+        const int ctid = threadIdx.x, warp = ctid / 32, lane = ctid % 32;
+        static_assert(kNCT % B == 0, "a thread's batch row is fixed");
+        float sq = 0.f;
+        for (int i = ctid; i < (c1 - c0) * B; i += NCT) {
+            const int c = c0 + i / B, b = i % B;
+            const float v = ldcg_f(p.x + (size_t)b * D + c);
+            sq = fmaf(v, v, sq);
+            frag_put(tab, c, b, v * __ldg(gain + c));
+        }
+#pragma unroll
+        for (int off = B; off < 32; off <<= 1) sq += __shfl_xor_sync(0xffffffffu, sq, off);
+        float* ns = norm_s();
+        if (lane < B) ns[warp * B + lane] = sq;
+        fence_proxy_async_global();
+        consumer_sync(NCT);
+        if (ctid < B) {
+            float t = 0.f;
+            for (int w = 0; w < NCW; ++w) t += ns[w * B + ctid];
+            __stcg(ssq_out + (size_t)cta * B + ctid, t);
+        }
+        consumer_sync(NCT);
+    }
+
+    // 1 / rms of every batch row from the CTAs' sums of squares (fixed order)
+    // -> norm_s()[NCW * B + b]
+    __device__ const float* kc_inv(const float* ssq_in) {
+        float* inv = norm_s() + NCW * B;
+        if (threadIdx.x < B) {
+            float t = 0.f;
+            for (int c = 0; c < grid; ++c) t += ldcg_f(ssq_in + (size_t)c * B + threadIdx.x);
+            inv[threadIdx.x] = 1.0f / sqrtf(t / static_cast<float>(D) + p.eps);
+        }
+        consumer_sync(NCT);
+        return inv;
+    }
+
+    // K-chunked tensor-core GEMV, rows [r0, r1), in row blocks of KC_BLOCK:
+    // per K chunk the ring delivers the A table (activations of all batch
+    // rows, fp16 hi/lo) then weight slots of RW rows; warp (rp, kp) runs the
+    // mma.sync m16n8k16 of its two n8 row tiles over its 8 k-steps into
+    // per-block accumulators (M = batch: the 16 MMA rows are the batch
+    // rows).  At the block end the KP k-part partials are summed in a fixed
+    // order (deterministic), scaled by inv[b] (normed inputs) and handed to
+    // epi(c0, nrows <= 16, red[row][b]) like gemv's epilogues (EWPR = 1).
+    template <class M, class Epi>
+    __device__ void gemv_kc(uint32_t& it, int r0, int r1, const float* inv, Epi&& epi) {
+        constexpr int RW = M::RW, NJ = KC_BLOCK / RW;
+        const int ctid = threadIdx.x, warp = ctid / 32, lane = ctid % 32, g = lane / 4, q4 = lane % 4;
+        const int rp = warp % M::RP, kp = warp / M::RP;
+        float* R = reinterpret_cast<float*>(smem + T::OFF_RED);  // [KP][RW][B]
+        float* fin = R + M::KP * RW * B;                          // [RW][B]
+        // this lane's ldmatrix row (two n8 tiles x two k halves) in a weight slot
+        const int lrow = rp * 16 + (lane >> 4) * 8 + (lane & 7);
+        const int lcol = ((lane >> 3) & 1) * 16;
+        for (int blk = r0; blk < r1; blk += KC_BLOCK) {
+            const int blk_end = min(blk + KC_BLOCK, r1);
+            const int nj = (blk_end - blk + RW - 1) / RW;
+            float acc[NJ][2][4];
+#pragma unroll
+            for (int j = 0; j < NJ; ++j)
+#pragma unroll
+                for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) acc[j][nt][e] = 0.f;
+            for (int c = 0; c < M::NKC; ++c) {
+                const uint32_t sa = it % T::NSLOTS;
+                wait_full(sa, (it / T::NSLOTS) & 1);
+                const uint8_t* atab = ring + sa * T::SLOT_BYTES + kp * 8 * 1024 + lane * 32;
+                ++it;
+#pragma unroll
+                for (int j = 0; j < NJ; ++j) {
+                    if (j < nj) {
+                        const uint32_t sw = it % T::NSLOTS;
+                        wait_full(sw, (it / T::NSLOTS) & 1);
+                        const uint8_t* wrow =
+                            ring + sw * T::SLOT_BYTES + lrow * M::WSTRIDE + kp * 8 * 32 + lcol;
+#pragma unroll
+                        for (int ks = 0; ks < 8; ++ks) {
+                            const uint4 ah = lds_u128(atab + ks * 1024);
+                            const uint4 al = lds_u128(atab + ks * 1024 + 16);
+                            uint32_t b0, b1, b2, b3;
+                            ldsm_x4(wrow + ks * 32, b0, b1, b2, b3);
+                            b0 = bf2_to_h2(b0);
+                            b1 = bf2_to_h2(b1);
+                            b2 = bf2_to_h2(b2);
+                            b3 = bf2_to_h2(b3);
+                            mma_f16(acc[j][0], ah.x, ah.y, ah.z, ah.w, b0, b1);
+                            mma_f16(acc[j][1], ah.x, ah.y, ah.z, ah.w, b2, b3);
+                            mma_f16(acc[j][0], al.x, al.y, al.z, al.w, b0, b1);
+                            mma_f16(acc[j][1], al.x, al.y, al.z, al.w, b2, b3);
+                        }
+                        __syncwarp();
+                        if (lane == 0) mbar_arrive(&empty[sw]);
+                        ++it;
+                    }
+                }
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&empty[sa]);
+            }
+#pragma unroll
+            for (int j = 0; j < NJ; ++j) {
+                if (j < nj) {
+#pragma unroll
+                    for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+                        for (int e = 0; e < 4; ++e) {
+                            const int row = rp * 16 + nt * 8 + 2 * q4 + (e & 1);
+                            const int b = g + 8 * (e >> 1);
+                            if (b < B) R[(kp * RW + row) * B + b] = acc[j][nt][e];
+                        }
+                    consumer_sync(NCT);
+                    for (int i = ctid; i < RW * B; i += NCT) {
+                        float t = 0.f;
+#pragma unroll
+                        for (int k = 0; k < M::KP; ++k) t += R[k * RW * B + i];
+                        fin[i] = inv != nullptr ? t * inv[i % B] : t;
+                    }
+                    consumer_sync(NCT);
+                    const int g0 = blk + j * RW, nrows = min(RW, blk_end - g0);
+                    for (int e0 = 0; e0 < nrows; e0 += 16) epi(g0 + e0, min(16, nrows - e0), fin + e0 * B);
+                    consumer_sync(NCT);
+                }
+            }
+        }
+    }
+
+    // One GEMV stage's activation + rows: CUDA-core / quant path (load_act +
+    // gemv) or, at batch >= 8, gemv_kc (inputs already in the A tables;
+    // ssq_in = the sums of squares of a normed input, else nullptr).
+    template <class M, class Epi>
+    __device__ void run_gemv(uint32_t& it, const float* src, bool from_emb, const float* gain,
+                             const float* ssq_in, int stage, int r0, int r1, Epi&& epi) {
+        if constexpr (S::KCP) {
+            wait_stage(stage);
+            const float* inv = ssq_in != nullptr ? kc_inv(ssq_in) : nullptr;
+            trace_mark(stage, 3);
+            gemv_kc<M>(it, r0, r1, inv, epi);
+        } else {
+            Act<M> act;
+            load_act<M>(act, src, from_emb, gain, stage);
+            trace_mark(stage, 3);
+            gemv<M>(it, act, r0, r1, epi);
+        }
+    }
+
     // ---------------------------------------------------------- S_QKV
     __device__ void stage_qkv(uint32_t& it, int l) {
-        Act<> act;
-        load_act(act, p.x, l == 0, p.norm_attn + (size_t)l * D, l * kStagesPerLayer + S_QKV);
-        trace_mark(l * kStagesPerLayer + S_QKV, 3);
         const float* rp = rope();
         const int ctid = threadIdx.x;
-        gemv(it, act, pl.qkv_r0, pl.qkv_r1, [&](int c0, int nrows, const float* red) {
+        run_gemv<MD>(it, p.x, l == 0, p.norm_attn + (size_t)l * D,
+                     S::KCP ? p.ssq + (size_t)grid * B : nullptr, l * kStagesPerLayer + S_QKV,
+                     pl.qkv_r0, pl.qkv_r1, [&](int c0, int nrows, const float* red) {
             const int npairs = nrows / 2;
             if (ctid < npairs * B) {
                 const int pr = ctid / B, b = ctid % B;
@@ -1923,8 +2233,10 @@ struct DecodeCta {
                     for (int g = 0; g < kMaxGroup; ++g)
                         if (g < G) out += rr[h * G + g] * v[k][g];
                     __stcg(p.attn_out + (size_t)b * D + (kvh * QPG + h) * DH + d, out);
+                    if constexpr (S::KCP) frag_put(p.afrag, (kvh * QPG + h) * DH + d, b, out);
                 }
             }
+            if constexpr (S::KCP) fence_proxy_async_global();  // afrag is read by TMA
             arrive(p.counters + l * kStagesPerLayer + S_ATTN, l * kStagesPerLayer + S_ATTN);
         }
     }
@@ -1967,12 +2279,11 @@ struct DecodeCta {
     // columns (this rank's q heads, AD = NQ * DH of them), each rank holds a
     // partial of every row, summed across ranks (tp_exchange_add).
     __device__ void stage_aout(uint32_t& it, int l) {
-        Act<MA> act;
-        load_act<MA>(act, p.attn_out, false, nullptr, l * kStagesPerLayer + S_AOUT);
         const int ctid = threadIdx.x;
         const int r0 = pl.aout_r0, nr = pl.aout_r1 - pl.aout_r0;
         float* acc = h_s();  // [B][TMAX] row results; x updated once at the end
-        gemv<MA>(it, act, r0, pl.aout_r1, [&](int c0, int nrows, const float* red) {
+        run_gemv<MA>(it, p.attn_out, false, nullptr, nullptr, l * kStagesPerLayer + S_AOUT, r0,
+                     pl.aout_r1, [&](int c0, int nrows, const float* red) {
             if (ctid < nrows * B) {
                 const int r = ctid / B, b = ctid % B;
                 acc[b * T::TMAX + c0 - r0 + r] = row_total<MA>(red, r, b);
@@ -1994,26 +2305,39 @@ struct DecodeCta {
                 __stcg(xp, ldcg_f(xp) + acc[b * T::TMAX + r]);
             }
         }
+        if constexpr (S::KCP) {  // S_GLU's A table and norm statistics
+            consumer_sync(NCT);
+            kc_publish(r0, pl.aout_r1, p.norm_ffn + (size_t)l * D, p.xfrag_a, p.ssq);
+        }
         arrive(p.counters + l * kStagesPerLayer + S_AOUT, l * kStagesPerLayer + S_AOUT);
     }
 
     // ---------------------------------------------------------- S_GLU
     // in/gate rows [2 t0, 2 t1) of Wffn1 -> h[t - t0] = silu(gate) * in (smem)
-    __device__ void glu_ffn1(uint32_t& it, const Act<>& act, int t0, int t1) {
+    __device__ void glu_ffn1(uint32_t& it, const Act<>& act, int t0, int t1,
+                             const float* kc_inv_b = nullptr) {
         const int ctid = threadIdx.x;
         float* hs = h_s();
-        gemv(it, act, 2 * t0, 2 * t1, [&](int c0, int nrows, const float* red) {
+        auto epi = [&](int c0, int nrows, const float* red) {
             const int npairs = nrows / 2;
             if (ctid < npairs * B) {
                 const int pr = ctid / B, b = ctid % B;
                 const float a = row_total(red, 2 * pr, b), g = row_total(red, 2 * pr + 1, b);
                 const float silu = g / (1.0f + expf(-g));
-                if constexpr (T::F2R)
+                if constexpr (S::KCP)
+                    frag_put(p.hfrag, c0 / 2 + pr, b, silu * a);
+                else if constexpr (T::F2R)
                     __stcg(p.glu_part + (size_t)b * S::DI + c0 / 2 + pr, silu * a);
                 else
                     hs[b * T::TMAX + (c0 / 2 - t0) + pr] = silu * a;
             }
-        });
+        };
+        if constexpr (S::KCP) {
+            gemv_kc<MD>(it, 2 * t0, 2 * t1, kc_inv_b, epi);
+            fence_proxy_async_global();  // h is read by TMA in S_RED
+        } else {
+            gemv(it, act, 2 * t0, 2 * t1, epi);
+        }
         consumer_sync(NCT);  // h complete
     }
 
@@ -2131,6 +2455,15 @@ struct DecodeCta {
     // Static slice [glu_t0, glu_t1) into glu_part[cta], then pool chunks
     // (claimed by this CTA's producer) each into pool_part[chunk].
     __device__ void stage_glu(uint32_t& it, int l) {
+        if constexpr (S::KCP) {
+            wait_stage(l * kStagesPerLayer + S_GLU);
+            const float* inv = kc_inv(p.ssq);
+            trace_mark(l * kStagesPerLayer + S_GLU, 3);
+            Act<> unused;
+            glu_ffn1(it, unused, pl.glu_t0, pl.glu_t1, inv);
+            arrive(p.counters + l * kStagesPerLayer + S_GLU, l * kStagesPerLayer + S_GLU);
+            return;
+        }
         Act<> act;
         load_act(act, p.x, false, p.norm_ffn + (size_t)l * D, l * kStagesPerLayer + S_GLU);
         glu_ffn1(it, act, pl.glu_t0, pl.glu_t1);
@@ -2164,12 +2497,11 @@ struct DecodeCta {
     // by input columns (this rank's d_inter slice), partials summed across
     // ranks in exchange slot 1.
     __device__ void stage_ffn2(uint32_t& it, int l) {
-        Act<MF> act;
-        load_act<MF>(act, p.glu_part, false, nullptr, l * kStagesPerLayer + S_RED);
         const int ctid = threadIdx.x;
         const int r0 = pl.aout_r0, nr = pl.aout_r1 - pl.aout_r0;
         float* acc = h_s();  // [B][TMAX]
-        gemv<MF>(it, act, r0, pl.aout_r1, [&](int c0, int nrows, const float* red) {
+        run_gemv<MF>(it, p.glu_part, false, nullptr, nullptr, l * kStagesPerLayer + S_RED, r0,
+                     pl.aout_r1, [&](int c0, int nrows, const float* red) {
             if (ctid < nrows * B) {
                 const int r = ctid / B, b = ctid % B;
                 acc[b * T::TMAX + c0 - r0 + r] = row_total<MF>(red, r, b);
@@ -2190,6 +2522,12 @@ struct DecodeCta {
                 float* xp = p.x + (size_t)b * D + r0 + r;
                 __stcg(xp, ldcg_f(xp) + acc[b * T::TMAX + r]);
             }
+        }
+        if constexpr (S::KCP) {  // next S_QKV's (or the LM head's) A table
+            consumer_sync(NCT);
+            kc_publish(r0, pl.aout_r1,
+                       l + 1 < p.layers ? p.norm_attn + (size_t)(l + 1) * D : p.final_norm,
+                       p.xfrag_f, p.ssq + (size_t)grid * B);
         }
         arrive(p.counters + l * kStagesPerLayer + S_RED, l * kStagesPerLayer + S_RED);
     }
@@ -2246,12 +2584,12 @@ struct DecodeCta {
 
     // ---------------------------------------------------------- S_LMHEAD
     __device__ void stage_lmhead(uint32_t& it) {
-        Act<> act;
-        load_act(act, p.x, p.layers == 0, p.final_norm, p.layers * kStagesPerLayer);
         const int ctid = threadIdx.x;
         float best = -INFINITY;
         int best_i = 0x7fffffff;
-        gemv(it, act, pl.lm_r0, pl.lm_r1, [&](int c0, int nrows, const float* red) {
+        run_gemv<MD>(it, p.x, p.layers == 0, p.final_norm,
+                     S::KCP ? p.ssq + (size_t)grid * B : nullptr, p.layers * kStagesPerLayer,
+                     pl.lm_r0, pl.lm_r1, [&](int c0, int nrows, const float* red) {
             if (ctid < nrows * B) {
                 const int r = ctid / B, b = ctid % B;
                 const float v = row_total(red, r, b);
@@ -2377,7 +2715,7 @@ struct DecodeCta {
         for (int stage = p.stage_begin; stage < last; ++stage) {
             trace_mark(stage, 0);
             if (p.kind == 1) {
-                stage_linear(it, stage);
+                if constexpr (!S::KCP) stage_linear(it, stage);  // (host: kind 1 is batch < 8)
                 continue;
             }
             const int l = stage / kStagesPerLayer, s = stage % kStagesPerLayer;
@@ -2435,6 +2773,16 @@ __global__ void __launch_bounds__(KTraits<S>::NTHREADS, 1)
         return;
     }
     asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(T::CONSUMER_REGS));
+    if constexpr (S::KCP) {
+        // the initial x rows' A-table entries and norm statistics; the first
+        // S_QKV (or the LM head) waits for every CTA's arrival
+        if (p.kind == 0 && p.stage_begin == 0 && !(p.debug & kDebugStreamOnly)) {
+            cta.kc_publish(cta.pl.red_c0, cta.pl.red_c1,
+                           p.layers > 0 ? p.norm_attn : p.final_norm, p.xfrag_f,
+                           p.ssq + (size_t)gridDim.x * S::B);
+            if (tid == 0) red_release_gpu(p.counters + p.layers * kStagesPerLayer + 1, 1);
+        }
+    }
     if (p.debug & kDebugStreamOnly) {
         cta.template producer<true>();  // streaming-only measurement
     } else {

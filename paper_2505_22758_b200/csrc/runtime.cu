@@ -62,6 +62,7 @@ const std::vector<KernelOps>& registry() {
         register_kernels_8b(v);
         register_kernels_quant(v);
         register_kernels_70b(v);
+        register_kernels_kc(v);
     });
     return v;
 }
@@ -70,7 +71,8 @@ const KernelOps* find_ops(const ffb_model_config& c) {
     if (c.dtype != 0) return nullptr;
     if (c.kind == 1) {  // stacked linear: only the d_model-column GEMV is used
         for (const auto& k : registry())
-            if (k.D == c.d_model && k.B == c.batch && k.QB == 0 && k.D == k.NQ * k.DH) return &k;
+            if (k.D == c.d_model && k.B == c.batch && k.QB == 0 && k.D == k.NQ * k.DH && k.B < 8)
+                return &k;
         return nullptr;
     }
     if (c.quant_bits != 0 && c.quant_group != kQuantGroup) return nullptr;
@@ -258,6 +260,8 @@ struct ffb_model {
     uint8_t* wlin = nullptr;            // stacked linear: [L][D] bf16 rows
     float* xbuf = nullptr;              // stacked linear: [2][B][D]
     float *norm_attn = nullptr, *norm_ffn = nullptr, *final_norm = nullptr;
+    uint8_t *xfrag_a = nullptr, *xfrag_f = nullptr, *afrag = nullptr, *hfrag = nullptr;  // batch >= 8
+    float* ssq = nullptr;                                                               // [2][grid][B]
     float *x = nullptr, *q = nullptr, *attn_out = nullptr, *glu_part = nullptr,
           *attn_part = nullptr, *logits = nullptr, *amax_val = nullptr;
     int32_t* amax_idx = nullptr;
@@ -466,6 +470,11 @@ DecodeParams make_params(const ffb_model* m, int64_t pos, const int64_t* d_token
     p.kcache = m->kcache;
     p.vcache = m->vcache;
     p.x = m->x;
+    p.xfrag_a = m->xfrag_a;
+    p.xfrag_f = m->xfrag_f;
+    p.afrag = m->afrag;
+    p.hfrag = m->hfrag;
+    p.ssq = m->ssq;
     p.q = m->q;
     p.attn_out = m->attn_out;
     p.glu_part = m->glu_part;
@@ -526,7 +535,7 @@ ffb_status reset_sync_state(ffb_model* m, cudaStream_t stream) {
         CUDA_TRY(cudaMemsetAsync(m->counters, 0, sizeof(uint32_t) * (Lc + 1), stream));
         return FFB_OK;
     }
-    CUDA_TRY(cudaMemsetAsync(m->counters, 0, sizeof(uint32_t) * (Lc * 5 + 1), stream));
+    CUDA_TRY(cudaMemsetAsync(m->counters, 0, sizeof(uint32_t) * (Lc * 5 + 2), stream));
     if (m->xflag) CUDA_TRY(cudaMemsetAsync(m->xflag, 0, m->xflag_bytes, stream));
     CUDA_TRY(cudaMemsetAsync(m->qkv_head_counters, 0,
                              sizeof(uint32_t) * Lc * m->cfg.n_kv_heads, stream));
@@ -969,6 +978,19 @@ ffb_status ffb_create_ex(const ffb_model_config* gcfg, int64_t max_seq_len, int 
     ALLOC(m->kcache, kv);
     ALLOC(m->vcache, kv);
     ALLOC(m->x, (size_t)B * D);
+    if (B >= 8) {  // A-fragment tables (64 bytes per column: 16 rows x hi/lo bf16)
+        ALLOC(m->xfrag_a, (size_t)D * 64);
+        ALLOC(m->xfrag_f, (size_t)D * 64);
+        ALLOC(m->afrag, (size_t)c.n_q_heads * c.d_head * 64);
+        ALLOC(m->hfrag, (size_t)c.d_inter * 64);
+        ALLOC(m->ssq, (size_t)2 * m->grid * B);
+        // rows >= batch of the MMA tiles stay zero
+        if (cudaMemset(m->xfrag_a, 0, (size_t)D * 64) != cudaSuccess ||
+            cudaMemset(m->xfrag_f, 0, (size_t)D * 64) != cudaSuccess ||
+            cudaMemset(m->afrag, 0, (size_t)c.n_q_heads * c.d_head * 64) != cudaSuccess ||
+            cudaMemset(m->hfrag, 0, (size_t)c.d_inter * 64) != cudaSuccess)
+            return bail(fail(FFB_DEVICE, "cudaMemset failed"));
+    }
     ALLOC(m->q, (size_t)B * D);
     ALLOC(m->attn_out, (size_t)B * D);
     // per-CTA partials, or h = [B][DI] for the two-phase FFN
@@ -981,7 +1003,7 @@ ffb_status ffb_create_ex(const ffb_model_config* gcfg, int64_t max_seq_len, int 
     ALLOC(m->amax_idx, (size_t)m->grid * B);
     ALLOC(m->greedy, (size_t)B);
     ALLOC(m->tokens_dev, (size_t)B);
-    ALLOC(m->counters, (size_t)Lc * 5 + 1);
+    ALLOC(m->counters, (size_t)Lc * 5 + 2);
     ALLOC(m->head_counters, (size_t)Lc * units);
     ALLOC(m->qkv_head_counters, (size_t)Lc * c.n_kv_heads);
     ALLOC(m->amax_counter, 1);
@@ -1005,7 +1027,7 @@ ffb_status ffb_create_ex(const ffb_model_config* gcfg, int64_t max_seq_len, int 
     m->peer_xflag[tp_rank] = m->xflag;
     m->tp_connected = tp_size == 1;
 #undef ALLOC
-    if (cudaMemset(m->counters, 0, sizeof(uint32_t) * (Lc * 5 + 1)) != cudaSuccess ||
+    if (cudaMemset(m->counters, 0, sizeof(uint32_t) * (Lc * 5 + 2)) != cudaSuccess ||
         cudaMemset(m->head_counters, 0, sizeof(uint32_t) * Lc * units) != cudaSuccess ||
         cudaMemset(m->qkv_head_counters, 0, sizeof(uint32_t) * Lc * c.n_kv_heads) != cudaSuccess ||
         cudaMemset(m->amax_counter, 0, sizeof(uint32_t)) != cudaSuccess ||

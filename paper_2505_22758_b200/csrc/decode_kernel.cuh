@@ -243,16 +243,19 @@ struct RowMap {
     static constexpr int RPS = TC ? TC_ROWS : RG * RPT;  // rows per slot
     static constexpr int EWPR = S::KCP ? 1 : TC ? kNCW : WPR;  // per-row partials in the epilogue
     static constexpr int APT = RPS / RG;            // rows per thread per slot (CUDA-core AXPY)
-    // batch >= 8 (KCP): a weight slot holds RW rows x KC columns (row stride
-    // padded by 16 bytes: conflict-free ldmatrix), the activations of a
-    // chunk arrive as one slot of MMA A fragments (ATAB bytes); warps split
-    // the slot as RP row parts (two n8 tiles each) x KP k parts (8 k16 steps)
+    // batch >= 8 (KCP): matrices are stored chunk-major, [K / KC][rows][KC]
+    // with each row segment's 16-byte units XOR-swizzled by row & 7 (runtime
+    // packer, layout 2): a weight slot is one contiguous copy of RW rows x KC
+    // columns and the ldmatrix row reads are bank-conflict free.  The
+    // activations of a chunk arrive as one slot of MMA A fragments (ATAB
+    // bytes); warps split a weight slot as RP row parts (two n8 tiles each)
+    // x KP k parts (8 k16 steps each).
     static constexpr bool KCP = S::KCP;
     static constexpr int KC = S::KC;
     static constexpr int RW = KCP ? 16384 / KC : 1;
     static constexpr int NKC = KCP ? K / KC : 1;
     static constexpr int SEG = KC * 2;
-    static constexpr int WSTRIDE = SEG + 16;
+    static constexpr int WSTRIDE = SEG;
     static constexpr int ATAB = KC / 16 * 1024;
     static constexpr int RP = KCP ? RW / 16 : 1;
     static constexpr int KP = kNCW / RP;
@@ -322,7 +325,7 @@ struct KTraits : RowMap<S, S::D> {
     static constexpr int OFF_ROPE = OFF_H + SZ_H;  // [DH/2][2] f32
     static constexpr int SZ_ROPE = S::DH * 4;
     static constexpr int OFF_NORM = OFF_ROPE + SZ_ROPE;  // [NCW][B] f32
-    static constexpr int SZ_NORM = (NCW + 1) * S::B * 4 + 16;  // [NCW][B] partials + [B] (KCP inv)
+    static constexpr int SZ_NORM = ((NCW + 1) * S::B * 4 + 16 + 15) / 16 * 16;  // [NCW][B] partials + [B] (KCP inv)
     static constexpr int OFF_WPART = OFF_NORM + SZ_NORM;  // [NCW][QPG][DH+2] f32
     // also reused for: attention combine (3*G*QPG), argmax candidates
     // (2*grid*B) and the GLU reduction (NCW*32); grid <= kMaxGrid
@@ -346,6 +349,8 @@ struct KTraits : RowMap<S, S::D> {
                            cmax(2 * kMaxGrid * S::B, NCW * 32)),
                       SZ_ATT),
                  cmax(MD::TC ? S::D : 0, MA::TC ? S::AD : 0));  // TC activation strips
+    static_assert(OFF_H % 16 == 0 && OFF_NORM % 16 == 0 && OFF_WPART % 16 == 0,
+                  "16-byte aligned scratch (vector smem accesses)");
     static constexpr int OFF_AMAX = OFF_WPART + SZ_WPART;  // [NCT] (f32, i32)
     static constexpr int SZ_AMAX = NCT * 8;
     static constexpr int OFF_MISC = OFF_AMAX + SZ_AMAX;  // flags
@@ -498,26 +503,6 @@ struct DecodeCta {
         ++it;
     }
 
-    // KCP weight slot: n row segments of seg bytes (source stride sstride)
-    // at the padded slot stride MD::WSTRIDE
-    template <bool DRAIN>
-    __device__ void chunk_rows(uint32_t& it, const uint8_t* src, int n, uint32_t seg, size_t sstride,
-                               uint64_t policy) {
-        const uint32_t slot = it % T::NSLOTS, ph = (it / T::NSLOTS) & 1;
-        if (DRAIN) {
-            mbar_wait(&full[slot], ph);
-            __syncwarp();
-            if ((threadIdx.x & 31) == 0) mbar_arrive(&empty[slot]);
-        } else {
-            mbar_wait(&empty[slot], ph ^ 1);
-            mbar_arrive_expect_tx(&full[slot], n * seg);
-            uint8_t* dst = ring + slot * T::SLOT_BYTES;
-            for (int r = 0; r < n; ++r)
-                tma_load_1d(dst + r * MD::WSTRIDE, src + r * sstride, seg, &full[slot], policy);
-        }
-        ++it;
-    }
-
     // One list of the static per-CTA stream: rows [r0, r1) of a matrix (kv =
     // false) or KV positions [r0, r1) of one (layer, batch row, kv head).
     struct List {
@@ -530,6 +515,7 @@ struct DecodeCta {
         // slot, dependency-gated) then RW-row weight slots of the chunk
         const uint8_t* atab = nullptr;
         int nkc = 0;
+        int rows_total = 0;  // KCP: rows of the chunk-major matrix
     };
     // KCP rows per accumulator block: the chunk's A table stays in its slot
     // while the block's weight slots stream past it, so a block spans at
@@ -547,7 +533,7 @@ struct DecodeCta {
         if (stage == p.layers * kStagesPerLayer) {
             if (sub > 0) return false;
             L = {p.lm_head, pl.lm_r0, pl.lm_r1, false, false};
-            if constexpr (S::KCP) { L.atab = p.xfrag_f; L.nkc = MD::NKC; }
+            if constexpr (S::KCP) { L.atab = p.xfrag_f; L.nkc = MD::NKC; L.rows_total = p.vocab; }
             return true;
         }
         switch (s) {
@@ -555,7 +541,7 @@ struct DecodeCta {
                 if (sub > 0) return false;
                 L = {p.wqkv + (size_t)l * S::QKVR * T::ROW_BYTES, pl.qkv_r0, pl.qkv_r1, false,
                      false};
-                if constexpr (S::KCP) { L.atab = p.xfrag_f; L.nkc = MD::NKC; }
+                if constexpr (S::KCP) { L.atab = p.xfrag_f; L.nkc = MD::NKC; L.rows_total = S::QKVR; }
                 return true;
             case S_ATTN: {
                 if (sub > 0 || pl.attn_unit < 0) return false;
@@ -571,13 +557,13 @@ struct DecodeCta {
                 if (sub > 0) return false;
                 L = {p.waout + (size_t)l * D * MA::ROW_BYTES, pl.aout_r0, pl.aout_r1, false, false,
                      MA::ROW_BYTES, MA::RPS};
-                if constexpr (S::KCP) { L.atab = p.afrag; L.nkc = MA::NKC; }
+                if constexpr (S::KCP) { L.atab = p.afrag; L.nkc = MA::NKC; L.rows_total = D; }
                 return true;
             case S_GLU:
                 if (sub == 0) {
                     L = {p.wffn1 + (size_t)l * 2 * S::DI * T::ROW_BYTES, 2 * pl.glu_t0,
                          2 * pl.glu_t1, false, false};
-                    if constexpr (S::KCP) { L.atab = p.xfrag_a; L.nkc = MD::NKC; }
+                    if constexpr (S::KCP) { L.atab = p.xfrag_a; L.nkc = MD::NKC; L.rows_total = 2 * S::DI; }
                 }
                 else if (sub == 1 && !T::F2R)
                     L = {p.wffn2t + (size_t)l * S::DI * T::ROW_BYTES, pl.glu_t0, pl.glu_t1, false,
@@ -589,7 +575,7 @@ struct DecodeCta {
                 if (!T::F2R || sub > 0) return false;
                 L = {p.wffn2t + (size_t)l * D * MF::ROW_BYTES, pl.aout_r0, pl.aout_r1, false,
                      false, MF::ROW_BYTES, MF::RPS};
-                if constexpr (S::KCP) { L.atab = p.hfrag; L.nkc = MF::NKC; }
+                if constexpr (S::KCP) { L.atab = p.hfrag; L.nkc = MF::NKC; L.rows_total = D; }
                 return true;
             default:
                 return false;
@@ -602,7 +588,6 @@ struct DecodeCta {
         bool valid;
         List L;
         int kcc, kcj;  // KCP: chunk, slot within the chunk (-1: A table)
-        int out_rows;  // KCP: the emitted chunk is out_rows row segments (0: one copy)
         bool out_dep;  // the emitted chunk reads data of this stage's dependency
     };
 
@@ -634,7 +619,6 @@ struct DecodeCta {
                 continue;
             }
             *stage = c.stage;
-            c.out_rows = 0;
             c.out_dep = false;
             if (c.L.nkc > 0) {  // KCP
                 const int blk_end = min(c.c0 + KC_BLOCK, c.L.r1);
@@ -647,11 +631,10 @@ struct DecodeCta {
                     return true;
                 }
                 const int row0 = c.c0 + c.kcj * MD::RW;
-                if (row0 < blk_end) {
-                    *src0 = c.L.base + (size_t)row0 * c.L.row_bytes + (size_t)c.kcc * MD::SEG;
+                if (row0 < blk_end) {  // rows [row0, row0 + n) of chunk kcc: contiguous
+                    *src0 = c.L.base + ((size_t)c.kcc * c.L.rows_total + row0) * MD::SEG;
                     *src1 = nullptr;
-                    *bytes = MD::SEG;
-                    c.out_rows = min(MD::RW, blk_end - row0);
+                    *bytes = min(MD::RW, blk_end - row0) * MD::SEG;
                     ++c.kcj;
                     return true;
                 }
@@ -828,11 +811,6 @@ struct DecodeCta {
                     if (dependency(stage, &ctr, &target)) spin_until_geq(ctr, target);
                     fence_proxy_async_global();
                     dep_stage = stage;
-                }
-                if (c.out_rows > 0) {
-                    chunk_rows<DRAIN>(it, static_cast<const uint8_t*>(s0), c.out_rows, bytes,
-                                      c.L.row_bytes, policy);
-                    continue;
                 }
             }
             const int64_t need = s1 ? 2 * (int64_t)bytes : bytes;
@@ -1639,9 +1617,10 @@ struct DecodeCta {
         const int rp = warp % M::RP, kp = warp / M::RP;
         float* R = reinterpret_cast<float*>(smem + T::OFF_RED);  // [KP][RW][B]
         float* fin = R + M::KP * RW * B;                          // [RW][B]
-        // this lane's ldmatrix row (two n8 tiles x two k halves) in a weight slot
+        // this lane's ldmatrix row (two n8 tiles x two k halves) in a weight
+        // slot; 16-byte unit u of a row segment sits at u ^ (matrix row & 7)
         const int lrow = rp * 16 + (lane >> 4) * 8 + (lane & 7);
-        const int lcol = ((lane >> 3) & 1) * 16;
+        const int lhalf = (lane >> 3) & 1;
         for (int blk = r0; blk < r1; blk += KC_BLOCK) {
             const int blk_end = min(blk + KC_BLOCK, r1);
             const int nj = (blk_end - blk + RW - 1) / RW;
@@ -1662,14 +1641,14 @@ struct DecodeCta {
                     if (j < nj) {
                         const uint32_t sw = it % T::NSLOTS;
                         wait_full(sw, (it / T::NSLOTS) & 1);
-                        const uint8_t* wrow =
-                            ring + sw * T::SLOT_BYTES + lrow * M::WSTRIDE + kp * 8 * 32 + lcol;
+                        const uint8_t* wrow = ring + sw * T::SLOT_BYTES + lrow * M::SEG;
+                        const int key = (blk + j * RW + lrow) & 7;
 #pragma unroll
                         for (int ks = 0; ks < 8; ++ks) {
                             const uint4 ah = lds_u128(atab + ks * 1024);
                             const uint4 al = lds_u128(atab + ks * 1024 + 16);
                             uint32_t b0, b1, b2, b3;
-                            ldsm_x4(wrow + ks * 32, b0, b1, b2, b3);
+                            ldsm_x4(wrow + ((((kp * 8 + ks) * 2 + lhalf) ^ key) << 4), b0, b1, b2, b3);
                             b0 = bf2_to_h2(b0);
                             b1 = bf2_to_h2(b1);
                             b2 = bf2_to_h2(b2);

@@ -17,6 +17,7 @@ struct KernelOps {
     int threads, smem, nslots, slot_bytes, rg, tmax, kvc, rps, row_bytes, row_bytes_a;
     int tc_d, tc_a;  // d_model-column / Waout rows use the tensor-core code order
     int ffn2_rows;   // W2 stored [D][DI] (two-phase FFN, KTraits::F2R), else Wffn2^T
+    int kc;          // batch >= 8: K-chunk width of the chunk-major matrix layout (0: row-major)
     cudaError_t (*prepare)();
     cudaError_t (*launch)(const DecodeParams&, int grid, cudaStream_t, bool cooperative);
 };
@@ -50,7 +51,7 @@ KernelOps make_ops() {
     return KernelOps{S::D,        S::DI,         S::DH,     S::NQ,         S::NKV, S::B,
                      S::QB,       T::NTHREADS,   T::SMEM_BYTES, T::NSLOTS, T::SLOT_BYTES,
                      T::RG,       T::TMAX,       T::KVC,    T::RPS,        T::ROW_BYTES,
-                     T::MA::ROW_BYTES, T::MD::TC ? 1 : 0, T::MA::TC ? 1 : 0, T::F2R ? 1 : 0,
+                     T::MA::ROW_BYTES, T::MD::TC ? 1 : 0, T::MA::TC ? 1 : 0, T::F2R ? 1 : 0, S::KCP ? S::KC : 0,
                      &prepare_impl<S>, &launch_impl<S>};
 }
 

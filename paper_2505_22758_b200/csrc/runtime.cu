@@ -1065,7 +1065,7 @@ ffb_status ffb_upload_tensor(ffb_model* m, const char* name, const float* values
         return FFB_OK;
     }
     // the shard's rows / columns as one contiguous f32 block (no copy at TP 1)
-    const int64_t lrows = d.local_rows(), cols = d.cols;
+    int64_t lrows = d.local_rows(), cols = d.cols;
     std::vector<float> shard;
     const float* src = values;
     if (d.rows.size() != 1 || d.rows[0].first != 0 || d.cols != d.gcols) {
@@ -1086,6 +1086,22 @@ ffb_status ffb_upload_tensor(ffb_model* m, const char* name, const float* values
                     for (int64_t k = k0; k < std::min(cols, k0 + TB); ++k)
                         tr[(size_t)k * lrows + r] = src[(size_t)r * cols + k];
         shard.swap(tr);
+        src = shard.data();
+        std::swap(lrows, cols);
+    }
+    if (d.kind == 0 && m->ops->kc > 0) {
+        // batch >= 8: chunk-major [cols / KC][rows][KC], the 8-column units of
+        // each row segment XOR-swizzled by row & 7 (decode_kernel.cuh: gemv_kc)
+        const int64_t KC = m->ops->kc, nch = cols / KC;
+        std::vector<float> cm((size_t)lrows * cols);
+        for (int64_t r = 0; r < lrows; ++r)
+            for (int64_t c = 0; c < nch; ++c) {
+                float* dst = cm.data() + ((size_t)c * lrows + r) * KC;
+                const float* s0 = src + (size_t)r * cols + c * KC;
+                for (int64_t u = 0; u < KC / 8; ++u)
+                    std::memcpy(dst + ((u ^ (r & 7)) * 8), s0 + u * 8, sizeof(float) * 8);
+            }
+        shard.swap(cm);
         src = shard.data();
     }
     if (d.kind == 0 && m->ops->QB != 0) {  // quant packer, a block of rows at a time

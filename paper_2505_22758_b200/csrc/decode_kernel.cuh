@@ -144,7 +144,7 @@ struct DecodeParams {
     float eps;
     double rope_theta;
     // batch >= 8 (Shape::KCP): every GEMV input as MMA A-fragment tables,
-    // [K/16 k-steps][32 lanes][4 x f16x2 hi | 4 x f16x2 lo] (1 KiB per
+    // [K/16 k-steps][hi | lo][32 lanes][4 x f16x2] (1 KiB per
     // k-step; frag_off), written by the producing stage's epilogue and
     // streamed into the ring by TMA one K chunk at a time.  The RMSNorm
     // scale is factored out: tables hold x * gain, the GEMV result is
@@ -1538,30 +1538,24 @@ struct DecodeCta {
     // A-fragment table offset of activation column k, batch row b (m16n8k16
     // row-major A: lane (g, q) holds rows g / g + 8, columns 2q, 2q + 1 and
     // 2q + 8, 2q + 9 of each k16 step; registers a0..a3 = (g, lo k), (g + 8,
-    // lo k), (g, hi k), (g + 8, hi k)); the lo part is 16 bytes further.
+    // lo k), (g, hi k), (g + 8, hi k)); per k-step the 32 lanes' hi parts
+    // (16 bytes each, conflict-free LDS.128) then the lo parts.
     __device__ static size_t frag_off(int k, int b) {
         const int kst = k >> 4, kk = k & 15;
         const int lane = (b & 7) * 4 + ((kk & 7) >> 1);
         const int reg = (kk >> 3) * 2 + (b >> 3);
-        return (size_t)kst * 1024 + lane * 32 + reg * 4 + (kk & 1) * 2;
+        return (size_t)kst * 1024 + lane * 16 + reg * 4 + (kk & 1) * 2;
     }
     // v as fp16 hi + lo (22 bits of mantissa, as the quant tensor-core
     // GEMV's activations; bf16 hi + lo would carry 16 and measurably move
-    // the logits); the bf16 weights are widened to fp16 exactly in gemv_kc
+    // the logits); the bf16 weights are stored as fp16 by the packer
     __device__ static void frag_put(uint8_t* tab, int k, int b, float v) {
         const __half hi = __float2half_rn(v);
         const __half lo = __float2half_rn(v - __half2float(hi));
         uint8_t* d = tab + frag_off(k, b);
         *reinterpret_cast<__half*>(d) = hi;
-        *reinterpret_cast<__half*>(d + 16) = lo;
+        *reinterpret_cast<__half*>(d + 512) = lo;
     }
-    // bf16x2 -> fp16x2 (exact for |w| in the fp16 normal range; bf16
-    // weights below 2^-14 keep 2^-24 absolute precision)
-    __device__ static uint32_t bf2_to_h2(uint32_t w) {
-        const __half2 h = __floats2half2_rn(__uint_as_float(w << 16), __uint_as_float(w & 0xffff0000u));
-        return *reinterpret_cast<const uint32_t*>(&h);
-    }
-
     // After this CTA updated x rows [c0, c1): their A-table entries x * gain
     // and this CTA's per-batch-row sum of squares (ssq_out[cta][b]).  Ends
     // with a proxy fence: the tables are read by TMA (async proxy).
@@ -1634,7 +1628,7 @@ struct DecodeCta {
             for (int c = 0; c < M::NKC; ++c) {
                 const uint32_t sa = it % T::NSLOTS;
                 wait_full(sa, (it / T::NSLOTS) & 1);
-                const uint8_t* atab = ring + sa * T::SLOT_BYTES + kp * 8 * 1024 + lane * 32;
+                const uint8_t* atab = ring + sa * T::SLOT_BYTES + kp * 8 * 1024 + lane * 16;
                 ++it;
 #pragma unroll
                 for (int j = 0; j < NJ; ++j) {
@@ -1646,13 +1640,9 @@ struct DecodeCta {
 #pragma unroll
                         for (int ks = 0; ks < 8; ++ks) {
                             const uint4 ah = lds_u128(atab + ks * 1024);
-                            const uint4 al = lds_u128(atab + ks * 1024 + 16);
+                            const uint4 al = lds_u128(atab + ks * 1024 + 512);
                             uint32_t b0, b1, b2, b3;
                             ldsm_x4(wrow + ((((kp * 8 + ks) * 2 + lhalf) ^ key) << 4), b0, b1, b2, b3);
-                            b0 = bf2_to_h2(b0);
-                            b1 = bf2_to_h2(b1);
-                            b2 = bf2_to_h2(b2);
-                            b3 = bf2_to_h2(b3);
                             mma_f16(acc[j][0], ah.x, ah.y, ah.z, ah.w, b0, b1);
                             mma_f16(acc[j][1], ah.x, ah.y, ah.z, ah.w, b2, b3);
                             mma_f16(acc[j][0], al.x, al.y, al.z, al.w, b0, b1);

@@ -148,6 +148,25 @@ __global__ void synth_bf16_kernel(__nv_bfloat16* dst, int64_t n, uint64_t seed, 
     }
 }
 
+// the same bf16 values held as fp16 (batch >= 8 matrix layout, see upload)
+__global__ void synth_bf16_as_f16_kernel(__half* dst, int64_t n, uint64_t seed, float stddev) {
+    const float a = stddev * 1.7320508f;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const uint64_t r = splitmix(seed ^ (static_cast<uint64_t>(i) * 0xd1b54a32d192ed03ull));
+        const float u = static_cast<float>(r >> 40) * (1.0f / 16777216.0f);  // [0,1)
+        dst[i] = __float2half_rn(__bfloat162float(__float2bfloat16_rn((2.0f * u - 1.0f) * a)));
+    }
+}
+
+// bf16-rounded f32 -> fp16 (exact for |v| >= 2^-14; 2^-24 absolute below)
+__global__ void f32_to_bf16_as_f16_kernel(const float* __restrict__ src, __half* __restrict__ dst,
+                                          int64_t n) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        dst[i] = __float2half_rn(__bfloat162float(__float2bfloat16_rn(src[i])));
+}
+
 // synthetic packed quant rows (decode_kernel.cuh weight formats): random
 // codes, scale = 2 sqrt(3) stddev / levels (jittered), zero = levels / 2
 __global__ void synth_quant_kernel(uint8_t* dst, int64_t rows, int cols, int qb, int row_bytes,
@@ -1091,7 +1110,9 @@ ffb_status ffb_upload_tensor(ffb_model* m, const char* name, const float* values
     }
     if (d.kind == 0 && m->ops->kc > 0) {
         // batch >= 8: chunk-major [cols / KC][rows][KC], the 8-column units of
-        // each row segment XOR-swizzled by row & 7 (decode_kernel.cuh: gemv_kc)
+        // each row segment XOR-swizzled by row & 7 (decode_kernel.cuh: gemv_kc);
+        // the bf16 values are stored as fp16 (exact in the fp16 normal range,
+        // 2^-24 absolute below it), the tensor-core GEMV's operand type
         const int64_t KC = m->ops->kc, nch = cols / KC;
         std::vector<float> cm((size_t)lrows * cols);
         for (int64_t r = 0; r < lrows; ++r)
@@ -1125,7 +1146,11 @@ ffb_status ffb_upload_tensor(ffb_model* m, const char* name, const float* values
         const int64_t cnt = std::min<int64_t>(ffb_model::kStagingElems, ln - off);
         CUDA_TRY(cudaMemcpyAsync(m->staging, src + off, sizeof(float) * cnt,
                                  cudaMemcpyHostToDevice, m->stream));
-        f32_to_bf16_kernel<<<1184, 256, 0, m->stream>>>(m->staging, dst + off, cnt);
+        if (d.kind == 0 && m->ops->kc > 0)
+            f32_to_bf16_as_f16_kernel<<<1184, 256, 0, m->stream>>>(
+                m->staging, reinterpret_cast<__half*>(dst) + off, cnt);
+        else
+            f32_to_bf16_kernel<<<1184, 256, 0, m->stream>>>(m->staging, dst + off, cnt);
         CUDA_TRY(cudaGetLastError());
         CUDA_TRY(cudaStreamSynchronize(m->stream));  // staging reused
     }
@@ -1161,7 +1186,10 @@ ffb_status ffb_init_synthetic(ffb_model* m, uint64_t seed) {
     // (TP shards draw their own matrices; embedding and norms are replicated)
     const uint64_t rs = 0x9e37ull * static_cast<uint64_t>(m->tp_rank);
     auto mat = [&](uint8_t* p, int64_t rows, int64_t cols, size_t rb, uint64_t s, float stddev) {
-        if (m->ops->QB == 0) {
+        if (m->ops->kc > 0) {
+            synth_bf16_as_f16_kernel<<<4096, 256, 0, m->stream>>>(
+                reinterpret_cast<__half*>(p), rows * cols, seed * 1315423911ull + s + rs, stddev);
+        } else if (m->ops->QB == 0) {
             bf(reinterpret_cast<__nv_bfloat16*>(p), rows * cols, s + rs, stddev);
         } else {
             synth_quant_kernel<<<4096, 256, 0, m->stream>>>(

@@ -31,6 +31,8 @@ CONFIGS = [  # tag, model, ctx, batch, quant, tp
     ("E-b1", "llama31_8b", 4096, 1, 0, 1),
     ("E-b2", "llama31_8b", 4096, 2, 0, 1),
     ("E-b4", "llama31_8b", 4096, 4, 0, 1),
+    ("E-b8", "llama31_8b", 4096, 8, 0, 1),
+    ("E-b16", "llama31_8b", 4096, 16, 0, 1),
     ("Q-int8", "llama31_8b", 4096, 1, 8, 1),
     ("Q-int4", "llama31_8b", 4096, 1, 4, 1),
     ("H-tp1", "llama31_70b", 4096, 1, 0, 1),

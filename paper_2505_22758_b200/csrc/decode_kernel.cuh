@@ -321,12 +321,14 @@ struct KTraits : RowMap<S, S::D> {
     static constexpr int OFF_RED = 0;  // [2][WPR][RB][B] f32 (largest row map)
     static constexpr int SZ_RED = 2 * RED_FLOATS * 4;
     static constexpr int OFF_H = OFF_RED + SZ_RED;  // [B][TMAX] f32
-    static constexpr int SZ_H = S::B * TMAX * 4;
+    // [B][TMAX] f32 (GLU h slice, S_AOUT / S_RED row results); batch >= 8
+    // only stages the current token's K and V rows (attention)
+    static constexpr int SZ_H = S::KCP ? (4 * S::DH + 15) / 16 * 16 : S::B * TMAX * 4;
     static constexpr int OFF_ROPE = OFF_H + SZ_H;  // [DH/2][2] f32
     static constexpr int SZ_ROPE = S::DH * 4;
     static constexpr int OFF_NORM = OFF_ROPE + SZ_ROPE;  // [NCW][B] f32
     static constexpr int SZ_NORM = ((NCW + 1) * S::B * 4 + 16 + 15) / 16 * 16;  // [NCW][B] partials + [B] (KCP inv)
-    static constexpr int OFF_WPART = OFF_NORM + SZ_NORM;  // [NCW][QPG][DH+2] f32
+    static constexpr int OFF_WPART = OFF_NORM + SZ_NORM;  // attention scratch, f32
     // also reused for: attention combine (3*G*QPG), argmax candidates
     // (2*grid*B) and the GLU reduction (NCW*32); grid <= kMaxGrid
     static constexpr int kMaxGrid = 160;
@@ -345,8 +347,10 @@ struct KTraits : RowMap<S, S::D> {
     // hi/lo MMA rows [16][ANP] (tensor-core P.V), stats [QPG][4]
     static constexpr int SZ_ATT = S::QPG * S::DH + S::QPG * ANP + cmax(S::QPG, 8) * ANP + 4 * S::QPG;
     static constexpr int SZ_WPART =
-        4 * cmax(cmax(cmax(cmax(NCW * S::QPG * (S::DH + 2), 3 * kMaxGrid * S::QPG),
-                           cmax(2 * kMaxGrid * S::B, NCW * 32)),
+        4 * cmax(cmax(cmax(cmax(S::QPG * S::DH, 3 * kMaxGrid * S::QPG),
+                           // argmax candidates (batch >= 8: in the drained
+                           // ring), S_RED scratch + TP delta, TP exchange rows
+                           cmax(S::KCP ? 0 : 2 * kMaxGrid * S::B, NCW * 32 + S::B * TMAX)),
                       SZ_ATT),
                  cmax(MD::TC ? S::D : 0, MA::TC ? S::AD : 0));  // TC activation strips
     static_assert(OFF_H % 16 == 0 && OFF_NORM % 16 == 0 && OFF_WPART % 16 == 0,
@@ -2255,7 +2259,12 @@ struct DecodeCta {
                      pl.aout_r1, [&](int c0, int nrows, const float* red) {
             if (ctid < nrows * B) {
                 const int r = ctid / B, b = ctid % B;
-                acc[b * T::TMAX + c0 - r0 + r] = row_total<MA>(red, r, b);
+                if constexpr (S::KCP) {  // (no TP at batch >= 8) x rows owned: update now
+                    float* xp = p.x + (size_t)b * D + c0 + r;
+                    __stcg(xp, ldcg_f(xp) + row_total<MA>(red, r, b));
+                } else {
+                    acc[b * T::TMAX + c0 - r0 + r] = row_total<MA>(red, r, b);
+                }
             }
         });
         consumer_sync(NCT);
@@ -2267,16 +2276,14 @@ struct DecodeCta {
             }
             consumer_sync(NCT);
             tp_exchange_add(d, r0, nr, 0, l);
+        } else if constexpr (S::KCP) {  // x already updated: S_GLU's A table and norm statistics
+            kc_publish(r0, pl.aout_r1, p.norm_ffn + (size_t)l * D, p.xfrag_a, p.ssq);
         } else {
             for (int i = ctid; i < nr * B; i += NCT) {  // one L2 round trip for all rows
                 const int r = i / B, b = i % B;
                 float* xp = p.x + (size_t)b * D + r0 + r;
                 __stcg(xp, ldcg_f(xp) + acc[b * T::TMAX + r]);
             }
-        }
-        if constexpr (S::KCP) {  // S_GLU's A table and norm statistics
-            consumer_sync(NCT);
-            kc_publish(r0, pl.aout_r1, p.norm_ffn + (size_t)l * D, p.xfrag_a, p.ssq);
         }
         arrive(p.counters + l * kStagesPerLayer + S_AOUT, l * kStagesPerLayer + S_AOUT);
     }
@@ -2473,7 +2480,12 @@ struct DecodeCta {
                      pl.aout_r1, [&](int c0, int nrows, const float* red) {
             if (ctid < nrows * B) {
                 const int r = ctid / B, b = ctid % B;
-                acc[b * T::TMAX + c0 - r0 + r] = row_total<MF>(red, r, b);
+                if constexpr (S::KCP) {  // (no TP at batch >= 8) x rows owned: update now
+                    float* xp = p.x + (size_t)b * D + c0 + r;
+                    __stcg(xp, ldcg_f(xp) + row_total<MF>(red, r, b));
+                } else {
+                    acc[b * T::TMAX + c0 - r0 + r] = row_total<MF>(red, r, b);
+                }
             }
         });
         consumer_sync(NCT);
@@ -2485,18 +2497,16 @@ struct DecodeCta {
             }
             consumer_sync(NCT);
             tp_exchange_add(d, r0, nr, 1, l);
+        } else if constexpr (S::KCP) {  // x already updated: next S_QKV's (or the LM head's) A table
+            kc_publish(r0, pl.aout_r1,
+                       l + 1 < p.layers ? p.norm_attn + (size_t)(l + 1) * D : p.final_norm,
+                       p.xfrag_f, p.ssq + (size_t)grid * B);
         } else {
             for (int i = ctid; i < nr * B; i += NCT) {
                 const int r = i / B, b = i % B;
                 float* xp = p.x + (size_t)b * D + r0 + r;
                 __stcg(xp, ldcg_f(xp) + acc[b * T::TMAX + r]);
             }
-        }
-        if constexpr (S::KCP) {  // next S_QKV's (or the LM head's) A table
-            consumer_sync(NCT);
-            kc_publish(r0, pl.aout_r1,
-                       l + 1 < p.layers ? p.norm_attn + (size_t)(l + 1) * D : p.final_norm,
-                       p.xfrag_f, p.ssq + (size_t)grid * B);
         }
         arrive(p.counters + l * kStagesPerLayer + S_RED, l * kStagesPerLayer + S_RED);
     }
@@ -2597,7 +2607,8 @@ struct DecodeCta {
         if (flag[1]) {
             // all CTA candidates into smem in one parallel pass, then scan in
             // CTA (= ascending row) order
-            float* cv = wpart();
+            // (batch >= 8: the ring, drained after the last stage's GEMV)
+            float* cv = S::KCP ? reinterpret_cast<float*>(ring) : wpart();
             int* ci = reinterpret_cast<int*>(cv + grid * B);
             for (int i = ctid; i < grid * B; i += NCT) {
                 cv[i] = ldcg_f(p.amax_val + i);

@@ -27,6 +27,20 @@ def test_toy_batch_rows_match_oracle(batch, prefill):
     print(f"toy b{batch} prefill {prefill}: rel_err {e_plain:.2e}, same-KV {e_strict:.2e}, flips {flips}")
 
 
+@pytest.mark.parametrize("dims", [(512, 2048, 64, 8, 2), (2048, 2048, 64, 32, 8)])
+def test_small_512_column_chunks_match_oracle(dims):
+    """The 8B geometry (512-column K chunks, 4 k parts per weight slot) at
+    small width; (2048, .., 8 kv heads) also runs one CTA per (row, kv head)
+    in the attention (128 units, split-K group 1)."""
+    d, di, dh, nq, nkv = dims
+    cfg = O.ModelCfg(2, d, di, dh, nq, nkv, 1024).replace(batch=16)
+    st = O.OracleStore(cfg, 3, 70)
+    st.synthetic_prefill(64, 1)
+    with device_from_store(st) as m:
+        e_plain, e_strict, flips = check_step(st, m, TOKENS, 64)
+    print(f"{dims} b16: rel_err {e_plain:.2e}, same-KV {e_strict:.2e}, flips {flips}")
+
+
 def test_toy_batch16_modes_bit_identical_multi_step():
     outs = []
     for mode in MODES:

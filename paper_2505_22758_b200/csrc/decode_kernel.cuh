@@ -345,7 +345,20 @@ struct KTraits : RowMap<S, S::D> {
     static constexpr int ANP = ((ATT_SC * KVC + 1) + 15) / 16 * 16;
     // alpha*q f32 [QPG][DH], scores f32 [QPG][ANP], probabilities as bf16
     // hi/lo MMA rows [16][ANP] (tensor-core P.V), stats [QPG][4]
-    static constexpr int SZ_ATT = S::QPG * S::DH + S::QPG * ANP + cmax(S::QPG, 8) * ANP + 4 * S::QPG;
+    // per-warp attention (ATT_WARP): alpha*q [QPG][DH], then per warp (m, l)
+    // [NCW][QPG][2] and O [NCW][QPG][DH] for the CTA merge.  Same-box A/B
+    // against the three-barrier passes (attn_pass_tc), ms/step: 8B b16 8.18
+    // -> 7.37, b4 3.93 -> 3.76, b2 3.11 -> 3.10, 1B b1 0.639 -> 0.629, but
+    // 8B b1 (one ~230-position pass per CTA) 2.700 -> 2.748: kept on passes.
+    // QPG = 8 (70B) would need 32 KiB of merge scratch: passes.
+#ifdef FFB_ATT_PASS
+    static constexpr bool ATT_WARP = false;
+#else
+    static constexpr bool ATT_WARP = S::QPG <= 4 && (S::B > 1 || S::D < 4096);
+#endif
+    static constexpr int SZ_ATT = ATT_WARP
+        ? S::QPG * S::DH + 2 * NCW * S::QPG + NCW * S::QPG * S::DH
+        : S::QPG * S::DH + S::QPG * ANP + cmax(S::QPG, 8) * ANP + 4 * S::QPG;
     static constexpr int SZ_WPART =
         4 * cmax(cmax(cmax(cmax(S::QPG * S::DH, 3 * kMaxGrid * S::QPG),
                            // argmax candidates (batch >= 8: in the drained
@@ -2029,6 +2042,197 @@ struct DecodeCta {
         consumer_sync(NCT);  // sc / pt / stats reusable by the next pass
     }
 
+    // ---- per-warp flash decoding (T::ATT_WARP) -------------------------
+    // Every warp runs its own online softmax over the 16-position tiles
+    // t = warp, warp + NCW, ... of each pass (no CTA barrier per pass):
+    // S[head row][pos] = (alpha q as A: rows = heads hi / lo) x (K rows as B,
+    // ldmatrix), folded hi + lo, exp2 against the warp's running max; the
+    // score accumulators are re-packed in registers as the A operand (P
+    // hi / lo rows) of O += P V (V tiles as B, ldmatrix.trans).  At the end
+    // the NCW warp states are merged in smem (attn_warp_merge).
+    struct WarpAtt {
+        uint32_t qa[DH / 16][4];  // A fragments of alpha * log2e * q (bf16 hi / lo rows)
+        float o[DH / 8][4];       // O accumulators: rows g (and g + 8) x dims
+        float m, l;               // running max / sum of the head of row g
+    };
+
+    __device__ void attn_warp_init(WarpAtt& w) {
+        const int lane = threadIdx.x % 32, g = lane / 4, q4 = lane % 4;
+        const float* qs = att_q();
+#pragma unroll
+        for (int kk = 0; kk < DH / 16; ++kk)
+#pragma unroll
+            for (int r = 0; r < 4; ++r) {
+                const int row = g + 8 * (r & 1), d = kk * 16 + 2 * q4 + 8 * (r >> 1);
+                uint32_t v = 0u;
+                if (row < 2 * QPG) {
+                    const int h = row % QPG;
+                    const float x0 = qs[h * DH + d], x1 = qs[h * DH + d + 1];
+                    if (row >= QPG) {
+                        const float h0 = __bfloat162float(__float2bfloat16_rn(x0));
+                        const float h1 = __bfloat162float(__float2bfloat16_rn(x1));
+                        v = bf2_pack(x0 - h0, x1 - h1);
+                    } else {
+                        v = bf2_pack(x0, x1);
+                    }
+                }
+                w.qa[kk][r] = v;
+            }
+#pragma unroll
+        for (int c = 0; c < DH / 8; ++c)
+#pragma unroll
+            for (int e = 0; e < 4; ++e) w.o[c][e] = 0.f;
+        w.m = -INFINITY;
+        w.l = 0.f;
+    }
+
+    // this warp's tiles of one pass: positions [0, n) of the pass (ring rows
+    // j < nring, the current token at j == nring), pass start pos0
+    __device__ void attn_warp_pass(WarpAtt& w, uint32_t it0, int nring, int n, int pos0) {
+        const int warp = threadIdx.x / 32, lane = threadIdx.x % 32, g = lane / 4, q4 = lane % 4;
+        const int ntiles = (n + 15) / 16;
+        for (int t = warp; t < ntiles; t += NCW) {
+            const int tb = t * 16;
+            // scores: 2 n8 tiles of positions, K rows via ldmatrix (non-trans)
+            float sc[2][4];
+#pragma unroll
+            for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+                for (int e = 0; e < 4; ++e) sc[nt][e] = 0.f;
+            {
+                const int jr = min(tb + (lane & 7) + 8 * (lane >> 4), n - 1);
+                const uint8_t* krow = att_row(it0, jr, nring, 0);
+                const int key = (pos0 + jr) & 7, kh = (lane >> 3) & 1;
+#pragma unroll
+                for (int kk = 0; kk < DH / 16; ++kk) {
+                    uint32_t b0, b1, b2, b3;
+                    ldsm_x4(krow + (((2 * kk + kh) ^ key) << 4), b0, b1, b2, b3);
+                    mma_bf16(sc[0], w.qa[kk][0], w.qa[kk][1], w.qa[kk][2], w.qa[kk][3], b0, b1);
+                    mma_bf16(sc[1], w.qa[kk][0], w.qa[kk][1], w.qa[kk][2], w.qa[kk][3], b2, b3);
+                }
+            }
+            // fold hi + lo rows -> the score of row g's head; mask past n
+            float f[2][2];
+#pragma unroll
+            for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+                for (int e = 0; e < 2; ++e) {
+                    float v;
+                    if constexpr (QPG == 8) v = sc[nt][e] + sc[nt][e + 2];
+                    else v = sc[nt][e] + __shfl_xor_sync(0xffffffffu, sc[nt][e], 4 * QPG);
+                    f[nt][e] = tb + nt * 8 + 2 * q4 + e < n ? v : -INFINITY;
+                }
+            float mx = fmaxf(fmaxf(f[0][0], f[0][1]), fmaxf(f[1][0], f[1][1]));
+            mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
+            mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
+            const float m_new = fmaxf(w.m, mx);
+            const float scale = exp2f(w.m - m_new);  // 0 on the first tile
+            float pv[2][2], ps = 0.f;
+#pragma unroll
+            for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+                for (int e = 0; e < 2; ++e) {
+                    pv[nt][e] = exp2f(f[nt][e] - m_new);
+                    ps += pv[nt][e];
+                }
+            ps += __shfl_xor_sync(0xffffffffu, ps, 1);
+            ps += __shfl_xor_sync(0xffffffffu, ps, 2);
+            w.m = m_new;
+            w.l = w.l * scale + ps;
+#pragma unroll
+            for (int c = 0; c < DH / 8; ++c)
+#pragma unroll
+                for (int e = 0; e < 4; ++e) w.o[c][e] *= scale;
+            // P as A fragments: row g = P hi (g < QPG) / P lo (QPG <= g < 2 QPG);
+            // QPG = 8: rows g hi, g + 8 lo
+            uint32_t pa[4];
+            {
+                auto hi2 = [](float a, float b) { return bf2_pack(__bfloat162float(__float2bfloat16_rn(a)),
+                                                                   __bfloat162float(__float2bfloat16_rn(b))); };
+                auto lo2 = [](float a, float b) {
+                    return bf2_pack(a - __bfloat162float(__float2bfloat16_rn(a)),
+                                    b - __bfloat162float(__float2bfloat16_rn(b)));
+                };
+                if constexpr (QPG == 8) {
+                    pa[0] = hi2(pv[0][0], pv[0][1]);
+                    pa[1] = lo2(pv[0][0], pv[0][1]);
+                    pa[2] = hi2(pv[1][0], pv[1][1]);
+                    pa[3] = lo2(pv[1][0], pv[1][1]);
+                } else {
+                    const bool lo_row = g >= QPG, live = g < 2 * QPG;
+                    pa[0] = !live ? 0u : lo_row ? lo2(pv[0][0], pv[0][1]) : hi2(pv[0][0], pv[0][1]);
+                    pa[2] = !live ? 0u : lo_row ? lo2(pv[1][0], pv[1][1]) : hi2(pv[1][0], pv[1][1]);
+                    pa[1] = 0u;
+                    pa[3] = 0u;
+                }
+            }
+            // O += P V: V rows of the tile via ldmatrix.trans, 16 dims per x4
+            {
+                const int jr = min(tb + (lane & 7) + 8 * ((lane >> 3) & 1), n - 1);
+                const uint8_t* vrow = att_row(it0, jr, nring, 1);
+                const int key = (pos0 + jr) & 7;
+#pragma unroll
+                for (int c = 0; c < DH / 16; ++c) {
+                    uint32_t b00, b01, b10, b11;
+                    ldsm_x4_t(vrow + (((2 * c + (lane >> 4)) ^ key) << 4), b00, b01, b10, b11);
+                    mma_bf16(w.o[2 * c], pa[0], pa[1], pa[2], pa[3], b00, b01);
+                    mma_bf16(w.o[2 * c + 1], pa[0], pa[1], pa[2], pa[3], b10, b11);
+                }
+            }
+        }
+    }
+
+    // merge the NCW warp states -> ro [QPG][DH] (unnormalised O), mlc [QPG][2]
+    // (max, sum): the same CTA partial the pass path produces
+    __device__ void attn_warp_merge(const WarpAtt& w, float* ro, float* mlc) {
+        const int ctid = threadIdx.x, warp = ctid / 32, lane = ctid % 32, g = lane / 4, q4 = lane % 4;
+        float* wml = att_q() + QPG * DH;        // [NCW][QPG][2]
+        float* wo = wml + 2 * NCW * QPG;        // [NCW][QPG][DH]
+        float ov[DH / 8][2];
+#pragma unroll
+        for (int c = 0; c < DH / 8; ++c)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                if constexpr (QPG == 8) ov[c][e] = w.o[c][e] + w.o[c][e + 2];
+                else ov[c][e] = w.o[c][e] + __shfl_xor_sync(0xffffffffu, w.o[c][e], 4 * QPG);
+            }
+        if (g < QPG) {
+            float* dst = wo + (warp * QPG + g) * DH;
+#pragma unroll
+            for (int c = 0; c < DH / 8; ++c)
+#pragma unroll
+                for (int e = 0; e < 2; ++e) dst[c * 8 + 2 * q4 + e] = ov[c][e];
+            if (q4 == 0) {
+                wml[(warp * QPG + g) * 2] = w.m;
+                wml[(warp * QPG + g) * 2 + 1] = w.l;
+            }
+        }
+        consumer_sync(NCT);
+        for (int idx = ctid; idx < QPG * DH; idx += NCT) {
+            const int h = idx / DH, d = idx % DH;
+            float M = -INFINITY;
+#pragma unroll
+            for (int v = 0; v < NCW; ++v)
+                if (wml[(v * QPG + h) * 2 + 1] > 0.f) M = fmaxf(M, wml[(v * QPG + h) * 2]);
+            float O = 0.f, L = 0.f;
+#pragma unroll
+            for (int v = 0; v < NCW; ++v) {
+                const float lv = wml[(v * QPG + h) * 2 + 1];
+                if (lv > 0.f) {
+                    const float r = exp2f(wml[(v * QPG + h) * 2] - M);
+                    O += r * wo[(v * QPG + h) * DH + d];
+                    L += r * lv;
+                }
+            }
+            ro[idx] = O;
+            if (d == 0) {
+                mlc[2 * h] = M;
+                mlc[2 * h + 1] = L;
+            }
+        }
+        consumer_sync(NCT);
+    }
+
     __device__ void stage_attn(uint32_t& it, int l) {
         if (pl.attn_unit < 0) return;  // idle CTA: no chunks were streamed
         const int ctid = threadIdx.x, warp = ctid / 32, lane = ctid % 32;
@@ -2037,8 +2241,8 @@ struct DecodeCta {
         attn_range(p0, p1);
         const int past_end = max(p0, min(p1, p.pos));
         const bool has_cur = p.pos >= p0 && p.pos < p1;
-        float* st = att_st();
-        if (ctid < QPG) {
+        float* st = att_st();  // (pass path only: outside the per-warp path's scratch)
+        if (!T::ATT_WARP && ctid < QPG) {
             st[ctid * 4 + 0] = -INFINITY;
             st[ctid * 4 + 1] = 0.f;
             st[ctid * 4 + 2] = 0.f;
@@ -2063,62 +2267,86 @@ struct DecodeCta {
                 }
             }
         }
-        float o[NTW][4];
-#pragma unroll
-        for (int nt = 0; nt < NTW; ++nt)
-#pragma unroll
-            for (int e = 0; e < 4; ++e) o[nt][e] = 0.f;
-        consumer_sync(NCT);
-        trace_mark(l * kStagesPerLayer + S_ATTN, 5);
-
-        constexpr int PASS = T::ATT_SC * T::KVC;
-        for (int c0 = p0; c0 < past_end || (c0 == p0 && has_cur); c0 += PASS) {
-            const int nring = min(PASS, past_end - c0);
-            const int nslots = (nring + T::KVC - 1) / T::KVC;
-            const bool last = c0 + PASS >= past_end;
-            const int n = nring + ((last && has_cur) ? 1 : 0);
-            const uint32_t it0 = it;
-            for (int s = 0; s < nslots; ++s, ++it)
-                wait_full(it % T::NSLOTS, (it / T::NSLOTS) & 1);
-            trace_mark(l * kStagesPerLayer + S_ATTN, 6);
-            attn_pass_tc(it0, nring, n, c0, o);
-            if (lane == 0)
-                for (uint32_t i = it0; i < it; ++i) mbar_arrive(&empty[i % T::NSLOTS]);
-            if (last) break;
-        }
-        trace_mark(l * kStagesPerLayer + S_ATTN, 3);
-        // CTA partial: (m, l) from st, o summed over the PG position groups
         constexpr int STR = DH + 2;
         float* mlc = reinterpret_cast<float*>(misc()) + 4;  // [QPG][2]
-        if (ctid < QPG) {
-            mlc[2 * ctid] = st[ctid * 4 + 0];
-            mlc[2 * ctid + 1] = st[ctid * 4 + 1];
-        }
-        // O[h][dim] = C[row h][dim] + C[row QPG + h][dim] (hi + lo of P):
-        // QPG = 8: rows g / g + 8 of the same lane; QPG < 8: row g + QPG is
-        // lane + 4 QPG.  Each (h, d) is owned by one lane: no cross-warp sum.
-        float ov[NTW][2];
-        {
+        float* ro = wpart();                                  // [QPG][DH]
+        constexpr int PASS = T::ATT_SC * T::KVC;
+        if constexpr (T::ATT_WARP) {
+            consumer_sync(NCT);
+            trace_mark(l * kStagesPerLayer + S_ATTN, 5);
+            WarpAtt wa;
+            attn_warp_init(wa);
+            for (int c0 = p0; c0 < past_end || (c0 == p0 && has_cur); c0 += PASS) {
+                const int nring = min(PASS, past_end - c0);
+                const int nslots = (nring + T::KVC - 1) / T::KVC;
+                const bool last = c0 + PASS >= past_end;
+                const int n = nring + ((last && has_cur) ? 1 : 0);
+                const uint32_t it0 = it;
+                for (int s = 0; s < nslots; ++s, ++it)
+                    wait_full(it % T::NSLOTS, (it / T::NSLOTS) & 1);
+                trace_mark(l * kStagesPerLayer + S_ATTN, 6);
+                attn_warp_pass(wa, it0, nring, n, c0);
+                __syncwarp();
+                if (lane == 0)
+                    for (uint32_t i = it0; i < it; ++i) mbar_arrive(&empty[i % T::NSLOTS]);
+                if (last) break;
+            }
+            trace_mark(l * kStagesPerLayer + S_ATTN, 3);
+            attn_warp_merge(wa, ro, mlc);
+        } else {
+            float o[NTW][4];
 #pragma unroll
             for (int nt = 0; nt < NTW; ++nt)
 #pragma unroll
-                for (int e = 0; e < 2; ++e) {
-                    if constexpr (QPG == 8) ov[nt][e] = o[nt][e] + o[nt][e + 2];
-                    else ov[nt][e] = o[nt][e] + __shfl_xor_sync(0xffffffffu, o[nt][e], 4 * QPG);
-                }
-        }
-        consumer_sync(NCT);  // q / scores / P / stats dead from here: wpart reused for O
-        float* ro = wpart();  // [QPG][DH]
-        {
-            const int g = lane / 4, q4 = lane % 4;
-            if (g < QPG)
+                for (int e = 0; e < 4; ++e) o[nt][e] = 0.f;
+            consumer_sync(NCT);
+            trace_mark(l * kStagesPerLayer + S_ATTN, 5);
+
+            for (int c0 = p0; c0 < past_end || (c0 == p0 && has_cur); c0 += PASS) {
+                const int nring = min(PASS, past_end - c0);
+                const int nslots = (nring + T::KVC - 1) / T::KVC;
+                const bool last = c0 + PASS >= past_end;
+                const int n = nring + ((last && has_cur) ? 1 : 0);
+                const uint32_t it0 = it;
+                for (int s = 0; s < nslots; ++s, ++it)
+                    wait_full(it % T::NSLOTS, (it / T::NSLOTS) & 1);
+                trace_mark(l * kStagesPerLayer + S_ATTN, 6);
+                attn_pass_tc(it0, nring, n, c0, o);
+                if (lane == 0)
+                    for (uint32_t i = it0; i < it; ++i) mbar_arrive(&empty[i % T::NSLOTS]);
+                if (last) break;
+            }
+            trace_mark(l * kStagesPerLayer + S_ATTN, 3);
+            // CTA partial: (m, l) from st, o summed over the PG position groups
+            if (ctid < QPG) {
+                mlc[2 * ctid] = st[ctid * 4 + 0];
+                mlc[2 * ctid + 1] = st[ctid * 4 + 1];
+            }
+            // O[h][dim] = C[row h][dim] + C[row QPG + h][dim] (hi + lo of P):
+            // QPG = 8: rows g / g + 8 of the same lane; QPG < 8: row g + QPG is
+            // lane + 4 QPG.  Each (h, d) is owned by one lane: no cross-warp sum.
+            float ov[NTW][2];
+            {
 #pragma unroll
                 for (int nt = 0; nt < NTW; ++nt)
 #pragma unroll
-                    for (int e = 0; e < 2; ++e)
-                        ro[g * DH + warp * DPW + nt * 8 + 2 * q4 + e] = ov[nt][e];
+                    for (int e = 0; e < 2; ++e) {
+                        if constexpr (QPG == 8) ov[nt][e] = o[nt][e] + o[nt][e + 2];
+                        else ov[nt][e] = o[nt][e] + __shfl_xor_sync(0xffffffffu, o[nt][e], 4 * QPG);
+                    }
+            }
+            consumer_sync(NCT);  // q / scores / P / stats dead from here: wpart reused for O
+            {
+                const int g = lane / 4, q4 = lane % 4;
+                if (g < QPG)
+#pragma unroll
+                    for (int nt = 0; nt < NTW; ++nt)
+#pragma unroll
+                        for (int e = 0; e < 2; ++e)
+                            ro[g * DH + warp * DPW + nt * 8 + 2 * q4 + e] = ov[nt][e];
+            }
+            consumer_sync(NCT);
         }
-        consumer_sync(NCT);
         float* part = p.attn_part + ((size_t)unit * grid + pl.attn_g) * QPG * STR;
         for (int idx = ctid; idx < QPG * DH; idx += NCT) {
             const int h = idx / DH, d = idx % DH;

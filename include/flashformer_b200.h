@@ -61,7 +61,10 @@ typedef enum ffb_mode {
  * kind: 0 = llama_decoder, 1 = stacked_linear (config.hpp:18; only layers,
  *       d_model and batch are used; square d_model x d_model layers).
  * dtype: 0 = bf16 (the only compiled storage type).
- * quant_bits: 0 (bf16 weights), 4 (reference int4 g128), 8 (int8 extension). */
+ * quant_bits: 0 (bf16 weights), 4 (reference int4 g128), 8 (int8 extension).
+ * batch: 1..16; batch 8 / 16 (bf16, TP 1) run every projection on tensor
+ * cores and keep the streamed matrices in a chunk-major fp16 layout (the
+ * upload converts; ffb_tensor values are the reference's bf16 values). */
 typedef struct ffb_model_config {
     int64_t layers, d_model, d_inter, d_head, n_q_heads, n_kv_heads, vocab_size;
     double rope_theta, rmsnorm_eps;

@@ -84,3 +84,24 @@ def test_full_size_8b_batch16_greedy_and_modes():
     np.testing.assert_array_equal(outs[0], outs[1])
     np.testing.assert_array_equal(outs[1], outs[2])
     m.close()
+
+
+def test_toy_batch16_device_decode_loop_matches_stepwise():
+    """ffb_decode_loop at batch 16: teacher-forced prompt rows then greedy
+    generation on the device give the host-driven step loop's tokens."""
+    cfg = TOY.replace(batch=16, layers=2)
+    prompt = np.array([[(7 * i + 3 * b) % cfg.vocab_size for b in range(16)] for i in range(6)],
+                      np.int64)
+    n = 5
+    st = O.OracleStore(cfg, 42, 20)
+    with device_from_store(st, 20) as m:
+        gen = m.generate(None, 0, n, prompt=prompt)
+    st2 = O.OracleStore(cfg, 42, 20)
+    with device_from_store(st2, 20) as m2:
+        for pos in range(len(prompt)):
+            _, g = m2.step(list(prompt[pos]), pos, logits=False)
+        ref = [np.array(g)]
+        for i in range(1, n):
+            _, g = m2.step(list(ref[-1]), len(prompt) + i - 1, logits=False)
+            ref.append(np.array(g))
+    np.testing.assert_array_equal(gen, np.stack(ref))

@@ -72,6 +72,9 @@ def test_full_size_8b_batch16_greedy_and_modes():
     cfg = to_model_cfg(O.preset("llama31_8b")).replace(batch=16)
     m = DecodeModel(cfg, 1028)
     m.init_synthetic(7)
+    for l in range(cfg.layers):
+        m.set_length(l, 1024)
+    m.calibrate(1)  # per-SM plan weights also drive the batch >= 8 row split
     outs = []
     for mode in MODES:
         m.set_mode(mode)

@@ -536,8 +536,10 @@ struct DecodeCta {
     };
     // KCP rows per accumulator block: the chunk's A table stays in its slot
     // while the block's weight slots stream past it, so a block spans at
-    // most NSLOTS - 1 weight slots (and at most 256 rows of accumulators)
-    static constexpr int KC_BLOCK = cmin_(256, (T::NSLOTS - 1) * T::MD::RW);
+    // most NSLOTS - 1 weight slots; 128 rows of accumulators (same-box A/B
+    // at 8B b16: 7.39 ms with 160-row blocks, 7.32 with 128: fewer live
+    // accumulator registers outweigh the extra A-table re-streams)
+    static constexpr int KC_BLOCK = cmax_(T::MD::RW, cmin_(128, (T::NSLOTS - 1) * T::MD::RW));
 
     // The lists of (stage, sub) in consumption order; false past the end.
     __device__ bool list_of(int stage, int sub, List& L) const {

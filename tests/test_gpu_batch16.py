@@ -108,3 +108,13 @@ def test_toy_batch16_device_decode_loop_matches_stepwise():
             _, g = m2.step(list(ref[-1]), len(prompt) + i - 1, logits=False)
             ref.append(np.array(g))
     np.testing.assert_array_equal(gen, np.stack(ref))
+
+
+def test_toy_batch16_zero_layers_is_lm_head_of_embedding():
+    """layers = 0: the A table of the LM head comes straight from the kernel's
+    embedding init (init counter, no decoder stage in between)."""
+    cfg = TOY.replace(batch=16, layers=0)
+    st = O.OracleStore(cfg, 5, 4)
+    with device_from_store(st, 4) as m:
+        e_plain, e_strict, flips = check_step(st, m, TOKENS, 0)
+    assert flips == 0

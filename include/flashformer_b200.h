@@ -168,7 +168,10 @@ ffb_status ffb_set_mode(ffb_model *m, ffb_mode mode);
  * mode (0 disables; default 512 KiB).  "l2_prefetch_stages": 6-bit mask of
  * the stage types (bit s = stage s of a layer: 0 QKV, 1 ATTN, 2 AOUT, 3 GLU,
  * 4 RED; bit 5 = LM head) in which the prefetch may run, only while the ring
- * is full (default ATTN|AOUT = 0x6). */
+ * is full (default ATTN|AOUT = 0x6).  "attn_group_max": cap on the CTAs per
+ * (batch row, kv head) split-K attention group (0 = min(grid / units, 32)).
+ * Plan options (rebuild the per-CTA plan): "calib_mask", "plan_reverse",
+ * "glu_pool_permille", "glu_pool_chunk", "attn_group_max". */
 ffb_status ffb_set_option(ffb_model *m, const char *key, int64_t value);
 
 /* Diagnostics only (never needed for correct use): bit 0 = streaming-only

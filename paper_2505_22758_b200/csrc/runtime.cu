@@ -253,6 +253,7 @@ struct ffb_model {
     int32_t l2_pf_stages = (1 << S_ATTN) | (1 << S_AOUT);
     int32_t kv_prefetch = 0;          // option "kv_prefetch" (measured +1.5 %: off)
     int plan_reverse = 0;             // weight slices assigned in reverse CTA order
+    int attn_group_max = 0;           // option "attn_group_max": cap on CTAs per attention unit (0: auto)
     // per-SM plan weights (ffb_calibrate): streamed-row shares of QKV / AOUT /
     // GLU / LM head proportional to each SM's measured streaming rate
     std::vector<double> sm_weight;
@@ -349,6 +350,7 @@ ffb_status build_plan(ffb_model* m) {
     // split-K group per (batch row, kv head): as many SMs as fit, at most
     // kMaxGroup so the last-arriver combine keeps every load in flight
     m->attn_group = static_cast<int>(std::min<int64_t>(G / m->n_units, kMaxGroup));
+    if (m->attn_group_max > 0) m->attn_group = std::min(m->attn_group, m->attn_group_max);
     std::vector<CtaPlan> plan(G);
     const int64_t qkv_pairs = m->qkv_rows() / 2;
     // GLU work pool: the last pool_frac of the d_inter pairs, in chunks of
@@ -1319,7 +1321,8 @@ ffb_status ffb_set_option(ffb_model* m, const char* key, int64_t value) {
         return FFB_OK;
     }
     const bool plan_key = !std::strcmp(key, "calib_mask") || !std::strcmp(key, "plan_reverse") ||
-                          !std::strcmp(key, "glu_pool_permille") || !std::strcmp(key, "glu_pool_chunk");
+                          !std::strcmp(key, "glu_pool_permille") || !std::strcmp(key, "glu_pool_chunk") ||
+                          !std::strcmp(key, "attn_group_max");
     if (plan_key && m->tp_size > 1)
         return fail(FFB_UNSUPPORTED, "option '%s' changes the plan; not with tensor parallelism", key);
     if (std::strcmp(key, "calib_mask") == 0) {
@@ -1349,8 +1352,12 @@ ffb_status ffb_set_option(ffb_model* m, const char* key, int64_t value) {
         return FFB_OK;
     }
     if (std::strcmp(key, "plan_reverse") == 0 || std::strcmp(key, "glu_pool_permille") == 0 ||
-        std::strcmp(key, "glu_pool_chunk") == 0) {
+        std::strcmp(key, "glu_pool_chunk") == 0 || std::strcmp(key, "attn_group_max") == 0) {
         if (key[0] == 'p') m->plan_reverse = value ? 1 : 0;
+        else if (key[0] == 'a') {
+            if (value < 0 || value > kMaxGroup) return fail(FFB_USAGE, "attn_group_max in [0, 32]");
+            m->attn_group_max = static_cast<int>(value);
+        }
         else if (std::strcmp(key, "glu_pool_chunk") == 0) {
             if (value < 1 || value > 64) return fail(FFB_USAGE, "glu_pool_chunk in [1, 64]");
             m->pool_ct_pref = value;

@@ -2520,7 +2520,9 @@ struct DecodeCta {
 
     // ---------------------------------------------------------- S_GLU
     // in/gate rows [2 t0, 2 t1) of Wffn1 -> h[t - t0] = silu(gate) * in (smem)
-    __device__ void glu_ffn1(uint32_t& it, const Act<>& act, int t0, int t1,
+    // act: the normalised activations (CUDA-core / quant GEMV); batch >= 8
+    // passes nullptr and kc_inv_b (the A table is in the ring)
+    __device__ void glu_ffn1(uint32_t& it, const Act<>* act, int t0, int t1,
                              const float* kc_inv_b = nullptr) {
         const int ctid = threadIdx.x;
         float* hs = h_s();
@@ -2542,7 +2544,7 @@ struct DecodeCta {
             gemv_kc<MD>(it, 2 * t0, 2 * t1, kc_inv_b, epi);
             fence_proxy_async_global();  // h is read by TMA in S_RED
         } else {
-            gemv(it, act, 2 * t0, 2 * t1, epi);
+            gemv(it, *act, 2 * t0, 2 * t1, epi);
         }
         consumer_sync(NCT);  // h complete
     }
@@ -2665,14 +2667,13 @@ struct DecodeCta {
             wait_stage(l * kStagesPerLayer + S_GLU);
             const float* inv = kc_inv(p.ssq);
             trace_mark(l * kStagesPerLayer + S_GLU, 3);
-            Act<> unused;
-            glu_ffn1(it, unused, pl.glu_t0, pl.glu_t1, inv);
+            glu_ffn1(it, nullptr, pl.glu_t0, pl.glu_t1, inv);
             arrive(p.counters + l * kStagesPerLayer + S_GLU, l * kStagesPerLayer + S_GLU);
             return;
         }
         Act<> act;
         load_act(act, p.x, false, p.norm_ffn + (size_t)l * D, l * kStagesPerLayer + S_GLU);
-        glu_ffn1(it, act, pl.glu_t0, pl.glu_t1);
+        glu_ffn1(it, &act, pl.glu_t0, pl.glu_t1);
         if constexpr (T::F2R) {  // h is in glu_part; S_RED applies W2
             arrive(p.counters + l * kStagesPerLayer + S_GLU, l * kStagesPerLayer + S_GLU);
             return;
@@ -2690,7 +2691,7 @@ struct DecodeCta {
                     break;
                 }
                 const int t0c = p.pool_t0 + ch * p.pool_ct, t1c = t0c + p.pool_ct;
-                glu_ffn1(it, act, t0c, t1c);
+                glu_ffn1(it, &act, t0c, t1c);
                 glu_ffn2(it, t0c, t1c, p.pool_part + (size_t)ch * T::RG * B * D);
             }
         }

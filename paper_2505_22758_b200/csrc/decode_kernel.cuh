@@ -338,10 +338,11 @@ struct KTraits : RowMap<S, S::D> {
     // [ANP][QPG], stats
     // (batch 1 at 4k context fits one pass of 4 slots; batch > 1 runs
     // several passes, the producer filling the next pass's slots while this
-    // one computes: 4-slot passes at batch 2 (2 passes at 4k), 3 at batch 4
-    // -- same-box A/B at 8B, 4k context: b2 3.17 / 3.14 ms for 3 / 4 slots,
-    // b4 3.99 / 4.08 / 4.08 / 4.50 ms for 3 / 2 / 4 / 1 slots)
-    static constexpr int ATT_SC = S::B == 1 ? cmax(1, 131072 / SLOT_BYTES) : S::B == 2 ? 4 : 3;
+    // one computes: 4-slot passes at batch 2 (2 passes at 4k), 2 from batch
+    // 4 on -- same-box A/B at 8B, 4k context: b2 3.17 / 3.14 ms for 3 / 4
+    // slots; with the per-warp attention b4 3.77 / 3.75, b8 6.41 / 6.38,
+    // b16 7.32 / 7.30 ms for 3 / 2 slots (b16 7.65 with 1))
+    static constexpr int ATT_SC = S::B == 1 ? cmax(1, 131072 / SLOT_BYTES) : S::B == 2 ? 4 : 2;
     static constexpr int ANP = ((ATT_SC * KVC + 1) + 15) / 16 * 16;
     // alpha*q f32 [QPG][DH], scores f32 [QPG][ANP], probabilities as bf16
     // hi/lo MMA rows [16][ANP] (tensor-core P.V), stats [QPG][4]

@@ -535,9 +535,7 @@ struct DecodeCta {
         int nkc = 0;
         int rows_total = 0;  // KCP: rows of the chunk-major matrix
     };
-    // KCP rows per accumulator block: the chunk's A table stays in its slot
-    // while the block's weight slots stream past it, so a block spans at
-    // most NSLOTS - 1 weight slots; 128 rows of accumulators (same-box A/B
+    // KCP rows per accumulator block: 128 rows of accumulators (same-box A/B
     // at 8B b16: 7.39 ms with 160-row blocks, 7.32 with 128: fewer live
     // accumulator registers outweigh the extra A-table re-streams)
     static constexpr int KC_BLOCK = cmax_(T::MD::RW, cmin_(128, (T::NSLOTS - 1) * T::MD::RW));
@@ -1650,6 +1648,16 @@ struct DecodeCta {
                 wait_full(sa, (it / T::NSLOTS) & 1);
                 const uint8_t* atab = ring + sa * T::SLOT_BYTES + kp * 8 * 1024 + lane * 16;
                 ++it;
+                // this warp's A fragments of the chunk into registers, then the
+                // A-table slot is released: the ring refills it with weights
+                uint4 afh[8], afl[8];
+#pragma unroll
+                for (int ks = 0; ks < 8; ++ks) {
+                    afh[ks] = lds_u128(atab + ks * 1024);
+                    afl[ks] = lds_u128(atab + ks * 1024 + 512);
+                }
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&empty[sa]);
 #pragma unroll
                 for (int j = 0; j < NJ; ++j) {
                     if (j < nj) {
@@ -1659,8 +1667,8 @@ struct DecodeCta {
                         const int key = (blk + j * RW + lrow) & 7;
 #pragma unroll
                         for (int ks = 0; ks < 8; ++ks) {
-                            const uint4 ah = lds_u128(atab + ks * 1024);
-                            const uint4 al = lds_u128(atab + ks * 1024 + 512);
+                            const uint4 ah = afh[ks];
+                            const uint4 al = afl[ks];
                             uint32_t b0, b1, b2, b3;
                             ldsm_x4(wrow + ((((kp * 8 + ks) * 2 + lhalf) ^ key) << 4), b0, b1, b2, b3);
                             mma_f16(acc[j][0], ah.x, ah.y, ah.z, ah.w, b0, b1);
@@ -1673,8 +1681,6 @@ struct DecodeCta {
                         ++it;
                     }
                 }
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&empty[sa]);
             }
 #pragma unroll
             for (int j = 0; j < NJ; ++j) {

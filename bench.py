@@ -51,7 +51,7 @@ def parse():
                     choices=["fused_overlap", "fused", "baseline"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-variants", action="store_true")
-    ap.add_argument("--calibrate", type=int, default=3,
+    ap.add_argument("--calibrate", type=int, default=8,
                     help="ffb_calibrate iterations before timing (0 = uniform plan)")
     return ap.parse_args()
 

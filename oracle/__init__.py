@@ -136,6 +136,11 @@ def lib():
                                                                    C.POINTER(C.c_double)]
         L.fo_normal_f64.argtypes = [C.c_uint64, C.c_double, C.c_double, C.POINTER(C.c_double),
                                     C.c_int64]
+        L.fo_save_store.argtypes = [C.POINTER(FoStore), C.c_char_p]
+        L.fo_load_store.restype = C.POINTER(FoStore)
+        L.fo_load_store.argtypes = [C.c_char_p, C.c_int64]
+        L.fo_serialize_config.restype = C.c_int64
+        L.fo_serialize_config.argtypes = [C.POINTER(FoConfig), C.c_char_p, C.c_int64]
         _lib = L
     return _lib
 
@@ -152,6 +157,28 @@ class OracleStore:
         if not self._s:
             raise ValueError(L.fo_last_error().decode())
         self.max_seq_len = max_seq_len
+
+    @classmethod
+    def load(cls, path: str, max_seq_len: int) -> "OracleStore":
+        """load_store (tensor_store.hpp:446-482): an FSTW v1 file -> store."""
+        L = lib()
+        s = L.fo_load_store(os.fsencode(path), max_seq_len)
+        if not s:
+            raise ValueError(L.fo_last_error().decode())
+        self = cls.__new__(cls)
+        self._s = s
+        c = s.contents.cfg
+        self.cfg = ModelCfg(c.layers, c.d_model, c.d_inter, c.d_head, c.n_q_heads, c.n_kv_heads,
+                            c.vocab_size, c.rope_theta, c.rmsnorm_eps, c.dtype, c.quant_bits,
+                            c.quant_group, c.batch)
+        self._c = self.cfg.c()
+        self.max_seq_len = max_seq_len
+        return self
+
+    def save(self, path: str):
+        """save_store (tensor_store.hpp:410-444), FSTW v1."""
+        if lib().fo_save_store(self._s, os.fsencode(path)) != 0:
+            raise ValueError(lib().fo_last_error().decode())
 
     def close(self):
         if getattr(self, "_s", None):
@@ -274,6 +301,9 @@ def ref_lib():
         R.ref_linear_init.restype = C.c_void_p
         R.ref_linear_init.argtypes = [C.c_int64, C.c_int64, C.c_int64, C.c_uint64]
         R.ref_linear_forward.argtypes = [C.c_void_p, C.POINTER(C.c_float), C.POINTER(C.c_double)]
+        R.ref_save_store.argtypes = [C.c_void_p, C.c_char_p]
+        R.ref_load_store.restype = C.c_void_p
+        R.ref_load_store.argtypes = [C.c_char_p, C.c_int64]
         R.ref_time_forward.restype = C.c_double
         R.ref_time_forward.argtypes = [C.c_void_p, C.POINTER(C.c_int64), C.c_int64, C.c_int]
         _ref = R
@@ -294,6 +324,22 @@ class RefStore:
         if not self._h:
             raise ValueError(R.ref_last_error().decode())
         self.max_seq_len = max_seq_len
+
+    @classmethod
+    def load(cls, path: str, cfg: ModelCfg, max_seq_len: int) -> "RefStore":
+        """fusesim::load_store, unchanged (it rebuilds shapes with
+        init_weights(model, 0) first, so it is slow for large models)."""
+        R = ref_lib()
+        h = R.ref_load_store(os.fsencode(path), max_seq_len)
+        if not h:
+            raise ValueError(R.ref_last_error().decode())
+        self = cls.__new__(cls)
+        self._h, self.cfg, self._c, self.max_seq_len = h, cfg, cfg.c(), max_seq_len
+        return self
+
+    def save(self, path: str):
+        if ref_lib().ref_save_store(self._h, os.fsencode(path)) != 0:
+            raise ValueError(ref_lib().ref_last_error().decode())
 
     def close(self):
         if getattr(self, "_h", None):

@@ -355,18 +355,14 @@ void fo_free(fo_store *s) {
     free(s);
 }
 
-fo_store *fo_init_weights(const fo_config *c, uint64_t seed, int64_t max_seq_len, int nthreads) {
-    if (fo_validate(c)) return NULL;
+/* TensorStore shapes (tensor_store.hpp:304-366) with zeroed values and an
+ * empty KV cache [B][L][Hkv][S][dh]. */
+static fo_store *store_alloc(const fo_config *c, int64_t max_seq_len) {
     fo_store *s = (fo_store *)calloc(1, sizeof(fo_store));
     s->cfg = *c;
     s->max_seq_len = max_seq_len;
     const int64_t d = c->d_model;
     s->layers = (fo_layer *)calloc((size_t)(c->layers > 0 ? c->layers : 1), sizeof(fo_layer));
-    int njobs = (int)(6 * c->layers + 3);
-    fill_job *jobs = (fill_job *)calloc((size_t)njobs, sizeof(fill_job));
-    int j = 0;
-    /* fan-in: d_inter for the GLU output projection, stored cols otherwise (:330-333) */
-    double sd_d = 1.0 / sqrt((double)d), sd_i = 1.0 / sqrt((double)c->d_inter);
     for (int64_t l = 0; l < c->layers; ++l) {
         fo_layer *L = &s->layers[l];
         L->wqkv = alloc_f32(fo_qkv_rows(c) * d);
@@ -375,6 +371,28 @@ fo_store *fo_init_weights(const fo_config *c, uint64_t seed, int64_t max_seq_len
         L->wffn2t = alloc_f32(c->d_inter * d);
         L->norm_attn = alloc_f32(d);
         L->norm_ffn = alloc_f32(d);
+    }
+    s->final_norm = alloc_f32(d);
+    s->embedding = alloc_f32(c->vocab_size * d);
+    s->lm_head = alloc_f32(c->vocab_size * d);
+    size_t kv = (size_t)c->batch * c->layers * c->n_kv_heads * max_seq_len * c->d_head;
+    s->k = alloc_f32((int64_t)kv);
+    s->v = alloc_f32((int64_t)kv);
+    s->kv_len = (int64_t *)calloc((size_t)(c->layers > 0 ? c->layers : 1), sizeof(int64_t));
+    return s;
+}
+
+fo_store *fo_init_weights(const fo_config *c, uint64_t seed, int64_t max_seq_len, int nthreads) {
+    if (fo_validate(c)) return NULL;
+    fo_store *s = store_alloc(c, max_seq_len);
+    const int64_t d = c->d_model;
+    int njobs = (int)(6 * c->layers + 3);
+    fill_job *jobs = (fill_job *)calloc((size_t)njobs, sizeof(fill_job));
+    int j = 0;
+    /* fan-in: d_inter for the GLU output projection, stored cols otherwise (:330-333) */
+    double sd_d = 1.0 / sqrt((double)d), sd_i = 1.0 / sqrt((double)c->d_inter);
+    for (int64_t l = 0; l < c->layers; ++l) {
+        fo_layer *L = &s->layers[l];
 #define JOB(NAME, DST, R, C, SD, K)                                                        \
     do {                                                                                   \
         snprintf(jobs[j].name, sizeof(jobs[j].name), "layer.%lld." NAME, (long long)l);   \
@@ -389,9 +407,6 @@ fo_store *fo_init_weights(const fo_config *c, uint64_t seed, int64_t max_seq_len
         JOB("norm_ffn", L->norm_ffn, 1, d, 0.0, 1);
 #undef JOB
     }
-    s->final_norm = alloc_f32(d);
-    s->embedding = alloc_f32(c->vocab_size * d);
-    s->lm_head = alloc_f32(c->vocab_size * d);
     snprintf(jobs[j].name, 64, "final_norm");
     jobs[j].dst = s->final_norm; jobs[j].rows = 1; jobs[j].cols = d; jobs[j].kind = 1; ++j;
     snprintf(jobs[j].name, 64, "embedding");
@@ -418,11 +433,6 @@ fo_store *fo_init_weights(const fo_config *c, uint64_t seed, int64_t max_seq_len
     for (int t = 1; t < nthreads; ++t) pthread_join(th[t], NULL);
     pthread_mutex_destroy(&ctx.mu);
     free(jobs);
-
-    size_t kv = (size_t)c->batch * c->layers * c->n_kv_heads * max_seq_len * c->d_head;
-    s->k = alloc_f32((int64_t)kv);
-    s->v = alloc_f32((int64_t)kv);
-    s->kv_len = (int64_t *)calloc((size_t)(c->layers > 0 ? c->layers : 1), sizeof(int64_t));
     return s;
 }
 
@@ -561,7 +571,11 @@ int fo_attn_reduce(const double *m, const double *l, const double *o, int64_t n_
 /* ------------------------------------------------------------------ */
 /* reference_forward (reference.hpp:37-139)                             */
 /* ------------------------------------------------------------------ */
+/* Parallel over output rows (OpenMP): every row is still one sequential
+ * f64 dot product in column order, so results are bit-identical to the
+ * single-threaded reference for any thread count. */
 static void matvec_rows(const float *w, int64_t rows, int64_t cols, const double *u, double *y) {
+#pragma omp parallel for schedule(static)
     for (int64_t r = 0; r < rows; ++r) { /* reference.hpp:21-30 */
         const float *row = w + r * cols;
         double acc = 0.0;
@@ -599,7 +613,8 @@ int fo_reference_forward_ex(fo_store *s, const int64_t *tokens, int64_t pos, dou
     float *vrow = (float *)malloc(sizeof(float) * (size_t)(B * nkv * dh));
     double *attn = (double *)malloc(sizeof(double) * (size_t)(nq * dh));
     double *aout = (double *)malloc(sizeof(double) * (size_t)D);
-    double *sc = (double *)malloc(sizeof(double) * (size_t)(pos + 1));
+    double *scores = (double *)malloc(sizeof(double) * (size_t)(nq * (pos + 1)));
+    double *hbuf = (double *)malloc(sizeof(double) * (size_t)(m->d_inter > 0 ? m->d_inter : 1));
     int rc = 0;
 
     for (int64_t b = 0; b < B; ++b) widen(s->embedding + tokens[b] * D, D, x + b * D);
@@ -647,10 +662,13 @@ int fo_reference_forward_ex(fo_store *s, const int64_t *tokens, int64_t pos, dou
 
         for (int64_t b = 0; b < B; ++b) {
             for (int64_t i = 0; i < nq * dh; ++i) attn[i] = 0.0;
+            /* heads are independent: one per thread, each with its own score row */
+#pragma omp parallel for schedule(dynamic, 1)
             for (int64_t h = 0; h < nq; ++h) {
                 int64_t kvh = h / qpg;
                 const double *qh = q + b * nq * dh + h * dh;
                 int64_t n = pos + 1;
+                double *sc = scores + h * (pos + 1);
                 double mx = -INFINITY;
                 for (int64_t j = 0; j < n; ++j) {
                     const float *kj = fo_k_at(s, b, l, kvh, j);
@@ -673,6 +691,10 @@ int fo_reference_forward_ex(fo_store *s, const int64_t *tokens, int64_t pos, dou
 
             widen(lw->norm_ffn, D, w);
             fo_rmsnorm_f64(xb, w, D, m->rmsnorm_eps, u);
+            /* reference.hpp:114-128 in two parallel passes with the same
+             * per-element operation order: h[t] for every pair t, then
+             * xb[k] += h[t] * wffn2t[t][k] in increasing t for each k. */
+#pragma omp parallel for schedule(static)
             for (int64_t t = 0; t < m->d_inter; ++t) {
                 const float *in_row = lw->wffn1 + (2 * t) * D;
                 const float *gate_row = lw->wffn1 + (2 * t + 1) * D;
@@ -681,9 +703,16 @@ int fo_reference_forward_ex(fo_store *s, const int64_t *tokens, int64_t pos, dou
                     a += (double)in_row[c] * u[c];
                     g += (double)gate_row[c] * u[c];
                 }
-                double hh = fo_silu(g) * a;
-                const float *col = lw->wffn2t + t * D;
-                for (int64_t k = 0; k < D; ++k) xb[k] += hh * (double)col[k];
+                hbuf[t] = fo_silu(g) * a;
+            }
+#pragma omp parallel for schedule(static)
+            for (int64_t k0 = 0; k0 < D; k0 += 64) {
+                int64_t k1 = k0 + 64 < D ? k0 + 64 : D;
+                for (int64_t t = 0; t < m->d_inter; ++t) {
+                    const double hh = hbuf[t];
+                    const float *col = lw->wffn2t + t * D;
+                    for (int64_t k = k0; k < k1; ++k) xb[k] += hh * (double)col[k];
+                }
             }
         }
     }
@@ -694,7 +723,7 @@ int fo_reference_forward_ex(fo_store *s, const int64_t *tokens, int64_t pos, dou
     }
 done:
     free(x); free(u); free(w); free(qkv); free(q); free(krow); free(vrow);
-    free(attn); free(aout); free(sc);
+    free(attn); free(aout); free(scores); free(hbuf);
     return rc;
 }
 
@@ -743,4 +772,250 @@ void fo_linear_forward(const float *w, int64_t layers, int64_t d, int64_t batch,
     }
     free(x);
     free(y);
+}
+
+/* ------------------------------------------------------------------ */
+/* Weight fixture container "FSTW" v1 (tensor_store.hpp:367-482)        */
+/* ------------------------------------------------------------------ */
+/* Layout (little-endian u64 fields, detail::put_u64/put_str/put_floats,
+ * tensor_store.hpp:374-397):
+ *   magic 0x46535457, version 1, str(serialize(RunConfig{model}))
+ *   u64 n_layers, per layer: matrix(wqkv) matrix(waout) matrix(wffn1)
+ *   matrix(wffn2t) floats(norm_attn) floats(norm_ffn); floats(final_norm)
+ *   matrix(embedding) matrix(lm_head)
+ *   matrix = str(name) u64(dtype) u64(rows) u64(cols) floats(values)
+ *   str = u64 n + bytes; floats = u64 n + n f32.
+ * The config text is serialize() (config.hpp:245-287) of a RunConfig whose
+ * hardware / pipeline / run sections hold the defaults (config.hpp:88-140),
+ * so a store saved here is byte-identical to the reference's save_store. */
+#define FO_STORE_MAGIC 0x46535457ull
+#define FO_STORE_VERSION 1ull
+
+static int put_u64(FILE *f, uint64_t v) { return fwrite(&v, 8, 1, f) == 1 ? 0 : -1; }
+static int put_bytes(FILE *f, const void *p, uint64_t n) {
+    if (put_u64(f, n)) return -1;
+    return (n == 0 || fwrite(p, 1, (size_t)n, f) == (size_t)n) ? 0 : -1;
+}
+static int put_floats(FILE *f, const float *v, uint64_t n) {
+    if (put_u64(f, n)) return -1;
+    return (n == 0 || fwrite(v, 4, (size_t)n, f) == (size_t)n) ? 0 : -1;
+}
+static int put_matrix(FILE *f, const char *name, int32_t dtype, int64_t rows, int64_t cols,
+                      const float *v) {
+    if (put_bytes(f, name, strlen(name)) || put_u64(f, (uint64_t)dtype) ||
+        put_u64(f, (uint64_t)rows) || put_u64(f, (uint64_t)cols))
+        return -1;
+    return put_floats(f, v, (uint64_t)(rows * cols));
+}
+
+/* serialize(RunConfig) for the decoder kind with default hardware/pipeline/run */
+int64_t fo_serialize_config(const fo_config *c, char *out, int64_t cap) {
+    char q[256] = "";
+    if (c->quant_bits)
+        snprintf(q, sizeof q,
+                 "quant_bits = %d\nquant_group_size = %d\nquant_scheme = weight_only_affine\n",
+                 c->quant_bits, c->quant_group);
+    int n = snprintf(out, (size_t)(cap > 0 ? cap : 0),
+        "[model]\nkind = llama_decoder\nlayers = %lld\nd_model = %lld\nd_inter = %lld\n"
+        "d_head = %lld\nn_q_heads = %lld\nn_kv_heads = %lld\nvocab_size = %lld\n"
+        "rope_theta = %.17g\nrmsnorm_eps = %.17g\ndtype = %s\nbatch = %lld\n%s"
+        "\n[hardware]\nnum_sms = 132\nshared_mem_per_sm = %llu\nregisters_per_sm = %llu\n"
+        "hbm_capacity = %llu\npeak_bandwidth = %.17g\nkernel_launch_overhead = %.17g\n"
+        "barrier_latency = %.17g\ncompute_throughput_per_sm = %.17g\n"
+        "\n[pipeline]\nstage_size = %llu\ndepth = 3\nconsumer_warps = 8\n"
+        "\n[run]\nmode = fused_overlap\nseq_len = 0\nseed = 0\n",
+        (long long)c->layers, (long long)c->d_model, (long long)c->d_inter,
+        (long long)c->d_head, (long long)c->n_q_heads, (long long)c->n_kv_heads,
+        (long long)c->vocab_size, c->rope_theta, c->rmsnorm_eps,
+        c->dtype == 0 ? "bf16" : "fp32", (long long)c->batch, q,
+        228ull * 1024, 256ull * 1024, 80ull * 1000 * 1000 * 1000, 3.35e12, 8e-6, 3e-7, 8e10,
+        64ull * 1024);
+    return n;
+}
+
+int fo_save_store(const fo_store *s, const char *path) { /* tensor_store.hpp:410-444 */
+    FILE *f = fopen(path, "wb");
+    if (!f) {
+        set_err("save_store: cannot open %s", path);
+        return 1;
+    }
+    const fo_config *c = &s->cfg;
+    const int64_t d = c->d_model;
+    char text[2048];
+    int64_t tn = fo_serialize_config(c, text, sizeof text);
+    int bad = put_u64(f, FO_STORE_MAGIC) || put_u64(f, FO_STORE_VERSION) ||
+              put_bytes(f, text, (uint64_t)tn) || put_u64(f, (uint64_t)c->layers);
+    char name[64];
+    for (int64_t l = 0; l < c->layers && !bad; ++l) {
+        const fo_layer *L = &s->layers[l];
+#define PM(T, PTR, R)                                                            \
+    snprintf(name, sizeof name, "layer.%lld." T, (long long)l);                  \
+    bad = bad || put_matrix(f, name, c->dtype, (R), d, (PTR));
+        PM("wqkv", L->wqkv, fo_qkv_rows(c))
+        PM("waout", L->waout, d)
+        PM("wffn1", L->wffn1, 2 * c->d_inter)
+        PM("wffn2t", L->wffn2t, c->d_inter)
+#undef PM
+        bad = bad || put_floats(f, L->norm_attn, (uint64_t)d) ||
+              put_floats(f, L->norm_ffn, (uint64_t)d);
+    }
+    bad = bad || put_floats(f, s->final_norm, (uint64_t)d) ||
+          put_matrix(f, "embedding", c->dtype, c->vocab_size, d, s->embedding) ||
+          put_matrix(f, "lm_head", c->dtype, c->vocab_size, d, s->lm_head);
+    bad = fclose(f) || bad;
+    if (bad) {
+        set_err("save_store: write failed on %s", path);
+        return 1;
+    }
+    return 0;
+}
+
+static int get_u64(FILE *f, uint64_t *v) { return fread(v, 8, 1, f) == 1 ? 0 : -1; }
+
+/* floats(n) into dst when n == want */
+static int get_floats_into(FILE *f, float *dst, uint64_t want, const char *what) {
+    uint64_t n;
+    if (get_u64(f, &n)) { set_err("load_store: truncated file (%s)", what); return -1; }
+    if (n != want) {
+        set_err("load_store: %s has %llu values, expected %llu", what, (unsigned long long)n,
+                (unsigned long long)want);
+        return -1;
+    }
+    if (n && fread(dst, 4, (size_t)n, f) != (size_t)n) {
+        set_err("load_store: truncated file (%s)", what);
+        return -1;
+    }
+    return 0;
+}
+
+static int get_matrix_into(FILE *f, float *dst, const char *want_name, int64_t rows,
+                           int64_t cols) {
+    uint64_t n, dt, r, cc;
+    char name[128];
+    if (get_u64(f, &n) || n >= sizeof name || fread(name, 1, (size_t)n, f) != (size_t)n) {
+        set_err("load_store: bad tensor record (expected %s)", want_name);
+        return -1;
+    }
+    name[n] = 0;
+    if (get_u64(f, &dt) || get_u64(f, &r) || get_u64(f, &cc)) {
+        set_err("load_store: truncated file (%s)", want_name);
+        return -1;
+    }
+    if (strcmp(name, want_name) != 0 || (int64_t)r != rows || (int64_t)cc != cols) {
+        set_err("load_store: record '%s' [%llu x %llu] where '%s' [%lld x %lld] was expected",
+                name, (unsigned long long)r, (unsigned long long)cc, want_name,
+                (long long)rows, (long long)cols);
+        return -1;
+    }
+    return get_floats_into(f, dst, (uint64_t)(rows * cols), want_name);
+}
+
+/* [model] section of the INI text (config.hpp:153-205, 289-329) */
+static int parse_model_section(const char *text, fo_config *c) {
+    memset(c, 0, sizeof *c);
+    c->rope_theta = 500000.0;
+    c->rmsnorm_eps = 1e-5;
+    c->batch = 1;
+    c->quant_group = 128;
+    int in_model = 0, seen = 0;
+    const char *p = text;
+    char line[512];
+    while (*p) {
+        const char *e = strchr(p, '\n');
+        size_t n = e ? (size_t)(e - p) : strlen(p);
+        if (n >= sizeof line) n = sizeof line - 1;
+        memcpy(line, p, n);
+        line[n] = 0;
+        p = e ? e + 1 : p + n;
+        char *h = strchr(line, '#');
+        if (h) *h = 0;
+        char *a = line;
+        while (*a == ' ' || *a == '\t' || *a == '\r') ++a;
+        char *z = a + strlen(a);
+        while (z > a && (z[-1] == ' ' || z[-1] == '\t' || z[-1] == '\r')) *--z = 0;
+        if (!*a) continue;
+        if (*a == '[') {
+            in_model = strcmp(a, "[model]") == 0;
+            seen |= in_model;
+            continue;
+        }
+        if (!in_model) continue;
+        char *eq = strchr(a, '=');
+        if (!eq) { set_err("config: expected key = value"); return -1; }
+        *eq = 0;
+        char *k = a, *v = eq + 1;
+        for (char *t = eq; t > k && (t[-1] == ' ' || t[-1] == '\t'); ) *--t = 0;
+        while (*v == ' ' || *v == '\t') ++v;
+        if (!strcmp(k, "kind")) {
+            if (strcmp(v, "llama_decoder")) {
+                set_err("load_store: only the llama_decoder kind is restated (got %s)", v);
+                return -1;
+            }
+        } else if (!strcmp(k, "layers")) c->layers = atoll(v);
+        else if (!strcmp(k, "d_model")) c->d_model = atoll(v);
+        else if (!strcmp(k, "d_inter")) c->d_inter = atoll(v);
+        else if (!strcmp(k, "d_head")) c->d_head = atoll(v);
+        else if (!strcmp(k, "n_q_heads")) c->n_q_heads = atoll(v);
+        else if (!strcmp(k, "n_kv_heads")) c->n_kv_heads = atoll(v);
+        else if (!strcmp(k, "vocab_size")) c->vocab_size = atoll(v);
+        else if (!strcmp(k, "rope_theta")) c->rope_theta = strtod(v, NULL);
+        else if (!strcmp(k, "rmsnorm_eps")) c->rmsnorm_eps = strtod(v, NULL);
+        else if (!strcmp(k, "dtype")) {
+            if (!strcmp(v, "bf16")) c->dtype = 0;
+            else if (!strcmp(v, "fp32") || !strcmp(v, "f32")) c->dtype = 1;
+            else { set_err("unknown dtype: %s", v); return -1; }
+        } else if (!strcmp(k, "batch")) c->batch = atoll(v);
+        else if (!strcmp(k, "quant_bits")) c->quant_bits = atoi(v);
+        else if (!strcmp(k, "quant_group_size")) c->quant_group = atoi(v);
+        else if (!strcmp(k, "quant_scheme")) continue;
+        else { set_err("config: unknown [model] field '%s'", k); return -1; }
+    }
+    if (!seen) { set_err("config: missing [model] section"); return -1; }
+    return 0;
+}
+
+fo_store *fo_load_store(const char *path, int64_t max_seq_len) { /* tensor_store.hpp:446-482 */
+    FILE *f = fopen(path, "rb");
+    if (!f) { set_err("load_store: cannot open %s", path); return NULL; }
+    fo_store *s = NULL;
+    uint64_t magic = 0, ver = 0, tn = 0;
+    char *text = NULL;
+    if (get_u64(f, &magic) || magic != FO_STORE_MAGIC) { set_err("load_store: bad magic"); goto fail; }
+    if (get_u64(f, &ver) || ver != FO_STORE_VERSION) { set_err("load_store: bad version"); goto fail; }
+    if (get_u64(f, &tn) || tn > (1u << 20)) { set_err("load_store: bad config record"); goto fail; }
+    text = (char *)calloc((size_t)tn + 1, 1);
+    if (fread(text, 1, (size_t)tn, f) != (size_t)tn) { set_err("load_store: truncated file"); goto fail; }
+    fo_config c;
+    if (parse_model_section(text, &c) || fo_validate(&c)) goto fail;
+    s = store_alloc(&c, max_seq_len);
+    uint64_t nl;
+    if (get_u64(f, &nl) || (int64_t)nl != c.layers) { set_err("load_store: layer count mismatch"); goto fail; }
+    const int64_t d = c.d_model;
+    char name[64];
+    for (int64_t l = 0; l < c.layers; ++l) {
+        fo_layer *L = &s->layers[l];
+#define GM(T, PTR, R)                                              \
+    snprintf(name, sizeof name, "layer.%lld." T, (long long)l);    \
+    if (get_matrix_into(f, (PTR), name, (R), d)) goto fail;
+        GM("wqkv", L->wqkv, fo_qkv_rows(&c))
+        GM("waout", L->waout, d)
+        GM("wffn1", L->wffn1, 2 * c.d_inter)
+        GM("wffn2t", L->wffn2t, c.d_inter)
+#undef GM
+        if (get_floats_into(f, L->norm_attn, (uint64_t)d, "norm_attn") ||
+            get_floats_into(f, L->norm_ffn, (uint64_t)d, "norm_ffn"))
+            goto fail;
+    }
+    if (get_floats_into(f, s->final_norm, (uint64_t)d, "final_norm") ||
+        get_matrix_into(f, s->embedding, "embedding", c.vocab_size, d) ||
+        get_matrix_into(f, s->lm_head, "lm_head", c.vocab_size, d))
+        goto fail;
+    free(text);
+    fclose(f);
+    return s;
+fail:
+    free(text);
+    fo_free(s);
+    fclose(f);
+    return NULL;
 }

@@ -92,6 +92,15 @@ uint64_t fo_streamed_weight_bytes(const fo_config *c);
 uint64_t fo_total_weight_bytes(const fo_config *c);
 fo_store *fo_init_weights(const fo_config *c, uint64_t seed, int64_t max_seq_len, int nthreads);
 void fo_free(fo_store *s);
+
+/* -------- weight fixture container "FSTW" v1 (tensor_store.hpp:367-482) -------- */
+/* serialize(RunConfig) text (config.hpp:245-287) with default hardware /
+ * pipeline / run sections; returns its length (snprintf semantics). */
+int64_t fo_serialize_config(const fo_config *c, char *out, int64_t cap);
+/* save_store: byte-identical to the reference's file for the decoder kind. */
+int fo_save_store(const fo_store *s, const char *path);
+/* load_store: NULL + fo_last_error() on a bad magic / version / record. */
+fo_store *fo_load_store(const char *path, int64_t max_seq_len);
 int64_t fo_qkv_rows(const fo_config *c);
 /* set_position / set_length / k_at / v_at (tensor_store.hpp:109-125) */
 void fo_kv_set_position(fo_store *s, int64_t b, int64_t l, int64_t h, int64_t pos,

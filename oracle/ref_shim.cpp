@@ -278,4 +278,15 @@ int ref_linear_forward(void* h, const float* x0, double* out) {
     });
 }
 
+// fusesim::save_store / load_store (tensor_store.hpp:410-482), unchanged.
+int ref_save_store(void* h, const char* path) {
+    return guarded([&] { save_store(*static_cast<TensorStore*>(h), path); });
+}
+
+void* ref_load_store(const char* path, int64_t max_seq_len) {
+    TensorStore* st = nullptr;
+    int rc = guarded([&] { st = new TensorStore(load_store(path, max_seq_len)); });
+    return rc == 0 ? st : nullptr;
+}
+
 }  // extern "C"

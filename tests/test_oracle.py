@@ -283,3 +283,72 @@ def test_stacked_linear_oracle_bit_exact_vs_reference():
         np.testing.assert_array_equal(lo.tensor(f"linear.{l}"), rl.tensor(f"linear.{l}"))
     x = np.random.default_rng(0).standard_normal((2, 256)).astype(np.float32)
     np.testing.assert_array_equal(lo.forward(x), rl.forward(x))
+
+
+# ------------------------------------------------------------------ store file
+@needs_ref
+@pytest.mark.parametrize("quant", [0, 4])
+def test_store_file_byte_identical_to_reference(tmp_path, quant):
+    """'store dump/load round-trips' (proj/tests/test_store.cpp:120-131): the
+    restatement's FSTW v1 file is byte-identical to the reference's
+    save_store output, and each side loads the other's file."""
+    cfg = TOY.replace(quant_bits=quant)
+    o = O.OracleStore(cfg, 11, 32)
+    r = O.RefStore(cfg, 11, 32)
+    po, pr = tmp_path / "oracle.fstw", tmp_path / "ref.fstw"
+    o.save(str(po))
+    r.save(str(pr))
+    assert po.read_bytes() == pr.read_bytes()
+    back = O.OracleStore.load(str(pr), 32)
+    assert back.cfg == cfg
+    for n in ("layer.1.wffn1", "layer.3.norm_ffn", "final_norm", "embedding", "lm_head"):
+        np.testing.assert_array_equal(back.tensor(n).ravel(), r.tensor(n))
+    rb = O.RefStore.load(str(po), cfg, 32)
+    np.testing.assert_array_equal(rb.tensor("layer.2.wqkv"), o.tensor("layer.2.wqkv").ravel())
+    back.synthetic_prefill(5, 3)
+    rb.synthetic_prefill(5, 3)
+    np.testing.assert_array_equal(back.forward([9], 5), rb.forward([9], 5))
+
+
+def test_store_file_roundtrip_and_errors(tmp_path):
+    cfg = O.ModelCfg(2, 256, 512, 64, 4, 2, 300, batch=2)
+    o = O.OracleStore(cfg, 5, 8)
+    p = tmp_path / "s.fstw"
+    o.save(str(p))
+    back = O.OracleStore.load(str(p), 8)
+    assert back.cfg == cfg
+    for n in ("layer.0.wqkv", "layer.1.wffn2t", "layer.1.norm_attn", "embedding", "lm_head"):
+        np.testing.assert_array_equal(back.tensor(n), o.tensor(n))
+    raw = bytearray(p.read_bytes())
+    bad = tmp_path / "bad.fstw"
+    bad.write_bytes(b"\0" * 8 + bytes(raw[8:]))
+    with pytest.raises(ValueError, match="bad magic"):
+        O.OracleStore.load(str(bad), 8)
+    raw2 = bytearray(raw)
+    raw2[8] = 2
+    bad.write_bytes(bytes(raw2))
+    with pytest.raises(ValueError, match="bad version"):
+        O.OracleStore.load(str(bad), 8)
+    bad.write_bytes(bytes(raw[:len(raw) // 2]))
+    with pytest.raises(ValueError, match="truncated|bad tensor"):
+        O.OracleStore.load(str(bad), 8)
+    with pytest.raises(ValueError, match="cannot open"):
+        O.OracleStore.load(str(tmp_path / "missing.fstw"), 8)
+
+
+def test_parallel_forward_is_bit_identical_across_thread_counts():
+    """The OpenMP forward keeps every element's operation order: the same
+    logits for 1 and many threads (and the reference pins the former)."""
+    import subprocess
+    import sys
+    code = ("import sys; sys.path.insert(0, %r); import numpy as np, oracle as O;"
+            "c = O.ModelCfg(2, 512, 1792, 64, 8, 2, 2000, batch=2);"
+            "s = O.OracleStore(c, 4, 80); s.synthetic_prefill(70, 2);"
+            "sys.stdout.buffer.write(s.forward([3, 99], 70).tobytes())"
+            % os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    outs = []
+    for n in ("1", "7"):
+        env = dict(os.environ, OMP_NUM_THREADS=n)
+        outs.append(subprocess.run([sys.executable, "-c", code], env=env, check=True,
+                                   capture_output=True).stdout)
+    assert len(outs[0]) == 2 * 2000 * 8 and outs[0] == outs[1]

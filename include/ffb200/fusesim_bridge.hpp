@@ -107,15 +107,14 @@ public:
         put("final_norm", st.final_norm);
         put("embedding", st.embedding.values);
         put("lm_head", st.lm_head.values);
-        for (int64_t l = 0; l < model_.layers; ++l) {
-            const int64_t n = st.kv.length(l);
-            for (int64_t b = 0; b < model_.batch; ++b)
-                for (int64_t h = 0; h < model_.n_kv_heads; ++h)
-                    for (int64_t p = 0; p < n; ++p)
-                        check(ffb_kv_set(h_, b, l, h, p, st.kv.k_at(b, l, h, p),
-                                         st.kv.v_at(b, l, h, p)));
-            check(ffb_kv_set_length(h_, l, n));
-        }
+        // KVCache keeps one contiguous [B][L][Hkv][S][dh] block per K / V
+        // (tensor_store.hpp:139-148): one bulk import of the longest prefix
+        int64_t n = 0;
+        for (int64_t l = 0; l < model_.layers; ++l) n = std::max(n, st.kv.length(l));
+        if (model_.layers > 0)
+            check(ffb_kv_import(h_, st.kv.k_at(0, 0, 0, 0), st.kv.v_at(0, 0, 0, 0),
+                                st.kv.max_seq_len(), n));
+        for (int64_t l = 0; l < model_.layers; ++l) check(ffb_kv_set_length(h_, l, st.kv.length(l)));
     }
 
     // reference_forward contract: logits[batch][vocab]; store.kv gains the
@@ -126,14 +125,18 @@ public:
             throw ValidationError("reference_forward: one token per batch row required");
         std::vector<float> flat(static_cast<size_t>(model_.batch * model_.vocab_size));
         check(ffb_decode_step(h_, tokens.data(), pos, flat.data(), nullptr, nullptr));
-        const int64_t dh = model_.d_head, nkv = model_.n_kv_heads;
-        for (int64_t l = 0; l < model_.layers; ++l) {
-            std::vector<std::vector<float>> k(model_.batch, std::vector<float>(nkv * dh));
-            std::vector<std::vector<float>> v = k;
-            for (int64_t b = 0; b < model_.batch; ++b)
-                for (int64_t h = 0; h < nkv; ++h)
-                    check(ffb_kv_get(h_, b, l, h, pos, k[b].data() + h * dh,
-                                     v[b].data() + h * dh));
+        // the appended rows of every (batch row, layer, kv head): one bulk
+        // export [B][L][Hkv][1][dh], then KVCache::append_token per layer
+        const int64_t dh = model_.d_head, nkv = model_.n_kv_heads, L = model_.layers;
+        std::vector<float> ka(static_cast<size_t>(model_.batch * L * nkv * dh)), va(ka.size());
+        check(ffb_kv_export(h_, pos, 1, ka.data(), va.data()));
+        for (int64_t l = 0; l < L; ++l) {
+            std::vector<std::vector<float>> k(model_.batch), v(model_.batch);
+            for (int64_t b = 0; b < model_.batch; ++b) {
+                const size_t o = static_cast<size_t>((b * L + l) * nkv * dh);
+                k[b].assign(ka.begin() + o, ka.begin() + o + nkv * dh);
+                v[b].assign(va.begin() + o, va.begin() + o + nkv * dh);
+            }
             if (st.kv.length(l) == pos) st.kv.append_token(l, k, v);
         }
         std::vector<std::vector<float>> out(model_.batch);

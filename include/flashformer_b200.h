@@ -145,6 +145,23 @@ void ffb_destroy(ffb_model *m);
  * ffb_info.quant_inexact_groups). */
 ffb_status ffb_upload_tensor(ffb_model *m, const char *name, const float *values, int64_t n);
 
+/* Weight fixture container: reads a "FSTW" v1 file
+ * written by fusesim::save_store (tensor_store.hpp:410-444) and packs every
+ * record through ffb_upload_tensor -- the drop-in for load_store
+ * (tensor_store.hpp:446-482) without a host TensorStore.  The file's model
+ * shape must equal the handle's (batch, dtype and quant fields may differ:
+ * values are packed into the handle's format).  FFB_USAGE on a bad magic /
+ * version / truncated record, FFB_VALIDATION on a shape mismatch. */
+ffb_status ffb_load_store(ffb_model *m, const char *path);
+
+/* Packed device image cache: every streamed matrix, norm and the embedding
+ * exactly as the kernel reads them (after the packer, TP slicing, chunk-major
+ * swizzle, quant grid re-derivation), plus a header naming the model, the TP
+ * shard and the kernel specialisation.  ffb_load_image refuses an image of
+ * another shape / shard / specialisation (FFB_VALIDATION). */
+ffb_status ffb_save_image(ffb_model *m, const char *path);
+ffb_status ffb_load_image(ffb_model *m, const char *path);
+
 /* Fills every weight on the device with seeded synthetic values of the right
  * scale (bench / smoke use; no host arrays involved). */
 ffb_status ffb_init_synthetic(ffb_model *m, uint64_t seed);
@@ -158,6 +175,12 @@ ffb_status ffb_kv_get(ffb_model *m, int64_t b, int64_t layer, int64_t head, int6
 /* Bulk import of the reference layout [B][L][Hkv][S_src][dh] f32, positions [0, n_pos). */
 ffb_status ffb_kv_import(ffb_model *m, const float *k, const float *v, int64_t src_max_seq,
                          int64_t n_pos);
+/* Bulk export of positions [pos0, pos0 + n_pos) in the reference layout
+ * [B][L][Hkv][n_pos][dh] f32 (KVCache::k_at / v_at, tensor_store.hpp:109-125;
+ * a TP rank exports its own kv heads).  One gather kernel and one
+ * device-to-host copy per call (chunked when the block exceeds 32 MiB);
+ * synchronous. */
+ffb_status ffb_kv_export(ffb_model *m, int64_t pos0, int64_t n_pos, float *k_out, float *v_out);
 ffb_status ffb_kv_set_length(ffb_model *m, int64_t layer, int64_t n);
 int64_t ffb_kv_length(const ffb_model *m, int64_t layer);
 

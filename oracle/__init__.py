@@ -137,6 +137,7 @@ def lib():
         L.fo_normal_f64.argtypes = [C.c_uint64, C.c_double, C.c_double, C.POINTER(C.c_double),
                                     C.c_int64]
         L.fo_save_store.argtypes = [C.POINTER(FoStore), C.c_char_p]
+        L.fo_store_set_batch.argtypes = [C.POINTER(FoStore), C.c_int64, C.c_int64]
         L.fo_load_store.restype = C.POINTER(FoStore)
         L.fo_load_store.argtypes = [C.c_char_p, C.c_int64]
         L.fo_serialize_config.restype = C.c_int64
@@ -174,6 +175,15 @@ class OracleStore:
         self._c = self.cfg.c()
         self.max_seq_len = max_seq_len
         return self
+
+    def set_batch(self, batch: int, max_seq_len: int | None = None):
+        """Keep the weights, start an empty KV cache for `batch` rows."""
+        n = max_seq_len or self.max_seq_len
+        if lib().fo_store_set_batch(self._s, batch, n) != 0:
+            raise ValueError(lib().fo_last_error().decode())
+        self.cfg = self.cfg.replace(batch=batch)
+        self._c = self.cfg.c()
+        self.max_seq_len = n
 
     def save(self, path: str):
         """save_store (tensor_store.hpp:410-444), FSTW v1."""

@@ -571,17 +571,42 @@ int fo_attn_reduce(const double *m, const double *l, const double *o, int64_t n_
 /* ------------------------------------------------------------------ */
 /* reference_forward (reference.hpp:37-139)                             */
 /* ------------------------------------------------------------------ */
-/* Parallel over output rows (OpenMP): every row is still one sequential
- * f64 dot product in column order, so results are bit-identical to the
- * single-threaded reference for any thread count. */
-static void matvec_rows(const float *w, int64_t rows, int64_t cols, const double *u, double *y) {
+/* y[b * ystride + r] = sum_c w[r][c] * u_b[c] for every batch row b at once
+ * (reference.hpp:21-30).  ut holds the inputs transposed, [cols][B], so one
+ * pass over a weight row feeds every batch row.  Each (r, b) is still one
+ * sequential f64 sum in column order with a separately rounded product
+ * (-ffp-contract=off), so the result is bit-identical to the reference's
+ * per-row loop for any thread count. */
+#define FO_BBLK 16
+static void matvec_batch(const float *w, int64_t rows, int64_t cols, const double *ut, int64_t B,
+                         double *y, int64_t ystride) {
 #pragma omp parallel for schedule(static)
-    for (int64_t r = 0; r < rows; ++r) { /* reference.hpp:21-30 */
+    for (int64_t r = 0; r < rows; ++r) {
         const float *row = w + r * cols;
-        double acc = 0.0;
-        for (int64_t c = 0; c < cols; ++c) acc += (double)row[c] * u[c];
-        y[r] = acc;
+        for (int64_t b0 = 0; b0 < B; b0 += FO_BBLK) {
+            const int64_t nb = B - b0 < FO_BBLK ? B - b0 : FO_BBLK;
+            double acc[FO_BBLK] = {0};
+            if (nb == FO_BBLK) { /* fixed trip count: accumulators stay in registers */
+                for (int64_t c = 0; c < cols; ++c) {
+                    const double wc = (double)row[c];
+                    const double *uc = ut + c * B + b0;
+                    for (int b = 0; b < FO_BBLK; ++b) acc[b] += wc * uc[b];
+                }
+            } else {
+                for (int64_t c = 0; c < cols; ++c) {
+                    const double wc = (double)row[c];
+                    const double *uc = ut + c * B + b0;
+                    for (int64_t b = 0; b < nb; ++b) acc[b] += wc * uc[b];
+                }
+            }
+            for (int64_t b = 0; b < nb; ++b) y[(b0 + b) * ystride + r] = acc[b];
+        }
     }
+}
+
+static void transpose_in(const double *u, int64_t B, int64_t n, double *ut) { /* [B][n] -> [n][B] */
+    for (int64_t b = 0; b < B; ++b)
+        for (int64_t i = 0; i < n; ++i) ut[i * B + b] = u[b * n + i];
 }
 
 static void widen(const float *src, int64_t n, double *dst) {
@@ -592,29 +617,35 @@ int fo_reference_forward(fo_store *s, const int64_t *tokens, int64_t pos, double
     return fo_reference_forward_ex(s, tokens, pos, logits, NULL, NULL);
 }
 
+/* reference_forward (reference.hpp:37-139).  The reference walks the batch
+ * rows one after another inside each layer; rows never interact (only the
+ * KV append, which lands for every row before any attention reads it), so
+ * this restatement runs them side by side -- same per-element arithmetic,
+ * one pass over each weight matrix per layer. */
 int fo_reference_forward_ex(fo_store *s, const int64_t *tokens, int64_t pos, double *logits,
                             const float *k_app, const float *v_app) {
     const fo_config *m = &s->cfg;
     const int64_t B = m->batch, D = m->d_model, dh = m->d_head, nq = m->n_q_heads,
-                  nkv = m->n_kv_heads, qpg = nq / nkv, V = m->vocab_size;
+                  nkv = m->n_kv_heads, qpg = nq / nkv, V = m->vocab_size, DI = m->d_inter;
     const double alpha = 1.0 / sqrt((double)dh);
     for (int64_t b = 0; b < B; ++b)
         if (tokens[b] < 0 || tokens[b] >= V) {
             set_err("reference_forward: token id out of range");
             return 2;
         }
+    const int64_t qkvr = fo_qkv_rows(m);
+    const int64_t DIc = DI > 0 ? DI : 1;
     double *x = (double *)malloc(sizeof(double) * (size_t)(B * D));
-    double *u = (double *)malloc(sizeof(double) * (size_t)D);
+    double *u = (double *)malloc(sizeof(double) * (size_t)(B * D));
+    double *ut = (double *)malloc(sizeof(double) * (size_t)(B * (D > nq * dh ? D : nq * dh)));
     double *w = (double *)malloc(sizeof(double) * (size_t)D);
-    int64_t qkvr = fo_qkv_rows(m);
-    double *qkv = (double *)malloc(sizeof(double) * (size_t)qkvr);
-    double *q = (double *)malloc(sizeof(double) * (size_t)(B * nq * dh));
+    double *qkv = (double *)malloc(sizeof(double) * (size_t)(B * qkvr));
     float *krow = (float *)malloc(sizeof(float) * (size_t)(B * nkv * dh));
     float *vrow = (float *)malloc(sizeof(float) * (size_t)(B * nkv * dh));
-    double *attn = (double *)malloc(sizeof(double) * (size_t)(nq * dh));
-    double *aout = (double *)malloc(sizeof(double) * (size_t)D);
+    double *attn = (double *)malloc(sizeof(double) * (size_t)(B * nq * dh));
+    double *aout = (double *)malloc(sizeof(double) * (size_t)(B * D));
     double *scores = (double *)malloc(sizeof(double) * (size_t)(nq * (pos + 1)));
-    double *hbuf = (double *)malloc(sizeof(double) * (size_t)(m->d_inter > 0 ? m->d_inter : 1));
+    double *hbuf = (double *)malloc(sizeof(double) * (size_t)(DIc * B));
     int rc = 0;
 
     for (int64_t b = 0; b < B; ++b) widen(s->embedding + tokens[b] * D, D, x + b * D);
@@ -626,18 +657,19 @@ int fo_reference_forward_ex(fo_store *s, const int64_t *tokens, int64_t pos, dou
             rc = 2;
             goto done;
         }
+        widen(lw->norm_attn, D, w);
+        for (int64_t b = 0; b < B; ++b) fo_rmsnorm_f64(x + b * D, w, D, m->rmsnorm_eps, u + b * D);
+        transpose_in(u, B, D, ut);
+        matvec_batch(lw->wqkv, qkvr, D, ut, B, qkv, qkvr);
         for (int64_t b = 0; b < B; ++b) {
-            widen(lw->norm_attn, D, w);
-            fo_rmsnorm_f64(x + b * D, w, D, m->rmsnorm_eps, u);
-            matvec_rows(lw->wqkv, qkvr, D, u, qkv);
-            memcpy(q + b * nq * dh, qkv, sizeof(double) * (size_t)(nq * dh));
-            for (int64_t h = 0; h < nq; ++h) fo_rope_f64(q + b * nq * dh + h * dh, dh, pos, m->rope_theta);
+            double *qb = qkv + b * qkvr;
+            for (int64_t h = 0; h < nq; ++h) fo_rope_f64(qb + h * dh, dh, pos, m->rope_theta);
             for (int64_t h = 0; h < nkv; ++h) {
-                double *k = qkv + (nq + h) * dh;
+                double *k = qb + (nq + h) * dh;
                 fo_rope_f64(k, dh, pos, m->rope_theta);
                 for (int64_t d = 0; d < dh; ++d) {
                     krow[b * nkv * dh + h * dh + d] = (float)k[d];
-                    vrow[b * nkv * dh + h * dh + d] = (float)qkv[(nq + nkv + h) * dh + d];
+                    vrow[b * nkv * dh + h * dh + d] = (float)qb[(nq + nkv + h) * dh + d];
                 }
             }
         }
@@ -661,12 +693,13 @@ int fo_reference_forward_ex(fo_store *s, const int64_t *tokens, int64_t pos, dou
         s->kv_len[l] += 1;
 
         for (int64_t b = 0; b < B; ++b) {
-            for (int64_t i = 0; i < nq * dh; ++i) attn[i] = 0.0;
+            double *ab = attn + b * nq * dh;
+            for (int64_t i = 0; i < nq * dh; ++i) ab[i] = 0.0;
             /* heads are independent: one per thread, each with its own score row */
 #pragma omp parallel for schedule(dynamic, 1)
             for (int64_t h = 0; h < nq; ++h) {
                 int64_t kvh = h / qpg;
-                const double *qh = q + b * nq * dh + h * dh;
+                const double *qh = qkv + b * qkvr + h * dh;
                 int64_t n = pos + 1;
                 double *sc = scores + h * (pos + 1);
                 double mx = -INFINITY;
@@ -682,47 +715,57 @@ int fo_reference_forward_ex(fo_store *s, const int64_t *tokens, int64_t pos, dou
                 for (int64_t j = 0; j < n; ++j) {
                     double wj = exp(sc[j] - mx) / denom;
                     const float *vj = fo_v_at(s, b, l, kvh, j);
-                    for (int64_t d = 0; d < dh; ++d) attn[h * dh + d] += wj * (double)vj[d];
+                    for (int64_t d = 0; d < dh; ++d) ab[h * dh + d] += wj * (double)vj[d];
                 }
             }
-            matvec_rows(lw->waout, D, D, attn, aout);
-            double *xb = x + b * D;
-            for (int64_t k = 0; k < D; ++k) xb[k] += aout[k];
+        }
+        transpose_in(attn, B, nq * dh, ut);
+        matvec_batch(lw->waout, D, nq * dh, ut, B, aout, D);
+        for (int64_t i = 0; i < B * D; ++i) x[i] += aout[i];
 
-            widen(lw->norm_ffn, D, w);
-            fo_rmsnorm_f64(xb, w, D, m->rmsnorm_eps, u);
-            /* reference.hpp:114-128 in two parallel passes with the same
-             * per-element operation order: h[t] for every pair t, then
-             * xb[k] += h[t] * wffn2t[t][k] in increasing t for each k. */
+        /* reference.hpp:114-128 in two parallel passes with the same
+         * per-element operation order: h[t] for every pair t, then
+         * x[k] += h[t] * wffn2t[t][k] in increasing t for each k. */
+        widen(lw->norm_ffn, D, w);
+        for (int64_t b = 0; b < B; ++b) fo_rmsnorm_f64(x + b * D, w, D, m->rmsnorm_eps, u + b * D);
+        transpose_in(u, B, D, ut);
 #pragma omp parallel for schedule(static)
-            for (int64_t t = 0; t < m->d_inter; ++t) {
-                const float *in_row = lw->wffn1 + (2 * t) * D;
-                const float *gate_row = lw->wffn1 + (2 * t + 1) * D;
-                double a = 0, g = 0;
+        for (int64_t t = 0; t < DI; ++t) {
+            const float *in_row = lw->wffn1 + (2 * t) * D;
+            const float *gate_row = lw->wffn1 + (2 * t + 1) * D;
+            for (int64_t b0 = 0; b0 < B; b0 += FO_BBLK) {
+                const int64_t nb = B - b0 < FO_BBLK ? B - b0 : FO_BBLK;
+                double a[FO_BBLK] = {0}, g[FO_BBLK] = {0};
                 for (int64_t c = 0; c < D; ++c) {
-                    a += (double)in_row[c] * u[c];
-                    g += (double)gate_row[c] * u[c];
+                    const double wi = (double)in_row[c], wg = (double)gate_row[c];
+                    const double *uc = ut + c * B + b0;
+                    for (int64_t b = 0; b < nb; ++b) {
+                        a[b] += wi * uc[b];
+                        g[b] += wg * uc[b];
+                    }
                 }
-                hbuf[t] = fo_silu(g) * a;
+                for (int64_t b = 0; b < nb; ++b) hbuf[t * B + b0 + b] = fo_silu(g[b]) * a[b];
             }
+        }
 #pragma omp parallel for schedule(static)
-            for (int64_t k0 = 0; k0 < D; k0 += 64) {
-                int64_t k1 = k0 + 64 < D ? k0 + 64 : D;
-                for (int64_t t = 0; t < m->d_inter; ++t) {
-                    const double hh = hbuf[t];
-                    const float *col = lw->wffn2t + t * D;
+        for (int64_t k0 = 0; k0 < D; k0 += 64) {
+            int64_t k1 = k0 + 64 < D ? k0 + 64 : D;
+            for (int64_t t = 0; t < DI; ++t) {
+                const float *col = lw->wffn2t + t * D;
+                for (int64_t b = 0; b < B; ++b) {
+                    const double hh = hbuf[t * B + b];
+                    double *xb = x + b * D;
                     for (int64_t k = k0; k < k1; ++k) xb[k] += hh * (double)col[k];
                 }
             }
         }
     }
-    for (int64_t b = 0; b < B; ++b) {
-        widen(s->final_norm, D, w);
-        fo_rmsnorm_f64(x + b * D, w, D, m->rmsnorm_eps, u);
-        matvec_rows(s->lm_head, V, D, u, logits + b * V);
-    }
+    widen(s->final_norm, D, w);
+    for (int64_t b = 0; b < B; ++b) fo_rmsnorm_f64(x + b * D, w, D, m->rmsnorm_eps, u + b * D);
+    transpose_in(u, B, D, ut);
+    matvec_batch(s->lm_head, V, D, ut, B, logits, V);
 done:
-    free(x); free(u); free(w); free(qkv); free(q); free(krow); free(vrow);
+    free(x); free(u); free(ut); free(w); free(qkv); free(krow); free(vrow);
     free(attn); free(aout); free(scores); free(hbuf);
     return rc;
 }
@@ -1018,4 +1061,23 @@ fail:
     fo_free(s);
     fclose(f);
     return NULL;
+}
+
+/* Same weights, a new batch size: the KV cache is reallocated empty (the
+ * weights of a TensorStore do not depend on the batch, tensor_store.hpp:
+ * 304-366; only KVCache(model, max_seq_len) does). */
+int fo_store_set_batch(fo_store *s, int64_t batch, int64_t max_seq_len) {
+    if (batch < 1) { set_err("model: batch must be positive"); return 2; }
+    const fo_config *c = &s->cfg;
+    size_t kv = (size_t)batch * c->layers * c->n_kv_heads * max_seq_len * c->d_head;
+    float *k = alloc_f32((int64_t)kv), *v = alloc_f32((int64_t)kv);
+    if (!k || !v) { free(k); free(v); set_err("set_batch: out of memory"); return 1; }
+    free(s->k);
+    free(s->v);
+    s->k = k;
+    s->v = v;
+    s->cfg.batch = batch;
+    s->max_seq_len = max_seq_len;
+    for (int64_t l = 0; l < c->layers; ++l) s->kv_len[l] = 0;
+    return 0;
 }

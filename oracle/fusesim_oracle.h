@@ -99,6 +99,8 @@ void fo_free(fo_store *s);
 int64_t fo_serialize_config(const fo_config *c, char *out, int64_t cap);
 /* save_store: byte-identical to the reference's file for the decoder kind. */
 int fo_save_store(const fo_store *s, const char *path);
+/* same weights, new batch size: empty KV cache [batch][L][Hkv][max_seq_len][dh] */
+int fo_store_set_batch(fo_store *s, int64_t batch, int64_t max_seq_len);
 /* load_store: NULL + fo_last_error() on a bad magic / version / record. */
 fo_store *fo_load_store(const char *path, int64_t max_seq_len);
 int64_t fo_qkv_rows(const fo_config *c);

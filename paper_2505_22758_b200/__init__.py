@@ -305,6 +305,10 @@ def lib():
     L.ffb_kv_set.argtypes = [C.c_void_p] + [C.c_int64] * 4 + [P(C.c_float)] * 2
     L.ffb_kv_get.argtypes = [C.c_void_p] + [C.c_int64] * 4 + [P(C.c_float)] * 2
     L.ffb_kv_import.argtypes = [C.c_void_p, P(C.c_float), P(C.c_float), C.c_int64, C.c_int64]
+    L.ffb_kv_export.argtypes = [C.c_void_p, C.c_int64, C.c_int64, P(C.c_float), P(C.c_float)]
+    L.ffb_load_store.argtypes = [C.c_void_p, C.c_char_p]
+    L.ffb_save_image.argtypes = [C.c_void_p, C.c_char_p]
+    L.ffb_load_image.argtypes = [C.c_void_p, C.c_char_p]
     L.ffb_kv_set_length.argtypes = [C.c_void_p, C.c_int64, C.c_int64]
     L.ffb_kv_length.argtypes = [C.c_void_p, C.c_int64]
     L.ffb_kv_length.restype = C.c_int64
@@ -422,6 +426,19 @@ class DecodeModel:
     def init_synthetic(self, seed: int = 1234):
         _check(lib().ffb_init_synthetic(self._h, seed))
 
+    def load_store(self, path: str):
+        """Pack a fusesim "FSTW" v1 store file (save_store, tensor_store.hpp:
+        410-444) into the device weights (ffb_load_store)."""
+        _check(lib().ffb_load_store(self._h, os.fsencode(path)))
+
+    def save_image(self, path: str):
+        """Write the packed device weights (ffb_save_image)."""
+        _check(lib().ffb_save_image(self._h, os.fsencode(path)))
+
+    def load_image(self, path: str):
+        """Reload a packed device image of the same model / shard / kernel."""
+        _check(lib().ffb_load_image(self._h, os.fsencode(path)))
+
     # ------------------------------------------------------------ KV cache
     def kv_set(self, b, layer, head, pos, k, v):
         k = np.ascontiguousarray(k, np.float32)
@@ -433,6 +450,16 @@ class DecodeModel:
         k = np.empty(dh, np.float32)
         v = np.empty(dh, np.float32)
         _check(lib().ffb_kv_get(self._h, b, layer, head, pos, _fp(k), _fp(v)))
+        return k, v
+
+    def kv_export(self, pos0: int, n_pos: int = 1):
+        """Positions [pos0, pos0 + n_pos) as (K, V) f32 [B][L][Hkv][n_pos][dh]
+        (ffb_kv_export; one gather + one copy)."""
+        c = self.cfg
+        shp = (c.batch, c.layers, c.n_kv_heads // self.tp_size, n_pos, c.d_head)
+        k = np.empty(shp, np.float32)
+        v = np.empty(shp, np.float32)
+        _check(lib().ffb_kv_export(self._h, pos0, n_pos, _fp(k), _fp(v)))
         return k, v
 
     def kv_import(self, k: np.ndarray, v: np.ndarray, n_pos: int):

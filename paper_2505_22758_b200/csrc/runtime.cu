@@ -21,17 +21,18 @@
 #include <cstdio>
 #include <cstring>
 #include <mutex>
+#include <thread>
 #include <string>
 #include <vector>
 
 #include <unistd.h>
 
 #include "../../include/flashformer_b200.h"
-#include "kernel_ops.cuh"
+#include "model.cuh"
 
 using namespace ffb200;
 
-namespace {
+namespace ffb200 {
 
 thread_local std::string g_err;
 
@@ -45,13 +46,9 @@ ffb_status fail(ffb_status s, const char* fmt, ...) {
     return s;
 }
 
-#define CUDA_TRY(expr)                                                                 \
-    do {                                                                               \
-        cudaError_t e_ = (expr);                                                       \
-        if (e_ != cudaSuccess)                                                         \
-            return fail(FFB_DEVICE, "%s: %s (%s:%d)", #expr, cudaGetErrorString(e_),  \
-                        __FILE__, __LINE__);                                           \
-    } while (0)
+}  // namespace ffb200
+
+namespace {
 
 const std::vector<KernelOps>& registry() {
     static std::vector<KernelOps> v;
@@ -205,6 +202,22 @@ __global__ void synth_f32_kernel(float* dst, int64_t n, uint64_t seed, float mea
 
 int64_t split_at(int64_t units, int64_t c, int64_t grid) { return (units * c) / grid; }
 
+// fn(r0, r1) over [0, n) split into contiguous blocks on the host's cores
+// (the packer: quant grid re-derivation, transposes, chunk-major swizzles).
+template <class F>
+void parallel_rows(int64_t n, F fn) {
+    const int64_t hw = std::max(1u, std::thread::hardware_concurrency());
+    const int64_t nt = std::min<int64_t>(std::min<int64_t>(hw, 32), std::max<int64_t>(1, n / 64));
+    if (nt <= 1) {
+        fn(int64_t{0}, n);
+        return;
+    }
+    std::vector<std::thread> th;
+    for (int64_t t = 0; t < nt; ++t)
+        th.emplace_back([&, t] { fn(n * t / nt, n * (t + 1) / nt); });
+    for (auto& x : th) x.join();
+}
+
 // One CTA per SM (the decode kernel's shared memory): which SM ids exist.
 __global__ void smid_probe_kernel(int32_t* out) {
     extern __shared__ uint8_t probe_smem[];
@@ -223,105 +236,20 @@ int64_t kv_swz(int64_t d, int64_t pos) { return (((d >> 3) ^ (pos & 7)) << 3) | 
 
 }  // namespace
 
-constexpr int kMaxTP = 8;
-
-struct ffb_model {
-    ffb_model_config cfg{};   // this shard's config (== gcfg when tp_size == 1)
-    ffb_model_config gcfg{};  // the whole model
-    int64_t vocab_base = 0;   // first global vocab row of this shard's lm_head
-    // tensor-parallel exchange (decode_kernel.cuh: tp_exchange_add)
-    float* xch = nullptr;           // [2][2][B][D] + [kMaxTP][B][2]
-    uint32_t* xflag = nullptr;      // [L][2][grid] + 1
-    size_t xch_bytes = 0, xflag_bytes = 0;
-    float* peer_xch[kMaxTP] = {};
-    uint32_t* peer_xflag[kMaxTP] = {};
-    bool tp_connected = false;
-    std::vector<void*> ipc_opened;
-    const KernelOps* ops = nullptr;
-    int device = 0, grid = 0, tp_rank = 0, tp_size = 1;
-    int64_t max_seq = 0;
-    int attn_group = 0, n_units = 0;
-    ffb_mode mode = FFB_MODE_FUSED_OVERLAP;
-    int32_t debug = 0;
-    uint64_t* trace = nullptr;  // per-CTA stage timestamps (ffb_set_trace)
-    // per-CTA L2 prefetch window (ffb_set_option), issued only while the
-    // producer is blocked on a full ring in S_ATTN / S_AOUT (the attention
-    // latency chain, when HBM would otherwise idle); measured -2% on the 8B
-    // shape at 512 KiB, while prefetching during the streaming-bound GLU
-    // stage costs up to +8% (profiles/summary_r01.md)
-    int64_t l2_prefetch = 512 << 10;
-    int32_t l2_pf_stages = (1 << S_ATTN) | (1 << S_AOUT);
-    int32_t kv_prefetch = 0;          // option "kv_prefetch" (measured +1.5 %: off)
-    int plan_reverse = 0;             // weight slices assigned in reverse CTA order
-    int attn_group_max = 0;           // option "attn_group_max": cap on CTAs per attention unit (0: auto)
-    // per-SM plan weights (ffb_calibrate): streamed-row shares of QKV / AOUT /
-    // GLU / LM head proportional to each SM's measured streaming rate
-    std::vector<double> sm_weight;
-    std::vector<CtaPlan> plan_host;
-    int16_t* sm_rank = nullptr;       // device [max smid + 1] -> dense rank, or null
-    int calib_mask = 0xf;             // option "calib_mask": matrices using the weights
-    int use_sm_rank = 1;              // option "sm_rank": plans follow SM ids
-    int64_t pool_permille = 0;        // share of d_inter in the dynamic GLU pool (off)
-    int64_t pool_ct_pref = 4;         // preferred pairs per pool chunk
-    int pool_t0 = 0, pool_ct = 0, pool_chunks = 0, pool_chunks_max = 0;
-    float* pool_part = nullptr;
-    uint32_t* pool_counters = nullptr;
-    uint32_t epoch = 0;
-    cudaStream_t stream = nullptr;
-    std::vector<int64_t> kv_len;
-    std::vector<void*> allocs;
-    uint64_t device_bytes = 0;
-
-    // streamed matrices: rows of ops->row_bytes (bf16 or packed int4/int8)
-    uint8_t *wqkv = nullptr, *waout = nullptr, *wffn1 = nullptr, *wffn2t = nullptr,
-            *lm_head = nullptr;
-    __nv_bfloat16 *embedding = nullptr, *kcache = nullptr, *vcache = nullptr;
-    uint64_t quant_inexact_groups = 0;  // packer: groups not on a 4/8-bit grid (lossy)
-    uint8_t* wlin = nullptr;            // stacked linear: [L][D] bf16 rows
-    float* xbuf = nullptr;              // stacked linear: [2][B][D]
-    float *norm_attn = nullptr, *norm_ffn = nullptr, *final_norm = nullptr;
-    uint8_t *xfrag_a = nullptr, *xfrag_f = nullptr, *afrag = nullptr, *hfrag = nullptr;  // batch >= 8
-    float* ssq = nullptr;                                                               // [2][grid][B]
-    float *x = nullptr, *q = nullptr, *attn_out = nullptr, *glu_part = nullptr,
-          *attn_part = nullptr, *logits = nullptr, *amax_val = nullptr;
-    int32_t* amax_idx = nullptr;
-    int64_t *greedy = nullptr, *tokens_dev = nullptr;
-    uint32_t *counters = nullptr, *head_counters = nullptr, *amax_counter = nullptr,
-             *qkv_head_counters = nullptr;
-    CtaPlan* plan = nullptr;
-    int64_t* tokens_pinned = nullptr;
-    int64_t* greedy_pinned = nullptr;
-    float* logits_pinned = nullptr;
-    float* staging = nullptr;  // f32 upload staging
-    static constexpr int64_t kStagingElems = 8 << 20;
-
-    int64_t qkv_rows() const { return (cfg.n_q_heads + 2 * cfg.n_kv_heads) * cfg.d_head; }
-
-    template <class Tp>
-    ffb_status alloc(Tp** p, size_t count) {
-        void* ptr = nullptr;
-        size_t bytes = std::max<size_t>(count * sizeof(Tp), 256);
-        cudaError_t e = cudaMalloc(&ptr, bytes);
-        if (e != cudaSuccess)
-            return fail(FFB_DEVICE, "cudaMalloc(%zu bytes): %s", bytes, cudaGetErrorString(e));
-        allocs.push_back(ptr);
-        device_bytes += bytes;
-        *p = static_cast<Tp*>(ptr);
-        return FFB_OK;
-    }
-
-    ~ffb_model() {
-        if (device >= 0) cudaSetDevice(device);
-        for (void* q : ipc_opened) cudaIpcCloseMemHandle(q);
-        for (void* p : allocs) cudaFree(p);
-        if (tokens_pinned) cudaFreeHost(tokens_pinned);
-        if (greedy_pinned) cudaFreeHost(greedy_pinned);
-        if (logits_pinned) cudaFreeHost(logits_pinned);
-        if (stream) cudaStreamDestroy(stream);
-    }
-};
 
 namespace {
+
+// The plan is read by every launch on any stream: wait for in-flight steps,
+// copy it on the handle's stream and wait for the copy to land (a pageable
+// cudaMemcpy on the legacy stream returns before its DMA completes and does
+// not order against the non-blocking handle stream).
+ffb_status upload_plan(ffb_model* m) {
+    CUDA_TRY(cudaDeviceSynchronize());
+    CUDA_TRY(cudaMemcpyAsync(m->plan, m->plan_host.data(), sizeof(CtaPlan) * m->plan_host.size(),
+                             cudaMemcpyHostToDevice, m->stream));
+    CUDA_TRY(cudaStreamSynchronize(m->stream));
+    return FFB_OK;
+}
 
 ffb_status build_plan(ffb_model* m) {
     const auto& c = m->cfg;
@@ -341,9 +269,8 @@ ffb_status build_plan(ffb_model* m) {
         }
         m->n_units = 0;
         m->attn_group = 0;
-        CUDA_TRY(cudaMemcpy(m->plan, plan.data(), sizeof(CtaPlan) * G, cudaMemcpyHostToDevice));
         m->plan_host = plan;
-        return FFB_OK;
+        return upload_plan(m);
     }
     m->n_units = static_cast<int>(c.batch * c.n_kv_heads);
     if (m->n_units > G) return fail(FFB_UNSUPPORTED, "batch * n_kv_heads exceeds the SM count");
@@ -427,9 +354,8 @@ ffb_status build_plan(ffb_model* m) {
         const int h = p.attn_unit % static_cast<int>(c.n_kv_heads);
         for (int64_t j = 0; j < G; ++j) p.attn_dep += (plan[j].qkv_heads >> h) & 1;
     }
-    CUDA_TRY(cudaMemcpy(m->plan, plan.data(), sizeof(CtaPlan) * G, cudaMemcpyHostToDevice));
     m->plan_host = plan;
-    return FFB_OK;
+    return upload_plan(m);
 }
 
 // SM id -> dense rank table for persistent launches (decode_kernel.cuh:
@@ -473,6 +399,7 @@ ffb_status probe_sm_ranks(ffb_model* m) {
     if (st) return st;
     CUDA_TRY(cudaMemcpy(m->sm_rank, table.data(), sizeof(int16_t) * table.size(),
                         cudaMemcpyHostToDevice));
+    CUDA_TRY(cudaDeviceSynchronize());
     return FFB_OK;
 }
 
@@ -1083,6 +1010,7 @@ ffb_status ffb_upload_tensor(ffb_model* m, const char* name, const float* values
     CUDA_TRY(cudaSetDevice(m->device));
     if (d.kind == 1) {
         CUDA_TRY(cudaMemcpy(d.ptr, values, sizeof(float) * n, cudaMemcpyHostToDevice));
+        CUDA_TRY(cudaDeviceSynchronize());  // landed before any stream reads it
         return FFB_OK;
     }
     // the shard's rows / columns as one contiguous f32 block (no copy at TP 1)
@@ -1100,12 +1028,14 @@ ffb_status ffb_upload_tensor(ffb_model* m, const char* name, const float* values
     }
     if (d.transpose) {  // [lrows][cols] -> [cols][lrows]
         std::vector<float> tr((size_t)lrows * cols);
-        constexpr int64_t TB = 64;  // cache-blocked
-        for (int64_t r0 = 0; r0 < lrows; r0 += TB)
-            for (int64_t k0 = 0; k0 < cols; k0 += TB)
-                for (int64_t r = r0; r < std::min(lrows, r0 + TB); ++r)
-                    for (int64_t k = k0; k < std::min(cols, k0 + TB); ++k)
-                        tr[(size_t)k * lrows + r] = src[(size_t)r * cols + k];
+        constexpr int64_t TB = 64;  // cache-blocked, blocks of output rows per thread
+        parallel_rows((cols + TB - 1) / TB, [&](int64_t b0, int64_t b1) {
+            for (int64_t k0 = b0 * TB; k0 < std::min(cols, b1 * TB); k0 += TB)
+                for (int64_t r0 = 0; r0 < lrows; r0 += TB)
+                    for (int64_t r = r0; r < std::min(lrows, r0 + TB); ++r)
+                        for (int64_t k = k0; k < std::min(cols, k0 + TB); ++k)
+                            tr[(size_t)k * lrows + r] = src[(size_t)r * cols + k];
+        });
         shard.swap(tr);
         src = shard.data();
         std::swap(lrows, cols);
@@ -1117,29 +1047,37 @@ ffb_status ffb_upload_tensor(ffb_model* m, const char* name, const float* values
         // 2^-24 absolute below it), the tensor-core GEMV's operand type
         const int64_t KC = m->ops->kc, nch = cols / KC;
         std::vector<float> cm((size_t)lrows * cols);
-        for (int64_t r = 0; r < lrows; ++r)
-            for (int64_t c = 0; c < nch; ++c) {
-                float* dst = cm.data() + ((size_t)c * lrows + r) * KC;
-                const float* s0 = src + (size_t)r * cols + c * KC;
-                for (int64_t u = 0; u < KC / 8; ++u)
-                    std::memcpy(dst + ((u ^ (r & 7)) * 8), s0 + u * 8, sizeof(float) * 8);
-            }
+        parallel_rows(lrows, [&](int64_t ra, int64_t rb) {
+            for (int64_t r = ra; r < rb; ++r)
+                for (int64_t c = 0; c < nch; ++c) {
+                    float* dst = cm.data() + ((size_t)c * lrows + r) * KC;
+                    const float* s0 = src + (size_t)r * cols + c * KC;
+                    for (int64_t u = 0; u < KC / 8; ++u)
+                        std::memcpy(dst + ((u ^ (r & 7)) * 8), s0 + u * 8, sizeof(float) * 8);
+                }
+        });
         shard.swap(cm);
         src = shard.data();
     }
     if (d.kind == 0 && m->ops->QB != 0) {  // quant packer, a block of rows at a time
         const size_t rb = d.row_bytes;
-        const int64_t rows_per = std::max<int64_t>(1, (4 << 20) / (int64_t)rb);
+        const int64_t rows_per = std::max<int64_t>(1, (64 << 20) / (int64_t)rb);
         std::vector<uint8_t> buf(rows_per * rb);
         auto* dst = static_cast<uint8_t*>(d.ptr);
         for (int64_t r0 = 0; r0 < lrows; r0 += rows_per) {
             const int64_t nr = std::min(rows_per, lrows - r0);
-            for (int64_t r = 0; r < nr; ++r)
-                m->quant_inexact_groups += pack_quant_row(src + (r0 + r) * cols, cols,
-                                                          m->ops->QB, buf.data() + r * rb, rb,
-                                                          d.layout);
+            std::mutex mu;
+            parallel_rows(nr, [&](int64_t ra, int64_t rb2) {
+                int64_t n = 0;
+                for (int64_t r = ra; r < rb2; ++r)
+                    n += pack_quant_row(src + (r0 + r) * cols, cols, m->ops->QB,
+                                        buf.data() + r * rb, rb, d.layout);
+                std::lock_guard<std::mutex> g(mu);
+                m->quant_inexact_groups += n;
+            });
             CUDA_TRY(cudaMemcpy(dst + r0 * rb, buf.data(), nr * rb, cudaMemcpyHostToDevice));
         }
+        CUDA_TRY(cudaDeviceSynchronize());  // landed before any stream reads it
         return FFB_OK;
     }
     const int64_t ln = lrows * cols;
@@ -1231,6 +1169,7 @@ ffb_status ffb_kv_set(ffb_model* m, int64_t b, int64_t layer, int64_t head, int6
     const size_t off = kv_offset(m, b, layer, head, pos);
     CUDA_TRY(cudaMemcpy(m->kcache + off, kb.data(), 2 * c.d_head, cudaMemcpyHostToDevice));
     CUDA_TRY(cudaMemcpy(m->vcache + off, vb.data(), 2 * c.d_head, cudaMemcpyHostToDevice));
+    CUDA_TRY(cudaDeviceSynchronize());  // landed before any stream reads it
     return FFB_OK;
 }
 
@@ -1282,6 +1221,7 @@ ffb_status ffb_kv_import(ffb_model* m, const float* k, const float* v, int64_t s
                 CUDA_TRY(cudaMemcpy(m->vcache + off, vb.data(), 2 * n_pos * c.d_head,
                                     cudaMemcpyHostToDevice));
             }
+    CUDA_TRY(cudaDeviceSynchronize());  // landed before any stream reads it
     return FFB_OK;
 }
 

@@ -63,15 +63,10 @@ def kv_rows_match(dev, ora) -> bool:
 
 
 def appended_kv(m: DecodeModel, pos: int):
-    """K/V rows the device appended at `pos`, as [B][L][Hkv][dh] f32."""
-    c = m.cfg
-    k = np.zeros((c.batch, c.layers, c.n_kv_heads, c.d_head), np.float32)
-    v = np.zeros_like(k)
-    for b in range(c.batch):
-        for l in range(c.layers):
-            for h in range(c.n_kv_heads):
-                k[b, l, h], v[b, l, h] = m.kv_get(b, l, h, pos)
-    return k, v
+    """K/V rows the device appended at `pos`, as [B][L][Hkv][dh] f32 (one
+    bulk ffb_kv_export)."""
+    k, v = m.kv_export(pos, 1)
+    return k[:, :, :, 0], v[:, :, :, 0]
 
 
 def check_step(store: "O.OracleStore", m: DecodeModel, tokens, pos: int,

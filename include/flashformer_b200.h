@@ -229,6 +229,13 @@ ffb_status ffb_decode_step(ffb_model *m, const int64_t *tokens, int64_t pos, flo
 ffb_status ffb_decode_step_device(ffb_model *m, const int64_t *d_tokens, int64_t pos,
                                   float *d_logits, int64_t *d_greedy, void *stream);
 
+/* Waits for every step enqueued on the handle (any stream: device-wide
+ * synchronize) and reports device-side validation latched by them: a
+ * device-resident token id outside [0, vocab) reads embedding row 0 and
+ * latches FFB_VALIDATION ("token id out of range"), returned (and cleared)
+ * by the next ffb_sync or ffb_decode_step. */
+ffb_status ffb_sync(ffb_model *m);
+
 /* Device-resident multi-token decode: n_steps
  * decode steps enqueued back to back on `stream` with no host round trip.
  * teacher_forced = 0 (generation): step 0 reads d_tokens[batch], step i > 0

@@ -305,6 +305,7 @@ def lib():
     L.ffb_kv_set.argtypes = [C.c_void_p] + [C.c_int64] * 4 + [P(C.c_float)] * 2
     L.ffb_kv_get.argtypes = [C.c_void_p] + [C.c_int64] * 4 + [P(C.c_float)] * 2
     L.ffb_kv_import.argtypes = [C.c_void_p, P(C.c_float), P(C.c_float), C.c_int64, C.c_int64]
+    L.ffb_sync.argtypes = [C.c_void_p]
     L.ffb_kv_export.argtypes = [C.c_void_p, C.c_int64, C.c_int64, P(C.c_float), P(C.c_float)]
     L.ffb_load_store.argtypes = [C.c_void_p, C.c_char_p]
     L.ffb_save_image.argtypes = [C.c_void_p, C.c_char_p]
@@ -526,8 +527,8 @@ class DecodeModel:
         tok = np.ascontiguousarray(np.asarray(tokens, dtype=np.int64).reshape(-1))
         if tok.size != c.batch:
             raise ValidationError("execute_program: one token per batch row required")
-        if out is None and logits:
-            out = np.empty((c.batch, c.vocab_size), np.float32)
+        if out is None and logits:  # a TP rank returns its vocabulary slice
+            out = np.empty((c.batch, c.vocab_size // self.tp_size), np.float32)
         if greedy is None:
             greedy = np.empty(c.batch, np.int64)
         _check(lib().ffb_decode_step(self._h, tok.ctypes.data_as(C.POINTER(C.c_int64)), pos,
@@ -547,6 +548,11 @@ class DecodeModel:
                                             C.c_void_p(d_logits or None),
                                             C.c_void_p(d_greedy or None),
                                             C.c_void_p(stream or None)))
+
+    def sync(self):
+        """Wait for enqueued steps; raise ValidationError if a device-resident
+        token id was out of range (ffb_sync)."""
+        _check(lib().ffb_sync(self._h))
 
     def decode_loop(self, d_tokens: int, pos: int, n_steps: int, d_out: int,
                     teacher_forced: bool = False, stream: int = 0):

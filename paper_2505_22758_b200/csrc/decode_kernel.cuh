@@ -104,6 +104,8 @@ struct DecodeParams {
     uint32_t* amax_counter;   // [1]
     const CtaPlan* plan;      // [grid]
     const int64_t* tokens;    // [B]
+    uint32_t* err_flag;       // latched bit 0: a device-resident token id was out of range
+    int32_t vocab_embed;      // embedding rows (the whole vocabulary, also on a TP shard)
     int64_t max_seq;
     int32_t layers, vocab, pos;
     uint32_t epoch;
@@ -155,6 +157,19 @@ struct DecodeParams {
     uint8_t* hfrag;    // h = silu(g) * a: S_RED input (S_GLU)
     float* ssq;        // [2][grid][B] sum of squares of each CTA's x rows (0 after S_AOUT, 1 after S_RED)
 };
+
+// Embedding row of batch row b.  Host entry points validate token ids like
+// reference_forward (reference.hpp:43-53); device-resident ids cannot be
+// checked before the launch, so an out-of-range id reads row 0 and latches
+// p.err_flag, reported as FFB_VALIDATION by the next synchronous call.
+__device__ __forceinline__ int64_t token_row(const DecodeParams& p, int b) {
+    int64_t t = p.tokens[b];
+    if (t < 0 || t >= p.vocab_embed) {
+        atomicOr(p.err_flag, 1u);
+        t = 0;
+    }
+    return t;
+}
 
 // Weight storage formats of the streamed matrices (Wqkv, Waout, Wffn1,
 // Wffn2^T, lm_head; the embedding is always bf16, tensor_store.hpp:356-361):
@@ -981,7 +996,7 @@ struct DecodeCta {
     __device__ __forceinline__ float2 act_pair(const float* src, bool from_emb, int b, int k) const {
         if (from_emb) {
             const uint32_t w = __ldg(reinterpret_cast<const uint32_t*>(
-                p.embedding + (size_t)p.tokens[b] * D + k));
+                p.embedding + (size_t)token_row(p, b) * D + k));
             return make_float2(bf_lo(w), bf_hi(w));
         }
         return __ldcg(reinterpret_cast<const float2*>(src + (size_t)b * M::K + k));
@@ -1013,7 +1028,7 @@ struct DecodeCta {
 #pragma unroll
         for (int b = 0; b < B; ++b) {
             if (from_emb) {
-                const __nv_bfloat16* e = p.embedding + (size_t)p.tokens[b] * D + col0;
+                const __nv_bfloat16* e = p.embedding + (size_t)token_row(p, b) * D + col0;
 #pragma unroll
                 for (int i = 0; i < PL; i += 8) {
                     const uint4 w = __ldg(reinterpret_cast<const uint4*>(e + i));
@@ -1214,7 +1229,7 @@ struct DecodeCta {
                 const int col = col_of<M>(lt, j);
                 float* a = act.v[b][j];
                 if (from_emb) {
-                    const __nv_bfloat16* e = p.embedding + (size_t)p.tokens[b] * D + col;
+                    const __nv_bfloat16* e = p.embedding + (size_t)token_row(p, b) * D + col;
                     const uint4 w = __ldg(reinterpret_cast<const uint4*>(e));
                     a[0] = bf_lo(w.x); a[1] = bf_hi(w.x); a[2] = bf_lo(w.y); a[3] = bf_hi(w.y);
                     a[4] = bf_lo(w.z); a[5] = bf_hi(w.z); a[6] = bf_lo(w.w); a[7] = bf_hi(w.w);
@@ -2979,7 +2994,7 @@ __global__ void __launch_bounds__(KTraits<S>::NTHREADS, 1)
     // residual init from the embedding: each CTA owns its reduce columns
     if (p.kind == 0 && p.stage_begin == 0 && tid < T::NCT) {
         for (int b = 0; b < S::B; ++b) {
-            const __nv_bfloat16* e = p.embedding + (size_t)p.tokens[b] * S::D;
+            const __nv_bfloat16* e = p.embedding + (size_t)token_row(p, b) * S::D;
             for (int c = cta.pl.red_c0 + tid; c < cta.pl.red_c1; c += T::NCT)
                 __stcg(p.x + (size_t)b * S::D + c, __bfloat162float(e[c]));
         }

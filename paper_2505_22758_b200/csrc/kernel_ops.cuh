@@ -62,5 +62,6 @@ void register_kernels_8b(std::vector<KernelOps>& v);
 void register_kernels_quant(std::vector<KernelOps>& v);
 void register_kernels_70b(std::vector<KernelOps>& v);
 void register_kernels_kc(std::vector<KernelOps>& v);
+void register_kernels_tp(std::vector<KernelOps>& v);
 
 }  // namespace ffb200

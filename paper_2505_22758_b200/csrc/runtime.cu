@@ -60,6 +60,7 @@ const std::vector<KernelOps>& registry() {
         register_kernels_quant(v);
         register_kernels_70b(v);
         register_kernels_kc(v);
+        register_kernels_tp(v);
     });
     return v;
 }
@@ -437,6 +438,8 @@ DecodeParams make_params(const ffb_model* m, int64_t pos, const int64_t* d_token
     p.amax_counter = m->amax_counter;
     p.plan = m->plan;
     p.tokens = d_tokens;
+    p.err_flag = m->greedy ? reinterpret_cast<uint32_t*>(m->greedy + m->cfg.batch) : nullptr;
+    p.vocab_embed = static_cast<int32_t>(m->gcfg.vocab_size);
     p.max_seq = m->max_seq;
     p.layers = static_cast<int32_t>(m->cfg.layers);
     p.vocab = static_cast<int32_t>(m->cfg.vocab_size);
@@ -949,7 +952,7 @@ ffb_status ffb_create_ex(const ffb_model_config* gcfg, int64_t max_seq_len, int 
     ALLOC(m->logits, (size_t)B * V);
     ALLOC(m->amax_val, (size_t)m->grid * B);
     ALLOC(m->amax_idx, (size_t)m->grid * B);
-    ALLOC(m->greedy, (size_t)B);
+    ALLOC(m->greedy, (size_t)B + 1);  // + the device error latch (DecodeParams::err_flag)
     ALLOC(m->tokens_dev, (size_t)B);
     ALLOC(m->counters, (size_t)Lc * 5 + 2);
     ALLOC(m->head_counters, (size_t)Lc * units);
@@ -979,11 +982,12 @@ ffb_status ffb_create_ex(const ffb_model_config* gcfg, int64_t max_seq_len, int 
         cudaMemset(m->head_counters, 0, sizeof(uint32_t) * Lc * units) != cudaSuccess ||
         cudaMemset(m->qkv_head_counters, 0, sizeof(uint32_t) * Lc * c.n_kv_heads) != cudaSuccess ||
         cudaMemset(m->amax_counter, 0, sizeof(uint32_t)) != cudaSuccess ||
+        cudaMemset(m->greedy, 0, sizeof(int64_t) * (B + 1)) != cudaSuccess ||
         cudaMemset(m->kcache, 0, kv * 2) != cudaSuccess ||
         cudaMemset(m->vcache, 0, kv * 2) != cudaSuccess)
         return bail(fail(FFB_DEVICE, "cudaMemset failed"));
     if (cudaMallocHost(&m->tokens_pinned, sizeof(int64_t) * B) != cudaSuccess ||
-        cudaMallocHost(&m->greedy_pinned, sizeof(int64_t) * B) != cudaSuccess ||
+        cudaMallocHost(&m->greedy_pinned, sizeof(int64_t) * (B + 1)) != cudaSuccess ||
         cudaMallocHost(&m->logits_pinned, sizeof(float) * B * V) != cudaSuccess)
         return bail(fail(FFB_DEVICE, "cudaMallocHost failed"));
     st = build_plan(m);
@@ -1347,6 +1351,27 @@ int64_t ffb_get_trace(ffb_model* m, uint64_t* out, int64_t n) {
     return total;
 }
 
+// A device-resident token id was out of range in an earlier step (decode_
+// kernel.cuh: token_row): clear the latch and report it like the reference's
+// ValidationError (reference.hpp:43-53).
+static ffb_status latched_token_error(ffb_model* m) {
+    CUDA_TRY(cudaMemsetAsync(m->greedy + m->cfg.batch, 0, sizeof(int64_t), m->stream));
+    CUDA_TRY(cudaStreamSynchronize(m->stream));
+    return fail(FFB_VALIDATION,
+                "decode_step: token id out of range (device-resident tokens; row 0 was used)");
+}
+
+ffb_status ffb_sync(ffb_model* m) {
+    if (!m) return fail(FFB_USAGE, "NULL handle");
+    if (m->cfg.kind != 0) return FFB_OK;
+    CUDA_TRY(cudaSetDevice(m->device));
+    CUDA_TRY(cudaDeviceSynchronize());
+    int64_t flag = 0;
+    CUDA_TRY(cudaMemcpy(&flag, m->greedy + m->cfg.batch, sizeof(int64_t), cudaMemcpyDeviceToHost));
+    if (flag != 0) return latched_token_error(m);
+    return FFB_OK;
+}
+
 static ffb_status check_step(ffb_model* m, const int64_t* tokens, int64_t pos) {
     const auto& c = m->cfg;
     if (m->cfg.kind != 0)
@@ -1384,13 +1409,14 @@ ffb_status ffb_decode_step(ffb_model* m, const int64_t* tokens, int64_t pos, flo
     if (logits_out)
         CUDA_TRY(cudaMemcpyAsync(direct ? logits_out : m->logits_pinned, m->logits, lbytes,
                                  cudaMemcpyDeviceToHost, s));
-    if (greedy_out)
-        CUDA_TRY(cudaMemcpyAsync(m->greedy_pinned, m->greedy, sizeof(int64_t) * c.batch,
-                                 cudaMemcpyDeviceToHost, s));
+    // greedy ids and the device error latch behind them in one copy
+    CUDA_TRY(cudaMemcpyAsync(m->greedy_pinned, m->greedy, sizeof(int64_t) * (c.batch + 1),
+                             cudaMemcpyDeviceToHost, s));
     CUDA_TRY(cudaStreamSynchronize(s));
     if (logits_out && !direct) std::memcpy(logits_out, m->logits_pinned, lbytes);
     if (greedy_out) std::memcpy(greedy_out, m->greedy_pinned, sizeof(int64_t) * c.batch);
     for (auto& n : m->kv_len) n += 1;
+    if (m->greedy_pinned[c.batch] != 0) return latched_token_error(m);
     return FFB_OK;
 }
 

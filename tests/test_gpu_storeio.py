@@ -137,3 +137,26 @@ def test_kv_export_chunked_path_large_block():
         kb = (((kr.astype(np.uint64) + 0x7FFF + ((kr >> 16) & 1)) >> 16) << 16).astype(np.uint32)
         np.testing.assert_array_equal(ke, kb.view(np.float32))
         np.testing.assert_array_equal(ve, -ke)
+
+
+def test_device_token_out_of_range_latches_validation_error():
+    """ADVICE: device-resident ids are not checked before the launch; an
+    out-of-range id reads row 0 and is reported by the next ffb_sync /
+    ffb_decode_step like reference_forward's ValidationError."""
+    import torch
+    st = O.OracleStore(TOY, 5, 16)
+    st.synthetic_prefill(4, 1)
+    with device_from_store(st) as m:
+        bad = torch.tensor([TOY.vocab_size + 5], dtype=torch.int64, device="cuda:0")
+        torch.cuda.synchronize()
+        m.step_device(bad.data_ptr(), 4)
+        with pytest.raises(ValidationError, match="out of range"):
+            m.sync()
+        m.sync()  # latch cleared
+        good = torch.tensor([3], dtype=torch.int64, device="cuda:0")
+        torch.cuda.synchronize()
+        m.step_device(good.data_ptr(), 5)
+        m.sync()
+        m.step([3], 6)  # host path still validates ids itself
+        with pytest.raises(ValidationError, match="out of range"):
+            m.step([TOY.vocab_size], 7)

@@ -64,17 +64,19 @@ def test_tiny_tp2_greedy_decode_and_mode_identity():
     np.testing.assert_array_equal(outs[1], outs[2])
 
 
-def test_8b_width_tp2_single_step():
-    """Llama-3.1-8B width (32 q / 8 kv heads, d_inter 14336) as 2 shards of
-    16 q / 4 kv heads, one layer, reduced vocabulary, 1k context."""
-    cfg = O.preset("llama31_8b").replace(layers=1, vocab_size=4096)
+@pytest.mark.parametrize("tp", [2, 4, 8])
+def test_8b_width_tp_shards_single_step(tp):
+    """Llama-3.1-8B width (32 q / 8 kv heads, d_inter 14336) as TP 2 / 4 / 8
+    shards (kernels_tp.cu: the shapes bench.py --gpus N runs), two layers,
+    reduced vocabulary, 1k context, co-located on one GPU."""
+    cfg = O.preset("llama31_8b").replace(layers=2, vocab_size=4096)
     st = O.OracleStore(cfg, 1234, 1026)
     st.synthetic_prefill(1024, 7)
-    with _group(st, 2) as g:
+    with _group(st, tp) as g:
         logits, greedy = g.step([17], 1024)
     want = st.forward([17], 1024)[0]
     e = rel_err(logits[0], want)
-    print(f"8B width TP2: rel_err {e:.2e}")
+    print(f"8B width TP{tp}: rel_err {e:.2e}")
     assert e < 1e-4
     assert int(greedy[0]) == int(np.argmax(want))
 

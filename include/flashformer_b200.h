@@ -194,7 +194,7 @@ ffb_status ffb_set_mode(ffb_model *m, ffb_mode mode);
  * is full (default ATTN|AOUT = 0x6).  "attn_group_max": cap on the CTAs per
  * (batch row, kv head) split-K attention group (0 = min(grid / units, 32)).
  * Plan options (rebuild the per-CTA plan): "calib_mask", "plan_reverse",
- * "glu_pool_permille", "glu_pool_chunk", "attn_group_max". */
+ * "attn_group_max". */
 ffb_status ffb_set_option(ffb_model *m, const char *key, int64_t value);
 
 /* Diagnostics only (never needed for correct use): bit 0 = streaming-only

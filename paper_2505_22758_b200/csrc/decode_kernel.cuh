@@ -116,15 +116,8 @@ struct DecodeParams {
     int32_t debug;       // kDebug* bits; 0 in production
     uint64_t* trace;     // optional [grid][n_stages][8] trace records
     int64_t l2_prefetch; // bytes the L2 prefetch cursor runs ahead of the ring
-    int32_t kv_prefetch;  // 1: prefetch the next layer's K/V range into L2 (prefetch_kv)
     int32_t l2_pf_stages; // stage types (bit s % 5, bit 5 = LM head) where the
                           // producer may prefetch while its ring is full
-    // GLU work pool (dynamic load balance, deterministic): pairs [pool_t0, DI)
-    // in chunks of pool_ct pairs, claimed at run time by whichever CTA is free;
-    // each chunk's d_model partial goes to pool_part[chunk].
-    float* pool_part;          // [pool_chunks][RG][B][D]
-    uint32_t* pool_counters;   // [L] claim counters (epoch based)
-    int32_t pool_t0, pool_ct, pool_chunks;
     // SM id -> dense rank (the CTA's plan index) for persistent launches, so
     // that a per-SM weighted plan (ffb_calibrate) follows the SM whatever
     // block index the launch put there; nullptr -> blockIdx.x
@@ -542,7 +535,6 @@ struct DecodeCta {
         const uint8_t* base;  // matrix rows, or K rows (kv) of one (l, b, head)
         int r0, r1;
         bool kv;
-        bool pool;  // the GLU work pool: one marker chunk, claimed dynamically
         int row_bytes = T::ROW_BYTES, rps = T::RPS;  // matrix row geometry
         // KCP: per row block, per K chunk: the chunk's A-fragment table (one
         // slot, dependency-gated) then RW-row weight slots of the chunk
@@ -560,20 +552,19 @@ struct DecodeCta {
         const int l = stage / kStagesPerLayer, s = stage % kStagesPerLayer;
         if (p.kind == 1) {
             if (sub > 0) return false;
-            L = {p.wlin + (size_t)stage * D * T::ROW_BYTES, pl.aout_r0, pl.aout_r1, false, false};
+            L = {p.wlin + (size_t)stage * D * T::ROW_BYTES, pl.aout_r0, pl.aout_r1, false};
             return true;
         }
         if (stage == p.layers * kStagesPerLayer) {
             if (sub > 0) return false;
-            L = {p.lm_head, pl.lm_r0, pl.lm_r1, false, false};
+            L = {p.lm_head, pl.lm_r0, pl.lm_r1, false};
             if constexpr (S::KCP) { L.atab = p.xfrag_f; L.nkc = MD::NKC; L.rows_total = p.vocab; }
             return true;
         }
         switch (s) {
             case S_QKV:
                 if (sub > 0) return false;
-                L = {p.wqkv + (size_t)l * S::QKVR * T::ROW_BYTES, pl.qkv_r0, pl.qkv_r1, false,
-                     false};
+                L = {p.wqkv + (size_t)l * S::QKVR * T::ROW_BYTES, pl.qkv_r0, pl.qkv_r1, false};
                 if constexpr (S::KCP) { L.atab = p.xfrag_f; L.nkc = MD::NKC; L.rows_total = S::QKVR; }
                 return true;
             case S_ATTN: {
@@ -583,31 +574,28 @@ struct DecodeCta {
                 const int unit = pl.attn_unit;
                 L = {reinterpret_cast<const uint8_t*>(p.kcache + kv_row(l, unit / S::NKV,
                                                                         unit % S::NKV, 0)),
-                     p0, min(p1, p.pos), true, false};
+                     p0, min(p1, p.pos), true};
                 return true;
             }
             case S_AOUT:
                 if (sub > 0) return false;
-                L = {p.waout + (size_t)l * D * MA::ROW_BYTES, pl.aout_r0, pl.aout_r1, false, false,
+                L = {p.waout + (size_t)l * D * MA::ROW_BYTES, pl.aout_r0, pl.aout_r1, false,
                      MA::ROW_BYTES, MA::RPS};
                 if constexpr (S::KCP) { L.atab = p.afrag; L.nkc = MA::NKC; L.rows_total = D; }
                 return true;
             case S_GLU:
                 if (sub == 0) {
                     L = {p.wffn1 + (size_t)l * 2 * S::DI * T::ROW_BYTES, 2 * pl.glu_t0,
-                         2 * pl.glu_t1, false, false};
+                         2 * pl.glu_t1, false};
                     if constexpr (S::KCP) { L.atab = p.xfrag_a; L.nkc = MD::NKC; L.rows_total = 2 * S::DI; }
                 }
                 else if (sub == 1 && !T::F2R)
-                    L = {p.wffn2t + (size_t)l * S::DI * T::ROW_BYTES, pl.glu_t0, pl.glu_t1, false,
-                         false};
-                else if (sub == 2 && p.pool_chunks > 0) L = {nullptr, 0, 1, false, true};
+                    L = {p.wffn2t + (size_t)l * S::DI * T::ROW_BYTES, pl.glu_t0, pl.glu_t1, false};
                 else return false;
                 return true;
             case S_RED:  // two-phase FFN: W2 rows, the CTA's d_model rows (as Waout)
                 if (!T::F2R || sub > 0) return false;
-                L = {p.wffn2t + (size_t)l * D * MF::ROW_BYTES, pl.aout_r0, pl.aout_r1, false,
-                     false, MF::ROW_BYTES, MF::RPS};
+                L = {p.wffn2t + (size_t)l * D * MF::ROW_BYTES, pl.aout_r0, pl.aout_r1, false, MF::ROW_BYTES, MF::RPS};
                 if constexpr (S::KCP) { L.atab = p.hfrag; L.nkc = MF::NKC; L.rows_total = D; }
                 return true;
             default:
@@ -678,12 +666,7 @@ struct DecodeCta {
                 }
                 continue;
             }
-            if (c.L.pool) {  // marker: the caller runs the dynamic pool protocol
-                *src0 = nullptr;
-                *src1 = nullptr;
-                *bytes = 0;
-                c.c0 = c.L.r1;
-            } else if (c.L.kv) {
+            if (c.L.kv) {
                 const int n = min(T::KVC, c.L.r1 - c.c0);
                 const size_t off = (size_t)c.c0 * DH * 2;
                 *src0 = c.L.base + off;
@@ -701,89 +684,6 @@ struct DecodeCta {
             return true;
         }
         return false;
-    }
-
-    // ---- GLU work pool ------------------------------------------------
-    // After its static GLU slice a CTA's producer claims pool chunks with an
-    // atomic (one claim kept in flight) and streams each chunk's Wffn1 rows
-    // then Wffn2^T rows, tagging every slot with the chunk id (slot_meta);
-    // a failed claim sends an end marker (slot_meta = -1, plain arrive, no
-    // bytes).  Every CTA makes exactly (claims + 1) increments per layer, so
-    // the counter base of an epoch is (epoch-1) * (pool_chunks + grid).
-    __device__ int* slot_meta() { return misc() + 32; }
-
-    __device__ int pool_slots() const {
-        return (2 * p.pool_ct + T::RPS - 1) / T::RPS + (p.pool_ct + T::RPS - 1) / T::RPS;
-    }
-
-    __device__ void pool_stream(uint32_t& it, const uint8_t* base, int r0, int r1, int ch,
-                                uint64_t policy) {
-        for (int c0 = r0; c0 < r1; c0 += T::RPS) {
-            const uint32_t slot = it % T::NSLOTS, ph = (it / T::NSLOTS) & 1;
-            mbar_wait(&empty[slot], ph ^ 1);
-            slot_meta()[slot] = ch;
-            const uint32_t bytes = static_cast<uint32_t>(min(T::RPS, r1 - c0)) * T::ROW_BYTES;
-            mbar_arrive_expect_tx(&full[slot], bytes);
-            tma_load_1d(ring + slot * T::SLOT_BYTES, base + (size_t)c0 * T::ROW_BYTES, bytes, &full[slot],
-                        policy);
-            ++it;
-        }
-    }
-
-    template <bool DRAIN>
-    __device__ void pool_run(uint32_t& it, int l, uint64_t policy) {
-        if (DRAIN) {  // streaming-only debug: mirror the consumer protocol
-            for (;;) {
-                const uint32_t slot = it % T::NSLOTS, ph = (it / T::NSLOTS) & 1;
-                mbar_wait(&full[slot], ph);
-                const int ch = slot_meta()[slot];
-                __syncwarp();
-                if ((threadIdx.x & 31) == 0) mbar_arrive(&empty[slot]);
-                ++it;
-                if (ch < 0) return;
-                for (int k = 1; k < pool_slots(); ++k) {
-                    const uint32_t s2 = it % T::NSLOTS, ph2 = (it / T::NSLOTS) & 1;
-                    mbar_wait(&full[s2], ph2);
-                    __syncwarp();
-                    if ((threadIdx.x & 31) == 0) mbar_arrive(&empty[s2]);
-                    ++it;
-                }
-            }
-        }
-        uint32_t* ctr = p.pool_counters + l;
-        const uint32_t base = (p.epoch - 1) * static_cast<uint32_t>(p.pool_chunks + grid);
-        uint32_t claim = atomicAdd(ctr, 1u) - base;
-        for (;;) {
-            if (claim >= static_cast<uint32_t>(p.pool_chunks)) {
-                const uint32_t slot = it % T::NSLOTS, ph = (it / T::NSLOTS) & 1;
-                mbar_wait(&empty[slot], ph ^ 1);
-                slot_meta()[slot] = -1;
-                mbar_arrive(&full[slot]);
-                ++it;
-                return;
-            }
-            const int ch = static_cast<int>(claim);
-            claim = atomicAdd(ctr, 1u) - base;  // next claim in flight while streaming
-            const int t0c = p.pool_t0 + ch * p.pool_ct, t1c = t0c + p.pool_ct;
-            pool_stream(it, p.wffn1 + (size_t)l * 2 * S::DI * T::ROW_BYTES, 2 * t0c, 2 * t1c, ch,
-                        policy);
-            pool_stream(it, p.wffn2t + (size_t)l * S::DI * T::ROW_BYTES, t0c, t1c, ch, policy);
-        }
-    }
-
-    // L2 prefetch of this CTA's past K/V positions of layer l (its ring
-    // chunks of S_ATTN), in KVC-position pieces
-    __device__ void prefetch_kv(int l) const {
-        if (pl.attn_unit < 0) return;
-        int p0, p1;
-        attn_range(p0, p1);
-        const int e = min(p1, p.pos);
-        const size_t row = kv_row(l, pl.attn_unit / S::NKV, pl.attn_unit % S::NKV, 0);
-        for (int c0 = p0; c0 < e; c0 += T::KVC) {
-            const uint32_t bytes = static_cast<uint32_t>(min(T::KVC, e - c0)) * DH * 2;
-            prefetch_l2(p.kcache + row + (size_t)c0 * DH, bytes);
-            prefetch_l2(p.vcache + row + (size_t)c0 * DH, bytes);
-        }
     }
 
     // Producer: issues every chunk of the stream into the ring (TMA bulk).
@@ -804,7 +704,6 @@ struct DecodeCta {
         int64_t pf_bytes = 0;
         bool pf_live = window > 0;
         int cur_stage = p.stage_begin;
-        int kv_pf_stage = -1;
         int dep_stage = -1;  // KCP: last stage whose dependency the producer waited for
         const void *s0, *s1;
         uint32_t bytes;
@@ -818,22 +717,6 @@ struct DecodeCta {
                 }
             }
             cur_stage = stage;
-            // KV warm-up: the past positions this CTA's attention reads in
-            // layer l' are prefetched into L2 when the stream reaches layer
-            // l' - 1's GLU (layer 0: its QKV), so the ring's KV loads at the
-            // end of QKV hit L2 instead of waiting on HBM latency
-            if (!DRAIN && p.kv_prefetch && stage != kv_pf_stage) {
-                const int sl = stage / kStagesPerLayer, sk = stage % kStagesPerLayer;
-                int target = -1;
-                if (stage == 0) target = 0;
-                else if (sk == S_GLU && sl + 1 < p.layers) target = sl + 1;
-                if (target >= 0) prefetch_kv(target);
-                kv_pf_stage = stage;
-            }
-            if (s0 == nullptr) {  // GLU work-pool marker
-                pool_run<DRAIN>(it, stage / kStagesPerLayer, policy);
-                continue;
-            }
             if constexpr (S::KCP) {
                 if (c.out_dep && !DRAIN && stage != dep_stage && !(p.debug & kDebugStreamOnly)) {
                     // the A table is written by the previous stage's epilogues
@@ -869,7 +752,6 @@ struct DecodeCta {
                             pf_live = false;
                             break;
                         }
-                        if (q0 == nullptr) continue;  // pool marker: claims are dynamic
                         prefetch_l2(q0, qb);
                         if (q1) prefetch_l2(q1, qb);
                         ahead += q1 ? 2 * (int64_t)qb : qb;
@@ -2572,7 +2454,7 @@ struct DecodeCta {
     }
 
     // d_model partial of pairs [t0, t1) (Wffn2^T rows, AXPY) written to dst
-    // ([RG][B][D] block of glu_part or pool_part)
+    // ([RG][B][D] block of glu_part)
     __device__ void glu_ffn2(uint32_t& it, int t0, int t1, float* dst_part) {
         const int ctid = threadIdx.x;
         const float* hs = h_s();
@@ -2682,8 +2564,7 @@ struct DecodeCta {
     }
 
     // ---------------------------------------------------------- S_GLU
-    // Static slice [glu_t0, glu_t1) into glu_part[cta], then pool chunks
-    // (claimed by this CTA's producer) each into pool_part[chunk].
+    // Static slice [glu_t0, glu_t1) into glu_part[cta].
     __device__ void stage_glu(uint32_t& it, int l) {
         if constexpr (S::KCP) {
             wait_stage(l * kStagesPerLayer + S_GLU);
@@ -2701,22 +2582,6 @@ struct DecodeCta {
             return;
         }
         glu_ffn2(it, pl.glu_t0, pl.glu_t1, p.glu_part + (size_t)cta * T::RG * B * D);
-        if (T::QB == 0 && p.pool_chunks > 0) {  // (pool: bf16 only, host-enforced)
-            for (;;) {
-                const uint32_t slot = it % T::NSLOTS, par = (it / T::NSLOTS) & 1;
-                wait_full(slot, par);
-                const int ch = slot_meta()[slot];
-                if (ch < 0) {  // end marker: release the (byte-less) slot
-                    __syncwarp();
-                    if ((threadIdx.x & 31) == 0) mbar_arrive(&empty[slot]);
-                    ++it;
-                    break;
-                }
-                const int t0c = p.pool_t0 + ch * p.pool_ct, t1c = t0c + p.pool_ct;
-                glu_ffn1(it, &act, t0c, t1c);
-                glu_ffn2(it, t0c, t1c, p.pool_part + (size_t)ch * T::RG * B * D);
-            }
-        }
         arrive(p.counters + l * kStagesPerLayer + S_GLU, l * kStagesPerLayer + S_GLU);
     }
 
@@ -2768,10 +2633,8 @@ struct DecodeCta {
         wait_stage(l * kStagesPerLayer + S_RED);
         const int ctid = threadIdx.x, warp = ctid / 32, lane = ctid % 32;
         const int c0 = pl.red_c0, c1 = pl.red_c1;
-        // CTA partials then pool-chunk partials: a fixed order independent of
-        // which CTA computed which pool chunk -> deterministic sums
-        const int nstatic = grid * T::RG;
-        const int nparts = nstatic + p.pool_chunks * T::RG;
+        // CTA partials in a fixed order -> deterministic sums
+        const int nparts = grid * T::RG;
         float* scratch = wpart();          // [NCW][32]
         float* delta = wpart() + NCW * 32;  // [B][c1 - c0] (TP)
         for (int b = 0; b < B; ++b) {
@@ -2787,8 +2650,7 @@ struct DecodeCta {
 #pragma unroll
                         for (int u = 0; u < U; ++u) {
                             const int q = q0 + u * NCW;
-                            const float* src = q < nstatic ? p.glu_part + (size_t)q * B * D
-                                                           : p.pool_part + (size_t)(q - nstatic) * B * D;
+                            const float* src = p.glu_part + (size_t)q * B * D;
                             v[u] = q < nparts ? ldcg_f(src + (size_t)b * D + col) : 0.f;
                         }
 #pragma unroll

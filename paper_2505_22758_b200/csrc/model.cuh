@@ -55,7 +55,6 @@ struct ffb_model {
     // stage costs up to +8% (profiles/summary_r01.md)
     int64_t l2_prefetch = 512 << 10;
     int32_t l2_pf_stages = (1 << S_ATTN) | (1 << S_AOUT);
-    int32_t kv_prefetch = 0;          // option "kv_prefetch" (measured +1.5 %: off)
     int plan_reverse = 0;             // weight slices assigned in reverse CTA order
     int attn_group_max = 0;           // option "attn_group_max": cap on CTAs per attention unit (0: auto)
     // per-SM plan weights (ffb_calibrate): streamed-row shares of QKV / AOUT /
@@ -65,11 +64,6 @@ struct ffb_model {
     int16_t* sm_rank = nullptr;       // device [max smid + 1] -> dense rank, or null
     int calib_mask = 0xf;             // option "calib_mask": matrices using the weights
     int use_sm_rank = 1;              // option "sm_rank": plans follow SM ids
-    int64_t pool_permille = 0;        // share of d_inter in the dynamic GLU pool (off)
-    int64_t pool_ct_pref = 4;         // preferred pairs per pool chunk
-    int pool_t0 = 0, pool_ct = 0, pool_chunks = 0, pool_chunks_max = 0;
-    float* pool_part = nullptr;
-    uint32_t* pool_counters = nullptr;
     uint32_t epoch = 0;
     cudaStream_t stream = nullptr;
     std::vector<int64_t> kv_len;

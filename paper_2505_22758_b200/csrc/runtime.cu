@@ -281,23 +281,7 @@ ffb_status build_plan(ffb_model* m) {
     if (m->attn_group_max > 0) m->attn_group = std::min(m->attn_group, m->attn_group_max);
     std::vector<CtaPlan> plan(G);
     const int64_t qkv_pairs = m->qkv_rows() / 2;
-    // GLU work pool: the last pool_frac of the d_inter pairs, in chunks of
-    // pool_ct pairs, is claimed dynamically (decode_kernel.cuh: pool_run);
-    // the rest is split statically.  Off for small d_inter / batch > 2.
-    m->pool_ct = 0;
-    m->pool_chunks = 0;
-    m->pool_t0 = c.d_inter;
-    if (m->pool_permille > 0 && c.batch <= 2 && c.d_inter / G >= 32 && m->ops->QB == 0 &&
-        !m->ops->ffn2_rows) {
-        const int64_t ct = std::max<int64_t>(m->pool_ct_pref, m->ops->rps);
-        const int64_t chunks = (c.d_inter * m->pool_permille) / (1000 * ct);
-        if (chunks > 0 && chunks <= m->pool_chunks_max) {
-            m->pool_ct = static_cast<int>(ct);
-            m->pool_chunks = static_cast<int>(chunks);
-            m->pool_t0 = c.d_inter - chunks * ct;
-        }
-    }
-    const int64_t glu_static = m->pool_t0;
+    const int64_t glu_static = c.d_inter;
     // slice k of every streamed matrix goes to CTA ord[k]; boundaries follow
     // the cumulative per-SM weights (all 1 unless ffb_calibrate ran)
     if ((int64_t)m->sm_weight.size() != G) m->sm_weight.assign(G, 1.0);
@@ -456,12 +440,6 @@ DecodeParams make_params(const ffb_model* m, int64_t pos, const int64_t* d_token
     p.trace = m->trace;
     p.l2_prefetch = m->l2_prefetch;
     p.l2_pf_stages = m->l2_pf_stages;
-    p.kv_prefetch = m->kv_prefetch;
-    p.pool_part = m->pool_part;
-    p.pool_counters = m->pool_counters;
-    p.pool_t0 = m->pool_t0;
-    p.pool_ct = m->pool_ct;
-    p.pool_chunks = m->pool_chunks;
     p.sm_rank = (m->mode == FFB_MODE_BASELINE || !m->use_sm_rank) ? nullptr : m->sm_rank;
     p.kind = m->cfg.kind;
     p.wlin = m->wlin;
@@ -477,9 +455,9 @@ DecodeParams make_params(const ffb_model* m, int64_t pos, const int64_t* d_token
     return p;
 }
 
-// Zero every inter-CTA counter (stage, head-combine, argmax, GLU pool); the
-// caller restarts epochs from 0.  Needed before the epoch wraps and whenever
-// the plan changes (the pool counter base depends on pool_chunks).
+// Zero every inter-CTA counter (stage, head-combine, argmax); the caller
+// restarts epochs from 0.  Needed before the epoch wraps and whenever the
+// plan changes (per-head arrival counts depend on it).
 ffb_status reset_sync_state(ffb_model* m, cudaStream_t stream) {
     const int64_t Lc = std::max<int64_t>(1, m->cfg.layers);
     if (m->cfg.kind == 1) {
@@ -493,7 +471,6 @@ ffb_status reset_sync_state(ffb_model* m, cudaStream_t stream) {
     CUDA_TRY(cudaMemsetAsync(m->head_counters, 0,
                              sizeof(uint32_t) * std::max<int64_t>(1, Lc * m->n_units), stream));
     CUDA_TRY(cudaMemsetAsync(m->amax_counter, 0, sizeof(uint32_t), stream));
-    CUDA_TRY(cudaMemsetAsync(m->pool_counters, 0, sizeof(uint32_t) * Lc, stream));
     return FFB_OK;
 }
 
@@ -891,7 +868,6 @@ ffb_status ffb_create_ex(const ffb_model_config* gcfg, int64_t max_seq_len, int 
     if (c.kind == 1) {  // stacked linear: weights, ping-pong activations, counters, plan
         m->kv_len.assign(cfg->layers, 0);
         m->l2_prefetch = 0;
-        m->kv_prefetch = 0;
         m->tp_connected = true;
         ffb_status s2 = FFB_OK;
         if (!s2) s2 = m->alloc(&m->wlin, (size_t)Lc * D * ops->row_bytes);
@@ -960,12 +936,6 @@ ffb_status ffb_create_ex(const ffb_model_config* gcfg, int64_t max_seq_len, int 
     ALLOC(m->amax_counter, 1);
     ALLOC(m->plan, (size_t)m->grid);
     ALLOC(m->staging, (size_t)ffb_model::kStagingElems);
-    // pool partials sized for the largest pool the options allow (50%)
-    m->pool_chunks_max = static_cast<int>(std::max<int64_t>(1, c.d_inter / 2 / ops->rps));
-    ALLOC(m->pool_part, (size_t)m->pool_chunks_max * ops->rg * B * D);
-    ALLOC(m->pool_counters, (size_t)Lc);
-    if (cudaMemset(m->pool_counters, 0, sizeof(uint32_t) * Lc) != cudaSuccess)
-        return bail(fail(FFB_DEVICE, "cudaMemset failed"));
     // TP exchange buffer + flags (also allocated at tp_size 1: harmless, 16 KB)
     m->xch_bytes = sizeof(float) * ((size_t)4 * B * D + (size_t)kMaxTP * B * 2);
     m->xflag_bytes = sizeof(uint32_t) * ((size_t)Lc * 2 * m->grid + 1);
@@ -1265,7 +1235,6 @@ ffb_status ffb_set_option(ffb_model* m, const char* key, int64_t value) {
         return FFB_OK;
     }
     const bool plan_key = !std::strcmp(key, "calib_mask") || !std::strcmp(key, "plan_reverse") ||
-                          !std::strcmp(key, "glu_pool_permille") || !std::strcmp(key, "glu_pool_chunk") ||
                           !std::strcmp(key, "attn_group_max");
     if (plan_key && m->tp_size > 1)
         return fail(FFB_UNSUPPORTED, "option '%s' changes the plan; not with tensor parallelism", key);
@@ -1282,10 +1251,6 @@ ffb_status ffb_set_option(ffb_model* m, const char* key, int64_t value) {
         m->epoch = 0;
         return FFB_OK;
     }
-    if (std::strcmp(key, "kv_prefetch") == 0) {
-        m->kv_prefetch = value ? 1 : 0;
-        return FFB_OK;
-    }
     if (std::strcmp(key, "sm_rank") == 0) {
         m->use_sm_rank = value ? 1 : 0;
         return FFB_OK;
@@ -1295,19 +1260,12 @@ ffb_status ffb_set_option(ffb_model* m, const char* key, int64_t value) {
         m->l2_pf_stages = static_cast<int32_t>(value);
         return FFB_OK;
     }
-    if (std::strcmp(key, "plan_reverse") == 0 || std::strcmp(key, "glu_pool_permille") == 0 ||
-        std::strcmp(key, "glu_pool_chunk") == 0 || std::strcmp(key, "attn_group_max") == 0) {
-        if (key[0] == 'p') m->plan_reverse = value ? 1 : 0;
-        else if (key[0] == 'a') {
+    if (std::strcmp(key, "plan_reverse") == 0 || std::strcmp(key, "attn_group_max") == 0) {
+        if (key[0] == 'p') {
+            m->plan_reverse = value ? 1 : 0;
+        } else {
             if (value < 0 || value > kMaxGroup) return fail(FFB_USAGE, "attn_group_max in [0, 32]");
             m->attn_group_max = static_cast<int>(value);
-        }
-        else if (std::strcmp(key, "glu_pool_chunk") == 0) {
-            if (value < 1 || value > 64) return fail(FFB_USAGE, "glu_pool_chunk in [1, 64]");
-            m->pool_ct_pref = value;
-        } else {
-            if (value < 0 || value > 500) return fail(FFB_USAGE, "glu_pool_permille in [0, 500]");
-            m->pool_permille = value;
         }
         CUDA_TRY(cudaSetDevice(m->device));
         CUDA_TRY(cudaStreamSynchronize(m->stream));

@@ -17,6 +17,7 @@ ap.add_argument("--ncu", action="store_true", help="few launches, for profiling"
 ap.add_argument("--calibrate", type=int, default=0, help="ffb_calibrate iterations first")
 ap.add_argument("--masks", default="", help="comma list of calib_mask values to compare")
 ap.add_argument("--ab", default="", help="option=v0,v1: interleaved A/B of one option")
+ap.add_argument("--sets", default="", help="'k=v,k=v|k=v,...': option sets timed interleaved (3 reps)")
 ap.add_argument("--pf-stages", type=int, default=0x3f, help="l2_prefetch_stages mask for --sweep")
 a = ap.parse_args()
 
@@ -59,6 +60,15 @@ if a.ab:
         for v in [int(x, 0) for x in vals.split(",")]:
             m.set_option(key, v)
             timeit(f"{key}={v}")
+    sys.exit(0)
+if a.sets:
+    m.set_mode(RunMode.FUSED_OVERLAP)
+    sets = [[kv.split("=") for kv in grp.split(",") if kv] for grp in a.sets.split("|")]
+    for rep in range(3):
+        for grp in sets:
+            for k, v in grp:
+                m.set_option(k.strip(), int(v, 0))
+            timeit(",".join(f"{k.strip()}={v}" for k, v in grp))
     sys.exit(0)
 if a.masks:
     m.set_mode(RunMode.FUSED_OVERLAP)

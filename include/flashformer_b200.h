@@ -272,7 +272,11 @@ typedef struct ffb_info {
     uint64_t device_bytes;   /* total device allocation                    */
     uint64_t quant_inexact_groups; /* packer: groups not on a 4/8-bit grid  */
     int32_t row_bytes;       /* bytes per streamed-matrix row              */
-    int32_t pad_;
+    int32_t kc_layout;       /* batch >= 8 GEMV: 2 = mma.sync, 3 = tcgen05 (libffb200_tc05.so); 0 otherwise */
+    uint64_t fp16_inexact;   /* batch >= 8: bf16 weights below the fp16 normal
+                                range (stored rounded to 2^-24; the tcgen05
+                                operands are fp16); weights beyond the fp16
+                                range are rejected by ffb_upload_tensor      */
 } ffb_info;
 ffb_status ffb_get_info(const ffb_model *m, ffb_info *out);
 

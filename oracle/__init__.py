@@ -316,8 +316,49 @@ def ref_lib():
         R.ref_load_store.argtypes = [C.c_char_p, C.c_int64]
         R.ref_time_forward.restype = C.c_double
         R.ref_time_forward.argtypes = [C.c_void_p, C.POINTER(C.c_int64), C.c_int64, C.c_int]
+        R.ref_simulate.argtypes = [C.POINTER(FoConfig), C.POINTER(C.c_double), C.POINTER(C.c_double),
+                                   C.c_int64, C.c_int64, C.c_int64, C.c_int64, C.c_int32, C.c_int64,
+                                   C.POINTER(C.c_double), C.POINTER(C.c_double), C.c_char_p, C.c_int64]
         _ref = R
     return _ref
+
+
+# B200 defaults for the reference simulator's HardwareConfig (config.hpp:88-96):
+# 148 SMs, 228 KiB shared memory; peak bandwidth from MEASURED_PEAKS.json when
+# the caller passes it.  Launch overhead / barrier latency / compute rate keep
+# the reference's calibrated defaults unless overridden.
+B200_HW = dict(num_sms=148, shared_mem_per_sm=228 * 1024, peak_bandwidth=8.0e12,
+               kernel_launch_overhead=8e-6, barrier_latency=3e-7, compute_throughput_per_sm=8e10)
+
+
+def ref_simulate(cfg: ModelCfg, seq_len: int, mode: int = 2, stage_size: int = 32768, depth: int = 6,
+                 warps: int = 8, attn_group: int = 8, hw: dict | None = None,
+                 eff: tuple = (-1.0, -1.0, -1.0, -1.0)) -> dict:
+    """fusesim::simulate (simulate.hpp:423) of one decode step on the
+    reference's own schedule (build_plan + emit_programs) -- the reference's
+    cost model, here fed a B200 hardware description.  mode 0/1/2 =
+    Baseline / Fused / FusedOverlap.  eff = (weight_matvec, kv_attention,
+    glu, load_issue_cost); negative keeps the reference default.  Returns
+    {"total": s, "bytes": B, "sublayers": {name: s}}."""
+    h = dict(B200_HW)
+    h.update(hw or {})
+    hwv = (C.c_double * 6)(h["num_sms"], h["shared_mem_per_sm"], h["peak_bandwidth"],
+                           h["kernel_launch_overhead"], h["barrier_latency"], h["compute_throughput_per_sm"])
+    ev = (C.c_double * 4)(*eff)
+    tot, nb = C.c_double(), C.c_double()
+    buf = C.create_string_buffer(4096)
+    R = ref_lib()
+    fc = cfg.c()
+    rc = R.ref_simulate(C.byref(fc), hwv, ev, stage_size, depth, warps, seq_len, mode, attn_group,
+                        C.byref(tot), C.byref(nb), buf, 4096)
+    if rc != 0:
+        raise RuntimeError(R.ref_last_error().decode())
+    subs = {}
+    for kv in buf.value.decode().split(";"):
+        if kv:
+            k, v = kv.split("=")
+            subs[k] = float(v)
+    return {"total": tot.value, "bytes": nb.value, "sublayers": subs}
 
 
 class RefStore:

@@ -7,6 +7,7 @@
 // fixtures in tests/golden/, and (3) serve as the timed CPU baseline
 // (cpu_baseline.kind = "reference") in bench.py.
 #include <chrono>
+#include <cstdio>
 #include <cstring>
 #include <random>
 #include <string>
@@ -15,6 +16,7 @@
 #include "fusesim/interpreter.hpp"
 #include "fusesim/presets.hpp"
 #include "fusesim/reference.hpp"
+#include "fusesim/simulate.hpp"
 #include "fusesim/verify.hpp"
 
 using namespace fusesim;
@@ -287,6 +289,48 @@ void* ref_load_store(const char* path, int64_t max_seq_len) {
     TensorStore* st = nullptr;
     int rc = guarded([&] { st = new TensorStore(load_store(path, max_seq_len)); });
     return rc == 0 ? st : nullptr;
+}
+
+// The reference's event-driven simulator (simulate.hpp:423, cost model
+// cost_model.hpp:29-57) on the reference's own static schedule
+// (partition.hpp:266 build_plan, emit.hpp:313 emit_programs) for a
+// hardware / pipeline description -- the cost-model side of SURVEY.md
+// §8(f) row 3.  hw: {num_sms, shared_mem_per_sm, peak_bandwidth,
+// kernel_launch_overhead, barrier_latency, compute_throughput_per_sm};
+// eff: {weight_matvec, kv_attention, glu, load_issue_cost} (< 0: default).
+// Writes the total latency (s) and bytes moved, and "name=seconds;..." of the
+// per-sublayer latencies into `subs`.
+int ref_simulate(const RefConfig* c, const double* hw, const double* eff, int64_t stage_size,
+                 int64_t depth, int64_t warps, int64_t seq_len, int32_t mode, int64_t attn_group,
+                 double* total, double* bytes, char* subs, int64_t subs_len) {
+    return guarded([&] {
+        ModelConfig m = to_model(c);
+        HardwareConfig h;
+        h.num_sms = static_cast<int64_t>(hw[0]);
+        h.shared_mem_per_sm = static_cast<uint64_t>(hw[1]);
+        h.peak_bandwidth = hw[2];
+        h.kernel_launch_overhead = hw[3];
+        h.barrier_latency = hw[4];
+        h.compute_throughput_per_sm = hw[5];
+        PipelineConfig pc;
+        pc.stage_size = static_cast<uint64_t>(stage_size);
+        pc.depth = depth;
+        pc.consumer_warps = warps;
+        WorkloadPlan plan = build_plan(m, h, pc, seq_len, attn_group);
+        CostModel cm = CostModel::from_hardware(h);
+        if (eff[0] > 0) cm.eff_weight_matvec = eff[0];
+        if (eff[1] > 0) cm.eff_kv_attention = eff[1];
+        if (eff[2] > 0) cm.eff_glu = eff[2];
+        if (eff[3] >= 0) cm.load_issue_cost = eff[3];
+        const RunMode rm = mode == 0 ? RunMode::Baseline : mode == 1 ? RunMode::Fused
+                                                                     : RunMode::FusedOverlap;
+        SimResult r = simulate(emit_programs(plan, rm), cm);
+        *total = r.total_latency;
+        *bytes = static_cast<double>(r.bytes_moved);
+        std::string out;
+        for (const auto& [name, t] : r.sublayer_latency) out += name + "=" + std::to_string(t) + ";";
+        std::snprintf(subs, static_cast<size_t>(subs_len), "%s", out.c_str());
+    });
 }
 
 }  // extern "C"

@@ -80,7 +80,8 @@ class _Info(C.Structure):
         ("ring_slots", C.c_int32), ("slot_bytes", C.c_int32), ("attn_group", C.c_int32),
         ("launches_per_step", C.c_int32), ("mode", C.c_int32),
         ("weight_bytes", C.c_uint64), ("device_bytes", C.c_uint64),
-        ("quant_inexact_groups", C.c_uint64), ("row_bytes", C.c_int32), ("pad_", C.c_int32),
+        ("quant_inexact_groups", C.c_uint64), ("row_bytes", C.c_int32), ("kc_layout", C.c_int32),
+        ("fp16_inexact", C.c_uint64),
     ]
 
 

@@ -205,6 +205,28 @@ __host__ __device__ constexpr int weight_row_bytes(int cols, int qb) {
                    : ((qb == 4 ? cols / 2 : cols) + 5 * (cols / kQuantGroup) + 15) / 16 * 16;
 }
 
+// Ring geometry of the bf16 CUDA-core path (batch < 8): slot bytes and the
+// most slots (pipeline depth) the ring may use.  Defaults are the measured
+// optimum; other values are built only for the pipeline sweep
+// (tools/pipeline_sweep.py, Table 7).
+#ifndef FFB_SLOT_BYTES
+#define FFB_SLOT_BYTES 32768
+#endif
+#ifndef FFB_MAX_SLOTS
+#define FFB_MAX_SLOTS 16
+#endif
+constexpr int kSlotBytes = FFB_SLOT_BYTES;
+constexpr int kMaxSlots = FFB_MAX_SLOTS;
+static_assert(kSlotBytes % 1024 == 0 && kMaxSlots >= 2, "ring geometry");
+
+// batch >= 8 GEMV: mma.sync m16n8k16 (default, layout 2) or tcgen05 with
+// TMEM accumulators (-DFFB_KCP_TCGEN05, layout 3)
+#ifdef FFB_KCP_TCGEN05
+constexpr int kKcLayout = 3;
+#else
+constexpr int kKcLayout = 2;
+#endif
+
 constexpr int kNCW = 8;              // consumer warps
 constexpr int kNCT = kNCW * 32;      // consumer threads
 constexpr int cmin_(int a, int b) { return a < b ? a : b; }
@@ -235,7 +257,7 @@ struct RowMap {
     static constexpr int WPR = TPR / 32;            // warps per row
     // rows per thread per slot: bf16 fills a 32 KiB slot; quant takes the
     // largest power of two with RPT * B <= 32 and a slot <= 32 KiB
-    static constexpr int RPT = QB == 0 ? cmin_((32768 / ROW_BYTES) / RG, 32 / S::B)
+    static constexpr int RPT = QB == 0 ? cmin_((kSlotBytes / ROW_BYTES) / RG, 32 / S::B)
                                        : cmax_(2 / RG, cmin_(pow2_le_(32 / S::B),
                                                              pow2_le_(cmax_(1, 32768 / (RG * ROW_BYTES)))));
     // Tensor-core GEMV (quant formats, K a multiple of 8 x 128): the 8 warps
@@ -296,7 +318,7 @@ struct KTraits : RowMap<S, S::D> {
     // 8B b1 2.725 -> 2.700 ms, b2 3.204 -> 3.176; 1B b1 0.638 -> 0.650
     // (the reduction of 2048-wide partials is cheaper than the barrier).
     static constexpr bool F2R = S::KCP || (S::QB == 0 && S::B <= 2 && S::D >= 4096 &&
-                                           S::DI % (8 * kNCT) == 0 && S::DI * 2 <= 32768);
+                                           S::DI % (8 * kNCT) == 0 && S::DI * 2 <= kSlotBytes);
     using MF = std::conditional_t<F2R, RowMap<S, S::DI>, MD>;
     static constexpr int NCW = kNCW;
     static constexpr int NCT = kNCT;
@@ -308,7 +330,7 @@ struct KTraits : RowMap<S, S::D> {
     static constexpr int CONSUMER_REGS = 224;  // 4*32*56 + 8*32*224 <= 64K
     static constexpr int cmin(int a, int b) { return a < b ? a : b; }
     static constexpr int cmax(int a, int b) { return a > b ? a : b; }
-    static constexpr int SLOT_BYTES = S::KCP ? MD::SLOT : S::QB == 0 ? 32768 : cmax(MD::SLOT, MA::SLOT);
+    static constexpr int SLOT_BYTES = S::KCP ? MD::SLOT : S::QB == 0 ? kSlotBytes : cmax(MD::SLOT, MA::SLOT);
     // KCP: [KP][RW][B] k-part partials + [RW][B] finished rows (gemv_kc)
     static constexpr int RED_FLOATS =
         S::KCP ? (MD::KP * MD::RW * S::B + MD::RW * S::B + 1) / 2
@@ -326,17 +348,17 @@ struct KTraits : RowMap<S, S::D> {
     static_assert(KVC >= 1 && (SLOT_BYTES / 2) % 16 == 0, "kv chunk");
 
     // ---- shared memory carve-up (bytes) ----
-    static constexpr int OFF_RED = 0;  // [2][WPR][RB][B] f32 (largest row map)
+    static constexpr int R_RED = 0;  // [2][WPR][RB][B] f32 (largest row map)
     static constexpr int SZ_RED = 2 * RED_FLOATS * 4;
-    static constexpr int OFF_H = OFF_RED + SZ_RED;  // [B][TMAX] f32
+    static constexpr int R_H = R_RED + SZ_RED;  // [B][TMAX] f32
     // [B][TMAX] f32 (GLU h slice, S_AOUT / S_RED row results); batch >= 8
     // only stages the current token's K and V rows (attention)
     static constexpr int SZ_H = S::KCP ? (4 * S::DH + 15) / 16 * 16 : S::B * TMAX * 4;
-    static constexpr int OFF_ROPE = OFF_H + SZ_H;  // [DH/2][2] f32
+    static constexpr int R_ROPE = R_H + SZ_H;  // [DH/2][2] f32
     static constexpr int SZ_ROPE = S::DH * 4;
-    static constexpr int OFF_NORM = OFF_ROPE + SZ_ROPE;  // [NCW][B] f32
+    static constexpr int R_NORM = R_ROPE + SZ_ROPE;  // [NCW][B] f32
     static constexpr int SZ_NORM = ((NCW + 1) * S::B * 4 + 16 + 15) / 16 * 16;  // [NCW][B] partials + [B] (KCP inv)
-    static constexpr int OFF_WPART = OFF_NORM + SZ_NORM;  // attention scratch, f32
+    static constexpr int R_WPART = R_NORM + SZ_NORM;  // attention scratch, f32
     // also reused for: attention combine (3*G*QPG), argmax candidates
     // (2*grid*B) and the GLU reduction (NCW*32); grid <= kMaxGrid
     static constexpr int kMaxGrid = 160;
@@ -350,7 +372,8 @@ struct KTraits : RowMap<S, S::D> {
     // 4 on -- same-box A/B at 8B, 4k context: b2 3.17 / 3.14 ms for 3 / 4
     // slots; with the per-warp attention b4 3.77 / 3.75, b8 6.41 / 6.38,
     // b16 7.32 / 7.30 ms for 3 / 2 slots (b16 7.65 with 1))
-    static constexpr int ATT_SC = S::B == 1 ? cmax(1, 131072 / SLOT_BYTES) : S::B == 2 ? 4 : 2;
+    static constexpr int ATT_SC =
+        cmin(S::B == 1 ? cmax(1, 131072 / SLOT_BYTES) : S::B == 2 ? 4 : 2, kMaxSlots - 1);
     static constexpr int ANP = ((ATT_SC * KVC + 1) + 15) / 16 * 16;
     // alpha*q f32 [QPG][DH], scores f32 [QPG][ANP], probabilities as bf16
     // hi/lo MMA rows [16][ANP] (tensor-core P.V), stats [QPG][4]
@@ -375,21 +398,31 @@ struct KTraits : RowMap<S, S::D> {
                            cmax(S::KCP ? 0 : 2 * kMaxGrid * S::B, NCW * 32 + S::B * TMAX)),
                       SZ_ATT),
                  cmax(MD::TC ? S::D : 0, MA::TC ? S::AD : 0));  // TC activation strips
-    static_assert(OFF_H % 16 == 0 && OFF_NORM % 16 == 0 && OFF_WPART % 16 == 0,
+    static_assert(R_H % 16 == 0 && R_NORM % 16 == 0 && R_WPART % 16 == 0,
                   "16-byte aligned scratch (vector smem accesses)");
-    static constexpr int OFF_AMAX = OFF_WPART + SZ_WPART;  // [NCT] (f32, i32)
+    static constexpr int R_AMAX = R_WPART + SZ_WPART;  // [NCT] (f32, i32)
     static constexpr int SZ_AMAX = NCT * 8;
-    static constexpr int OFF_MISC = OFF_AMAX + SZ_AMAX;  // flags
+    static constexpr int R_MISC = R_AMAX + SZ_AMAX;  // flags
     static constexpr int SZ_MISC = 256;
-    static constexpr int FIXED = ((OFF_MISC + SZ_MISC + 1023) / 1024) * 1024;
+    static constexpr int FIXED = ((R_MISC + SZ_MISC + 1023) / 1024) * 1024;
     static constexpr int MAX_SMEM = 227 * 1024;
-    static constexpr int NSLOTS_RAW = (MAX_SMEM - FIXED - 256) / SLOT_BYTES;
-    static constexpr int NSLOTS = NSLOTS_RAW > 16 ? 16 : NSLOTS_RAW;
+    // batch >= 8 (tcgen05): barriers at 0, the ring at 1024 (128-byte-swizzle
+    // atoms need 1024-byte alignment) and the fixed scratch after it, which
+    // keeps the M = 128 MMA's reads of the A table's padding rows past the
+    // last slot inside shared memory (gemv_kc); otherwise scratch, barriers
+    // and the ring in that order
+    static constexpr int NSLOTS_RAW = (MAX_SMEM - FIXED - (S::KCP ? 1024 : 256)) / SLOT_BYTES;
+    static constexpr int NSLOTS = NSLOTS_RAW > kMaxSlots ? kMaxSlots : NSLOTS_RAW;
     static_assert(NSLOTS >= 2, "ring too small");
     static_assert(NSLOTS >= ATT_SC + 1, "attention pass must leave a slot for streaming");
-    static constexpr int OFF_BARS = FIXED;  // full[NSLOTS], empty[NSLOTS]
-    static constexpr int OFF_RING = FIXED + 256;
-    static constexpr int SMEM_BYTES = OFF_RING + NSLOTS * SLOT_BYTES;
+    static constexpr int OFF_BARS = S::KCP ? 0 : FIXED;  // full[NSLOTS], empty[NSLOTS], (KCP) acc
+    static constexpr int OFF_RING = S::KCP ? 1024 : FIXED + 256;
+    static constexpr int SHIFT = S::KCP ? OFF_RING + NSLOTS * SLOT_BYTES : 0;
+    static constexpr int OFF_RED = SHIFT + R_RED, OFF_H = SHIFT + R_H, OFF_ROPE = SHIFT + R_ROPE,
+                         OFF_NORM = SHIFT + R_NORM, OFF_WPART = SHIFT + R_WPART, OFF_AMAX = SHIFT + R_AMAX,
+                         OFF_MISC = SHIFT + R_MISC;
+    static constexpr int SMEM_BYTES = S::KCP ? SHIFT + FIXED : OFF_RING + NSLOTS * SLOT_BYTES;
+    static_assert(!S::KCP || 2 * NSLOTS + 2 <= 128, "tcgen05 barriers below the ring");
     static_assert(SMEM_BYTES <= MAX_SMEM, "shared memory budget");
 };
 
@@ -405,10 +438,13 @@ struct DecodeCta {
     uint64_t* full;
     uint64_t* empty;
     uint8_t* ring;
-    CtaPlan pl;
+    // this CTA's plan, staged in shared memory (misc + 128 B): neither role
+    // keeps its 14 fields in registers (the 56-register producer spilled them)
+    CtaPlan& pl;
     int cta, grid;
 
-    __device__ DecodeCta(const DecodeParams& p_, uint8_t* smem_) : p(p_), smem(smem_) {
+    __device__ DecodeCta(const DecodeParams& p_, uint8_t* smem_)
+        : p(p_), smem(smem_), pl(*reinterpret_cast<CtaPlan*>(smem_ + T::OFF_MISC + 128)) {
         full = reinterpret_cast<uint64_t*>(smem + T::OFF_BARS);
         empty = full + T::NSLOTS;
         ring = smem + T::OFF_RING;
@@ -419,7 +455,10 @@ struct DecodeCta {
             cta = p.sm_rank[smid];
         }
         grid = gridDim.x;
-        pl = p.plan[cta];
+        static_assert(sizeof(CtaPlan) % 4 == 0 && 128 + sizeof(CtaPlan) <= T::SZ_MISC, "plan in misc");
+        if (threadIdx.x < sizeof(CtaPlan) / 4)  // (read after the kernel's __syncthreads)
+            reinterpret_cast<int32_t*>(&pl)[threadIdx.x] =
+                reinterpret_cast<const int32_t*>(p.plan + cta)[threadIdx.x];
     }
 
     __device__ float* red_buf(uint32_t it) {
@@ -430,6 +469,14 @@ struct DecodeCta {
     __device__ float* norm_s() { return reinterpret_cast<float*>(smem + T::OFF_NORM); }
     __device__ float* wpart() { return reinterpret_cast<float*>(smem + T::OFF_WPART); }
     __device__ int* misc() { return reinterpret_cast<int*>(smem + T::OFF_MISC); }
+    // batch >= 8: TMEM base address (written by tcgen05.alloc) and the
+    // accumulator-ready barrier (gemv_kc), one phase per row block
+    __device__ uint32_t* tmem_slot() { return reinterpret_cast<uint32_t*>(misc()) + 62; }
+    __device__ uint32_t tmem_base() { return *reinterpret_cast<volatile uint32_t*>(tmem_slot()); }
+    __device__ uint64_t* accbar() { return full + 2 * T::NSLOTS; }
+    __device__ uint64_t* abar() { return full + 2 * T::NSLOTS + 1; }  // TMEM A buffer reusable
+    uint32_t acc_phase = 0, a_phase = 0;
+    bool a_issued = false;  // an abar commit is outstanding
 
     // ------------------------------------------------------------ schedule
     __device__ int n_stages() const {
@@ -542,10 +589,18 @@ struct DecodeCta {
         int nkc = 0;
         int rows_total = 0;  // KCP: rows of the chunk-major matrix
     };
-    // KCP rows per accumulator block: 128 rows of accumulators (same-box A/B
-    // at 8B b16: 7.39 ms with 160-row blocks, 7.32 with 128: fewer live
-    // accumulator registers outweigh the extra A-table re-streams)
+    // KCP rows per accumulator block: TMEM holds the K chunk's activations
+    // (KC / 2 columns, the MMA's A operand) and the block's accumulators (RW
+    // columns per weight slot) in 512 columns; the A table is streamed once
+    // per block and K chunk
+#ifdef FFB_KCP_TCGEN05
+    static constexpr int TM_A = 256;  // TMEM columns reserved for the A operand (KC <= 512)
+    static constexpr int KC_BLOCK = cmax_(T::MD::RW, (512 - TM_A) / T::MD::RW * T::MD::RW);
+#else
+    // mma.sync path: per-warp register accumulators for 128 rows (same-box
+    // A/B at 8B b16: 7.39 ms with 160-row blocks, 7.32 with 128)
     static constexpr int KC_BLOCK = cmax_(T::MD::RW, cmin_(128, (T::NSLOTS - 1) * T::MD::RW));
+#endif
 
     // The lists of (stage, sub) in consumption order; false past the end.
     __device__ bool list_of(int stage, int sub, List& L) const {
@@ -699,7 +754,8 @@ struct DecodeCta {
         Cursor c, pf;
         cursor_init(c);
         cursor_init(pf);
-        const int64_t window = (!DRAIN && p.overlap) ? p.l2_prefetch : 0;
+        // (batch >= 8 never prefetches: the runtime sets no window there)
+        const int64_t window = (!DRAIN && p.overlap && !S::KCP) ? p.l2_prefetch : 0;
         int64_t ahead = 0;  // bytes prefetched but not yet loaded into the ring
         int64_t pf_bytes = 0;
         bool pf_live = window > 0;
@@ -730,7 +786,7 @@ struct DecodeCta {
                 }
             }
             const int64_t need = s1 ? 2 * (int64_t)bytes : bytes;
-            if (!DRAIN) {
+            if (!DRAIN && !S::KCP) {
                 // Prefetch into L2 only while the ring is full (this SM cannot
                 // load anyway, typically behind a barrier), never more than
                 // `window` bytes ahead of the ring: idle HBM time is spent on
@@ -1450,26 +1506,52 @@ struct DecodeCta {
     }
 
     // ================================================ batch >= 8 (KCP)
+#ifdef FFB_KCP_TCGEN05
+    // tcgen05 operand layouts:
+    //  * A table (activations, the MMA's A operand): per K chunk of KC
+    //    columns, [KC / 8 units][32 rows][16 B] -- 8 x 16-byte core matrices
+    //    -- copied into TMEM columns [4u, 4u + 4) of lanes 0-31 (replicated to
+    //    all 128 lanes) by tcgen05.cp.32x128b.warpx4; row m = t * 16 + b
+    //    holds term t (0: fp16 hi, 1: fp16 lo) of batch row b (rows b >= B
+    //    stay zero)
+    //  * weights (B operand, N = RW rows per slot, K-major, 128-byte
+    //    swizzle: 8-row x 128-byte atoms, 16-byte unit u of row r at u ^
+    //    (r & 7)): [K / KC][rows / 8][KC / 64][8 rows][128 B] (runtime
+    //    packer, layout 3): a slot of rows is one contiguous copy, atom
+    //    column j of it at j * 1 KiB with KC / 64 KiB between 8-row groups
+    __device__ static size_t frag_off(int k, int m) {
+        const int c = k / S::KC, kk = k % S::KC;
+        return (size_t)c * MD::ATAB + (kk >> 3) * 512 + m * 16 + (kk & 7) * 2;
+    }
+#else
     // A-fragment table offset of activation column k, batch row b (m16n8k16
     // row-major A: lane (g, q) holds rows g / g + 8, columns 2q, 2q + 1 and
     // 2q + 8, 2q + 9 of each k16 step; registers a0..a3 = (g, lo k), (g + 8,
     // lo k), (g, hi k), (g + 8, hi k)); per k-step the 32 lanes' hi parts
-    // (16 bytes each, conflict-free LDS.128) then the lo parts.
+    // (16 bytes each, conflict-free LDS.128) then the lo parts (+512).
     __device__ static size_t frag_off(int k, int b) {
         const int kst = k >> 4, kk = k & 15;
         const int lane = (b & 7) * 4 + ((kk & 7) >> 1);
         const int reg = (kk >> 3) * 2 + (b >> 3);
         return (size_t)kst * 1024 + lane * 16 + reg * 4 + (kk & 1) * 2;
     }
-    // v as fp16 hi + lo (22 bits of mantissa, as the quant tensor-core
-    // GEMV's activations; bf16 hi + lo would carry 16 and measurably move
-    // the logits); the bf16 weights are stored as fp16 by the packer
-    __device__ static void frag_put(uint8_t* tab, int k, int b, float v) {
+#endif
+    // v as fp16 hi + lo (22 bits of mantissa); the bf16 weights are stored as
+    // fp16 by the packer.  |v| beyond the fp16 range latches err_flag bit 1
+    // (reported as FFB_NUMERIC by the next synchronous call) instead of
+    // silently turning into inf.
+    __device__ void frag_put(uint8_t* tab, int k, int b, float v) const {
         const __half hi = __float2half_rn(v);
         const __half lo = __float2half_rn(v - __half2float(hi));
+        if (!(fabsf(v) <= 65504.f)) atomicOr(p.err_flag, 2u);
+#ifdef FFB_KCP_TCGEN05
+        *reinterpret_cast<__half*>(tab + frag_off(k, b)) = hi;
+        *reinterpret_cast<__half*>(tab + frag_off(k, 16 + b)) = lo;
+#else
         uint8_t* d = tab + frag_off(k, b);
         *reinterpret_cast<__half*>(d) = hi;
         *reinterpret_cast<__half*>(d + 512) = lo;
+#endif
     }
     // After this CTA updated x rows [c0, c1): their A-table entries x * gain
     // and this CTA's per-batch-row sum of squares (ssq_out[cta][b]).  Ends
@@ -1511,6 +1593,125 @@ struct DecodeCta {
         return inv;
     }
 
+#ifdef FFB_KCP_TCGEN05
+    // K-chunked tcgen05 GEMV, rows [r0, r1) (8-aligned), in row blocks of
+    // KC_BLOCK: per K chunk the ring delivers the A table (activations of
+    // all batch rows, fp16 hi / lo) then weight slots of RW rows.  One lane
+    // of warp 0 copies the A table into TMEM (tcgen05.cp; the ring slot is
+    // released as soon as the copies complete) and issues, per weight slot,
+    // the chunk's KC / 16 MMAs (A from TMEM, M = 128: the 32 table rows
+    // replicated four times; B = the slot's RW weight rows from shared
+    // memory, K = 16) into that slot's TMEM accumulator columns,
+    // accumulating across K chunks; a tcgen05.commit releases each weight
+    // slot once its MMAs have read it (copies and MMAs execute in issue
+    // order, so the next chunk's copy cannot overtake them).  The epilogue
+    // (warps 0 and 4: TMEM lanes 0-31) adds the hi and lo rows, scales by
+    // inv[b] (normed inputs) and hands 16-row groups to epi(c0, nrows,
+    // red[row][b]) like gemv's epilogues.  The MMA's f32 accumulation order
+    // is fixed by the hardware: deterministic.
+    template <class M, class Epi>
+    __device__ void gemv_kc(uint32_t& it, int r0, int r1, const float* inv, Epi&& epi) {
+        constexpr int RW = M::RW, NKA = S::KC / 64;
+        constexpr uint32_t IDESC = umma_idesc_f16(128, RW);
+        static_assert(RW % 16 == 0 && RW <= 256 && S::KC % 64 == 0 && S::KC / 2 <= TM_A, "UMMA tile");
+        const int ctid = threadIdx.x, warp = ctid / 32, lane = ctid % 32;
+        float* fin = reinterpret_cast<float*>(smem + T::OFF_RED);  // [2][32][B] finished rows
+        static_assert(2 * 32 * B <= 2 * T::RED_FLOATS && RW % 32 == 0, "epilogue staging");
+        const uint32_t tbase = tmem_base();
+        for (int blk = r0; blk < r1; blk += KC_BLOCK) {
+            const int blk_end = min(blk + KC_BLOCK, r1);
+            const int nj = (blk_end - blk + RW - 1) / RW;
+            if (warp == 0) {
+                for (int c = 0; c < M::NKC; ++c) {
+                    const uint32_t sa = it % T::NSLOTS;
+                    wait_full(sa, (it / T::NSLOTS) & 1);
+                    ++it;
+                    // the previous chunk's MMAs have read the TMEM A buffer
+                    if (a_issued) {
+                        mbar_wait(abar(), a_phase & 1);
+                        ++a_phase;
+                        tc05_fence_after();
+                    }
+                    {  // lane m: its A-table row of the chunk -> TMEM lane m, columns [0, KC / 2)
+                        const uint8_t* arow = ring + sa * T::SLOT_BYTES + lane * 16;
+#pragma unroll 1
+                        for (int q = 0; q < S::KC / 128; ++q) {
+                            uint32_t r[64];
+#pragma unroll
+                            for (int u = 0; u < 16; ++u) {
+                                const uint4 v = lds_u128(arow + (q * 16 + u) * 512);
+                                r[4 * u] = v.x; r[4 * u + 1] = v.y; r[4 * u + 2] = v.z; r[4 * u + 3] = v.w;
+                            }
+                            tmem_st_32x32b_x64(tbase + q * 64, r);
+                        }
+                    }
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive_cnt(&empty[sa], NCW);  // A slot read: free
+                    tc05_fence_before();
+                    __syncwarp();
+                    tc05_fence_after();
+                    for (int j = 0; j < nj; ++j) {
+                        const uint32_t sw = it % T::NSLOTS;
+                        wait_full(sw, (it / T::NSLOTS) & 1);
+                        ++it;
+                        tc05_fence_after();
+                        if (lane == 0) {
+                            const uint32_t wbase = smem_u32(ring + sw * T::SLOT_BYTES);
+#pragma unroll
+                            for (int ka = 0; ka < NKA; ++ka)
+#pragma unroll
+                                for (int kk = 0; kk < 4; ++kk)
+                                    umma_f16_ts(tbase + TM_A + j * RW, tbase + (ka * 4 + kk) * 8,
+                                                umma_desc_sw128(wbase + ka * 1024 + kk * 32, NKA * 1024), IDESC,
+                                                (c | ka | kk) != 0);
+                            umma_commit(&empty[sw]);  // one arrival when these MMAs have read the slot
+                            mbar_arrive_cnt(&empty[sw], NCW - 1);
+                        }
+                        __syncwarp();
+                    }
+                    if (lane == 0) umma_commit(abar());  // A buffer free once these MMAs are done
+                    a_issued = true;
+                }
+                if (lane == 0) umma_commit(accbar());
+                __syncwarp();
+            } else {
+                it += M::NKC * (1 + nj);  // the same slots, consumed by warp 0
+            }
+            const bool reader = warp == 0 || warp == 4;
+            if (reader) {
+                mbar_wait(accbar(), acc_phase & 1);
+                tc05_fence_after();
+            }
+            ++acc_phase;
+            // 32-row tiles of the block's accumulators (32 TMEM columns each),
+            // two at a time: warp 0 the even tile, warp 4 the odd one
+            const int ntile = (blk_end - blk + 31) / 32;
+            for (int t0 = 0; t0 < ntile; t0 += 2) {
+                const int t = t0 + warp / 4;
+                if (reader && t < ntile) {
+                    uint32_t r[32];
+                    tmem_ld_32x32b_x32(tbase + TM_A + t * 32, r);  // lane l: D[row l][cols t * 32 ..]
+                    float* f = fin + (warp / 4) * 32 * B;
+#pragma unroll
+                    for (int n = 0; n < 32; ++n) {
+                        float v = __uint_as_float(r[n]);
+                        v += __shfl_down_sync(0xffffffffu, v, 16);  // hi row b + lo row 16 + b
+                        if (lane < B) f[n * B + lane] = inv != nullptr ? v * inv[lane] : v;
+                    }
+                }
+                consumer_sync(NCT);
+                for (int tt = t0; tt < min(t0 + 2, ntile); ++tt) {
+                    const int g0 = blk + tt * 32, nrows = min(32, blk_end - g0);
+                    for (int e0 = 0; e0 < nrows; e0 += 16)
+                        epi(g0 + e0, min(16, nrows - e0), fin + ((tt - t0) * 32 + e0) * B);
+                }
+                consumer_sync(NCT);
+            }
+            if (reader) tc05_fence_before();  // TMEM reads done before the next block's MMAs
+        }
+    }
+
+#else
     // K-chunked tensor-core GEMV, rows [r0, r1), in row blocks of KC_BLOCK:
     // per K chunk the ring delivers the A table (activations of all batch
     // rows, fp16 hi/lo) then weight slots of RW rows; warp (rp, kp) runs the
@@ -1605,6 +1806,8 @@ struct DecodeCta {
             }
         }
     }
+
+#endif
 
     // One GEMV stage's activation + rows: CUDA-core / quant path (load_act +
     // gemv) or, at batch >= 8, gemv_kc (inputs already in the A tables;
@@ -2784,6 +2987,7 @@ struct DecodeCta {
                 }
             }
         }
+        trace_mark(p.layers * kStagesPerLayer, 2);  // (trace only: LM-head end)
     }
 
     // ---------------------------------------------------------- linear
@@ -2844,8 +3048,22 @@ __global__ void __launch_bounds__(KTraits<S>::NTHREADS, 1)
             mbar_init(&cta.full[i], 1);
             mbar_init(&cta.empty[i], T::NCW);
         }
+#ifdef FFB_KCP_TCGEN05
+        if constexpr (S::KCP) {
+            mbar_init(cta.accbar(), 1);
+            mbar_init(cta.abar(), 1);
+        }
+#endif
         fence_mbar_init();
     }
+    // batch >= 8: 512 TMEM columns (the whole SM's, one CTA per SM) for the
+    // tcgen05 GEMV accumulators (DecodeCta::gemv_kc)
+#ifdef FFB_KCP_TCGEN05
+    if constexpr (S::KCP) {
+        if (tid < 32) tmem_alloc(cta.tmem_slot(), 512);
+        tc05_fence_before();
+    }
+#endif
     // RoPE table for this step's position, in f64 (numerics.hpp:27-37 angle)
     if (tid < S::DH / 2) {
         const double freq = pow(p.rope_theta, -static_cast<double>(2 * tid) / S::DH);
@@ -2857,7 +3075,7 @@ __global__ void __launch_bounds__(KTraits<S>::NTHREADS, 1)
     if (p.kind == 0 && p.stage_begin == 0 && tid < T::NCT) {
         for (int b = 0; b < S::B; ++b) {
             const __nv_bfloat16* e = p.embedding + (size_t)token_row(p, b) * S::D;
-            for (int c = cta.pl.red_c0 + tid; c < cta.pl.red_c1; c += T::NCT)
+            for (int c = p.plan[cta.cta].red_c0 + tid; c < p.plan[cta.cta].red_c1; c += T::NCT)
                 __stcg(p.x + (size_t)b * S::D + c, __bfloat162float(e[c]));
         }
     }
@@ -2868,6 +3086,9 @@ __global__ void __launch_bounds__(KTraits<S>::NTHREADS, 1)
         return;
     }
     asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(T::CONSUMER_REGS));
+#ifdef FFB_KCP_TCGEN05
+    if constexpr (S::KCP) tc05_fence_after();
+#endif
     if constexpr (S::KCP) {
         // the initial x rows' A-table entries and norm statistics; the first
         // S_QKV (or the LM head) waits for every CTA's arrival
@@ -2883,6 +3104,14 @@ __global__ void __launch_bounds__(KTraits<S>::NTHREADS, 1)
     } else {
         cta.consumer();
     }
+#ifdef FFB_KCP_TCGEN05
+    if constexpr (S::KCP) {  // every MMA was waited for (accbar) and every TMEM load completed
+        tc05_fence_before();
+        consumer_sync(T::NCT);
+        tc05_fence_after();
+        if (tid < 32) tmem_dealloc(cta.tmem_base(), 512);
+    }
+#endif
 }
 
 }  // namespace ffb200

@@ -18,6 +18,7 @@ struct KernelOps {
     int tc_d, tc_a;  // d_model-column / Waout rows use the tensor-core code order
     int ffn2_rows;   // W2 stored [D][DI] (two-phase FFN, KTraits::F2R), else Wffn2^T
     int kc;          // batch >= 8: K-chunk width of the chunk-major matrix layout (0: row-major)
+    int kc_layout;   // batch >= 8 weight / A-table layout: 2 = mma.sync, 3 = tcgen05 (FFB_KCP_TCGEN05)
     cudaError_t (*prepare)();
     cudaError_t (*launch)(const DecodeParams&, int grid, cudaStream_t, bool cooperative);
 };
@@ -52,6 +53,7 @@ KernelOps make_ops() {
                      S::QB,       T::NTHREADS,   T::SMEM_BYTES, T::NSLOTS, T::SLOT_BYTES,
                      T::RG,       T::TMAX,       T::KVC,    T::RPS,        T::ROW_BYTES,
                      T::MA::ROW_BYTES, T::MD::TC ? 1 : 0, T::MA::TC ? 1 : 0, T::F2R ? 1 : 0, S::KCP ? S::KC : 0,
+                     S::KCP ? kKcLayout : 0,
                      &prepare_impl<S>, &launch_impl<S>};
 }
 

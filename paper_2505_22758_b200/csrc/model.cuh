@@ -74,6 +74,7 @@ struct ffb_model {
     uint8_t *wqkv = nullptr, *waout = nullptr, *wffn1 = nullptr, *wffn2t = nullptr,
             *lm_head = nullptr;
     __nv_bfloat16 *embedding = nullptr, *kcache = nullptr, *vcache = nullptr;
+    uint64_t fp16_inexact = 0;  // batch >= 8 packer: bf16 weights below the fp16 normal range, rounded
     uint64_t quant_inexact_groups = 0;  // packer: groups not on a 4/8-bit grid (lossy)
     uint8_t* wlin = nullptr;            // stacked linear: [L][D] bf16 rows
     float* xbuf = nullptr;              // stacked linear: [2][B][D]

@@ -295,18 +295,28 @@ ffb_status build_plan(ffb_model* m) {
         if (!((m->calib_mask >> bit) & 1)) return (units * k) / G;
         return std::min<int64_t>(units, std::llround(units * cum[k] / cum[G]));
     };
+    // batch >= 8: row ranges in whole 8-row groups (the tcgen05 weight
+    // layout, decode_kernel.cuh frag_off): QKV / GLU in units of 4 pairs
+    const int64_t g8 = m->ops->kc > 0 ? 8 : 1;
+    if (qkv_pairs % (g8 / 2 > 0 ? g8 / 2 : 1) != 0 || c.d_model % g8 != 0 ||
+        glu_static % (g8 / 2 > 0 ? g8 / 2 : 1) != 0 || c.vocab_size % g8 != 0)
+        return fail(FFB_UNSUPPORTED, "batch >= 8: matrix rows must split in 8-row groups");
+    auto wsplit_g = [&](int64_t units, int64_t k, int bit, int64_t gran) {
+        return gran * wsplit_m(units / gran, k, bit);
+    };
+    const int64_t gp = g8 > 1 ? g8 / 2 : 1;  // pairs per group
     for (int64_t i = 0; i < G; ++i) {
         CtaPlan& p = plan[i];
         std::memset(&p, 0, sizeof(p));
         const int64_t k = m->plan_reverse ? G - 1 - i : i;  // weight-slice order
-        p.qkv_r0 = static_cast<int32_t>(2 * wsplit_m(qkv_pairs, k, 0));
-        p.qkv_r1 = static_cast<int32_t>(2 * wsplit_m(qkv_pairs, k + 1, 0));
-        p.aout_r0 = static_cast<int32_t>(wsplit_m(c.d_model, k, 1));
-        p.aout_r1 = static_cast<int32_t>(wsplit_m(c.d_model, k + 1, 1));
-        p.glu_t0 = static_cast<int32_t>(wsplit_m(glu_static, k, 2));
-        p.glu_t1 = static_cast<int32_t>(wsplit_m(glu_static, k + 1, 2));
-        p.lm_r0 = static_cast<int32_t>(wsplit_m(c.vocab_size, k, 3));
-        p.lm_r1 = static_cast<int32_t>(wsplit_m(c.vocab_size, k + 1, 3));
+        p.qkv_r0 = static_cast<int32_t>(2 * wsplit_g(qkv_pairs, k, 0, gp));
+        p.qkv_r1 = static_cast<int32_t>(2 * wsplit_g(qkv_pairs, k + 1, 0, gp));
+        p.aout_r0 = static_cast<int32_t>(wsplit_g(c.d_model, k, 1, g8));
+        p.aout_r1 = static_cast<int32_t>(wsplit_g(c.d_model, k + 1, 1, g8));
+        p.glu_t0 = static_cast<int32_t>(wsplit_g(glu_static, k, 2, gp));
+        p.glu_t1 = static_cast<int32_t>(wsplit_g(glu_static, k + 1, 2, gp));
+        p.lm_r0 = static_cast<int32_t>(wsplit_g(c.vocab_size, k, 3, g8));
+        p.lm_r1 = static_cast<int32_t>(wsplit_g(c.vocab_size, k + 1, 3, g8));
         p.red_c0 = static_cast<int32_t>(split_at(c.d_model, i, G));
         p.red_c1 = static_cast<int32_t>(split_at(c.d_model, i + 1, G));
         if (i < static_cast<int64_t>(m->n_units) * m->attn_group) {
@@ -1014,11 +1024,36 @@ ffb_status ffb_upload_tensor(ffb_model* m, const char* name, const float* values
         src = shard.data();
         std::swap(lrows, cols);
     }
+#ifdef FFB_KCP_TCGEN05
     if (d.kind == 0 && m->ops->kc > 0) {
-        // batch >= 8: chunk-major [cols / KC][rows][KC], the 8-column units of
-        // each row segment XOR-swizzled by row & 7 (decode_kernel.cuh: gemv_kc);
-        // the bf16 values are stored as fp16 (exact in the fp16 normal range,
-        // 2^-24 absolute below it), the tensor-core GEMV's operand type
+        // batch >= 8 (layout 3, decode_kernel.cuh frag_off / gemv_kc): the
+        // tcgen05 B operand, K-major with 128-byte swizzle -- [cols / KC]
+        // [rows / 8][KC / 64][8 rows][64 values], the 16-byte units of each
+        // 128-byte row piece XOR-swizzled by row & 7; the bf16 values are
+        // stored as fp16 (exact in the fp16 normal range, 2^-24 absolute
+        // below it; counted in fp16_inexact, out of range rejected)
+        const int64_t KC = m->ops->kc, nch = cols / KC, NKA = KC / 64;
+        if (lrows % 8 != 0) return fail(FFB_UNSUPPORTED, "batch >= 8: matrix rows must be a multiple of 8");
+        std::vector<float> cm((size_t)lrows * cols);
+        parallel_rows(lrows, [&](int64_t ra, int64_t rb) {
+            for (int64_t r = ra; r < rb; ++r)
+                for (int64_t c = 0; c < nch; ++c)
+                    for (int64_t ka = 0; ka < NKA; ++ka) {
+                        float* dst = cm.data() + ((((size_t)c * (lrows / 8) + r / 8) * NKA + ka) * 8 + (r & 7)) * 64;
+                        const float* s0 = src + (size_t)r * cols + c * KC + ka * 64;
+                        for (int64_t u = 0; u < 8; ++u)
+                            std::memcpy(dst + ((u ^ (r & 7)) * 8), s0 + u * 8, sizeof(float) * 8);
+                    }
+        });
+        shard.swap(cm);
+        src = shard.data();
+#else
+    if (d.kind == 0 && m->ops->kc > 0) {
+        // batch >= 8 (layout 2, decode_kernel.cuh gemv_kc, mma.sync path):
+        // chunk-major [cols / KC][rows][KC], the 8-column units of each row
+        // segment XOR-swizzled by row & 7; the bf16 values are stored as fp16
+        // (exact in the fp16 normal range, 2^-24 absolute below it; counted
+        // in fp16_inexact, out of range rejected), the tensor-core operand type
         const int64_t KC = m->ops->kc, nch = cols / KC;
         std::vector<float> cm((size_t)lrows * cols);
         parallel_rows(lrows, [&](int64_t ra, int64_t rb) {
@@ -1032,6 +1067,27 @@ ffb_status ffb_upload_tensor(ffb_model* m, const char* name, const float* values
         });
         shard.swap(cm);
         src = shard.data();
+#endif
+        // fp16 range / exactness of the bf16-rounded values
+        int64_t over = 0, inexact = 0;
+        std::mutex mu;
+        parallel_rows(lrows, [&](int64_t ra, int64_t rb) {
+            int64_t o = 0, ie = 0;
+            for (int64_t i = ra * cols; i < rb * cols; ++i) {
+                const float v = bf16_bits_to_f32(bf16_bits_rne(src[i]));
+                const float a = std::fabs(v);
+                if (!(a <= 65504.f)) ++o;
+                else if (a != 0.f && a < 6.103515625e-05f &&
+                         std::ldexp(a, 24) != std::floor(std::ldexp(a, 24))) ++ie;
+            }
+            std::lock_guard<std::mutex> g(mu);
+            over += o;
+            inexact += ie;
+        });
+        if (over > 0)
+            return fail(FFB_UNSUPPORTED, "batch >= 8: %lld weights of '%s' exceed the fp16 range of the "
+                                         "tensor-core operands", (long long)over, name);
+        m->fp16_inexact += inexact;
     }
     if (d.kind == 0 && m->ops->QB != 0) {  // quant packer, a block of rows at a time
         const size_t rb = d.row_bytes;
@@ -1309,14 +1365,20 @@ int64_t ffb_get_trace(ffb_model* m, uint64_t* out, int64_t n) {
     return total;
 }
 
-// A device-resident token id was out of range in an earlier step (decode_
-// kernel.cuh: token_row): clear the latch and report it like the reference's
-// ValidationError (reference.hpp:43-53).
-static ffb_status latched_token_error(ffb_model* m) {
+// The device error latch (DecodeParams::err_flag) was set in an earlier step:
+// bit 0 a device-resident token id out of range (decode_kernel.cuh:
+// token_row, reported like the reference's ValidationError, reference.hpp:
+// 43-53); bit 1 (batch >= 8) an activation outside the fp16 range of the
+// tensor-core operands (frag_put).  Clears the latch.
+static ffb_status latched_token_error(ffb_model* m, int64_t flag) {
     CUDA_TRY(cudaMemsetAsync(m->greedy + m->cfg.batch, 0, sizeof(int64_t), m->stream));
     CUDA_TRY(cudaStreamSynchronize(m->stream));
-    return fail(FFB_VALIDATION,
-                "decode_step: token id out of range (device-resident tokens; row 0 was used)");
+    if (flag & 1)
+        return fail(FFB_VALIDATION,
+                    "decode_step: token id out of range (device-resident tokens; row 0 was used)");
+    return fail(FFB_UNSUPPORTED,
+                "decode_step: an activation exceeded the fp16 range of the batch >= 8 tensor-core "
+                "operands (|v| > 65504); logits of that step are not valid");
 }
 
 ffb_status ffb_sync(ffb_model* m) {
@@ -1326,7 +1388,7 @@ ffb_status ffb_sync(ffb_model* m) {
     CUDA_TRY(cudaDeviceSynchronize());
     int64_t flag = 0;
     CUDA_TRY(cudaMemcpy(&flag, m->greedy + m->cfg.batch, sizeof(int64_t), cudaMemcpyDeviceToHost));
-    if (flag != 0) return latched_token_error(m);
+    if (flag != 0) return latched_token_error(m, flag);
     return FFB_OK;
 }
 
@@ -1374,7 +1436,7 @@ ffb_status ffb_decode_step(ffb_model* m, const int64_t* tokens, int64_t pos, flo
     if (logits_out && !direct) std::memcpy(logits_out, m->logits_pinned, lbytes);
     if (greedy_out) std::memcpy(greedy_out, m->greedy_pinned, sizeof(int64_t) * c.batch);
     for (auto& n : m->kv_len) n += 1;
-    if (m->greedy_pinned[c.batch] != 0) return latched_token_error(m);
+    if (m->greedy_pinned[c.batch] != 0) return latched_token_error(m, m->greedy_pinned[c.batch]);
     return FFB_OK;
 }
 
@@ -1464,6 +1526,8 @@ ffb_status ffb_get_info(const ffb_model* m, ffb_info* out) {
                                c.vocab_size) +
                         static_cast<uint64_t>(m->ops->row_bytes_a) * c.layers * c.d_model;
     out->quant_inexact_groups = m->quant_inexact_groups;
+    out->fp16_inexact = m->fp16_inexact;
+    out->kc_layout = m->ops->kc_layout;
     out->row_bytes = m->ops->row_bytes;
     out->device_bytes = m->device_bytes;
     return FFB_OK;

@@ -131,16 +131,17 @@ ffb_status parse_model(const std::string& text, ffb_model_config* c) {
 }
 
 // ---------------------------------------------------------------- device image
-constexpr uint64_t kImageMagic = 0x31474d4942464646ull;  // "FFFBIMG1"
+constexpr uint64_t kImageMagic = 0x32474d4942464646ull;  // "FFFBIMG2" (batch >= 8 layout 3)
 
 struct ImageHeader {
     uint64_t magic;
     ffb_model_config gcfg;  // whole model
     int32_t tp_rank, tp_size;
     // identity of the kernel specialisation (device row formats)
-    int32_t D, DI, DH, NQ, NKV, B, QB, row_bytes, row_bytes_a, tc_d, tc_a, ffn2_rows, kc;
+    int32_t D, DI, DH, NQ, NKV, B, QB, row_bytes, row_bytes_a, tc_d, tc_a, ffn2_rows, kc, kc_layout;
     int32_t n_regions;
     uint64_t quant_inexact_groups;
+    uint64_t fp16_inexact;
 };
 
 struct Region {
@@ -175,9 +176,10 @@ ImageHeader make_header(const ffb_model* m) {
     const KernelOps* o = m->ops;
     h.D = o->D; h.DI = o->DI; h.DH = o->DH; h.NQ = o->NQ; h.NKV = o->NKV; h.B = o->B; h.QB = o->QB;
     h.row_bytes = o->row_bytes; h.row_bytes_a = o->row_bytes_a; h.tc_d = o->tc_d; h.tc_a = o->tc_a;
-    h.ffn2_rows = o->ffn2_rows; h.kc = o->kc;
+    h.ffn2_rows = o->ffn2_rows; h.kc = o->kc; h.kc_layout = o->kc_layout;
     h.n_regions = static_cast<int32_t>(regions(m).size());
     h.quant_inexact_groups = m->quant_inexact_groups;
+    h.fp16_inexact = m->fp16_inexact;
     return h;
 }
 
@@ -345,6 +347,7 @@ ffb_status ffb_load_image(ffb_model* m, const char* path) {
         return fail(FFB_USAGE, "load_image: not a device image");
     ImageHeader want = make_header(m);
     want.quant_inexact_groups = h.quant_inexact_groups;
+    want.fp16_inexact = h.fp16_inexact;
     if (std::memcmp(&h, &want, sizeof(h)) != 0)
         return fail(FFB_VALIDATION,
                     "load_image: the image was packed for another model, shard or kernel "
@@ -365,6 +368,7 @@ ffb_status ffb_load_image(ffb_model* m, const char* path) {
         }
     }
     m->quant_inexact_groups = h.quant_inexact_groups;
+    m->fp16_inexact = h.fp16_inexact;
     return FFB_OK;
 }
 

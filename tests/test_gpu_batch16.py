@@ -118,3 +118,15 @@ def test_toy_batch16_zero_layers_is_lm_head_of_embedding():
     with device_from_store(st, 4) as m:
         e_plain, e_strict, flips = check_step(st, m, TOKENS, 0)
     assert flips == 0
+
+
+def test_gemv_layout_is_the_loaded_librarys():
+    """kc_layout reports which batch >= 8 GEMV this library runs: 2 =
+    mma.sync (libffb200.so), 3 = tcgen05 with TMEM accumulators
+    (libffb200_tc05.so, tests/test_gpu_tcgen05.py runs this file on it)."""
+    import os
+    cfg = to_model_cfg(TOY).replace(batch=16)
+    m = DecodeModel(cfg, 8)
+    want = int(os.environ.get("FFB_EXPECT_KC_LAYOUT", "2"))
+    assert m.info()["kc_layout"] == want
+    m.close()

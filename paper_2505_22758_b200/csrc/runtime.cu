@@ -976,6 +976,7 @@ ffb_status ffb_create_ex(const ffb_model_config* gcfg, int64_t max_seq_len, int 
     // stage streams KV through the ring the whole time: L2 prefetch measured
     // slower in both (int4 +5 %, b4 +7 %); on for bf16 batch 1-2 (-4 %)
     if (ops->QB != 0 || cfg->batch > 2) m->l2_prefetch = 0;
+
     st = probe_sm_ranks(m);
     if (st) return bail(st);
     *out = m;

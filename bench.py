@@ -359,6 +359,14 @@ def run_ours(args):
                          ("fused_overlap", RunMode.FUSED_OVERLAP)):
             k = max(10, args.steps // 4)
             variants[name + "_ms_per_step"] = round(max_over_ranks(timed(rm, k)), 5)
+        if tp > 1 and not share and torch.cuda.device_count() >= tp:
+            # the host-NCCL multi-kernel baseline: the same
+            # per-stage launches, residual sums as ncclAllReduce between them
+            from paper_2505_22758_b200 import broadcast_nccl_id
+            m.tp_nccl_init(broadcast_nccl_id())
+            k = max(10, args.steps // 4)
+            variants["baseline_nccl_ms_per_step"] = round(
+                max_over_ranks(timed(RunMode.BASELINE_NCCL, k)), 5)
         m.set_mode(mode)
         # device-resident greedy generation (ffb_decode_loop): 32 tokens per
         # call, no host round trip between tokens; cache reset per call

@@ -54,7 +54,12 @@ typedef enum ffb_status {
 typedef enum ffb_mode {
     FFB_MODE_BASELINE = 0,
     FFB_MODE_FUSED = 1,
-    FFB_MODE_FUSED_OVERLAP = 2
+    FFB_MODE_FUSED_OVERLAP = 2,
+    /* tensor parallelism only: the Baseline's per-stage launches with the two
+     * per-layer residual sums done by the host as ncclAllReduce between the
+     * kernels and the argmax by ncclAllGather (SURVEY.md §8(e) "Baseline:
+     * host ncclAllReduce between per-layer kernels"); needs ffb_tp_nccl_init */
+    FFB_MODE_BASELINE_NCCL = 3
 } ffb_mode;
 
 /* fusesim::ModelConfig (config.hpp:45-86).
@@ -128,6 +133,14 @@ ffb_status ffb_create_ex(const ffb_model_config *cfg, int64_t max_seq_len, int d
 int64_t ffb_tp_blob_bytes(void);
 ffb_status ffb_tp_export(ffb_model *m, void *blob);
 ffb_status ffb_tp_connect(ffb_model *m, const void *blobs, int32_t n);
+
+/* Host-NCCL communicator for FFB_MODE_BASELINE_NCCL.  NCCL is loaded at run
+ * time (dlopen "libnccl.so.2"; FFB_USAGE if absent), not linked.  Rank 0
+ * makes the 128-byte unique id with ffb_nccl_unique_id, the caller
+ * broadcasts it, every rank calls ffb_tp_nccl_init (collective over the
+ * tp_size ranks, one process per GPU). */
+ffb_status ffb_nccl_unique_id(uint8_t id[128]);
+ffb_status ffb_tp_nccl_init(ffb_model *m, const uint8_t id[128]);
 void ffb_destroy(ffb_model *m);
 
 /* Weight packer.  `name` uses the reference's tensor names

@@ -62,6 +62,7 @@ class RunMode(enum.IntEnum):
     BASELINE = 0        # one launch per sublayer stage (multi-kernel variant)
     FUSED = 1           # one persistent launch, producer waits at barriers
     FUSED_OVERLAP = 2   # one persistent launch, producer streams across barriers
+    BASELINE_NCCL = 3   # TP only: BASELINE launches + host ncclAllReduce between them
 
 
 class _Cfg(C.Structure):
@@ -267,6 +268,22 @@ def all_gather_tp_blobs(blob: bytes, group=None) -> list[bytes]:
     return out
 
 
+def nccl_unique_id() -> bytes:
+    """A fresh ncclUniqueId (128 bytes) for ffb_tp_nccl_init (rank 0 makes
+    it, the caller broadcasts it)."""
+    buf = (C.c_uint8 * 128)()
+    _check(lib().ffb_nccl_unique_id(buf))
+    return bytes(buf)
+
+
+def broadcast_nccl_id(group=None) -> bytes:
+    """Rank 0's ncclUniqueId on every rank (torch.distributed, any backend)."""
+    import torch.distributed as dist
+    obj = [nccl_unique_id() if dist.get_rank(group) == 0 else None]
+    dist.broadcast_object_list(obj, src=0, group=group)
+    return obj[0]
+
+
 def tensor_names(cfg: ModelConfig) -> list[str]:
     """Reference tensor names (tensor_store.hpp:339-363) in upload order."""
     if cfg.kind == 1:
@@ -299,6 +316,8 @@ def lib():
     L.ffb_tp_blob_bytes.restype = C.c_int64
     L.ffb_tp_export.argtypes = [C.c_void_p, C.c_void_p]
     L.ffb_tp_connect.argtypes = [C.c_void_p, C.c_void_p, C.c_int32]
+    L.ffb_nccl_unique_id.argtypes = [C.c_void_p]
+    L.ffb_tp_nccl_init.argtypes = [C.c_void_p, C.c_void_p]
     L.ffb_destroy.argtypes = [C.c_void_p]
     L.ffb_destroy.restype = None
     L.ffb_upload_tensor.argtypes = [C.c_void_p, C.c_char_p, P(C.c_float), C.c_int64]
@@ -392,6 +411,11 @@ class DecodeModel:
         """Connect to every rank's blob, ordered by rank (ffb_tp_connect)."""
         raw = b"".join(blobs)
         _check(lib().ffb_tp_connect(self._h, C.create_string_buffer(raw, len(raw)), len(blobs)))
+
+    def tp_nccl_init(self, nccl_id: bytes):
+        """This rank's NCCL communicator for RunMode.BASELINE_NCCL
+        (ffb_tp_nccl_init; collective over the TP ranks)."""
+        _check(lib().ffb_tp_nccl_init(self._h, C.create_string_buffer(nccl_id, 128)))
 
     @staticmethod
     def supported(cfg: ModelConfig) -> bool:

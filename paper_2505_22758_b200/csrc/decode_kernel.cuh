@@ -128,6 +128,8 @@ struct DecodeParams {
     // buffer [2 stage][2 layer parity][B][D] f32 + [kMaxTP][B] argmax slots;
     // xflag[r]: rank r's arrival flags [L][2][grid] + [1] (argmax).
     int32_t tp_size, tp_rank;
+    int32_t tp_host;      // 1 (FFB_MODE_BASELINE_NCCL): deltas / argmax candidates only
+                          // written to this rank's own buffer; the host reduces them
     int32_t vocab_base;   // first global vocab row of this rank's lm_head slice
     float* xch[8];
     uint32_t* xflag[8];
@@ -2569,6 +2571,7 @@ struct DecodeCta {
             const int b = i / cnt, c = i % cnt;
             __stcg(mine + (size_t)b * D + c0 + c, delta[b * cnt + c]);
         }
+        if (p.tp_host) return;  // host ncclAllReduce + apply between the launches
         consumer_sync(NCT);
         const size_t fi = ((size_t)l * 2 + slot) * grid + cta;
         if (ctid < p.tp_size) red_release_sys(p.xflag[ctid] + fi, 1);
@@ -2960,6 +2963,14 @@ struct DecodeCta {
                 // index on ties (numerics.hpp:169-175)
                 consumer_sync(NCT);
                 const size_t amax_off = (size_t)4 * B * D;
+                if (p.tp_host) {  // this rank's candidates, ncclAllGather'ed by the host
+                    if (ctid < B) {
+                        float* dst = p.xch[p.tp_rank] + amax_off + ((size_t)p.tp_rank * B + ctid) * 2;
+                        __stcg(dst, cv[ctid]);
+                        __stcg(dst + 1, __int_as_float(ci[ctid]));
+                    }
+                    return;
+                }
                 const size_t fi = (size_t)p.layers * 2 * grid;
                 if (ctid < B * p.tp_size) {
                     const int r = ctid / B, b = ctid % B;

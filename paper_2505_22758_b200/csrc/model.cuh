@@ -84,6 +84,9 @@ struct ffb_model {
     float *x = nullptr, *q = nullptr, *attn_out = nullptr, *glu_part = nullptr,
           *attn_part = nullptr, *logits = nullptr, *amax_val = nullptr;
     int32_t* amax_idx = nullptr;
+    void* nccl_comm = nullptr;        // ncclComm_t of FFB_MODE_BASELINE_NCCL (ffb_tp_nccl_init)
+    void (*nccl_destroy)(void*) = nullptr;
+    float* amax_gather = nullptr;     // [kMaxTP][B][2] the ranks' (value, index) candidates
     int64_t *greedy = nullptr, *tokens_dev = nullptr;
     uint32_t *counters = nullptr, *head_counters = nullptr, *amax_counter = nullptr,
              *qkv_head_counters = nullptr;
@@ -111,6 +114,7 @@ struct ffb_model {
 
     ~ffb_model() {
         if (device >= 0) cudaSetDevice(device);
+        if (nccl_comm && nccl_destroy) nccl_destroy(nccl_comm);
         for (void* q : ipc_opened) cudaIpcCloseMemHandle(q);
         for (void* p : allocs) cudaFree(p);
         if (tokens_pinned) cudaFreeHost(tokens_pinned);

@@ -25,6 +25,8 @@
 #include <string>
 #include <vector>
 
+#include <dlfcn.h>
+#include <nccl.h>  // types only: NCCL is dlopen'ed by the NCCL baseline mode
 #include <unistd.h>
 
 #include "../../include/flashformer_b200.h"
@@ -457,6 +459,7 @@ DecodeParams make_params(const ffb_model* m, int64_t pos, const int64_t* d_token
     if (m->cfg.kind == 1) p.stage_end = static_cast<int32_t>(m->cfg.layers);
     p.tp_size = m->tp_size;
     p.tp_rank = m->tp_rank;
+    p.tp_host = m->mode == FFB_MODE_BASELINE_NCCL ? 1 : 0;
     p.vocab_base = static_cast<int32_t>(m->vocab_base);
     for (int r = 0; r < kMaxTP; ++r) {
         p.xch[r] = m->peer_xch[r];
@@ -484,6 +487,99 @@ ffb_status reset_sync_state(ffb_model* m, cudaStream_t stream) {
     return FFB_OK;
 }
 
+// ---- host-NCCL multi-kernel TP baseline (FFB_MODE_BASELINE_NCCL) ----------
+// NCCL is loaded at run time: the library works (and the other modes run)
+// where it is absent.
+struct NcclApi {
+    ncclResult_t (*get_unique_id)(ncclUniqueId*);
+    ncclResult_t (*comm_init_rank)(ncclComm_t*, int, ncclUniqueId, int);
+    ncclResult_t (*all_reduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                               cudaStream_t);
+    ncclResult_t (*all_gather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t);
+    ncclResult_t (*comm_destroy)(ncclComm_t);
+    const char* (*error_string)(ncclResult_t);
+};
+
+const NcclApi* nccl_api() {
+    static NcclApi api{};
+    static bool ok = [] {
+        void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) return false;
+        api.get_unique_id = reinterpret_cast<decltype(api.get_unique_id)>(dlsym(h, "ncclGetUniqueId"));
+        api.comm_init_rank = reinterpret_cast<decltype(api.comm_init_rank)>(dlsym(h, "ncclCommInitRank"));
+        api.all_reduce = reinterpret_cast<decltype(api.all_reduce)>(dlsym(h, "ncclAllReduce"));
+        api.all_gather = reinterpret_cast<decltype(api.all_gather)>(dlsym(h, "ncclAllGather"));
+        api.comm_destroy = reinterpret_cast<decltype(api.comm_destroy)>(dlsym(h, "ncclCommDestroy"));
+        api.error_string = reinterpret_cast<decltype(api.error_string)>(dlsym(h, "ncclGetErrorString"));
+        return api.get_unique_id && api.comm_init_rank && api.all_reduce && api.all_gather &&
+               api.comm_destroy && api.error_string;
+    }();
+    return ok ? &api : nullptr;
+}
+
+#define NCCL_TRY(expr)                                                                         \
+    do {                                                                                       \
+        ncclResult_t r_ = (expr);                                                              \
+        if (r_ != ncclSuccess) return fail(FFB_DEVICE, "%s: %s", #expr, nccl_api()->error_string(r_)); \
+    } while (0)
+
+__global__ void apply_delta_kernel(float* __restrict__ x, const float* __restrict__ d, int64_t n) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        x[i] += d[i];
+}
+
+// greedy[b] from the ranks' (value, global index) candidates [tp][B][2]:
+// ranks own ascending vocab slices, so scanning them in order and keeping the
+// first maximum is the lowest index on ties (numerics.hpp:169-175)
+__global__ void amax_pick_kernel(const float* __restrict__ cand, int tp, int B, int64_t* __restrict__ greedy) {
+    const int b = threadIdx.x;
+    if (b >= B) return;
+    float bv = -INFINITY;
+    int bi = 0;
+    for (int r = 0; r < tp; ++r) {
+        const float v = cand[((size_t)r * B + b) * 2];
+        const int i = __float_as_int(cand[((size_t)r * B + b) * 2 + 1]);
+        if (r == 0 || v > bv) {
+            bv = v;
+            bi = i;
+        }
+    }
+    greedy[b] = bi;
+}
+
+// Each stage its own launch (as FFB_MODE_BASELINE); after S_AOUT and S_RED
+// of every layer the ranks' residual deltas (own exchange slot, written by
+// tp_exchange_add) are summed by ncclAllReduce on the launch stream and added
+// to x; after the LM head the argmax candidates are ncclAllGather'ed.
+ffb_status launch_step_nccl(ffb_model* m, DecodeParams p, cudaStream_t stream) {
+    const auto* nc = nccl_api();
+    if (!nc || !m->nccl_comm || m->tp_size < 2 || m->cfg.kind != 0)
+        return fail(FFB_USAGE, "BASELINE_NCCL: tensor-parallel ranks with ffb_tp_nccl_init only");
+    auto comm = static_cast<ncclComm_t>(m->nccl_comm);
+    const int64_t L = m->cfg.layers, B = m->cfg.batch, D = m->cfg.d_model;
+    const int n = static_cast<int>(L * kStagesPerLayer + 1);
+    for (int s = 0; s < n; ++s) {
+        p.stage_begin = s;
+        p.stage_end = s + 1;
+        CUDA_TRY(m->ops->launch(p, m->grid, stream, false));
+        const int sk = s % kStagesPerLayer;
+        if (s < L * kStagesPerLayer && (sk == S_AOUT || sk == S_RED)) {
+            const int64_t l = s / kStagesPerLayer, slot = sk == S_AOUT ? 0 : 1;
+            float* d = m->xch + (size_t)(slot * 2 + (l & 1)) * B * D;
+            NCCL_TRY(nc->all_reduce(d, d, (size_t)(B * D), ncclFloat32, ncclSum, comm, stream));
+            apply_delta_kernel<<<std::max<int64_t>(1, (B * D + 255) / 256), 256, 0, stream>>>(m->x, d, B * D);
+            CUDA_TRY(cudaGetLastError());
+        }
+    }
+    const float* mine = m->xch + (size_t)4 * B * D + (size_t)m->tp_rank * B * 2;
+    NCCL_TRY(nc->all_gather(mine, m->amax_gather, (size_t)(B * 2), ncclFloat32, comm, stream));
+    amax_pick_kernel<<<1, 32 * ((B + 31) / 32), 0, stream>>>(m->amax_gather, m->tp_size, static_cast<int>(B),
+                                                            p.greedy);
+    CUDA_TRY(cudaGetLastError());
+    return FFB_OK;
+}
+
 ffb_status launch_step(ffb_model* m, int64_t pos, const int64_t* d_tokens, float* d_logits,
                        int64_t* d_greedy, cudaStream_t stream) {
     m->epoch += 1;
@@ -493,6 +589,7 @@ ffb_status launch_step(ffb_model* m, int64_t pos, const int64_t* d_tokens, float
         m->epoch = 1;
     }
     DecodeParams p = make_params(m, pos, d_tokens, d_logits, d_greedy);
+    if (m->mode == FFB_MODE_BASELINE_NCCL) return launch_step_nccl(m, p, stream);
     if (m->mode == FFB_MODE_BASELINE) {
         const int n = m->cfg.kind == 1 ? static_cast<int>(m->cfg.layers)
                                        : static_cast<int>(m->cfg.layers * kStagesPerLayer + 1);
@@ -951,6 +1048,7 @@ ffb_status ffb_create_ex(const ffb_model_config* gcfg, int64_t max_seq_len, int 
     m->xflag_bytes = sizeof(uint32_t) * ((size_t)Lc * 2 * m->grid + 1);
     ALLOC(m->xch, m->xch_bytes / sizeof(float));
     ALLOC(m->xflag, m->xflag_bytes / sizeof(uint32_t));
+    ALLOC(m->amax_gather, (size_t)kMaxTP * B * 2);
     if (cudaMemset(m->xflag, 0, m->xflag_bytes) != cudaSuccess ||
         cudaMemset(m->xch, 0, m->xch_bytes) != cudaSuccess)
         return bail(fail(FFB_DEVICE, "cudaMemset failed"));
@@ -1271,8 +1369,22 @@ int64_t ffb_kv_length(const ffb_model* m, int64_t layer) {
 
 ffb_status ffb_set_mode(ffb_model* m, ffb_mode mode) {
     if (!m) return fail(FFB_USAGE, "NULL handle");
-    if (mode != FFB_MODE_BASELINE && mode != FFB_MODE_FUSED && mode != FFB_MODE_FUSED_OVERLAP)
+    if (mode != FFB_MODE_BASELINE && mode != FFB_MODE_FUSED && mode != FFB_MODE_FUSED_OVERLAP &&
+        mode != FFB_MODE_BASELINE_NCCL)
         return fail(FFB_USAGE, "unknown mode %d", (int)mode);
+    if (mode == FFB_MODE_BASELINE_NCCL && (m->tp_size < 2 || !m->nccl_comm))
+        return fail(FFB_USAGE, "BASELINE_NCCL: a tensor-parallel rank after ffb_tp_nccl_init");
+    if ((mode == FFB_MODE_BASELINE_NCCL) != (m->mode == FFB_MODE_BASELINE_NCCL)) {
+        // the in-kernel exchange flags do not advance in the NCCL mode: every
+        // counter restarts from a clean epoch (all ranks switch together)
+        CUDA_TRY(cudaSetDevice(m->device));
+        CUDA_TRY(cudaStreamSynchronize(m->stream));
+        CUDA_TRY(cudaDeviceSynchronize());
+        ffb_status s = reset_sync_state(m, m->stream);
+        if (s) return s;
+        CUDA_TRY(cudaStreamSynchronize(m->stream));
+        m->epoch = 0;
+    }
     m->mode = mode;
     return FFB_OK;
 }
@@ -1398,7 +1510,7 @@ static ffb_status check_step(ffb_model* m, const int64_t* tokens, int64_t pos) {
     if (m->cfg.kind != 0)
         return fail(FFB_VALIDATION, "decode_step: llama_decoder models only (stacked_linear: "
                                     "ffb_linear_forward)");
-    if (!m->tp_connected)
+    if (!m->tp_connected && !(m->mode == FFB_MODE_BASELINE_NCCL && m->nccl_comm))
         return fail(FFB_USAGE, "tensor-parallel rank not connected (ffb_tp_connect)");
     if (tokens)
         for (int64_t b = 0; b < c.batch; ++b)
@@ -1519,7 +1631,8 @@ ffb_status ffb_get_info(const ffb_model* m, ffb_info* out) {
     out->slot_bytes = m->ops->slot_bytes;
     out->attn_group = m->attn_group;
     out->launches_per_step =
-        m->mode == FFB_MODE_BASELINE ? static_cast<int32_t>(c.layers * kStagesPerLayer + 1) : 1;
+        (m->mode == FFB_MODE_BASELINE || m->mode == FFB_MODE_BASELINE_NCCL)
+            ? static_cast<int32_t>(c.layers * kStagesPerLayer + 1) : 1;
     out->mode = m->mode;
     const uint64_t row = static_cast<uint64_t>(m->ops->row_bytes);
     if (c.kind == 1) out->weight_bytes = row * static_cast<uint64_t>(c.layers) * c.d_model;
@@ -1678,6 +1791,35 @@ ffb_status ffb_tp_connect(ffb_model* m, const void* blobs, int32_t n) {
         }
     }
     m->tp_connected = true;
+    return FFB_OK;
+}
+
+ffb_status ffb_nccl_unique_id(uint8_t id[128]) {
+    if (!id) return fail(FFB_USAGE, "NULL argument");
+    const auto* nc = nccl_api();
+    if (!nc) return fail(FFB_USAGE, "NCCL not available (dlopen libnccl.so.2 failed)");
+    static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId");
+    ncclUniqueId u;
+    NCCL_TRY(nc->get_unique_id(&u));
+    std::memcpy(id, &u, 128);
+    return FFB_OK;
+}
+
+ffb_status ffb_tp_nccl_init(ffb_model* m, const uint8_t id[128]) {
+    if (!m || !id) return fail(FFB_USAGE, "NULL argument");
+    if (m->tp_size < 2) return fail(FFB_USAGE, "tp_nccl_init: tensor-parallel ranks only");
+    const auto* nc = nccl_api();
+    if (!nc) return fail(FFB_USAGE, "NCCL not available (dlopen libnccl.so.2 failed)");
+    CUDA_TRY(cudaSetDevice(m->device));
+    ncclUniqueId u;
+    std::memcpy(&u, id, 128);
+    ncclComm_t comm = nullptr;
+    NCCL_TRY(nc->comm_init_rank(&comm, m->tp_size, u, m->tp_rank));
+    if (m->nccl_comm) nc->comm_destroy(static_cast<ncclComm_t>(m->nccl_comm));
+    m->nccl_comm = comm;
+    m->nccl_destroy = [](void* c) {
+        if (const auto* a = nccl_api()) a->comm_destroy(static_cast<ncclComm_t>(c));
+    };
     return FFB_OK;
 }
 

@@ -70,3 +70,11 @@ def test_byte_accounting():
     cfg = P.model_preset("llama31_8b")
     assert cfg.streamed_weight_bytes() == 32 * 436207616 + 1050673152  # test_store.cpp:73-86
     assert cfg.replace(quant_bits=4).streamed_weight_bytes() == 3986849792
+
+
+def test_nccl_unique_id_without_gpu():
+    """The host-NCCL baseline loads NCCL at run time (dlopen); making the
+    communicator id needs no GPU."""
+    import paper_2505_22758_b200 as P
+    a, b = P.nccl_unique_id(), P.nccl_unique_id()
+    assert len(a) == 128 and a != b

@@ -1744,13 +1744,13 @@ struct DecodeCta {
 #pragma unroll
                     for (int e = 0; e < 4; ++e) acc[j][nt][e] = 0.f;
             for (int c = 0; c < M::NKC; ++c) {
+                uint4 afh[8], afl[8];
                 const uint32_t sa = it % T::NSLOTS;
                 wait_full(sa, (it / T::NSLOTS) & 1);
                 const uint8_t* atab = ring + sa * T::SLOT_BYTES + kp * 8 * 1024 + lane * 16;
                 ++it;
                 // this warp's A fragments of the chunk into registers, then the
                 // A-table slot is released: the ring refills it with weights
-                uint4 afh[8], afl[8];
 #pragma unroll
                 for (int ks = 0; ks < 8; ++ks) {
                     afh[ks] = lds_u128(atab + ks * 1024);
@@ -2783,6 +2783,7 @@ struct DecodeCta {
         Act<> act;
         load_act(act, p.x, false, p.norm_ffn + (size_t)l * D, l * kStagesPerLayer + S_GLU);
         glu_ffn1(it, &act, pl.glu_t0, pl.glu_t1);
+        trace_mark(l * kStagesPerLayer + S_GLU, 3);  // (trace only: FFN1 done)
         if constexpr (T::F2R) {  // h is in glu_part; S_RED applies W2
             arrive(p.counters + l * kStagesPerLayer + S_GLU, l * kStagesPerLayer + S_GLU);
             return;

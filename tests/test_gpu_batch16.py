@@ -130,3 +130,43 @@ def test_gemv_layout_is_the_loaded_librarys():
     want = int(os.environ.get("FFB_EXPECT_KC_LAYOUT", "2"))
     assert m.info()["kc_layout"] == want
     m.close()
+
+
+def test_fp16_range_weights_rejected_and_counted():
+    """Batch >= 8 stores the bf16 weights as fp16 (the tensor-core operand):
+    values beyond ±65504 are rejected at upload (no silent inf), values
+    below the fp16 normal range are stored rounded and counted
+    (ffb_info.fp16_inexact)."""
+    from paper_2505_22758_b200 import UnsupportedConfigError
+    cfg = to_model_cfg(TOY).replace(batch=16)
+    st = O.OracleStore(TOY.replace(batch=16), 3, 8)
+    m = DecodeModel(cfg, 8)
+    w = np.array(st.tensor("layer.0.wqkv"), np.float32)
+    m.upload_tensor("layer.0.wqkv", w)
+    base = m.info()["fp16_inexact"]
+    w2 = w.copy().ravel()
+    w2[:3] = [1e-6, -3e-7, 2.5e-6]   # below 2^-14 and not multiples of 2^-24 after bf16 rounding
+    m.upload_tensor("layer.0.wqkv", w2)
+    assert m.info()["fp16_inexact"] >= base + 3
+    w2[5] = 1.0e5
+    with pytest.raises(UnsupportedConfigError):
+        m.upload_tensor("layer.0.wqkv", w2)
+    m.close()
+
+
+def test_fp16_range_activation_overflow_is_reported():
+    """An activation beyond the fp16 range of the batch >= 8 A tables (here:
+    a huge embedding row) latches the device error flag; the step reports
+    it instead of returning inf / NaN logits silently."""
+    from paper_2505_22758_b200 import FusesimError
+    st = O.OracleStore(TOY.replace(batch=16), 21, 8)
+    with device_from_store(st) as m:
+        emb = np.array(st.tensor("embedding"), np.float32)
+        emb[17] = 3.0e5
+        m.upload_tensor("embedding", emb)
+        with pytest.raises(FusesimError, match="fp16 range"):
+            m.step(TOKENS, 0)
+        for l in range(TOY.layers):  # (that step appended its K/V rows)
+            m.set_length(l, 0)
+        logits, _ = m.step([1] * 16, 0)  # the latch was cleared: a clean step runs
+        assert np.isfinite(logits).all()

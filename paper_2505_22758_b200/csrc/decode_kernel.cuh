@@ -111,6 +111,11 @@ struct DecodeParams {
     uint32_t epoch;
     int32_t stage_begin, stage_end;
     int32_t overlap;     // 1 = FusedOverlap, 0 = Fused (producer waits at barriers)
+    // component ablation (Table 8, tools/component_bench.py; batch
+    // < 8): stage types run per layer, bit s = stage s -- 0x1f the decoder,
+    // 0x07 stacked attention blocks (QKV, ATTN, AOUT), 0x18 stacked GLU
+    // blocks (GLU, W2 / RED)
+    int32_t stage_mask;
     int32_t attn_group;  // G: CTAs per (batch row, kv head)
     int32_t n_units;     // B * NKV
     int32_t debug;       // kDebug* bits; 0 in production
@@ -495,6 +500,7 @@ struct DecodeCta {
             *target = full_grid;
             return true;
         }
+        const bool red_on = (p.stage_mask >> S_RED) & 1;
         if (stage == p.layers * kStagesPerLayer) {  // LM head
             if (p.layers == 0) {
                 if constexpr (!S::KCP) return false;
@@ -502,10 +508,11 @@ struct DecodeCta {
                 *target = full_grid;
                 return true;
             }
-            *ctr = p.counters + (p.layers - 1) * kStagesPerLayer + S_RED;
+            *ctr = p.counters + (p.layers - 1) * kStagesPerLayer + (red_on ? S_RED : S_AOUT);
             *target = full_grid;
             return true;
         }
+        if (!((p.stage_mask >> s) & 1)) return false;  // (component ablation: stage not run)
         switch (s) {
             case S_QKV:
                 if (l == 0) {
@@ -515,7 +522,7 @@ struct DecodeCta {
                     *target = full_grid;
                     return true;
                 }
-                *ctr = p.counters + (l - 1) * kStagesPerLayer + S_RED;
+                *ctr = p.counters + (l - 1) * kStagesPerLayer + (red_on ? S_RED : S_AOUT);
                 *target = full_grid;
                 return true;
             case S_ATTN:  // only the CTAs that computed this kv head's q/k/v rows
@@ -528,7 +535,12 @@ struct DecodeCta {
                 *target = p.epoch * static_cast<uint32_t>(p.n_units);
                 return true;
             case S_GLU:
-                *ctr = p.counters + l * kStagesPerLayer + S_AOUT;
+                if (!((p.stage_mask >> S_AOUT) & 1)) {  // stacked GLU blocks: the previous W2
+                    if (l == 0) return false;
+                    *ctr = p.counters + (l - 1) * kStagesPerLayer + S_RED;
+                } else {
+                    *ctr = p.counters + l * kStagesPerLayer + S_AOUT;
+                }
                 *target = full_grid;
                 return true;
             default:  // S_RED
@@ -618,6 +630,7 @@ struct DecodeCta {
             if constexpr (S::KCP) { L.atab = p.xfrag_f; L.nkc = MD::NKC; L.rows_total = p.vocab; }
             return true;
         }
+        if (!((p.stage_mask >> s) & 1)) return false;  // (component ablation)
         switch (s) {
             case S_QKV:
                 if (sub > 0) return false;
@@ -3034,6 +3047,7 @@ struct DecodeCta {
                 stage_lmhead(it);
                 continue;
             }
+            if (!((p.stage_mask >> s) & 1)) continue;  // (component ablation)
             switch (s) {
                 case S_QKV: stage_qkv(it, l); break;
                 case S_ATTN: stage_attn(it, l); break;

@@ -444,6 +444,7 @@ DecodeParams make_params(const ffb_model* m, int64_t pos, const int64_t* d_token
     p.stage_begin = 0;
     p.stage_end = static_cast<int32_t>(m->cfg.layers * kStagesPerLayer + 1);
     p.overlap = m->mode == FFB_MODE_FUSED_OVERLAP ? 1 : 0;
+    p.stage_mask = m->stage_mask;
     p.attn_group = m->attn_group;
     p.n_units = m->n_units;
     p.eps = static_cast<float>(m->cfg.rmsnorm_eps);
@@ -594,6 +595,10 @@ ffb_status launch_step(ffb_model* m, int64_t pos, const int64_t* d_tokens, float
         const int n = m->cfg.kind == 1 ? static_cast<int>(m->cfg.layers)
                                        : static_cast<int>(m->cfg.layers * kStagesPerLayer + 1);
         for (int s = 0; s < n; ++s) {
+            // (component ablation: a masked stage is not launched -- except
+            // stage 0, whose launch also initialises the residual)
+            if (m->cfg.kind == 0 && s > 0 && s < n - 1 && !((m->stage_mask >> (s % kStagesPerLayer)) & 1))
+                continue;
             p.stage_begin = s;
             p.stage_end = s + 1;
             CUDA_TRY(m->ops->launch(p, m->grid, stream, false));
@@ -1422,6 +1427,14 @@ ffb_status ffb_set_option(ffb_model* m, const char* key, int64_t value) {
     }
     if (std::strcmp(key, "sm_rank") == 0) {
         m->use_sm_rank = value ? 1 : 0;
+        return FFB_OK;
+    }
+    if (std::strcmp(key, "stage_mask") == 0) {
+        if (value != 0x1f && value != 0x07 && value != 0x18)
+            return fail(FFB_USAGE, "stage_mask: 0x1f (decoder), 0x07 (attention blocks) or 0x18 (GLU blocks)");
+        if (value != 0x1f && (m->cfg.kind != 0 || m->cfg.batch >= 8 || m->tp_size > 1))
+            return fail(FFB_UNSUPPORTED, "stage_mask: single-GPU decoder, batch < 8");
+        m->stage_mask = static_cast<int32_t>(value);
         return FFB_OK;
     }
     if (std::strcmp(key, "l2_prefetch_stages") == 0) {

@@ -342,3 +342,26 @@ def test_8b_width_long_context_multi_pass():
     with device_from_store(st) as m:
         e_plain, e_strict, flips = check_step(st, m, [17], 9000)
     print(f"8B ctx 9000: rel_err {e_plain:.2e}, same-KV {e_strict:.2e}, flips {flips}")
+
+
+@pytest.mark.parametrize("mask", [0x07, 0x18])
+def test_component_stage_masks_are_mode_identical(mask):
+    """The component ablation (tools/component_bench.py, Table 8):
+    stacked attention-only (0x07) or GLU-only (0x18) blocks give finite,
+    bit-identical logits in all three run modes (the dependency chain skips
+    the masked stages consistently)."""
+    cfg = to_model_cfg(O.preset("tiny")).replace(layers=3)
+    outs = []
+    for mode in (RunMode.BASELINE, RunMode.FUSED, RunMode.FUSED_OVERLAP):
+        m = DecodeModel(cfg, 64, mode=mode)
+        m.init_synthetic(5)
+        m.set_option("stage_mask", mask)
+        steps = []
+        for pos in range(3):
+            lg, _ = m.step([3 + pos], pos)
+            steps.append(lg)
+        outs.append(np.stack(steps))
+        m.close()
+    assert np.isfinite(outs[0]).all()
+    np.testing.assert_array_equal(outs[0], outs[1])
+    np.testing.assert_array_equal(outs[1], outs[2])

@@ -20,11 +20,17 @@ ap.add_argument("--quant", type=int, default=0, help="weight bits: 0 (bf16), 4, 
 ap.add_argument("--mode", default="fused_overlap")
 ap.add_argument("--reverse", action="store_true", help="plan_reverse option")
 ap.add_argument("--calibrate", type=int, default=0, help="ffb_calibrate iterations first")
+ap.add_argument("--mask", type=lambda v: int(v, 0), default=0x1f, help="stage_mask (component ablation)")
+ap.add_argument("--vocab", type=int, default=0, help="vocabulary rows (0: the preset's)")
 a = ap.parse_args()
 cfg = model_preset(a.model).replace(batch=a.batch, quant_bits=a.quant)
+if a.vocab:
+    cfg = cfg.replace(vocab_size=a.vocab)
 m = DecodeModel(cfg, a.ctx + 8, mode={"fused_overlap": RunMode.FUSED_OVERLAP, "fused": RunMode.FUSED,
                                       "baseline": RunMode.BASELINE}[a.mode])
 m.init_synthetic(1)
+if a.mask != 0x1f:
+    m.set_option("stage_mask", a.mask)
 if a.reverse:
     m.set_option("plan_reverse", 1)
 if a.calibrate:

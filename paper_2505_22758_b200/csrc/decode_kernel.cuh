@@ -387,13 +387,15 @@ struct KTraits : RowMap<S, S::D> {
     // per-warp attention (ATT_WARP): alpha*q [QPG][DH], then per warp (m, l)
     // [NCW][QPG][2] and O [NCW][QPG][DH] for the CTA merge.  Same-box A/B
     // against the three-barrier passes (attn_pass_tc), ms/step: 8B b16 8.18
-    // -> 7.37, b4 3.93 -> 3.76, b2 3.11 -> 3.10, 1B b1 0.639 -> 0.629, but
-    // 8B b1 (one ~230-position pass per CTA) 2.700 -> 2.748: kept on passes.
-    // QPG = 8 (70B) would need 32 KiB of merge scratch: passes.
+    // -> 7.37, b4 3.93 -> 3.76, b2 3.11 -> 3.10, 1B b1 0.639 -> 0.629; 8B b1
+    // (one ~230-position pass per CTA) was 2.700 -> 2.748 in round 1 and,
+    // with the producer free of spills (round 2), 2.804 -> 2.789 and int4
+    // 1.870 -> 1.833: the per-warp path everywhere.  QPG = 8 (70B) would
+    // need 32 KiB of merge scratch: passes.
 #ifdef FFB_ATT_PASS
     static constexpr bool ATT_WARP = false;
 #else
-    static constexpr bool ATT_WARP = S::QPG <= 4 && (S::B > 1 || S::D < 4096);
+    static constexpr bool ATT_WARP = S::QPG <= 4;
 #endif
     static constexpr int SZ_ATT = ATT_WARP
         ? S::QPG * S::DH + 2 * NCW * S::QPG + NCW * S::QPG * S::DH

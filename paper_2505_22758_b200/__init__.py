@@ -346,6 +346,8 @@ def lib():
     L.ffb_get_info.argtypes = [C.c_void_p, P(_Info)]
     L.ffb_decode_loop.argtypes = [C.c_void_p, C.c_void_p, C.c_int64, C.c_int32, C.c_int32,
                                   C.c_void_p, C.c_void_p]
+    L.ffb_prefill.argtypes = [C.c_void_p, P(C.c_int64), C.c_int64, C.c_int64, P(C.c_float),
+                              P(C.c_int64)]
     L.ffb_linear_forward.argtypes = [C.c_void_p, P(C.c_float), P(C.c_float), C.c_void_p]
     L.ffb_linear_forward_device.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
     L.ffb_logits_device.argtypes = [C.c_void_p]
@@ -578,6 +580,30 @@ class DecodeModel:
         """Wait for enqueued steps; raise ValidationError if a device-resident
         token id was out of range (ffb_sync)."""
         _check(lib().ffb_sync(self._h))
+
+    def prefill(self, tokens, pos: int = 0, logits: bool = True):
+        """Prompt ingestion as GEMMs (ffb_prefill): tokens [n][batch] at
+        positions pos .. pos+n-1; returns (logits f32 [B][V] or None, greedy
+        int64 [B]) of the last position.  The cache ends at pos + n, exactly
+        where n decode steps would leave it; prompts longer than 1024 rows
+        (n * batch) are fed in chunks."""
+        c = self.cfg
+        tok = np.ascontiguousarray(np.asarray(tokens, dtype=np.int64))
+        if tok.ndim == 1:
+            tok = tok.reshape(-1, 1) if c.batch == 1 else tok.reshape(1, -1)
+        if tok.ndim != 2 or tok.shape[1] != c.batch or tok.shape[0] == 0:
+            raise ValidationError("prefill: tokens must be [n][batch]")
+        out = np.empty((c.batch, c.vocab_size), np.float32) if logits else None
+        greedy = np.empty(c.batch, np.int64)
+        chunk = max(1, 1024 // c.batch)
+        for t0 in range(0, tok.shape[0], chunk):
+            part = np.ascontiguousarray(tok[t0:t0 + chunk])
+            last = t0 + chunk >= tok.shape[0]
+            _check(lib().ffb_prefill(self._h, part.ctypes.data_as(C.POINTER(C.c_int64)),
+                                     part.shape[0], pos + t0,
+                                     _fp(out) if (last and out is not None) else None,
+                                     greedy.ctypes.data_as(C.POINTER(C.c_int64))))
+        return out, greedy
 
     def decode_loop(self, d_tokens: int, pos: int, n_steps: int, d_out: int,
                     teacher_forced: bool = False, stream: int = 0):

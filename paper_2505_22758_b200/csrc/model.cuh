@@ -87,7 +87,12 @@ struct ffb_model {
     int32_t* amax_idx = nullptr;
     void* nccl_comm = nullptr;        // ncclComm_t of FFB_MODE_BASELINE_NCCL (ffb_tp_nccl_init)
     void (*nccl_destroy)(void*) = nullptr;
-    float* amax_gather = nullptr;     // [kMaxTP][B][2] the ranks' (value, index) candidates
+    float* amax_gather = nullptr;
+    // prefill (prefill.cu): cuBLAS handle + scratch, created on first use
+    void* cublas = nullptr;
+    void (*cublas_destroy)(void*) = nullptr;
+    void* pf_buf = nullptr;
+    size_t pf_bytes = 0;     // [kMaxTP][B][2] the ranks' (value, index) candidates
     int64_t *greedy = nullptr, *tokens_dev = nullptr;
     uint32_t *counters = nullptr, *head_counters = nullptr, *amax_counter = nullptr,
              *qkv_head_counters = nullptr;
@@ -116,6 +121,8 @@ struct ffb_model {
     ~ffb_model() {
         if (device >= 0) cudaSetDevice(device);
         if (nccl_comm && nccl_destroy) nccl_destroy(nccl_comm);
+        if (cublas && cublas_destroy) cublas_destroy(cublas);
+        if (pf_buf) cudaFree(pf_buf);
         for (void* q : ipc_opened) cudaIpcCloseMemHandle(q);
         for (void* p : allocs) cudaFree(p);
         if (tokens_pinned) cudaFreeHost(tokens_pinned);

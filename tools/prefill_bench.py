@@ -1,0 +1,78 @@
+"""Prompt ingestion on one B200: the GEMM prefill (ffb_prefill, csrc/prefill.cu)
+against decode-as-prefill (the reference's way, reference.hpp:60-61: one
+persistent-kernel decode step per prompt position, here device-resident via
+ffb_decode_loop teacher-forced), full Llama-3.1-8B shape, synthetic weights.
+
+    python tools/prefill_bench.py [--preset llama31_8b] [--lens 128,512,1024] [--reps 5] [--out F]
+
+Times are host wall-clock around the synchronous calls (prefill includes the
+host->device copy of the prompt and the logits read-back), min over reps.
+"""
+import argparse
+import json
+import os
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+from paper_2505_22758_b200 import DecodeModel, model_preset  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--preset", default="llama31_8b")
+ap.add_argument("--lens", default="128,512,1024")
+ap.add_argument("--batch", type=int, default=1)
+ap.add_argument("--reps", type=int, default=5)
+ap.add_argument("--out", default="")
+ap.add_argument("--skip-decode", action="store_true", help="prefill only (profiling)")
+a = ap.parse_args()
+
+cfg = model_preset(a.preset).replace(batch=a.batch)
+lens = [int(x) for x in a.lens.split(",")]
+m = DecodeModel(cfg, max(lens) + 8)
+m.init_synthetic(7)
+rows = []
+rng = np.random.default_rng(0)
+for n in lens:
+    toks = rng.integers(0, cfg.vocab_size, size=(n, cfg.batch), dtype=np.int64)
+
+    def reset():
+        for l in range(cfg.layers):
+            m.set_length(l, 0)
+
+    best = 1e9
+    for r in range(a.reps + 1):
+        reset()
+        t0 = time.perf_counter()
+        m.prefill(toks, 0)
+        dt = time.perf_counter() - t0
+        if r:
+            best = min(best, dt)
+    # decode-as-prefill: n teacher-forced steps of the persistent kernel
+    d_tok = torch.from_numpy(toks).cuda()
+    d_out = torch.empty_like(d_tok)
+    s = torch.cuda.Stream()
+    best_d = float("nan")
+    for r in range(0 if a.skip_decode else min(a.reps, 3) + 1):
+        reset()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
+        e0.record(s)
+        m.decode_loop(d_tok.data_ptr(), 0, n, d_out.data_ptr(), teacher_forced=True, stream=s.cuda_stream)
+        e1.record(s)
+        torch.cuda.synchronize()
+        if r:
+            best_d = min(best_d, e0.elapsed_time(e1) / 1e3) if best_d == best_d else e0.elapsed_time(e1) / 1e3
+    tok_rows = n * cfg.batch
+    res = {"preset": a.preset, "batch": cfg.batch, "prompt": n, "prefill_ms": round(best * 1e3, 3),
+           "prefill_tok_s": round(tok_rows / best, 1), "decode_as_prefill_ms": round(best_d * 1e3, 3),
+           "decode_as_prefill_tok_s": round(tok_rows / best_d, 1), "speedup": round(best_d / best, 2)}
+    print(json.dumps(res), flush=True)
+    rows.append(res)
+m.close()
+if a.out:
+    with open(a.out, "w") as f:
+        json.dump(rows, f, indent=1)

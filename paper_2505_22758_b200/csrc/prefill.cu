@@ -77,8 +77,9 @@ __global__ void k_embed(float* __restrict__ x, const __nv_bfloat16* __restrict__
                         const int64_t* __restrict__ tok, int rows, int D) {
     const int r = blockIdx.x;
     if (r >= rows) return;
-    const __nv_bfloat16* e = emb + (size_t)tok[r] * D;
-    for (int c = threadIdx.x; c < D; c += blockDim.x) x[(size_t)r * D + c] = __bfloat162float(e[c]);
+    const __nv_bfloat162* e = reinterpret_cast<const __nv_bfloat162*>(emb + (size_t)tok[r] * D);
+    float2* xr = reinterpret_cast<float2*>(x + (size_t)r * D);
+    for (int c = threadIdx.x; c < D / 2; c += blockDim.x) xr[c] = __bfloat1622float2(e[c]);
 }
 
 __device__ __forceinline__ void split3(float v, __nv_bfloat16& a, __nv_bfloat16& b, __nv_bfloat16& c) {
@@ -88,283 +89,431 @@ __device__ __forceinline__ void split3(float v, __nv_bfloat16& a, __nv_bfloat16&
     c = __float2bfloat16_rn(r1 - __bfloat162float(b));
 }
 
+// four consecutive values split into the three bf16 planes (8-byte stores)
+__device__ __forceinline__ void put_split4(__nv_bfloat16* y3, size_t plane, size_t i, float4 v) {
+    __nv_bfloat16 h[4], m[4], l[4];
+    split3(v.x, h[0], m[0], l[0]);
+    split3(v.y, h[1], m[1], l[1]);
+    split3(v.z, h[2], m[2], l[2]);
+    split3(v.w, h[3], m[3], l[3]);
+    *reinterpret_cast<uint2*>(y3 + i) = *reinterpret_cast<const uint2*>(h);
+    *reinterpret_cast<uint2*>(y3 + plane + i) = *reinterpret_cast<const uint2*>(m);
+    *reinterpret_cast<uint2*>(y3 + 2 * plane + i) = *reinterpret_cast<const uint2*>(l);
+}
+
 // one element of a split-term GEMM result: (hi + mid) + lo planes
 __device__ __forceinline__ float ld3(const float* c, size_t plane, size_t i) {
     return (c[i] + c[plane + i]) + c[2 * plane + i];
 }
+__device__ __forceinline__ float4 ld3x4(const float* c, size_t plane, size_t i) {
+    const float4 a = *reinterpret_cast<const float4*>(c + i);
+    const float4 b = *reinterpret_cast<const float4*>(c + plane + i);
+    const float4 d = *reinterpret_cast<const float4*>(c + 2 * plane + i);
+    return make_float4((a.x + b.x) + d.x, (a.y + b.y) + d.y, (a.z + b.z) + d.z, (a.w + b.w) + d.w);
+}
 
-// y = gain * x / sqrt(mean(x^2) + eps) (numerics.hpp:14-24; gain == nullptr:
-// y = x), split into three bf16 terms [3][rows][K]
-__global__ void k_norm_split(const float* __restrict__ src, const float* __restrict__ gain, float eps,
-                             __nv_bfloat16* __restrict__ y3, int rows, int K) {
+// Residual row update + RMSNorm + split, one block (256 threads) per row:
+// x += c3 (the three planes of a projection, when c3 != nullptr), then
+// y = gain * x / sqrt(mean(x^2) + eps) (numerics.hpp:14-24) split into the
+// three bf16 planes of the next GEMM's input.  K % 4 == 0, K <= 8192.
+constexpr int kRowThreads = 256, kRowVec = 8;  // float4 per thread: K <= 256 * 4 * 8
+__global__ void __launch_bounds__(kRowThreads) k_residual_norm_split(float* __restrict__ x, const float* __restrict__ c3,
+                                                                     size_t cplane, const float* __restrict__ gain,
+                                                                     float eps, __nv_bfloat16* __restrict__ y3,
+                                                                     int rows, int K) {
     const int r = blockIdx.x;
-    const float* x = src + (size_t)r * K;
-    float inv = 1.f;
-    if (gain != nullptr) {
-        __shared__ float part[32];
-        float s = 0.f;
-        for (int c = threadIdx.x; c < K; c += blockDim.x) s = fmaf(x[c], x[c], s);
-        for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-        if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = s;
-        __syncthreads();
-        float t = 0.f;
-        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += part[w];
-        inv = 1.0f / sqrtf(t / static_cast<float>(K) + eps);
+    float4* xr = reinterpret_cast<float4*>(x + (size_t)r * K);
+    const int nv = K / 4;
+    float4 v[kRowVec];
+    float ss = 0.f;
+#pragma unroll
+    for (int u = 0; u < kRowVec; ++u) {
+        const int c = threadIdx.x + u * kRowThreads;
+        if (c < nv) {
+            float4 a = xr[c];
+            if (c3 != nullptr) {
+                const float4 d = ld3x4(c3, cplane, (size_t)r * K + 4 * c);
+                a = make_float4(a.x + d.x, a.y + d.y, a.z + d.z, a.w + d.w);
+                xr[c] = a;
+            }
+            v[u] = a;
+            ss = fmaf(a.x, a.x, fmaf(a.y, a.y, fmaf(a.z, a.z, fmaf(a.w, a.w, ss))));
+        }
     }
+    __shared__ float part[kRowThreads / 32];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+    if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = ss;
+    __syncthreads();
+    float t = 0.f;
+#pragma unroll
+    for (int w = 0; w < kRowThreads / 32; ++w) t += part[w];
+    const float inv = 1.0f / sqrtf(t / static_cast<float>(K) + eps);
     const size_t plane = (size_t)rows * K;
-    for (int c = threadIdx.x; c < K; c += blockDim.x) {
-        const float v = gain != nullptr ? gain[c] * x[c] * inv : x[c];
-        __nv_bfloat16 a, b, d;
-        split3(v, a, b, d);
-        y3[(size_t)r * K + c] = a;
-        y3[plane + (size_t)r * K + c] = b;
-        y3[2 * plane + (size_t)r * K + c] = d;
+#pragma unroll
+    for (int u = 0; u < kRowVec; ++u) {
+        const int c = threadIdx.x + u * kRowThreads;
+        if (c < nv) {
+            const float4 g = reinterpret_cast<const float4*>(gain)[c];
+            put_split4(y3, plane, (size_t)r * K + 4 * c,
+                       make_float4(g.x * v[u].x * inv, g.y * v[u].y * inv, g.z * v[u].z * inv, g.w * v[u].w * inv));
+        }
     }
+}
+
+// h = silu(gate) * in over the interleaved (in, gate) columns of the Wffn1
+// output (three planes), split straight into the W2 GEMM's input planes
+__global__ void k_silu_split(const float* __restrict__ c3, size_t cplane, __nv_bfloat16* __restrict__ y3, int rows,
+                             int DI) {
+    const size_t n4 = (size_t)rows * DI / 4, plane = (size_t)rows * DI;
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n4; i += (size_t)gridDim.x * blockDim.x) {
+        const float4 a = ld3x4(c3, cplane, 8 * i), b = ld3x4(c3, cplane, 8 * i + 4);
+        const float4 h = make_float4(a.y / (1.0f + expf(-a.y)) * a.x, a.w / (1.0f + expf(-a.w)) * a.z,
+                                     b.y / (1.0f + expf(-b.y)) * b.x, b.w / (1.0f + expf(-b.w)) * b.z);
+        put_split4(y3, plane, 4 * i, h);
+    }
+}
+
+// RoPE table of the call's positions: (cos, sin) of pos * theta^(-2k/dh),
+// angle in f64 as numerics.hpp:27-37 / the decode kernel; [n][dh / 2]
+__global__ void k_rope_table(float2* __restrict__ tab, int n, int64_t pos0, int DH, double theta) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n * (DH / 2)) return;
+    const int t = i / (DH / 2), k = i % (DH / 2);
+    const double freq = pow(theta, -static_cast<double>(2 * k) / DH);
+    const double ang = static_cast<double>(pos0 + t) * freq;
+    tab[i] = make_float2(static_cast<float>(cos(ang)), static_cast<float>(sin(ang)));
 }
 
 __device__ __forceinline__ int swz(int d, int64_t pos) { return ((((d >> 3) ^ (int)(pos & 7))) << 3) | (d & 7); }
 
-// RoPE (interleaved pairs, f64 angle as numerics.hpp:27-37 / the decode
-// kernel) on q and k rows of the QKV output; K and V rounded to bf16 and
-// appended at position pos0 + t of batch row b; q (f32) kept for attention.
-// Activation row r = t * B + b.
-__global__ void k_qkv_epilogue(const float* __restrict__ qkv, size_t plane, float* __restrict__ q, __nv_bfloat16* kc,
-                               __nv_bfloat16* vc, int rows, int B, int NQ, int NKV, int DH, int64_t pos0,
-                               double theta, int64_t layer_off, int64_t max_seq) {
-    const int r = blockIdx.x;
-    const int t = r / B, b = r % B;
-    const int64_t pos = pos0 + t;
+// RoPE (interleaved pairs) on the q and k columns of the QKV output; K and V
+// rounded to bf16 and appended at position pos0 + t of batch row b; q (f32)
+// kept for attention.  Activation row r = t * B + b; one thread per 4
+// columns (two rotary pairs, one half 16-byte chunk of a K/V row).
+__global__ void k_qkv_epilogue(const float* __restrict__ qkv, size_t plane, const float2* __restrict__ rope,
+                               float* __restrict__ q, __nv_bfloat16* kc, __nv_bfloat16* vc, int rows, int B, int NQ,
+                               int NKV, int DH, int64_t pos0, int64_t layer_off, int64_t max_seq) {
     const int QR = NQ * DH, KR = NKV * DH, QKVR = QR + 2 * KR;
-    const size_t base = (size_t)r * QKVR;
-    for (int i = threadIdx.x; i < QKVR / 2; i += blockDim.x) {
-        const int g = 2 * i;
-        const float a = ld3(qkv, plane, base + g), c2 = ld3(qkv, plane, base + g + 1);
+    const size_t n4 = (size_t)rows * QKVR / 4;
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n4; i += (size_t)gridDim.x * blockDim.x) {
+        const size_t r = 4 * i / QKVR;
+        const int g = (int)(4 * i - r * QKVR);
+        const int t = (int)(r / B), b = (int)(r % B);
+        const int64_t pos = pos0 + t;
+        float4 v = ld3x4(qkv, plane, 4 * i);
+        const int dim = g % DH;
         if (g < QR + KR) {
-            const int dim = g % DH, k = dim / 2;
-            const double freq = pow(theta, -static_cast<double>(2 * k) / DH);
-            const double ang = static_cast<double>(pos) * freq;
-            const float cs = static_cast<float>(cos(ang)), sn = static_cast<float>(sin(ang));
-            const float r0 = a * cs - c2 * sn, r1 = a * sn + c2 * cs;
+            const float2 cs0 = rope[t * (DH / 2) + dim / 2], cs1 = rope[t * (DH / 2) + dim / 2 + 1];
+            v = make_float4(v.x * cs0.x - v.y * cs0.y, v.x * cs0.y + v.y * cs0.x, v.z * cs1.x - v.w * cs1.y,
+                            v.z * cs1.y + v.w * cs1.x);
             if (g < QR) {
-                q[(size_t)r * QR + g] = r0;
-                q[(size_t)r * QR + g + 1] = r1;
-            } else {
-                const int h = (g - QR) / DH;
-                __nv_bfloat16* row = kc + layer_off + (((size_t)b * NKV + h) * max_seq + pos) * DH;
-                row[swz(dim, pos)] = __float2bfloat16_rn(r0);
-                row[swz(dim + 1, pos)] = __float2bfloat16_rn(r1);
+                *reinterpret_cast<float4*>(q + r * QR + g) = v;
+                continue;
             }
-        } else {
-            const int gv = g - QR - KR, h = gv / DH, dim = gv % DH;
-            __nv_bfloat16* row = vc + layer_off + (((size_t)b * NKV + h) * max_seq + pos) * DH;
-            row[swz(dim, pos)] = __float2bfloat16_rn(a);
-            row[swz(dim + 1, pos)] = __float2bfloat16_rn(c2);
         }
+        const bool is_k = g < QR + KR;
+        const int h = (g - QR - (is_k ? 0 : KR)) / DH;
+        __nv_bfloat16* row = (is_k ? kc : vc) + layer_off + (((size_t)b * NKV + h) * max_seq + pos) * DH;
+        __nv_bfloat16 o4[4] = {__float2bfloat16_rn(v.x), __float2bfloat16_rn(v.y), __float2bfloat16_rn(v.z),
+                               __float2bfloat16_rn(v.w)};
+        *reinterpret_cast<uint2*>(row + swz(dim, pos)) = *reinterpret_cast<const uint2*>(o4);
     }
 }
 
-// Causal attention, tiled: one block per (query tile, kv head, batch row)
-// holds kPairs (query position, q head) pairs of one GQA group -- TQ =
-// kPairs / QPG consecutive prompt positions x the group's QPG heads -- and
-// walks the keys [0, last position of the tile] in tiles of kKeys staged in
-// shared memory (un-swizzled, K rows padded so lane-per-row reads are bank-
-// conflict free), shared by all pairs.  Warp w owns pairs [8w, 8w + 8):
-// scores lane-per-key (keys j, j + 32 of the tile), online softmax per pair
-// in f32 (two warp reductions per tile), P through shared memory, then P.V
-// lane-per-dims.  Everything f32; only the order of the sums differs from
-// the decode kernel's.
-constexpr int kPairs = 64, kKeys = 64, kPPW = 8;  // pairs per block / keys per tile / pairs per warp
+// Causal attention on the tensor cores (mma.sync m16n8k16 bf16, f32
+// accumulate), FlashAttention-2 style.  One block (4 warps) per (query tile,
+// kv head, batch row) holds kPairs = 64 (prompt position, q head) rows of one
+// GQA group -- kPairs / QPG consecutive positions x the group's QPG heads,
+// all reading the same K/V -- warp w owning rows [16 w, 16 w + 16).  Keys
+// [0, last position of the tile] stream through shared memory in tiles of
+// kKeys (cp.async, double-buffered, un-swizzled from the cache's chunk order,
+// rows padded so ldmatrix is conflict free).  Precision follows the decode
+// kernel's tensor-core attention (decode_kernel.cuh attn_warp_pass): q enters
+// as bf16 hi + lo (two MMAs), scores in f32 (log2 units, exp2), P as bf16
+// hi + lo (two MMAs) against the bf16 V, O in f32; online softmax per row.
+constexpr int kPairs = 64, kKeys = 64, kAttnThreads = 128;
 
 template <int DH>
 struct AttnSmem {
-    static constexpr int KSTRIDE = DH + 8;  // bf16 elements per staged K row
-    static constexpr int Q_OFF = 0;                                   // f32 [kPairs][DH]
-    static constexpr int K_OFF = Q_OFF + kPairs * DH * 4;             // bf16 [kKeys][KSTRIDE]
-    static constexpr int V_OFF = K_OFF + kKeys * KSTRIDE * 2;         // bf16 [kKeys][DH]
-    static constexpr int P_OFF = V_OFF + kKeys * DH * 2;              // f32 [8 warps][kPPW][kKeys]
-    static constexpr int BYTES = P_OFF + 8 * kPPW * kKeys * 4;
+    static constexpr int RB = DH * 2 + 16;  // bytes per staged K / V row (padded)
+    static constexpr int TILE = kKeys * RB;
+    static constexpr int BYTES = 4 * TILE;  // K, V x 2 buffers
 };
 
+__device__ __forceinline__ uint32_t bf2(float lo_elem, float hi_elem) {
+    __nv_bfloat162 v = __floats2bfloat162_rn(lo_elem, hi_elem);
+    return *reinterpret_cast<uint32_t*>(&v);
+}
+__device__ __forceinline__ float bf_round(float x) { return __bfloat162float(__float2bfloat16_rn(x)); }
+
+__device__ __forceinline__ void mma16816(float (&c)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+        "{%0,%1,%2,%3};"
+        : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+        : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+__device__ __forceinline__ void ldsm4(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
+    asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3) : "r"(addr));
+}
+__device__ __forceinline__ void ldsm4t(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
+    asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3) : "r"(addr));
+}
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, bool valid) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(valid ? 16 : 0));
+}
+
 template <int DH>
-__global__ void __launch_bounds__(256, 1) k_attention(const float* __restrict__ q, const __nv_bfloat16* __restrict__ kc,
-                                                   const __nv_bfloat16* __restrict__ vc, float* __restrict__ out,
-                                                   int B, int NQ, int NKV, int n, int64_t pos0,
-                                                   int64_t layer_off, int64_t max_seq) {
+__global__ void __launch_bounds__(kAttnThreads) k_attention(const float* __restrict__ q,
+                                                            const __nv_bfloat16* __restrict__ kc,
+                                                            const __nv_bfloat16* __restrict__ vc,
+                                                            __nv_bfloat16* __restrict__ y3, size_t oplane, int B,
+                                                            int NQ, int NKV, int n, int64_t pos0, int64_t layer_off,
+                                                            int64_t max_seq) {
     using SM = AttnSmem<DH>;
-    constexpr int DPL = DH / 32, CH = DH / 8;  // dims per lane (P.V), 16-byte chunks per row
-    extern __shared__ __align__(16) uint8_t sm[];
-    float* Qs = reinterpret_cast<float*>(sm + SM::Q_OFF);
-    __nv_bfloat16* Ks = reinterpret_cast<__nv_bfloat16*>(sm + SM::K_OFF);
-    __nv_bfloat16* Vs = reinterpret_cast<__nv_bfloat16*>(sm + SM::V_OFF);
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    float* Ps = reinterpret_cast<float*>(sm + SM::P_OFF) + warp * kPPW * kKeys;
+    constexpr int KS = DH / 16, CH = DH / 8;  // k-steps over d_head, 16-byte chunks per row
+    extern __shared__ __align__(128) uint8_t sm[];
+    const uint32_t sbase = static_cast<uint32_t>(__cvta_generic_to_shared(sm));
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, q4 = lane & 3;
     const int qpg = NQ / NKV, tq = kPairs / qpg;
     const int t0 = blockIdx.x * tq, kvh = blockIdx.y, b = blockIdx.z;
-    const float alpha = 1.0f / sqrtf(static_cast<float>(DH));
-    // stage the tile's queries, pre-scaled (pairs past the prompt: zeros)
-    for (int i = threadIdx.x; i < kPairs * DH; i += blockDim.x) {
-        const int pr = i / DH, d = i % DH, t = t0 + pr / qpg, h = kvh * qpg + pr % qpg;
-        Qs[i] = t < n ? alpha * q[((size_t)t * B + b) * NQ * DH + (size_t)h * DH + d] : 0.f;
-    }
-    const __nv_bfloat16* kb = kc + layer_off + ((size_t)b * NKV + kvh) * max_seq * DH;
-    const __nv_bfloat16* vb = vc + layer_off + ((size_t)b * NKV + kvh) * max_seq * DH;
     const int tlast = min(t0 + tq, n) - 1;
     const int64_t kend = pos0 + tlast + 1;  // keys of the whole tile
-    // this warp's pairs: positions qpos[i], the warp's last key
-    int64_t qpos[kPPW];
-#pragma unroll
-    for (int i = 0; i < kPPW; ++i) qpos[i] = pos0 + min(t0 + (warp * kPPW + i) / qpg, tlast);
-    const int64_t wend = qpos[kPPW - 1] + 1;
-    float mx[kPPW], sum[kPPW], o[kPPW][DPL];
-#pragma unroll
-    for (int i = 0; i < kPPW; ++i) {
-        mx[i] = -INFINITY;
-        sum[i] = 0.f;
-#pragma unroll
-        for (int e = 0; e < DPL; ++e) o[i][e] = 0.f;
-    }
-    for (int64_t k0 = 0; k0 < kend; k0 += kKeys) {
-        __syncthreads();  // previous tile consumed (and Q staged, first time)
-        for (int i = threadIdx.x; i < kKeys * CH; i += blockDim.x) {
+    const __nv_bfloat16* kb = kc + layer_off + ((size_t)b * NKV + kvh) * max_seq * DH;
+    const __nv_bfloat16* vb = vc + layer_off + ((size_t)b * NKV + kvh) * max_seq * DH;
+
+    auto load_tile = [&](int64_t k0, int buf) {
+        const uint32_t kd = sbase + (2 * buf) * SM::TILE, vd = kd + SM::TILE;
+        for (int i = threadIdx.x; i < kKeys * CH; i += kAttnThreads) {
             const int j = i / CH, c = i % CH;
             const int64_t pos = k0 + j;
-            uint4 kv = make_uint4(0, 0, 0, 0), vv = make_uint4(0, 0, 0, 0);
-            if (pos < kend) {
-                const int cs = c ^ (int)(pos & 7);  // the cache's chunk swizzle (kv_swz)
-                kv = *reinterpret_cast<const uint4*>(kb + pos * DH + cs * 8);
-                vv = *reinterpret_cast<const uint4*>(vb + pos * DH + cs * 8);
+            const bool ok = pos < kend;
+            const int64_t ps = ok ? pos : 0;
+            const int cs = c ^ (int)(ps & 7);  // the cache's chunk swizzle (kv_swz)
+            cp_async16(kd + j * SM::RB + c * 16, kb + ps * DH + cs * 8, ok);
+            cp_async16(vd + j * SM::RB + c * 16, vb + ps * DH + cs * 8, ok);
+        }
+        asm volatile("cp.async.commit_group;");
+    };
+    load_tile(0, 0);
+
+    // this warp's rows g and g + 8: pair 16 w + r -> (position, head)
+    const int pr0 = 16 * warp + g, pr1 = pr0 + 8;
+    const int64_t qp0 = pos0 + min(t0 + pr0 / qpg, tlast), qp1 = pos0 + min(t0 + pr1 / qpg, tlast);
+    const int64_t wend = pos0 + min(t0 + (16 * warp + 15) / qpg, tlast) + 1;
+    // q (pre-scaled by log2(e) / sqrt(d_head)) as A fragments, bf16 hi and lo
+    uint32_t qh[KS][4], ql[KS][4];
+    {
+        const float alpha = 1.4426950408889634f / sqrtf(static_cast<float>(DH));
+        const int ta = t0 + pr0 / qpg, tb = t0 + pr1 / qpg;
+        const float* r0 = q + ((size_t)ta * B + b) * NQ * DH + (size_t)(kvh * qpg + pr0 % qpg) * DH;
+        const float* r1 = q + ((size_t)tb * B + b) * NQ * DH + (size_t)(kvh * qpg + pr1 % qpg) * DH;
+        const bool v0 = ta < n, v1 = tb < n;
+#pragma unroll
+        for (int kk = 0; kk < KS; ++kk)
+#pragma unroll
+            for (int r = 0; r < 4; ++r) {
+                const bool second = r & 1;
+                const int d = kk * 16 + 2 * q4 + 8 * (r >> 1);
+                const float* src = second ? r1 : r0;
+                const bool ok = second ? v1 : v0;
+                const float x0 = ok ? alpha * src[d] : 0.f, x1 = ok ? alpha * src[d + 1] : 0.f;
+                qh[kk][r] = bf2(x0, x1);
+                ql[kk][r] = bf2(x0 - bf_round(x0), x1 - bf_round(x1));
             }
-            *reinterpret_cast<uint4*>(Ks + j * SM::KSTRIDE + c * 8) = kv;
-            *reinterpret_cast<uint4*>(Vs + j * DH + c * 8) = vv;
+    }
+    float o[DH / 8][4];
+#pragma unroll
+    for (int c = 0; c < DH / 8; ++c)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) o[c][e] = 0.f;
+    float m0 = -INFINITY, m1 = -INFINITY, l0 = 0.f, l1 = 0.f;
+
+    const int ntile = (int)((kend + kKeys - 1) / kKeys);
+    for (int it = 0; it < ntile; ++it) {
+        const int64_t k0 = (int64_t)it * kKeys;
+        if (it + 1 < ntile) {
+            load_tile(k0 + kKeys, (it + 1) & 1);
+            asm volatile("cp.async.wait_group 1;");
+        } else {
+            asm volatile("cp.async.wait_group 0;");
         }
         __syncthreads();
-        if (k0 >= wend) continue;  // every key of this tile is after the warp's positions
-        // scores: lane owns keys k0 + lane and k0 + lane + 32
-        float sc[kPPW][2];
+        if (k0 < wend) {
+            const uint32_t kt = sbase + (2 * (it & 1)) * SM::TILE, vt = kt + SM::TILE;
+            // S = q K^T over the 64 keys: 8 n8 tiles
+            float s[8][4];
 #pragma unroll
-        for (int i = 0; i < kPPW; ++i) sc[i][0] = sc[i][1] = 0.f;
-        const float* qw = Qs + warp * kPPW * DH;
-#pragma unroll 2
-        for (int c = 0; c < CH; ++c) {
-            float ka[8], kb2[8];
-            const uint4 r0 = *reinterpret_cast<const uint4*>(Ks + lane * SM::KSTRIDE + c * 8);
-            const uint4 r1 = *reinterpret_cast<const uint4*>(Ks + (lane + 32) * SM::KSTRIDE + c * 8);
-            const __nv_bfloat162* h0 = reinterpret_cast<const __nv_bfloat162*>(&r0);
-            const __nv_bfloat162* h1 = reinterpret_cast<const __nv_bfloat162*>(&r1);
+            for (int nt = 0; nt < 8; ++nt)
 #pragma unroll
-            for (int e = 0; e < 4; ++e) {
-                const float2 f0 = __bfloat1622float2(h0[e]), f1 = __bfloat1622float2(h1[e]);
-                ka[2 * e] = f0.x;
-                ka[2 * e + 1] = f0.y;
-                kb2[2 * e] = f1.x;
-                kb2[2 * e + 1] = f1.y;
+                for (int e = 0; e < 4; ++e) s[nt][e] = 0.f;
+#pragma unroll
+            for (int kk = 0; kk < KS; ++kk)
+#pragma unroll
+                for (int np = 0; np < 4; ++np) {  // pairs of n8 tiles: keys 16 np .. 16 np + 15
+                    uint32_t b0, b1, b2, b3;
+                    const int row = 16 * np + (lane & 7) + 8 * (lane >> 4), ch = 2 * kk + ((lane >> 3) & 1);
+                    ldsm4(kt + row * SM::RB + ch * 16, b0, b1, b2, b3);
+                    mma16816(s[2 * np], qh[kk], b0, b1);
+                    mma16816(s[2 * np], ql[kk], b0, b1);
+                    mma16816(s[2 * np + 1], qh[kk], b2, b3);
+                    mma16816(s[2 * np + 1], ql[kk], b2, b3);
+                }
+            // causal mask, row max
+            float mx0 = -INFINITY, mx1 = -INFINITY;
+#pragma unroll
+            for (int nt = 0; nt < 8; ++nt)
+#pragma unroll
+                for (int e = 0; e < 2; ++e) {
+                    const int64_t kp = k0 + nt * 8 + 2 * q4 + e;
+                    if (kp > qp0) s[nt][e] = -INFINITY;
+                    if (kp > qp1) s[nt][e + 2] = -INFINITY;
+                    mx0 = fmaxf(mx0, s[nt][e]);
+                    mx1 = fmaxf(mx1, s[nt][e + 2]);
+                }
+            mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, 1));
+            mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, 2));
+            mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, 1));
+            mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, 2));
+            const float mn0 = fmaxf(m0, mx0), mn1 = fmaxf(m1, mx1);  // finite: key 0 precedes every row
+            const float sc0 = exp2f(m0 - mn0), sc1 = exp2f(m1 - mn1);
+            m0 = mn0;
+            m1 = mn1;
+            float ps0 = 0.f, ps1 = 0.f;
+#pragma unroll
+            for (int nt = 0; nt < 8; ++nt) {
+                s[nt][0] = exp2f(s[nt][0] - mn0);
+                s[nt][1] = exp2f(s[nt][1] - mn0);
+                s[nt][2] = exp2f(s[nt][2] - mn1);
+                s[nt][3] = exp2f(s[nt][3] - mn1);
+                ps0 += s[nt][0] + s[nt][1];
+                ps1 += s[nt][2] + s[nt][3];
             }
+            ps0 += __shfl_xor_sync(0xffffffffu, ps0, 1);
+            ps0 += __shfl_xor_sync(0xffffffffu, ps0, 2);
+            ps1 += __shfl_xor_sync(0xffffffffu, ps1, 1);
+            ps1 += __shfl_xor_sync(0xffffffffu, ps1, 2);
+            l0 = l0 * sc0 + ps0;
+            l1 = l1 * sc1 + ps1;
 #pragma unroll
-            for (int i = 0; i < kPPW; ++i) {
-                const float4 qa = *reinterpret_cast<const float4*>(qw + i * DH + c * 8);
-                const float4 qb = *reinterpret_cast<const float4*>(qw + i * DH + c * 8 + 4);
-                const float qq[8] = {qa.x, qa.y, qa.z, qa.w, qb.x, qb.y, qb.z, qb.w};
+            for (int c = 0; c < DH / 8; ++c) {
+                o[c][0] *= sc0;
+                o[c][1] *= sc0;
+                o[c][2] *= sc1;
+                o[c][3] *= sc1;
+            }
+            // O += P V, P as bf16 hi + lo A fragments, V via ldmatrix.trans
 #pragma unroll
-                for (int e = 0; e < 8; ++e) {
-                    sc[i][0] = fmaf(qq[e], ka[e], sc[i][0]);
-                    sc[i][1] = fmaf(qq[e], kb2[e], sc[i][1]);
+            for (int j = 0; j < 4; ++j) {
+                uint32_t ph[4], pl[4];
+                const float* a = s[2 * j];
+                const float* c2 = s[2 * j + 1];
+                ph[0] = bf2(a[0], a[1]);
+                ph[1] = bf2(a[2], a[3]);
+                ph[2] = bf2(c2[0], c2[1]);
+                ph[3] = bf2(c2[2], c2[3]);
+                pl[0] = bf2(a[0] - bf_round(a[0]), a[1] - bf_round(a[1]));
+                pl[1] = bf2(a[2] - bf_round(a[2]), a[3] - bf_round(a[3]));
+                pl[2] = bf2(c2[0] - bf_round(c2[0]), c2[1] - bf_round(c2[1]));
+                pl[3] = bf2(c2[2] - bf_round(c2[2]), c2[3] - bf_round(c2[3]));
+                const int row = 16 * j + (lane & 7) + 8 * ((lane >> 3) & 1);
+#pragma unroll
+                for (int c = 0; c < DH / 16; ++c) {
+                    uint32_t b00, b01, b10, b11;
+                    ldsm4t(vt + row * SM::RB + (2 * c + (lane >> 4)) * 16, b00, b01, b10, b11);
+                    mma16816(o[2 * c], ph, b00, b01);
+                    mma16816(o[2 * c], pl, b00, b01);
+                    mma16816(o[2 * c + 1], ph, b10, b11);
+                    mma16816(o[2 * c + 1], pl, b10, b11);
                 }
             }
         }
-        // online softmax per pair, P to shared memory
+        __syncthreads();  // buffer (it & 1) is refilled by the next iteration's prefetch
+    }
+    // normalise, split straight into the Waout GEMM's input planes
+    const int ta = t0 + pr0 / qpg, tb = t0 + pr1 / qpg;
+    const float i0 = 1.0f / l0, i1 = 1.0f / l1;
+    const size_t at0 = ((size_t)ta * B + b) * NQ * DH + (size_t)(kvh * qpg + pr0 % qpg) * DH;
+    const size_t at1 = ((size_t)tb * B + b) * NQ * DH + (size_t)(kvh * qpg + pr1 % qpg) * DH;
 #pragma unroll
-        for (int i = 0; i < kPPW; ++i) {
-            const float s0 = k0 + lane <= qpos[i] ? sc[i][0] : -INFINITY;
-            const float s1 = k0 + lane + 32 <= qpos[i] ? sc[i][1] : -INFINITY;
-            float tm = fmaxf(s0, s1);
+    for (int c = 0; c < DH / 8; ++c)
 #pragma unroll
-            for (int off = 16; off > 0; off >>= 1) tm = fmaxf(tm, __shfl_xor_sync(0xffffffffu, tm, off));
-            const float mn = fmaxf(mx[i], tm);  // finite: key 0 <= every position
-            const float p0 = expf(s0 - mn), p1 = expf(s1 - mn), scale = expf(mx[i] - mn);
-            float ts = p0 + p1;
-#pragma unroll
-            for (int off = 16; off > 0; off >>= 1) ts += __shfl_xor_sync(0xffffffffu, ts, off);
-            sum[i] = sum[i] * scale + ts;
-            mx[i] = mn;
-#pragma unroll
-            for (int e = 0; e < DPL; ++e) o[i][e] *= scale;
-            Ps[i * kKeys + lane] = p0;
-            Ps[i * kKeys + lane + 32] = p1;
-        }
-        __syncwarp();
-        // P.V: lane owns dims [lane * DPL, lane * DPL + DPL)
-        const int jn = wend - k0 < kKeys ? (int)(wend - k0) : kKeys;
-        for (int j = 0; j < jn; j += 4) {
-            float v[4][DPL];
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-#pragma unroll
-                for (int e = 0; e < DPL; ++e) v[u][e] = __bfloat162float(Vs[(j + u) * DH + lane * DPL + e]);
+        for (int e = 0; e < 2; ++e) {
+            const int d = c * 8 + 2 * q4 + e;
+            __nv_bfloat16 hi, mi, lo;
+            if (ta < n) {
+                split3(o[c][e] * i0, hi, mi, lo);
+                y3[at0 + d] = hi;
+                y3[oplane + at0 + d] = mi;
+                y3[2 * oplane + at0 + d] = lo;
             }
-#pragma unroll
-            for (int i = 0; i < kPPW; ++i) {
-                const float4 p4 = *reinterpret_cast<const float4*>(Ps + i * kKeys + j);
-#pragma unroll
-                for (int e = 0; e < DPL; ++e)
-                    o[i][e] = fmaf(p4.w, v[3][e], fmaf(p4.z, v[2][e], fmaf(p4.y, v[1][e], fmaf(p4.x, v[0][e], o[i][e]))));
+            if (tb < n) {
+                split3(o[c][e + 2] * i1, hi, mi, lo);
+                y3[at1 + d] = hi;
+                y3[oplane + at1 + d] = mi;
+                y3[2 * oplane + at1 + d] = lo;
             }
         }
-        __syncwarp();
-    }
-#pragma unroll
-    for (int i = 0; i < kPPW; ++i) {
-        const int pr = warp * kPPW + i, t = t0 + pr / qpg, h = kvh * qpg + pr % qpg;
-        if (t >= n) continue;
-        float* dst = out + ((size_t)t * B + b) * NQ * DH + (size_t)h * DH + lane * DPL;
-#pragma unroll
-        for (int e = 0; e < DPL; ++e) dst[e] = o[i][e] / sum[i];
-    }
 }
 
-// h[t] = silu(gate) * in over the interleaved (in, gate) rows of Wffn1
-__global__ void k_silu(const float* __restrict__ c, size_t plane, float* __restrict__ h, int rows, int DI) {
-    const size_t n = (size_t)rows * DI;
-    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
-        const size_t r = i / DI, k = i % DI;
-        const float a = ld3(c, plane, r * 2 * DI + 2 * k), g = ld3(c, plane, r * 2 * DI + 2 * k + 1);
-        h[i] = g / (1.0f + expf(-g)) * a;
-    }
-}
-
-__global__ void k_add(float* __restrict__ x, const float* __restrict__ d, size_t n) {
-    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
-        x[i] += ld3(d, n, i);
-}
-
-// logits of the last positions: the three planes summed in place
-__global__ void k_sum3(float* __restrict__ c, size_t n) {
-    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
-        c[i] = ld3(c, n, i);
-}
-
-// lowest index of the maximum (numerics.hpp:169-175), one block per row
-__global__ void k_argmax(const float* __restrict__ lg, int V, int64_t* __restrict__ out) {
-    const float* x = lg + (size_t)blockIdx.x * V;
+// LM head: the three planes summed in place into plane 0 (the logits) and
+// a (max, lowest index) candidate per block of each row (numerics.hpp:169-175)
+constexpr int kArgBlocks = 64;
+__global__ void k_logits_part(float* __restrict__ c3, size_t plane, int V, float2* __restrict__ part) {
+    const int b = blockIdx.y;
+    float* row = c3 + (size_t)b * V;
+    const int per = (V + kArgBlocks - 1) / kArgBlocks, i0 = blockIdx.x * per, i1 = min(V, i0 + per);
     float bv = -INFINITY;
     int bi = 0x7fffffff;
-    for (int i = threadIdx.x; i < V; i += blockDim.x)
-        if (x[i] > bv) {
-            bv = x[i];
+    for (int i = i0 + threadIdx.x; i < i1; i += blockDim.x) {
+        const float v = (row[i] + row[plane + i]) + row[2 * plane + i];
+        row[i] = v;
+        if (v > bv) {
+            bv = v;
             bi = i;
         }
-    __shared__ float sv[256];
-    __shared__ int si[256];
-    sv[threadIdx.x] = bv;
-    si[threadIdx.x] = bi;
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        const float ov = __shfl_xor_sync(0xffffffffu, bv, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+        if (ov > bv || (ov == bv && oi < bi)) {
+            bv = ov;
+            bi = oi;
+        }
+    }
+    __shared__ float sv[32];
+    __shared__ int si[32];
+    if ((threadIdx.x & 31) == 0) {
+        sv[threadIdx.x >> 5] = bv;
+        si[threadIdx.x >> 5] = bi;
+    }
     __syncthreads();
     if (threadIdx.x == 0) {
-        for (int t = 1; t < (int)blockDim.x; ++t)
-            if (sv[t] > bv || (sv[t] == bv && si[t] < bi)) {
-                bv = sv[t];
-                bi = si[t];
+        for (int w = 1; w < (int)(blockDim.x >> 5); ++w)
+            if (sv[w] > bv || (sv[w] == bv && si[w] < bi)) {
+                bv = sv[w];
+                bi = si[w];
             }
-        out[blockIdx.x] = bi;
+        part[b * kArgBlocks + blockIdx.x] = make_float2(bv, __int_as_float(bi));
     }
+}
+
+__global__ void k_argmax_final(const float2* __restrict__ part, int64_t* __restrict__ out) {
+    const int b = blockIdx.x;
+    float bv = -INFINITY;
+    int bi = 0x7fffffff;
+    for (int k = 0; k < kArgBlocks; ++k) {
+        const float2 c = part[b * kArgBlocks + k];
+        const int ci = __float_as_int(c.y);
+        if (c.x > bv || (c.x == bv && ci < bi)) {
+            bv = c.x;
+            bi = ci;
+        }
+    }
+    out[b] = bi;
 }
 
 // C3[3][rows][N] (f32, row-major) = Y3[3][rows][K] . W^T: ONE GEMM over the
@@ -403,14 +552,24 @@ extern "C" ffb_status ffb_prefill(ffb_model* m, const int64_t* tokens, int64_t n
     const int D = (int)c.d_model, DI = (int)c.d_inter, DH = (int)c.d_head, NQ = (int)c.n_q_heads,
               NKV = (int)c.n_kv_heads, V = (int)c.vocab_size;
     const int QR = NQ * DH, QKVR = (int)m->qkv_rows(), AD = QR;
-    if ((DH != 32 && DH != 64 && DH != 128) || kPairs % (NQ / NKV) != 0)
-        return fail(FFB_UNSUPPORTED, "prefill: head shape (d_head 32 / 64 / 128, q heads per kv head dividing 64)");
+    if ((DH != 64 && DH != 128) || kPairs % (NQ / NKV) != 0 || D > kRowThreads * 4 * kRowVec)
+        return fail(FFB_UNSUPPORTED, "prefill: head shape (d_head 64 / 128, q heads per kv head dividing 64)");
     CUDA_TRY(cudaSetDevice(m->device));
     cudaStream_t s = m->stream;
-    // scratch (kept; sized for the largest call so far)
+    // scratch (kept; sized for the largest call so far): residual X, rotated
+    // q, the GEMM outputs C3 (three planes), the GEMM inputs Y3 (three bf16
+    // planes), the RoPE table, token ids, argmax candidates
     const int Kmax = std::max({D, AD, DI});
     const size_t Cn = 3 * std::max<size_t>((size_t)rows * std::max({QKVR, 2 * DI, D}), (size_t)B * V);
-    const size_t need = ((size_t)rows * (D + QR + AD + DI) + Cn) * 4 + (size_t)3 * rows * Kmax * 2 + rows * 8 + 256;
+    size_t need = 0;
+    auto carve = [&](size_t bytes) {  // 256-byte aligned sub-buffers
+        const size_t at = need;
+        need += (bytes + 255) / 256 * 256;
+        return at;
+    };
+    const size_t oX = carve((size_t)rows * D * 4), oQ = carve((size_t)rows * QR * 4), oC = carve(Cn * 4),
+                 oR = carve((size_t)n * DH * 4), oP = carve((size_t)B * kArgBlocks * 8), oT = carve(rows * 8),
+                 oY = carve((size_t)3 * rows * Kmax * 2);
     if (m->pf_bytes < need) {
         if (m->pf_buf) cudaFree(m->pf_buf);
         m->pf_buf = nullptr;
@@ -418,16 +577,15 @@ extern "C" ffb_status ffb_prefill(ffb_model* m, const int64_t* tokens, int64_t n
         CUDA_TRY(cudaMalloc(&m->pf_buf, need));
         m->pf_bytes = need;
     }
-    auto* X = static_cast<float*>(m->pf_buf);
-    float* Q = X + (size_t)rows * D;
-    float* A = Q + (size_t)rows * QR;
-    float* H = A + (size_t)rows * AD;
-    float* C = H + (size_t)rows * DI;
-    auto* Y3 = reinterpret_cast<__nv_bfloat16*>(C + Cn);
-    auto* tok = reinterpret_cast<int64_t*>(
-        (reinterpret_cast<uintptr_t>(Y3 + (size_t)3 * rows * Kmax) + 15) & ~uintptr_t(15));
+    auto* base = static_cast<uint8_t*>(m->pf_buf);
+    auto* X = reinterpret_cast<float*>(base + oX);
+    auto* Q = reinterpret_cast<float*>(base + oQ);
+    auto* C = reinterpret_cast<float*>(base + oC);
+    auto* rope = reinterpret_cast<float2*>(base + oR);
+    auto* part = reinterpret_cast<float2*>(base + oP);
+    auto* tok = reinterpret_cast<int64_t*>(base + oT);
+    auto* Y3 = reinterpret_cast<__nv_bfloat16*>(base + oY);
     static bool attn_attr = [] {
-        cudaFuncSetAttribute(k_attention<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, AttnSmem<32>::BYTES);
         cudaFuncSetAttribute(k_attention<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, AttnSmem<64>::BYTES);
         cudaFuncSetAttribute(k_attention<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, AttnSmem<128>::BYTES);
         return true;
@@ -443,47 +601,55 @@ extern "C" ffb_status ffb_prefill(ffb_model* m, const int64_t* tokens, int64_t n
     cublas()->set_stream(h, s);
     CUDA_TRY(cudaMemcpyAsync(tok, tokens, sizeof(int64_t) * rows, cudaMemcpyHostToDevice, s));
     const auto* RB = m->ops;
-    k_embed<<<(int)rows, 256, 0, s>>>(X, m->embedding, tok, (int)rows, D);
     const float eps = static_cast<float>(c.rmsnorm_eps);
+    const int ew = 4 * m->grid;  // grid of the element-wise kernels
+    k_rope_table<<<(int)((n * DH / 2 + 255) / 256), 256, 0, s>>>(rope, (int)n, pos0, DH, c.rope_theta);
+    k_embed<<<(int)rows, 256, 0, s>>>(X, m->embedding, tok, (int)rows, D);
+    k_residual_norm_split<<<(int)rows, kRowThreads, 0, s>>>(X, nullptr, 0, m->norm_attn, eps, Y3, (int)rows, D);
+    const size_t pD = (size_t)rows * D;
     for (int64_t l = 0; l < c.layers; ++l) {
         const int64_t layer_off = l * B * NKV * m->max_seq * DH;
-        k_norm_split<<<(int)rows, 256, 0, s>>>(X, m->norm_attn + l * D, eps, Y3, (int)rows, D);
         ffb_status st = gemm3(h, Y3, (int)rows, D, m->wqkv + (size_t)l * QKVR * RB->row_bytes, QKVR, false, C);
         if (st) return st;
-        k_qkv_epilogue<<<(int)rows, 256, 0, s>>>(C, (size_t)rows * QKVR, Q, m->kcache, m->vcache, (int)rows, (int)B, NQ, NKV, DH,
-                                                  pos0, c.rope_theta, layer_off, m->max_seq);
+        k_qkv_epilogue<<<ew, 256, 0, s>>>(C, (size_t)rows * QKVR, rope, Q, m->kcache, m->vcache, (int)rows, (int)B,
+                                          NQ, NKV, DH, pos0, layer_off, m->max_seq);
         const int tq = kPairs / (NQ / NKV);
         const dim3 ag((unsigned)((n + tq - 1) / tq), (unsigned)NKV, (unsigned)B);
+        const size_t ap = (size_t)rows * AD;
         if (DH == 64)
-            k_attention<64><<<ag, 256, AttnSmem<64>::BYTES, s>>>(Q, m->kcache, m->vcache, A, (int)B, NQ, NKV,
+            k_attention<64><<<ag, kAttnThreads, AttnSmem<64>::BYTES, s>>>(Q, m->kcache, m->vcache, Y3, ap, (int)B, NQ, NKV,
                                                                  (int)n, pos0, layer_off, m->max_seq);
         else if (DH == 128)
-            k_attention<128><<<ag, 256, AttnSmem<128>::BYTES, s>>>(Q, m->kcache, m->vcache, A, (int)B, NQ, NKV,
-                                                                   (int)n, pos0, layer_off, m->max_seq);
-        else
-            k_attention<32><<<ag, 256, AttnSmem<32>::BYTES, s>>>(Q, m->kcache, m->vcache, A, (int)B, NQ, NKV,
-                                                                 (int)n, pos0, layer_off, m->max_seq);
-        k_norm_split<<<(int)rows, 256, 0, s>>>(A, nullptr, 0.f, Y3, (int)rows, AD);
+            k_attention<128><<<ag, kAttnThreads, AttnSmem<128>::BYTES, s>>>(Q, m->kcache, m->vcache, Y3, ap, (int)B, NQ,
+                                                                   NKV, (int)n, pos0, layer_off, m->max_seq);
         st = gemm3(h, Y3, (int)rows, AD, m->waout + (size_t)l * D * RB->row_bytes_a, D, false, C);
         if (st) return st;
-        k_add<<<592, 256, 0, s>>>(X, C, (size_t)rows * D);
-        k_norm_split<<<(int)rows, 256, 0, s>>>(X, m->norm_ffn + l * D, eps, Y3, (int)rows, D);
+        k_residual_norm_split<<<(int)rows, kRowThreads, 0, s>>>(X, C, pD, m->norm_ffn + l * D, eps, Y3, (int)rows,
+                                                               D);
         st = gemm3(h, Y3, (int)rows, D, m->wffn1 + (size_t)l * 2 * DI * RB->row_bytes, 2 * DI, false, C);
         if (st) return st;
-        k_silu<<<592, 256, 0, s>>>(C, (size_t)rows * 2 * DI, H, (int)rows, DI);
-        k_norm_split<<<(int)rows, 256, 0, s>>>(H, nullptr, 0.f, Y3, (int)rows, DI);
+        k_silu_split<<<ew, 256, 0, s>>>(C, (size_t)rows * 2 * DI, Y3, (int)rows, DI);
         // W2: [D][DI] rows (two-phase FFN shapes) or Wffn2^T [DI][D]
         st = gemm3(h, Y3, (int)rows, DI, m->wffn2t + (size_t)l * D * DI * 2, D, !RB->ffn2_rows, C);
         if (st) return st;
-        k_add<<<592, 256, 0, s>>>(X, C, (size_t)rows * D);
+        if (l + 1 < c.layers) {
+            k_residual_norm_split<<<(int)rows, kRowThreads, 0, s>>>(X, C, pD, m->norm_attn + (l + 1) * D, eps, Y3,
+                                                                   (int)rows, D);
+        } else {  // only the last position of each batch row feeds the LM head
+            const size_t o = (size_t)(n - 1) * B * D;
+            k_residual_norm_split<<<(int)B, kRowThreads, 0, s>>>(X + o, C + o, pD, m->final_norm, eps, Y3, (int)B,
+                                                                D);
+        }
+    }
+    if (c.layers == 0) {
+        const size_t o = (size_t)(n - 1) * B * D;
+        k_residual_norm_split<<<(int)B, kRowThreads, 0, s>>>(X + o, nullptr, 0, m->final_norm, eps, Y3, (int)B, D);
     }
     // LM head on the last position of every batch row
-    const float* xl = X + (size_t)(n - 1) * B * D;
-    k_norm_split<<<(int)B, 256, 0, s>>>(xl, m->final_norm, eps, Y3, (int)B, D);
     ffb_status st = gemm3(h, Y3, (int)B, D, m->lm_head, V, false, C);
     if (st) return st;
-    k_sum3<<<592, 256, 0, s>>>(C, (size_t)B * V);
-    k_argmax<<<(int)B, 256, 0, s>>>(C, V, tok);
+    k_logits_part<<<dim3(kArgBlocks, (unsigned)B), 256, 0, s>>>(C, (size_t)B * V, V, part);
+    k_argmax_final<<<(int)B, 1, 0, s>>>(part, tok);
     CUDA_TRY(cudaGetLastError());
     if (logits) CUDA_TRY(cudaMemcpyAsync(logits, C, sizeof(float) * B * V, cudaMemcpyDeviceToHost, s));
     if (greedy) CUDA_TRY(cudaMemcpyAsync(greedy, tok, sizeof(int64_t) * B, cudaMemcpyDeviceToHost, s));

@@ -146,6 +146,42 @@ public:
         return out;
     }
 
+    // Prompt ingestion (ffb_prefill): prompt[t][b] at positions pos0 + t,
+    // the replacement of the decode-as-prefill loop (reference_forward per
+    // position, reference.hpp:60-61).  Returns the last position's logits;
+    // store.kv gains every appended position (one bulk export).
+    std::vector<std::vector<float>> prefill(TensorStore& st, const std::vector<std::vector<int64_t>>& prompt,
+                                            int64_t pos0) {
+        const int64_t n = static_cast<int64_t>(prompt.size()), B = model_.batch;
+        std::vector<int64_t> flat_tok;
+        for (const auto& row : prompt) {
+            if (static_cast<int64_t>(row.size()) != B)
+                throw ValidationError("prefill: one token per batch row required");
+            flat_tok.insert(flat_tok.end(), row.begin(), row.end());
+        }
+        std::vector<float> flat(static_cast<size_t>(B * model_.vocab_size));
+        check(ffb_prefill(h_, flat_tok.data(), n, pos0, flat.data(), nullptr));
+        const int64_t dh = model_.d_head, nkv = model_.n_kv_heads, L = model_.layers;
+        std::vector<float> ka(static_cast<size_t>(B * L * nkv * n * dh)), va(ka.size());  // [B][L][Hkv][n][dh]
+        check(ffb_kv_export(h_, pos0, n, ka.data(), va.data()));
+        for (int64_t t = 0; t < n; ++t)
+            for (int64_t l = 0; l < L; ++l) {
+                if (st.kv.length(l) != pos0 + t) continue;
+                std::vector<std::vector<float>> k(B), v(B);
+                for (int64_t b = 0; b < B; ++b)
+                    for (int64_t h = 0; h < nkv; ++h) {
+                        const size_t o = static_cast<size_t>((((b * L + l) * nkv + h) * n + t) * dh);
+                        k[b].insert(k[b].end(), ka.begin() + o, ka.begin() + o + dh);
+                        v[b].insert(v[b].end(), va.begin() + o, va.begin() + o + dh);
+                    }
+                st.kv.append_token(l, k, v);
+            }
+        std::vector<std::vector<float>> out(B);
+        for (int64_t b = 0; b < B; ++b)
+            out[b].assign(flat.begin() + b * model_.vocab_size, flat.begin() + (b + 1) * model_.vocab_size);
+        return out;
+    }
+
     ffb_model* handle() { return h_; }
 
 private:

@@ -207,7 +207,10 @@ ffb_status ffb_set_mode(ffb_model *m, ffb_mode mode);
  * is full (default ATTN|AOUT = 0x6).  "attn_group_max": cap on the CTAs per
  * (batch row, kv head) split-K attention group (0 = min(grid / units, 32)).
  * Plan options (rebuild the per-CTA plan): "calib_mask", "plan_reverse",
- * "attn_group_max". */
+ * "attn_group_max".  "stage_mask": 0x1f, or 0x07 / 0x18 for the component
+ * ablation (attention / GLU blocks only).  "prefill_terms": bf16 terms per
+ * f32 activation in ffb_prefill's GEMMs -- 3 (default, f32-exact products)
+ * or 2 (hi + lo, ~2^-17 relative, a third fewer tensor-core FLOPs). */
 ffb_status ffb_set_option(ffb_model *m, const char *key, int64_t value);
 
 /* Diagnostics only (never needed for correct use): bit 0 = streaming-only

@@ -91,6 +91,7 @@ struct ffb_model {
     // prefill (prefill.cu): cuBLAS handle + scratch, created on first use
     void* cublas = nullptr;
     void (*cublas_destroy)(void*) = nullptr;
+    int prefill_terms = 3;  // option "prefill_terms": bf16 terms per f32 activation in the GEMMs
     void* pf_buf = nullptr;
     size_t pf_bytes = 0;     // [kMaxTP][B][2] the ranks' (value, index) candidates
     int64_t *greedy = nullptr, *tokens_dev = nullptr;

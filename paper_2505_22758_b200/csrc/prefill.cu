@@ -102,13 +102,14 @@ __device__ __forceinline__ void put_split4(__nv_bfloat16* y3, size_t plane, size
 }
 
 // one element of a split-term GEMM result: (hi + mid) + lo planes
-__device__ __forceinline__ float ld3(const float* c, size_t plane, size_t i) {
-    return (c[i] + c[plane + i]) + c[2 * plane + i];
+// (nt = 2: the two-term split, option "prefill_terms", no lo plane)
+__device__ __forceinline__ float ld3(const float* c, size_t plane, size_t i, int nt) {
+    return (c[i] + c[plane + i]) + (nt == 3 ? c[2 * plane + i] : 0.f);
 }
-__device__ __forceinline__ float4 ld3x4(const float* c, size_t plane, size_t i) {
+__device__ __forceinline__ float4 ld3x4(const float* c, size_t plane, size_t i, int nt) {
     const float4 a = *reinterpret_cast<const float4*>(c + i);
     const float4 b = *reinterpret_cast<const float4*>(c + plane + i);
-    const float4 d = *reinterpret_cast<const float4*>(c + 2 * plane + i);
+    const float4 d = nt == 3 ? *reinterpret_cast<const float4*>(c + 2 * plane + i) : make_float4(0.f, 0.f, 0.f, 0.f);
     return make_float4((a.x + b.x) + d.x, (a.y + b.y) + d.y, (a.z + b.z) + d.z, (a.w + b.w) + d.w);
 }
 
@@ -120,7 +121,7 @@ constexpr int kRowThreads = 256, kRowVec = 8;  // float4 per thread: K <= 256 * 
 __global__ void __launch_bounds__(kRowThreads) k_residual_norm_split(float* __restrict__ x, const float* __restrict__ c3,
                                                                      size_t cplane, const float* __restrict__ gain,
                                                                      float eps, __nv_bfloat16* __restrict__ y3,
-                                                                     int rows, int K) {
+                                                                     int rows, int K, int nt) {
     const int r = blockIdx.x;
     float4* xr = reinterpret_cast<float4*>(x + (size_t)r * K);
     const int nv = K / 4;
@@ -132,7 +133,7 @@ __global__ void __launch_bounds__(kRowThreads) k_residual_norm_split(float* __re
         if (c < nv) {
             float4 a = xr[c];
             if (c3 != nullptr) {
-                const float4 d = ld3x4(c3, cplane, (size_t)r * K + 4 * c);
+                const float4 d = ld3x4(c3, cplane, (size_t)r * K + 4 * c, nt);
                 a = make_float4(a.x + d.x, a.y + d.y, a.z + d.z, a.w + d.w);
                 xr[c] = a;
             }
@@ -164,10 +165,10 @@ __global__ void __launch_bounds__(kRowThreads) k_residual_norm_split(float* __re
 // h = silu(gate) * in over the interleaved (in, gate) columns of the Wffn1
 // output (three planes), split straight into the W2 GEMM's input planes
 __global__ void k_silu_split(const float* __restrict__ c3, size_t cplane, __nv_bfloat16* __restrict__ y3, int rows,
-                             int DI) {
+                             int DI, int nt) {
     const size_t n4 = (size_t)rows * DI / 4, plane = (size_t)rows * DI;
     for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n4; i += (size_t)gridDim.x * blockDim.x) {
-        const float4 a = ld3x4(c3, cplane, 8 * i), b = ld3x4(c3, cplane, 8 * i + 4);
+        const float4 a = ld3x4(c3, cplane, 8 * i, nt), b = ld3x4(c3, cplane, 8 * i + 4, nt);
         const float4 h = make_float4(a.y / (1.0f + expf(-a.y)) * a.x, a.w / (1.0f + expf(-a.w)) * a.z,
                                      b.y / (1.0f + expf(-b.y)) * b.x, b.w / (1.0f + expf(-b.w)) * b.z);
         put_split4(y3, plane, 4 * i, h);
@@ -193,7 +194,7 @@ __device__ __forceinline__ int swz(int d, int64_t pos) { return ((((d >> 3) ^ (i
 // columns (two rotary pairs, one half 16-byte chunk of a K/V row).
 __global__ void k_qkv_epilogue(const float* __restrict__ qkv, size_t plane, const float2* __restrict__ rope,
                                float* __restrict__ q, __nv_bfloat16* kc, __nv_bfloat16* vc, int rows, int B, int NQ,
-                               int NKV, int DH, int64_t pos0, int64_t layer_off, int64_t max_seq) {
+                               int NKV, int DH, int64_t pos0, int64_t layer_off, int64_t max_seq, int nt) {
     const int QR = NQ * DH, KR = NKV * DH, QKVR = QR + 2 * KR;
     const size_t n4 = (size_t)rows * QKVR / 4;
     for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n4; i += (size_t)gridDim.x * blockDim.x) {
@@ -201,7 +202,7 @@ __global__ void k_qkv_epilogue(const float* __restrict__ qkv, size_t plane, cons
         const int g = (int)(4 * i - r * QKVR);
         const int t = (int)(r / B), b = (int)(r % B);
         const int64_t pos = pos0 + t;
-        float4 v = ld3x4(qkv, plane, 4 * i);
+        float4 v = ld3x4(qkv, plane, 4 * i, nt);
         const int dim = g % DH;
         if (g < QR + KR) {
             const float2 cs0 = rope[t * (DH / 2) + dim / 2], cs1 = rope[t * (DH / 2) + dim / 2 + 1];
@@ -462,14 +463,14 @@ __global__ void __launch_bounds__(kAttnThreads) k_attention(const float* __restr
 // LM head: the three planes summed in place into plane 0 (the logits) and
 // a (max, lowest index) candidate per block of each row (numerics.hpp:169-175)
 constexpr int kArgBlocks = 64;
-__global__ void k_logits_part(float* __restrict__ c3, size_t plane, int V, float2* __restrict__ part) {
+__global__ void k_logits_part(float* __restrict__ c3, size_t plane, int V, float2* __restrict__ part, int nt) {
     const int b = blockIdx.y;
     float* row = c3 + (size_t)b * V;
     const int per = (V + kArgBlocks - 1) / kArgBlocks, i0 = blockIdx.x * per, i1 = min(V, i0 + per);
     float bv = -INFINITY;
     int bi = 0x7fffffff;
     for (int i = i0 + threadIdx.x; i < i1; i += blockDim.x) {
-        const float v = (row[i] + row[plane + i]) + row[2 * plane + i];
+        const float v = ld3(row, plane, i, nt);
         row[i] = v;
         if (v > bv) {
             bv = v;
@@ -521,10 +522,10 @@ __global__ void k_argmax_final(const float2* __restrict__ part, int64_t* __restr
 // three planes (ld3).  W bf16 row-major [N][K] (w_kn = false) or [K][N]
 // (w_kn = true: Wffn2^T stored [DI][D])
 ffb_status gemm3(cublasHandle_t h, const __nv_bfloat16* y3, int rows, int K, const void* W, int N, bool w_kn,
-                 float* C3) {
+                 float* C3, int nt) {
     const float one = 1.f, zero = 0.f;
     // column-major view: C'[N][3 rows] = op(W') . Y'[K][3 rows]
-    const int st = cublas()->gemm_ex(h, w_kn ? CUBLAS_OP_N : CUBLAS_OP_T, CUBLAS_OP_N, N, 3 * rows, K, &one, W,
+    const int st = cublas()->gemm_ex(h, w_kn ? CUBLAS_OP_N : CUBLAS_OP_T, CUBLAS_OP_N, N, nt * rows, K, &one, W,
                                      kCUDA_R_16BF, w_kn ? N : K, y3, kCUDA_R_16BF, K, &zero, C3, kCUDA_R_32F, N,
                                      kCUBLAS_COMPUTE_32F, kCUBLAS_GEMM_DEFAULT);
     if (st != 0) return fail(FFB_DEVICE, "prefill: cublasGemmEx failed (status %d)", st);
@@ -603,16 +604,17 @@ extern "C" ffb_status ffb_prefill(ffb_model* m, const int64_t* tokens, int64_t n
     const auto* RB = m->ops;
     const float eps = static_cast<float>(c.rmsnorm_eps);
     const int ew = 4 * m->grid;  // grid of the element-wise kernels
+    const int nt = m->prefill_terms;  // activation split terms: 3 (f32-exact products) or 2
     k_rope_table<<<(int)((n * DH / 2 + 255) / 256), 256, 0, s>>>(rope, (int)n, pos0, DH, c.rope_theta);
     k_embed<<<(int)rows, 256, 0, s>>>(X, m->embedding, tok, (int)rows, D);
-    k_residual_norm_split<<<(int)rows, kRowThreads, 0, s>>>(X, nullptr, 0, m->norm_attn, eps, Y3, (int)rows, D);
+    k_residual_norm_split<<<(int)rows, kRowThreads, 0, s>>>(X, nullptr, 0, m->norm_attn, eps, Y3, (int)rows, D, nt);
     const size_t pD = (size_t)rows * D;
     for (int64_t l = 0; l < c.layers; ++l) {
         const int64_t layer_off = l * B * NKV * m->max_seq * DH;
-        ffb_status st = gemm3(h, Y3, (int)rows, D, m->wqkv + (size_t)l * QKVR * RB->row_bytes, QKVR, false, C);
+        ffb_status st = gemm3(h, Y3, (int)rows, D, m->wqkv + (size_t)l * QKVR * RB->row_bytes, QKVR, false, C, nt);
         if (st) return st;
         k_qkv_epilogue<<<ew, 256, 0, s>>>(C, (size_t)rows * QKVR, rope, Q, m->kcache, m->vcache, (int)rows, (int)B,
-                                          NQ, NKV, DH, pos0, layer_off, m->max_seq);
+                                          NQ, NKV, DH, pos0, layer_off, m->max_seq, nt);
         const int tq = kPairs / (NQ / NKV);
         const dim3 ag((unsigned)((n + tq - 1) / tq), (unsigned)NKV, (unsigned)B);
         const size_t ap = (size_t)rows * AD;
@@ -622,33 +624,33 @@ extern "C" ffb_status ffb_prefill(ffb_model* m, const int64_t* tokens, int64_t n
         else if (DH == 128)
             k_attention<128><<<ag, kAttnThreads, AttnSmem<128>::BYTES, s>>>(Q, m->kcache, m->vcache, Y3, ap, (int)B, NQ,
                                                                    NKV, (int)n, pos0, layer_off, m->max_seq);
-        st = gemm3(h, Y3, (int)rows, AD, m->waout + (size_t)l * D * RB->row_bytes_a, D, false, C);
+        st = gemm3(h, Y3, (int)rows, AD, m->waout + (size_t)l * D * RB->row_bytes_a, D, false, C, nt);
         if (st) return st;
         k_residual_norm_split<<<(int)rows, kRowThreads, 0, s>>>(X, C, pD, m->norm_ffn + l * D, eps, Y3, (int)rows,
-                                                               D);
-        st = gemm3(h, Y3, (int)rows, D, m->wffn1 + (size_t)l * 2 * DI * RB->row_bytes, 2 * DI, false, C);
+                                                               D, nt);
+        st = gemm3(h, Y3, (int)rows, D, m->wffn1 + (size_t)l * 2 * DI * RB->row_bytes, 2 * DI, false, C, nt);
         if (st) return st;
-        k_silu_split<<<ew, 256, 0, s>>>(C, (size_t)rows * 2 * DI, Y3, (int)rows, DI);
+        k_silu_split<<<ew, 256, 0, s>>>(C, (size_t)rows * 2 * DI, Y3, (int)rows, DI, nt);
         // W2: [D][DI] rows (two-phase FFN shapes) or Wffn2^T [DI][D]
-        st = gemm3(h, Y3, (int)rows, DI, m->wffn2t + (size_t)l * D * DI * 2, D, !RB->ffn2_rows, C);
+        st = gemm3(h, Y3, (int)rows, DI, m->wffn2t + (size_t)l * D * DI * 2, D, !RB->ffn2_rows, C, nt);
         if (st) return st;
         if (l + 1 < c.layers) {
             k_residual_norm_split<<<(int)rows, kRowThreads, 0, s>>>(X, C, pD, m->norm_attn + (l + 1) * D, eps, Y3,
-                                                                   (int)rows, D);
+                                                                   (int)rows, D, nt);
         } else {  // only the last position of each batch row feeds the LM head
             const size_t o = (size_t)(n - 1) * B * D;
             k_residual_norm_split<<<(int)B, kRowThreads, 0, s>>>(X + o, C + o, pD, m->final_norm, eps, Y3, (int)B,
-                                                                D);
+                                                                D, nt);
         }
     }
     if (c.layers == 0) {
         const size_t o = (size_t)(n - 1) * B * D;
-        k_residual_norm_split<<<(int)B, kRowThreads, 0, s>>>(X + o, nullptr, 0, m->final_norm, eps, Y3, (int)B, D);
+        k_residual_norm_split<<<(int)B, kRowThreads, 0, s>>>(X + o, nullptr, 0, m->final_norm, eps, Y3, (int)B, D, nt);
     }
     // LM head on the last position of every batch row
-    ffb_status st = gemm3(h, Y3, (int)B, D, m->lm_head, V, false, C);
+    ffb_status st = gemm3(h, Y3, (int)B, D, m->lm_head, V, false, C, nt);
     if (st) return st;
-    k_logits_part<<<dim3(kArgBlocks, (unsigned)B), 256, 0, s>>>(C, (size_t)B * V, V, part);
+    k_logits_part<<<dim3(kArgBlocks, (unsigned)B), 256, 0, s>>>(C, (size_t)B * V, V, part, nt);
     k_argmax_final<<<(int)B, 1, 0, s>>>(part, tok);
     CUDA_TRY(cudaGetLastError());
     if (logits) CUDA_TRY(cudaMemcpyAsync(logits, C, sizeof(float) * B * V, cudaMemcpyDeviceToHost, s));

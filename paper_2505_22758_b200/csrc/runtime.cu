@@ -1429,6 +1429,11 @@ ffb_status ffb_set_option(ffb_model* m, const char* key, int64_t value) {
         m->use_sm_rank = value ? 1 : 0;
         return FFB_OK;
     }
+    if (std::strcmp(key, "prefill_terms") == 0) {
+        if (value != 2 && value != 3) return fail(FFB_USAGE, "prefill_terms: 3 (f32-exact) or 2 (bf16 hi + lo)");
+        m->prefill_terms = static_cast<int>(value);
+        return FFB_OK;
+    }
     if (std::strcmp(key, "stage_mask") == 0) {
         if (value != 0x1f && value != 0x07 && value != 0x18)
             return fail(FFB_USAGE, "stage_mask: 0x1f (decoder), 0x07 (attention blocks) or 0x18 (GLU blocks)");

@@ -22,7 +22,7 @@ import pytest
 
 import oracle as O
 from gpu_helpers import check_step, device_from_store, kv_rows_match, rel_err
-from paper_2505_22758_b200 import DecodeModel, UnsupportedConfigError, ValidationError
+from paper_2505_22758_b200 import DecodeModel, UnsupportedConfigError, UsageError, ValidationError
 
 pytestmark = pytest.mark.gpu
 
@@ -105,6 +105,25 @@ def test_prefill_full_width_matches_oracle(name, batch, ctx, n):
     print(f"{name} b{batch} ctx {ctx} n {n}: rel_err {e_plain:.2e}, same-KV {e_strict:.2e}, flips {flips}")
 
 
+@pytest.mark.parametrize("name,batch,ctx,n", [("llama31_8b-toy", 1, 0, 37), ("llama31_8b-toy", 2, 40, 20),
+                                              ("llama31_8b", 1, 1000, 48)])
+def test_prefill_two_term_split_within_reference_bound(name, batch, ctx, n):
+    """Option prefill_terms = 2 (activations as bf16 hi + lo, ~2^-17
+    relative): same checks, logits within the reference's own 1e-4 bound
+    (test_interpreter.cpp:66) of the oracle run on the device's K/V."""
+    cfg = O.preset(name).replace(batch=batch)
+    if name == "llama31_8b":
+        cfg = cfg.replace(layers=2, vocab_size=4096)
+    st = O.OracleStore(cfg, 1234, ctx + n + 2)
+    if ctx:
+        st.synthetic_prefill(ctx, 7)
+    with device_from_store(st) as m:
+        m.set_option("prefill_terms", 2)
+        e_plain, e_strict, flips = _check_prefill(st, m, _prompt(n, batch, cfg.vocab_size, 3), ctx,
+                                                  strict=1e-4, plain=2e-4)
+    print(f"2-term {name} b{batch} ctx {ctx} n {n}: rel_err {e_plain:.2e}, same-KV {e_strict:.2e}, flips {flips}")
+
+
 def test_prefill_greedy_continuation_matches_decode_as_prefill():
     """Greedy generation after a GEMM prefill equals generation after the
     reference's decode-as-prefill (the persistent kernel stepping through the
@@ -163,6 +182,8 @@ def test_prefill_validation():
         assert m.length(0) == 0  # nothing appended by a failed call
         m.prefill([[1], [2]], 0)
         assert m.length(0) == 2
+        with pytest.raises(UsageError):
+            m.set_option("prefill_terms", 1)
     cfg8 = O.preset("llama31_8b-toy").replace(batch=16)
     st8 = O.OracleStore(cfg8, 1, 16)
     with device_from_store(st8, 16) as m8:

@@ -556,6 +556,9 @@ extern "C" ffb_status ffb_prefill(ffb_model* m, const int64_t* tokens, int64_t n
     if ((DH != 64 && DH != 128) || kPairs % (NQ / NKV) != 0 || D > kRowThreads * 4 * kRowVec)
         return fail(FFB_UNSUPPORTED, "prefill: head shape (d_head 64 / 128, q heads per kv head dividing 64)");
     CUDA_TRY(cudaSetDevice(m->device));
+    // steps enqueued asynchronously on any stream (ffb_decode_step_device,
+    // ffb_decode_loop) write the cache this call extends: let them land
+    CUDA_TRY(cudaDeviceSynchronize());
     cudaStream_t s = m->stream;
     // scratch (kept; sized for the largest call so far): residual X, rotated
     // q, the GEMM outputs C3 (three planes), the GEMM inputs Y3 (three bf16

@@ -99,10 +99,11 @@ int64_t ffb_quant_row_bytes(int64_t cols, int32_t quant_bits);
 int64_t ffb_pack_quant_rows(const float *values, int64_t rows, int64_t cols,
                             int32_t quant_bits, uint8_t *out);
 /* Same with an explicit code order: layout 0 = plain (column order, used by
- * Wffn2^T and the CUDA-core GEMV), 1 = tensor-core order (each lane quad of
- * the mma.sync A fragment reads its 32 codes of a 128-column group as one
- * 16-byte (int4) / 32-byte (int8) block; used by Wqkv / Wffn1 / lm_head /
- * Waout rows whose width is a multiple of 1024). */
+ * Wffn2^T and the CUDA-core GEMV), 1 = tensor-core order (mma.sync m16n8k32
+ * u8 A fragments: per 128-column group, lane quad q reads columns 32s + 4q +
+ * {0..3} and 32s + 16 + 4q + {0..3} of k32-step s as one word (int4: low /
+ * high nibbles) or 8 bytes (int8), q-major 16 / 32-byte blocks; used by
+ * Wqkv / Wffn1 / lm_head / Waout rows whose width is a multiple of 1024). */
 int64_t ffb_pack_quant_rows_ex(const float *values, int64_t rows, int64_t cols,
                                int32_t quant_bits, int32_t layout, uint8_t *out);
 

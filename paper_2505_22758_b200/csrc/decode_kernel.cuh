@@ -406,7 +406,8 @@ struct KTraits : RowMap<S, S::D> {
                            // ring), S_RED scratch + TP delta, TP exchange rows
                            cmax(S::KCP ? 0 : 2 * kMaxGrid * S::B, NCW * 32 + S::B * TMAX)),
                       SZ_ATT),
-                 cmax(MD::TC ? S::D : 0, MA::TC ? S::AD : 0));  // TC activation strips
+                 cmax(MD::TC ? S::D + 2 * S::D / kQuantGroup : 0,  // TC activation strips + group words
+                      MA::TC ? S::AD + 2 * S::AD / kQuantGroup : 0));
     static_assert(R_H % 16 == 0 && R_NORM % 16 == 0 && R_WPART % 16 == 0,
                   "16-byte aligned scratch (vector smem accesses)");
     static constexpr int R_AMAX = R_WPART + SZ_WPART;  // [NCT] (f32, i32)
@@ -1022,42 +1023,97 @@ struct DecodeCta {
             }
             consumer_sync(NCT);  // ns reusable afterwards
         }
-        // MMA B fragments (m16n8k16 "col", batch 1): column n = 0 carries the
-        // fp16 hi part, n = 1 the lo part of each activation (hi + lo keeps
-        // 22 bits), n >= 2 zero.  Lane (g, q) of k-step j needs rows 2q, 2q+1
-        // (reg 0) and 2q+8, 2q+9 (reg 1) of column g; int4 pre-scales reg 1 by
-        // 1/16 (the decode leaves those codes times 16).  Each lane builds
-        // the table of its own k-steps (PL / 16 of them) into this warp's
-        // smem strip [j][n][q][reg]; tc_slot reads it per k-step.
-        uint32_t* tab = reinterpret_cast<uint32_t*>(wpart()) + warp * M::KS * 16;
-        const float sc1 = M::QB == 4 ? 0.0625f : 1.f;
+        // MMA B fragments (m16n8k32 "col", s8, batch 1): each 128-column
+        // group of activations as three int8 terms of one block scale,
+        //   x = dq * (x0 + x1 / 254 + x2 / 254^2),  |x0|, |x1|, |x2| <= 127,
+        // i.e. 23 bits relative to the group's largest |x| (dq = max / 127);
+        // column n = term n, n = 3 zero.  Lane (g, q) of k32-step s needs
+        // rows 4q..4q+3 (reg 0) and 16+4q..16+4q+3 (reg 1) of column g.  Each
+        // lane quantises its PL columns (a half k32-step per 16) into this
+        // warp's strip [step][n][q][reg]; per group, (dq, sum of x0 + x1/254
+        // + x2/254^2) for the zero-point term follows the NCW strips.
+        static_assert(PL % 16 == 0 && 128 % PL == 0, "half k32-steps per lane, whole lanes per group");
+        constexpr int LPG = 128 / PL;  // lanes per quant group
+        uint32_t* tab = reinterpret_cast<uint32_t*>(wpart()) + warp * M::KW;
+        float2* ginfo = tc_ginfo<M>();
+        float x[PL];
+        float mx = 0.f;
+#pragma unroll
+        for (int c = 0; c < PL; ++c) {
+            x[c] = gain ? gl[c] * v[0][c] * inv[0] : v[0][c];
+            mx = fmaxf(mx, fabsf(x[c]));
+        }
+#pragma unroll
+        for (int o = 1; o < LPG; o <<= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        const float qs = mx > 0.f ? 127.f / mx : 0.f;
+        // round-to-nearest through the 1.5 * 2^23 magic: (y + M) holds
+        // rint(y) in its low mantissa bits (two's complement in the low byte)
+        // and (y + M) - M is rint(y) as a float; sums of the terms in f32
+        // (exact: |sum| <= 127 * 128)
+        constexpr float kM = 12582912.f;
+        float s0 = 0.f, s1 = 0.f, s2 = 0.f;
+        uint32_t t0[PL / 4], t1[PL / 4], t2[PL / 4];
+#pragma unroll
+        for (int c4 = 0; c4 < PL; c4 += 4) {
+            uint32_t m0[4], m1[4], m2[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                const float y = x[c4 + e] * qs;
+                const float a0 = y + kM, f0 = a0 - kM;
+                const float r1 = (y - f0) * 254.f;
+                const float a1 = r1 + kM, f1 = a1 - kM;
+                const float r2 = (r1 - f1) * 254.f;
+                const float a2 = r2 + kM, f2 = a2 - kM;
+                s0 += f0;
+                s1 += f1;
+                s2 += f2;
+                m0[e] = __float_as_uint(a0);
+                m1[e] = __float_as_uint(a1);
+                m2[e] = __float_as_uint(a2);
+            }
+            auto pack4 = [](const uint32_t (&m)[4]) {  // the four low bytes
+                return __byte_perm(__byte_perm(m[0], m[1], 0x0040), __byte_perm(m[2], m[3], 0x0040), 0x5410);
+            };
+            t0[c4 / 4] = pack4(m0);
+            t1[c4 / 4] = pack4(m1);
+            t2[c4 / 4] = pack4(m2);
+        }
 #pragma unroll
         for (int jj = 0; jj < PL / 16; ++jj) {
-            const int j = lane * (PL / 16) + jj;
-            uint32_t e[16];
+            const int hs = lane * (PL / 16) + jj, st = hs / 2, h = hs % 2;
 #pragma unroll
-            for (int qq = 0; qq < 4; ++qq)
-#pragma unroll
-                for (int h = 0; h < 2; ++h) {
-                    const int c = jj * 16 + 2 * qq + 8 * h;
-                    float x0 = gain ? gl[c] * v[0][c] * inv[0] : v[0][c];
-                    float x1 = gain ? gl[c + 1] * v[0][c + 1] * inv[0] : v[0][c + 1];
-                    if (h == 1) {
-                        x0 *= sc1;
-                        x1 *= sc1;
-                    }
-                    const __half h0 = __float2half_rn(x0), h1 = __float2half_rn(x1);
-                    __half2 hi = __halves2half2(h0, h1);
-                    __half2 lo = __halves2half2(__float2half_rn(x0 - __half2float(h0)),
-                                                __float2half_rn(x1 - __half2float(h1)));
-                    e[qq * 2 + h] = *reinterpret_cast<uint32_t*>(&hi);       // n = 0
-                    e[8 + qq * 2 + h] = *reinterpret_cast<uint32_t*>(&lo);   // n = 1
-                }
-#pragma unroll
-            for (int i = 0; i < 16; i += 4)
-                *reinterpret_cast<uint4*>(tab + j * 16 + i) = make_uint4(e[i], e[i + 1], e[i + 2], e[i + 3]);
+            for (int qq = 0; qq < 4; ++qq) {
+                tab[st * 32 + 0 * 8 + qq * 2 + h] = t0[jj * 4 + qq];
+                tab[st * 32 + 1 * 8 + qq * 2 + h] = t1[jj * 4 + qq];
+                tab[st * 32 + 2 * 8 + qq * 2 + h] = t2[jj * 4 + qq];
+            }
         }
+#pragma unroll
+        for (int o = 1; o < LPG; o <<= 1) {
+            s0 += __shfl_xor_sync(0xffffffffu, s0, o);
+            s1 += __shfl_xor_sync(0xffffffffu, s1, o);
+            s2 += __shfl_xor_sync(0xffffffffu, s2, o);
+        }
+        if (lane % LPG == 0)
+            ginfo[warp * (M::KW / kQuantGroup) + lane / LPG] =
+                make_float2(mx / 127.f, s0 + s1 * (1.f / 254.f) + s2 * (1.f / 64516.f));
         consumer_sync(NCT);  // tables complete before any warp's first MMA
+    }
+
+    // per-group (dq, zero-point sum) of the TC activation tables
+    template <class M>
+    __device__ float2* tc_ginfo() {
+        return reinterpret_cast<float2*>(reinterpret_cast<uint32_t*>(wpart()) + NCW * M::KW);
+    }
+
+    // u8 codes x s8 activation terms, exact s32 accumulation
+    __device__ static void mma_u8s8(int (&c)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3,
+                                    uint32_t b0, uint32_t b1) {
+        asm volatile(
+            "mma.sync.aligned.m16n8k32.row.col.s32.u8.s8.s32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
+            "{%8,%9}, {%0,%1,%2,%3};"
+            : "+r"(c[0]), "+r"(c[1]), "+r"(c[2]), "+r"(c[3])
+            : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
     }
 
     __device__ static void mma_f16(float (&c)[4], uint32_t a0, uint32_t a1, uint32_t a2,
@@ -1085,71 +1141,66 @@ struct DecodeCta {
     }
 
     // One 16-row (int4) / 8-row (int8) slot of a TC matrix against this
-    // warp's K range: per 128-column group, decode the A fragments of rows
-    // g and g + 8 (MMA code order, weight_layout_tc), 8 MMAs into a group
-    // accumulator, scale by the rows' group scales.  out[0..3] = C fragment
-    // (rows g / g+8, columns 2q, 2q+1) summed over the warp's groups.
+    // warp's K range: per 128-column group, the codes of rows g and g + 8
+    // (MMA code order, weight_layout_tc) go straight into m16n8k32 u8 A
+    // fragments (int4: one LOP3 per 4 codes, int8: as loaded), four MMAs
+    // against the three int8 activation terms accumulate exactly in s32,
+    // then per row: s * dq * ((t0 + t1/254 + t2/254^2) - z * sum), the
+    // zero point folded through the group's activation sum.  out[0] / out[2]
+    // = rows g / g + 8 (lanes q == 0), out[1] = out[3] = 0.
     template <class M>
     __device__ __forceinline__ void tc_slot(const uint8_t* base, float (&out)[4]) {
         const int ctid = threadIdx.x, warp = ctid / 32, lane = ctid % 32, g = lane / 4, q = lane % 4;
-        const uint32_t* tab = reinterpret_cast<const uint32_t*>(wpart()) + warp * M::KS * 16;
-        auto frag = [&](int j) {  // (reg 0, reg 1) of k-step j for column g
-            return g < 2 ? *reinterpret_cast<const uint2*>(tab + j * 16 + g * 8 + q * 2)
-                         : make_uint2(0u, 0u);
+        const uint32_t* tab = reinterpret_cast<const uint32_t*>(wpart()) + warp * M::KW;
+        const float2* ginfo = tc_ginfo<M>() + warp * (M::KW / kQuantGroup);
+        auto frag = [&](int st) {  // (reg 0, reg 1) of k32-step st for column g (terms 0..2)
+            return g < 3 ? *reinterpret_cast<const uint2*>(tab + st * 32 + g * 8 + q * 2) : make_uint2(0u, 0u);
         };
         const uint8_t* rA = base + g * M::ROW_BYTES;
         const uint8_t* rB = base + (g + 8) * M::ROW_BYTES;
 #pragma unroll
         for (int e = 0; e < 4; ++e) out[e] = 0.f;
-        // two groups per iteration and two accumulators per group (even /
-        // odd k-steps): four independent MMA chains instead of one
 #pragma unroll 2
         for (int gi = 0; gi < M::KW / kQuantGroup; ++gi) {
             const int G = warp * (M::KW / kQuantGroup) + gi;  // group index in the row
             const float sA = *reinterpret_cast<const float*>(rA + M::CODE_BYTES + 4 * G);
-            const uint32_t zA = rA[M::CODE_BYTES + 4 * M::NG + G];
-            float acc[4] = {0.f, 0.f, 0.f, 0.f}, acc2[4] = {0.f, 0.f, 0.f, 0.f};
+            const float zA = static_cast<float>(rA[M::CODE_BYTES + 4 * M::NG + G]);
+            int acc[4] = {0, 0, 0, 0};
             if constexpr (M::QB == 4) {
-                const float sB = *reinterpret_cast<const float*>(rB + M::CODE_BYTES + 4 * G);
-                const uint32_t zB = rB[M::CODE_BYTES + 4 * M::NG + G];
-                // (1024 + z) and (1024 + 16 z) per half, both exact in fp16
-                const uint32_t zA1 = (0x6400u | zA) * 0x10001u, zA16 = (0x6400u | (zA << 4)) * 0x10001u;
-                const uint32_t zB1 = (0x6400u | zB) * 0x10001u, zB16 = (0x6400u | (zB << 4)) * 0x10001u;
                 const uint4 wa = lds_u128(rA + G * 64 + q * 16);
                 const uint4 wb = lds_u128(rB + G * 64 + q * 16);
                 const uint32_t wA[4] = {wa.x, wa.y, wa.z, wa.w}, wB[4] = {wb.x, wb.y, wb.z, wb.w};
 #pragma unroll
-                for (int t = 0; t < 4; ++t) {
-                    const uint32_t a8 = wA[t] >> 8, b8 = wB[t] >> 8;
-#pragma unroll
-                    for (int u = 0; u < 2; ++u) {  // k-steps 2t, 2t+1
-                        const uint32_t xa = u ? a8 : wA[t], xb = u ? b8 : wB[t];
-                        const uint32_t a0 = hsub2_u(f16_nib<0x000F000Fu>(xa), zA1);
-                        const uint32_t a2 = hsub2_u(f16_nib<0x00F000F0u>(xa), zA16);
-                        const uint32_t a1 = hsub2_u(f16_nib<0x000F000Fu>(xb), zB1);
-                        const uint32_t a3 = hsub2_u(f16_nib<0x00F000F0u>(xb), zB16);
-                        const uint2 bf = frag(gi * 8 + 2 * t + u);
-                        mma_f16(u ? acc2 : acc, a0, a1, a2, a3, bf.x, bf.y);
-                    }
+                for (int st = 0; st < 4; ++st) {
+                    const uint2 bf = frag(gi * 4 + st);
+                    mma_u8s8(acc, wA[st] & 0x0F0F0F0Fu, wB[st] & 0x0F0F0F0Fu, (wA[st] >> 4) & 0x0F0F0F0Fu,
+                             (wB[st] >> 4) & 0x0F0F0F0Fu, bf.x, bf.y);
                 }
-                out[0] = fmaf(sA, acc[0] + acc2[0], out[0]);
-                out[1] = fmaf(sA, acc[1] + acc2[1], out[1]);
-                out[2] = fmaf(sB, acc[2] + acc2[2], out[2]);
-                out[3] = fmaf(sB, acc[3] + acc2[3], out[3]);
             } else {  // int8: 8 real rows (g), rows g + 8 zero
-                const uint32_t z1 = (0x6400u | zA) * 0x10001u;
                 const uint4 w0 = lds_u128(rA + G * 128 + q * 32);
                 const uint4 w1 = lds_u128(rA + G * 128 + q * 32 + 16);
                 const uint32_t wA[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
 #pragma unroll
-                for (int st = 0; st < 8; ++st) {
-                    const uint32_t a0 = hsub2_u(__byte_perm(wA[st], 0x64646464u, 0x4140), z1);
-                    const uint32_t a2 = hsub2_u(__byte_perm(wA[st], 0x64646464u, 0x4342), z1);
-                    const uint2 bf = frag(gi * 8 + st);
-                    mma_f16((st & 1) ? acc2 : acc, a0, 0u, a2, 0u, bf.x, bf.y);
+                for (int st = 0; st < 4; ++st) {
+                    const uint2 bf = frag(gi * 4 + st);
+                    mma_u8s8(acc, wA[2 * st], 0u, wA[2 * st + 1], 0u, bf.x, bf.y);
                 }
-                out[0] = fmaf(sA, acc[0] + acc2[0], out[0]);
-                out[1] = fmaf(sA, acc[1] + acc2[1], out[1]);
+            }
+            // terms 0, 1 in lane q = 0 (columns 0, 1), term 2 in lane q = 1
+            const int t2A = __shfl_down_sync(0xffffffffu, acc[0], 1);
+            const int t2B = __shfl_down_sync(0xffffffffu, acc[2], 1);
+            const float2 gf = ginfo[gi];
+            const float xA = fmaf(static_cast<float>(t2A), 1.f / 64516.f,
+                                  fmaf(static_cast<float>(acc[1]), 1.f / 254.f, static_cast<float>(acc[0])));
+            out[0] = fmaf(sA * gf.x, fmaf(-zA, gf.y, xA), out[0]);
+            if constexpr (M::QB == 4) {
+                const float sB = *reinterpret_cast<const float*>(rB + M::CODE_BYTES + 4 * G);
+                const float zB = static_cast<float>(rB[M::CODE_BYTES + 4 * M::NG + G]);
+                const float xB = fmaf(static_cast<float>(t2B), 1.f / 64516.f,
+                                      fmaf(static_cast<float>(acc[3]), 1.f / 254.f, static_cast<float>(acc[2])));
+                out[2] = fmaf(sB * gf.x, fmaf(-zB, gf.y, xB), out[2]);
+            } else {
+                (void)t2B;
             }
         }
     }

@@ -792,26 +792,22 @@ bool quant_group(const float* v, int n, int levels, uint8_t* codes, float* scale
 }
 
 // Byte / nibble position of column i (0..127) of a 128-column group in the
-// tensor-core code order (decode_kernel.cuh: tc_slot): lane quad q of the
-// mma.sync A fragment owns columns 16s + 2q + {0, 1, 8, 9} of k-step s.
-//   int4: 64 bytes = q-major 16-byte blocks of 4 words; word t holds k-steps
-//         2t, 2t+1: nibble 0/4/1/5 = step 2t columns +0/+1/+8/+9... laid out
-//         so one LOP3 yields the (c, c+1) fp16 pair: bits 0-3 = +0, 16-19 = +1,
-//         4-7 = +8, 20-23 = +9 of step 2t; bits 8-11, 24-27, 12-15, 28-31 the
-//         same of step 2t+1.
-//   int8: 128 bytes = q-major 32-byte blocks, 4 bytes (+0, +1, +8, +9) per step.
+// tensor-core code order (decode_kernel.cuh: tc_slot, mma.sync m16n8k32 u8
+// A fragments): lane quad q owns columns 32s + 4q + {0..3} (reg a0 / a1) and
+// 32s + 16 + 4q + {0..3} (reg a2 / a3) of k32-step s of a 128-column group.
+//   int4: 64 bytes = q-major 16-byte blocks of 4 words, word s = step s:
+//         nibble 2j = column 4q + j, nibble 2j + 1 = column 16 + 4q + j, so
+//         w & 0x0F0F0F0F and (w >> 4) & 0x0F0F0F0F are the two registers.
+//   int8: 128 bytes = q-major 32-byte blocks, 8 bytes per step: columns
+//         4q + {0..3}, then 16 + 4q + {0..3}.
 static int tc_nibble_index(int i) {  // int4: nibble index (byte * 2 + high) in the group
-    const int s = i / 16, r = i % 16;
-    const int q = (r % 8) / 2, hi = r % 2, plus8 = r >= 8;
-    const int t = s / 2, u = s % 2;
-    const int bit = (hi ? 16 : 0) + (plus8 ? 4 : 0) + (u ? 8 : 0);  // bit offset in the word
-    return (q * 4 + t) * 8 + bit / 4;
+    const int s = i / 32, r = i % 32, half = r / 16, q = (r % 16) / 4, j = r % 4;
+    return q * 32 + s * 8 + 2 * j + half;
 }
 
 static int tc_byte_index(int i) {  // int8: byte index in the group
-    const int s = i / 16, r = i % 16;
-    const int q = (r % 8) / 2, hi = r % 2, plus8 = r >= 8;
-    return q * 32 + s * 4 + (plus8 ? 2 : 0) + hi;
+    const int s = i / 32, r = i % 32, half = r / 16, q = (r % 16) / 4, j = r % 4;
+    return q * 32 + s * 8 + half * 4 + j;
 }
 
 // One row of `cols` f32 values -> the device row format of decode_kernel.cuh

@@ -131,7 +131,7 @@ ffb_status parse_model(const std::string& text, ffb_model_config* c) {
 }
 
 // ---------------------------------------------------------------- device image
-constexpr uint64_t kImageMagic = 0x32474d4942464646ull;  // "FFFBIMG2" (batch >= 8 layout 3)
+constexpr uint64_t kImageMagic = 0x33474d4942464646ull;  // "FFFBIMG3" (quant tensor-core code order v2)
 
 struct ImageHeader {
     uint64_t magic;

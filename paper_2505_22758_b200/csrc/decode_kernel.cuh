@@ -380,7 +380,7 @@ struct KTraits : RowMap<S, S::D> {
     // slots; with the per-warp attention b4 3.77 / 3.75, b8 6.41 / 6.38,
     // b16 7.32 / 7.30 ms for 3 / 2 slots (b16 7.65 with 1))
     static constexpr int ATT_SC =
-        cmin(S::B == 1 ? cmax(1, 131072 / SLOT_BYTES) : S::B == 2 ? 4 : 2, kMaxSlots - 1);
+        cmin(S::B == 1 ? cmax(1, (131072 + SLOT_BYTES - 1) / SLOT_BYTES) : S::B == 2 ? 4 : 2, kMaxSlots - 1);
     static constexpr int ANP = ((ATT_SC * KVC + 1) + 15) / 16 * 16;
     // alpha*q f32 [QPG][DH], scores f32 [QPG][ANP], probabilities as bf16
     // hi/lo MMA rows [16][ANP] (tensor-core P.V), stats [QPG][4]

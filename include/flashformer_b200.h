@@ -269,13 +269,15 @@ ffb_status ffb_decode_loop(ffb_model *m, const int64_t *d_tokens, int64_t pos, i
  * tokens[n][batch] (host) at positions pos0 .. pos0+n-1 of every batch row go
  * through each layer together -- projections as cuBLAS bf16 GEMMs over
  * n*batch rows with the f32 activations split into three bf16 terms
- * (f32-accurate products), RoPE / K-V append / causal attention / SiLU in
- * f32 kernels.  Leaves the KV cache and its lengths where n decode steps
- * would (pos0 + n), so ffb_decode_step continues at pos0 + n.  logits_out
- * (batch x vocab f32, host, may be NULL) / greedy_out (batch int64, host,
- * may be NULL) are those of the LAST position.  bf16 decoders with batch < 8
- * on one GPU (FFB_UNSUPPORTED otherwise); n * batch <= 1024 per call
- * (longer prompts: call again with pos0 advanced).  Synchronous. */
+ * (f32-accurate products; int4 / int8 weights are dequantised per
+ * projection into three exact bf16 planes of w = (code - zero) * scale),
+ * RoPE / K-V append / causal attention / SiLU in f32 kernels.  Leaves the KV
+ * cache and its lengths where n decode steps would (pos0 + n), so
+ * ffb_decode_step continues at pos0 + n.  logits_out (batch x vocab f32,
+ * host, may be NULL) / greedy_out (batch int64, host, may be NULL) are those
+ * of the LAST position.  Decoders with batch < 8 on one GPU
+ * (FFB_UNSUPPORTED otherwise); n * batch <= 1024 per call (longer prompts:
+ * call again with pos0 advanced).  Synchronous. */
 ffb_status ffb_prefill(ffb_model *m, const int64_t *tokens, int64_t n, int64_t pos0,
                        float *logits_out, int64_t *greedy_out);
 

@@ -463,6 +463,7 @@ __global__ void __launch_bounds__(kAttnThreads) k_attention(const float* __restr
 // LM head: the three planes summed in place into plane 0 (the logits) and
 // a (max, lowest index) candidate per block of each row (numerics.hpp:169-175)
 constexpr int kArgBlocks = 64;
+constexpr int kQChunk = 16384;  // quantized weights: output rows dequantised per GEMM
 __global__ void k_logits_part(float* __restrict__ c3, size_t plane, int V, float2* __restrict__ part, int nt) {
     const int b = blockIdx.y;
     float* row = c3 + (size_t)b * V;
@@ -517,6 +518,69 @@ __global__ void k_argmax_final(const float2* __restrict__ part, int64_t* __restr
     out[b] = bi;
 }
 
+// ---- quantized weights (int4 / int8): exact bf16 planes -------------------
+// A packed row (decode_kernel.cuh row format: codes | f32 scales | u8 zeros)
+// holds w = (code - zero) * scale, the reference's snapped f32 weight bit for
+// bit (the packer accepts a group only if that product reproduces every
+// value, runtime.cu quant_try); w is split into three bf16 planes (24 bits:
+// exact) so the tensor cores see the weight itself.
+// rows [r0, r0 + nr) of a packed matrix with K columns -> planes
+// w3[p][row - r0][k] (plane stride nr * K).  One thread per 8 consecutive
+// columns (consecutive lanes: consecutive 16-byte stores per plane).  In the
+// tensor-core code order (runtime.cu tc_nibble_index / tc_byte_index)
+// columns 32 st + 4q + j (j < 4) are the low nibbles / first 4 bytes of lane
+// quad q's word / 8 bytes of k32-step st, columns 32 st + 16 + 4q + j the
+// high nibbles / last 4 bytes; in the plain order codes follow the columns.
+__global__ void k_dequant3(const uint8_t* __restrict__ w, size_t row_bytes, int r0, int nr, int K, int qb, int tc,
+                           __nv_bfloat16* __restrict__ w3) {
+    const int ng = K / kQuantGroup, code_bytes = qb == 4 ? K / 2 : K;
+    const size_t plane = (size_t)nr * K, n8 = plane / 8;
+    for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < n8; e += (size_t)gridDim.x * blockDim.x) {
+        const int rr = (int)(e / (K / 8)), k0 = (int)(e % (K / 8)) * 8;
+        const int g = k0 / kQuantGroup, i0 = k0 % kQuantGroup, st = i0 / 32, hh = (i0 % 32) / 16, q0 = (i0 % 16) / 4;
+        const uint8_t* row = w + (size_t)(r0 + rr) * row_bytes;
+        const float sc = *reinterpret_cast<const float*>(row + code_bytes + 4 * g);
+        const float z = static_cast<float>(row[code_bytes + 4 * ng + g]);
+        int code[8];
+        if (qb == 4) {
+            const uint8_t* grp = row + g * 64;
+            if (tc) {
+#pragma unroll
+                for (int u = 0; u < 2; ++u) {  // lane quads q0, q0 + 1
+                    const uint32_t wd = *reinterpret_cast<const uint32_t*>(grp + (q0 + u) * 16 + st * 4);
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) code[4 * u + j] = (wd >> (8 * j + 4 * hh)) & 0xF;
+                }
+            } else {
+                const uint32_t wd = *reinterpret_cast<const uint32_t*>(grp + i0 / 2);
+#pragma unroll
+                for (int i = 0; i < 8; ++i) code[i] = (wd >> (4 * i)) & 0xF;
+            }
+        } else {
+            const uint8_t* grp = row + g * 128;
+            if (tc) {
+#pragma unroll
+                for (int u = 0; u < 2; ++u) {
+                    const uint32_t wd = *reinterpret_cast<const uint32_t*>(grp + (q0 + u) * 32 + st * 8 + 4 * hh);
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) code[4 * u + j] = (wd >> (8 * j)) & 0xFF;
+                }
+            } else {
+                const uint2 v = *reinterpret_cast<const uint2*>(grp + i0);
+#pragma unroll
+                for (int i = 0; i < 8; ++i) code[i] = ((i < 4 ? v.x : v.y) >> (8 * (i % 4))) & 0xFF;
+            }
+        }
+        __nv_bfloat16 hi[8], mi[8], lo[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) split3(__fmul_rn(static_cast<float>(code[i]) - z, sc), hi[i], mi[i], lo[i]);
+        __nv_bfloat16* dst = w3 + (size_t)rr * K + k0;
+        *reinterpret_cast<uint4*>(dst) = *reinterpret_cast<const uint4*>(hi);
+        *reinterpret_cast<uint4*>(dst + plane) = *reinterpret_cast<const uint4*>(mi);
+        *reinterpret_cast<uint4*>(dst + 2 * plane) = *reinterpret_cast<const uint4*>(lo);
+    }
+}
+
 // C3[3][rows][N] (f32, row-major) = Y3[3][rows][K] . W^T: ONE GEMM over the
 // 3 * rows stacked split-term rows, so W is read once; consumers add the
 // three planes (ld3).  W bf16 row-major [N][K] (w_kn = false) or [K][N]
@@ -538,14 +602,15 @@ extern "C" ffb_status ffb_prefill(ffb_model* m, const int64_t* tokens, int64_t n
                                   int64_t* greedy) {
     if (!m || !tokens || n <= 0) return fail(FFB_USAGE, "prefill: NULL argument or n <= 0");
     const auto& c = m->cfg;
-    if (c.kind != 0 || m->ops->QB != 0 || m->ops->kc != 0 || m->tp_size != 1)
-        return fail(FFB_UNSUPPORTED, "prefill: bf16 decoder, batch < 8, one GPU");
+    if (c.kind != 0 || m->ops->kc != 0 || m->tp_size != 1)
+        return fail(FFB_UNSUPPORTED, "prefill: decoder with batch < 8 on one GPU");
     if (!cublas()) return fail(FFB_UNSUPPORTED, "prefill: cuBLAS not available (dlopen libcublas.so.12)");
     for (int64_t l = 0; l < c.layers; ++l)
         if (m->kv_len[l] != pos0)
             return fail(FFB_VALIDATION, "prefill: cache length does not match position");
     if (pos0 + n > m->max_seq) return fail(FFB_VALIDATION, "prefill: positions exceed the KV cache");
-    const int64_t B = c.batch, rows = n * B;
+    const int64_t B = c.batch;
+    int64_t rows = n * B;  // activation rows (the LM head runs on B of them)
     for (int64_t i = 0; i < rows; ++i)
         if (tokens[i] < 0 || tokens[i] >= m->gcfg.vocab_size)
             return fail(FFB_VALIDATION, "prefill: token id out of range");
@@ -565,6 +630,13 @@ extern "C" ffb_status ffb_prefill(ffb_model* m, const int64_t* tokens, int64_t n
     // planes), the RoPE table, token ids, argmax candidates
     const int Kmax = std::max({D, AD, DI});
     const size_t Cn = 3 * std::max<size_t>((size_t)rows * std::max({QKVR, 2 * DI, D}), (size_t)B * V);
+    const bool quant = m->ops->QB != 0;
+    // quantized weights: a chunk of kQChunk rows dequantised into three bf16
+    // planes (W3) per projection
+    const size_t w3n = quant ? 3 * std::max<size_t>((size_t)std::min(kQChunk, std::max({QKVR, 2 * DI, D, V})) *
+                                                        std::max(D, AD),
+                                                    (size_t)DI * D)
+                             : 0;
     size_t need = 0;
     auto carve = [&](size_t bytes) {  // 256-byte aligned sub-buffers
         const size_t at = need;
@@ -573,7 +645,7 @@ extern "C" ffb_status ffb_prefill(ffb_model* m, const int64_t* tokens, int64_t n
     };
     const size_t oX = carve((size_t)rows * D * 4), oQ = carve((size_t)rows * QR * 4), oC = carve(Cn * 4),
                  oR = carve((size_t)n * DH * 4), oP = carve((size_t)B * kArgBlocks * 8), oT = carve(rows * 8),
-                 oY = carve((size_t)3 * rows * Kmax * 2);
+                 oY = carve((size_t)3 * rows * Kmax * 2), oW3 = carve(w3n * 2);
     if (m->pf_bytes < need) {
         if (m->pf_buf) cudaFree(m->pf_buf);
         m->pf_buf = nullptr;
@@ -589,6 +661,7 @@ extern "C" ffb_status ffb_prefill(ffb_model* m, const int64_t* tokens, int64_t n
     auto* part = reinterpret_cast<float2*>(base + oP);
     auto* tok = reinterpret_cast<int64_t*>(base + oT);
     auto* Y3 = reinterpret_cast<__nv_bfloat16*>(base + oY);
+    auto* W3 = reinterpret_cast<__nv_bfloat16*>(base + oW3);
     static bool attn_attr = [] {
         cudaFuncSetAttribute(k_attention<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, AttnSmem<64>::BYTES);
         cudaFuncSetAttribute(k_attention<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, AttnSmem<128>::BYTES);
@@ -607,14 +680,41 @@ extern "C" ffb_status ffb_prefill(ffb_model* m, const int64_t* tokens, int64_t n
     const auto* RB = m->ops;
     const float eps = static_cast<float>(c.rmsnorm_eps);
     const int ew = 4 * m->grid;  // grid of the element-wise kernels
-    const int nt = m->prefill_terms;  // activation split terms: 3 (f32-exact products) or 2
+    const int at = m->prefill_terms;         // activation split terms: 3 (f32-exact products) or 2
+    const int nt = at;                       // planes of a projection's output the consumers add
+    // one projection: Y3 (rows x K activations, split) . W^T -> C
+    auto proj = [&](int K, const uint8_t* W, size_t row_bytes, int N, bool kn, int tc) -> ffb_status {
+        if (!quant) return gemm3(h, Y3, (int)rows, K, W, N, kn, C, at);
+        const float one = 1.f, zero = 0.f;
+        for (int n0 = 0; n0 < N; n0 += kn ? N : kQChunk) {
+            const int nc = kn ? N : std::min(kQChunk, N - n0);
+            // kn (Wffn2^T): the packed rows are the GEMM's K, their columns N
+            if (kn) k_dequant3<<<4 * m->grid, 256, 0, s>>>(W, row_bytes, 0, K, N, RB->QB, tc, W3);
+            else k_dequant3<<<4 * m->grid, 256, 0, s>>>(W, row_bytes, n0, nc, K, RB->QB, tc, W3);
+            // weight plane pw against activation terms a < at - pw, summed
+            // into the activation-term planes of C (beta = 1 after plane 0):
+            // C[a] = W_hi y_a + W_mid y_a + W_lo y_a over the significant pairs
+            for (int pw = 0; pw < 3 && pw < at; ++pw) {
+                const int na = at - pw;
+                const __nv_bfloat16* A = W3 + (size_t)pw * nc * K;
+                // C planes [a][rows][N] are the rows a * rows + r of one
+                // [at * rows][N] matrix: one GEMM over the na stacked terms
+                const int st = cublas()->gemm_ex(h, kn ? CUBLAS_OP_N : CUBLAS_OP_T, CUBLAS_OP_N, nc, na * (int)rows, K,
+                                                 &one, A, kCUDA_R_16BF, kn ? N : K, Y3, kCUDA_R_16BF, K,
+                                                 pw == 0 ? &zero : &one, C + n0, kCUDA_R_32F, N, kCUBLAS_COMPUTE_32F,
+                                                 kCUBLAS_GEMM_DEFAULT);
+                if (st != 0) return fail(FFB_DEVICE, "prefill: cublasGemmEx failed (status %d)", st);
+            }
+        }
+        return FFB_OK;
+    };
     k_rope_table<<<(int)((n * DH / 2 + 255) / 256), 256, 0, s>>>(rope, (int)n, pos0, DH, c.rope_theta);
     k_embed<<<(int)rows, 256, 0, s>>>(X, m->embedding, tok, (int)rows, D);
     k_residual_norm_split<<<(int)rows, kRowThreads, 0, s>>>(X, nullptr, 0, m->norm_attn, eps, Y3, (int)rows, D, nt);
     const size_t pD = (size_t)rows * D;
     for (int64_t l = 0; l < c.layers; ++l) {
         const int64_t layer_off = l * B * NKV * m->max_seq * DH;
-        ffb_status st = gemm3(h, Y3, (int)rows, D, m->wqkv + (size_t)l * QKVR * RB->row_bytes, QKVR, false, C, nt);
+        ffb_status st = proj(D, m->wqkv + (size_t)l * QKVR * RB->row_bytes, RB->row_bytes, QKVR, false, RB->tc_d);
         if (st) return st;
         k_qkv_epilogue<<<ew, 256, 0, s>>>(C, (size_t)rows * QKVR, rope, Q, m->kcache, m->vcache, (int)rows, (int)B,
                                           NQ, NKV, DH, pos0, layer_off, m->max_seq, nt);
@@ -627,15 +727,16 @@ extern "C" ffb_status ffb_prefill(ffb_model* m, const int64_t* tokens, int64_t n
         else if (DH == 128)
             k_attention<128><<<ag, kAttnThreads, AttnSmem<128>::BYTES, s>>>(Q, m->kcache, m->vcache, Y3, ap, (int)B, NQ,
                                                                    NKV, (int)n, pos0, layer_off, m->max_seq);
-        st = gemm3(h, Y3, (int)rows, AD, m->waout + (size_t)l * D * RB->row_bytes_a, D, false, C, nt);
+        st = proj(AD, m->waout + (size_t)l * D * RB->row_bytes_a, RB->row_bytes_a, D, false, RB->tc_a);
         if (st) return st;
         k_residual_norm_split<<<(int)rows, kRowThreads, 0, s>>>(X, C, pD, m->norm_ffn + l * D, eps, Y3, (int)rows,
                                                                D, nt);
-        st = gemm3(h, Y3, (int)rows, D, m->wffn1 + (size_t)l * 2 * DI * RB->row_bytes, 2 * DI, false, C, nt);
+        st = proj(D, m->wffn1 + (size_t)l * 2 * DI * RB->row_bytes, RB->row_bytes, 2 * DI, false, RB->tc_d);
         if (st) return st;
         k_silu_split<<<ew, 256, 0, s>>>(C, (size_t)rows * 2 * DI, Y3, (int)rows, DI, nt);
         // W2: [D][DI] rows (two-phase FFN shapes) or Wffn2^T [DI][D]
-        st = gemm3(h, Y3, (int)rows, DI, m->wffn2t + (size_t)l * D * DI * 2, D, !RB->ffn2_rows, C, nt);
+        st = quant ? proj(DI, m->wffn2t + (size_t)l * DI * RB->row_bytes, RB->row_bytes, D, true, 0)
+                   : proj(DI, m->wffn2t + (size_t)l * D * DI * 2, 0, D, !RB->ffn2_rows, 0);
         if (st) return st;
         if (l + 1 < c.layers) {
             k_residual_norm_split<<<(int)rows, kRowThreads, 0, s>>>(X, C, pD, m->norm_attn + (l + 1) * D, eps, Y3,
@@ -651,7 +752,13 @@ extern "C" ffb_status ffb_prefill(ffb_model* m, const int64_t* tokens, int64_t n
         k_residual_norm_split<<<(int)B, kRowThreads, 0, s>>>(X + o, nullptr, 0, m->final_norm, eps, Y3, (int)B, D, nt);
     }
     // LM head on the last position of every batch row
-    ffb_status st = gemm3(h, Y3, (int)B, D, m->lm_head, V, false, C, nt);
+    ffb_status st;
+    {
+        const int64_t rows_all = rows;
+        rows = B;  // the LM head's rows: the last position of each batch row
+        st = proj(D, m->lm_head, RB->row_bytes, V, false, RB->tc_d);
+        rows = rows_all;
+    }
     if (st) return st;
     k_logits_part<<<dim3(kArgBlocks, (unsigned)B), 256, 0, s>>>(C, (size_t)B * V, V, part, nt);
     k_argmax_final<<<(int)B, 1, 0, s>>>(part, tok);

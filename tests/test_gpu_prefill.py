@@ -124,6 +124,27 @@ def test_prefill_two_term_split_within_reference_bound(name, batch, ctx, n):
     print(f"2-term {name} b{batch} ctx {ctx} n {n}: rel_err {e_plain:.2e}, same-KV {e_strict:.2e}, flips {flips}")
 
 
+@pytest.mark.parametrize("qb,name,batch,ctx,n", [(4, "llama31_8b-toy", 1, 0, 29), (8, "llama31_8b-toy", 1, 30, 17), (4, "llama31_8b-toy", 4, 12, 9),
+                                                 (4, "llama31_8b", 1, 500, 24), (8, "llama31_8b", 1, 0, 16)])
+def test_prefill_quantized_weights_match_oracle(qb, name, batch, ctx, n):
+    """int4 / int8 weights (quant.hpp:17-60): the packed rows are dequantised
+    into three exact bf16 planes per projection (w = (code - zero) * scale,
+    the reference's snapped weight bit for bit), so the same bounds hold as
+    for bf16; the 8B width runs the tensor-core code order of the decode
+    kernel's rows (Wqkv / Waout / Wffn1 / lm_head), the toy the plain one."""
+    cfg = O.preset(name).replace(batch=batch, quant_bits=qb)
+    if name == "llama31_8b":
+        cfg = cfg.replace(layers=2, vocab_size=4096)
+    st = O.OracleStore(cfg, 77, ctx + n + 2)
+    if ctx:
+        st.synthetic_prefill(ctx, 7)
+    with device_from_store(st) as m:
+        assert m.info()["quant_inexact_groups"] == 0
+        e_plain, e_strict, flips = _check_prefill(st, m, _prompt(n, batch, cfg.vocab_size, 13), ctx)
+        check_step(st, m, [5, 9, 11, 13][:batch], ctx + n)
+    print(f"int{qb} {name} b{batch} ctx {ctx} n {n}: rel_err {e_plain:.2e}, same-KV {e_strict:.2e}, flips {flips}")
+
+
 def test_prefill_greedy_continuation_matches_decode_as_prefill():
     """Greedy generation after a GEMM prefill equals generation after the
     reference's decode-as-prefill (the persistent kernel stepping through the
@@ -184,7 +205,7 @@ def test_prefill_validation():
         assert m.length(0) == 2
         with pytest.raises(UsageError):
             m.set_option("prefill_terms", 1)
-    cfg8 = O.preset("llama31_8b-toy").replace(batch=16)
+    cfg8 = O.preset("llama31_8b-toy").replace(batch=16)  # batch >= 8 weight layout
     st8 = O.OracleStore(cfg8, 1, 16)
     with device_from_store(st8, 16) as m8:
         with pytest.raises(UnsupportedConfigError):

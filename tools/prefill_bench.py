@@ -25,13 +25,14 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--preset", default="llama31_8b")
 ap.add_argument("--lens", default="128,512,1024")
 ap.add_argument("--batch", type=int, default=1)
+ap.add_argument("--quant", type=int, default=0, help="weight bits: 0 (bf16), 4, 8")
 ap.add_argument("--reps", type=int, default=5)
 ap.add_argument("--out", default="")
 ap.add_argument("--skip-decode", action="store_true", help="prefill only (profiling)")
 ap.add_argument("--terms", default="3,2", help="activation split terms to time (option prefill_terms)")
 a = ap.parse_args()
 
-cfg = model_preset(a.preset).replace(batch=a.batch)
+cfg = model_preset(a.preset).replace(batch=a.batch, quant_bits=a.quant)
 lens = [int(x) for x in a.lens.split(",")]
 m = DecodeModel(cfg, max(lens) + 8)
 m.init_synthetic(7)
@@ -74,7 +75,7 @@ for n in lens:
         if r:
             best_d = min(best_d, e0.elapsed_time(e1) / 1e3) if best_d == best_d else e0.elapsed_time(e1) / 1e3
     tok_rows = n * cfg.batch
-    res = {"preset": a.preset, "batch": cfg.batch, "prompt": n, "prefill_ms": round(best * 1e3, 3),
+    res = {"preset": a.preset, "quant_bits": a.quant, "batch": cfg.batch, "prompt": n, "prefill_ms": round(best * 1e3, 3),
            "prefill_tok_s": round(tok_rows / best, 1), "decode_as_prefill_ms": round(best_d * 1e3, 3),
            "decode_as_prefill_tok_s": round(tok_rows / best_d, 1), "speedup": round(best_d / best, 2),
            "terms": a.terms, **{f"prefill_ms_{k}term": round(v * 1e3, 3) for k, v in bests.items()}}

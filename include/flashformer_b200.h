@@ -275,8 +275,9 @@ ffb_status ffb_decode_loop(ffb_model *m, const int64_t *d_tokens, int64_t pos, i
  * cache and its lengths where n decode steps would (pos0 + n), so
  * ffb_decode_step continues at pos0 + n.  logits_out (batch x vocab f32,
  * host, may be NULL) / greedy_out (batch int64, host, may be NULL) are those
- * of the LAST position.  Decoders with batch < 8 on one GPU
- * (FFB_UNSUPPORTED otherwise); n * batch <= 1024 per call (longer prompts:
+ * of the LAST position.  Decoders on one GPU (batch >= 8: the fp16
+ * tensor-core weight layout is unpacked per projection; tensor-parallel
+ * shards return FFB_UNSUPPORTED); n * batch <= 1024 per call (longer prompts:
  * call again with pos0 advanced).  Synchronous. */
 ffb_status ffb_prefill(ffb_model *m, const int64_t *tokens, int64_t n, int64_t pos0,
                        float *logits_out, int64_t *greedy_out);

@@ -581,6 +581,38 @@ __global__ void k_dequant3(const uint8_t* __restrict__ w, size_t row_bytes, int 
     }
 }
 
+// batch >= 8 weights (fp16 values of the bf16 weights, K-chunked and
+// swizzled for the decode kernel's tensor-core GEMV, runtime.cu upload):
+// rows [r0, r0 + nr) -> one bf16 plane w1[row - r0][k] = bf16(fp16 value).
+// That recovers the original bf16 weight wherever the fp16 value is within
+// half a bf16 ulp of it -- every value in the fp16 normal range and all but
+// the smallest subnormals (below ~2^-17 the fp16 storage itself rounded;
+// ffb_info.fp16_inexact counts those).  layout 2: [K / KC][rows][KC], 8-column
+// units of a row segment XOR-swizzled by row & 7; layout 3 (tcgen05 build):
+// [K / KC][rows / 8][KC / 64][8 rows][64], the same swizzle inside each
+// 128-byte piece.
+__global__ void k_unpack_kc(const __half* __restrict__ w, int rows, int r0, int nr, int K, int KC, int layout,
+                            __nv_bfloat16* __restrict__ w1) {
+    const size_t plane = (size_t)nr * K, n8 = plane / 8;
+    for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < n8; e += (size_t)gridDim.x * blockDim.x) {
+        const int rr = (int)(e / (K / 8)), k0 = (int)(e % (K / 8)) * 8, r = r0 + rr;
+        const int c = k0 / KC, kk = k0 % KC;
+        size_t pos;
+        if (layout == 3) {
+            const int ka = kk / 64, u = (kk % 64) / 8;
+            pos = ((((size_t)c * (rows / 8) + r / 8) * (KC / 64) + ka) * 8 + (r & 7)) * 64 + ((u ^ (r & 7)) * 8);
+        } else {
+            pos = ((size_t)c * rows + r) * KC + (((kk / 8) ^ (r & 7)) * 8);
+        }
+        const uint4 v = *reinterpret_cast<const uint4*>(w + pos);
+        const __half* hv = reinterpret_cast<const __half*>(&v);
+        __nv_bfloat16 hi[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) hi[i] = __float2bfloat16_rn(__half2float(hv[i]));
+        *reinterpret_cast<uint4*>(w1 + (size_t)rr * K + k0) = *reinterpret_cast<const uint4*>(hi);
+    }
+}
+
 // C3[3][rows][N] (f32, row-major) = Y3[3][rows][K] . W^T: ONE GEMM over the
 // 3 * rows stacked split-term rows, so W is read once; consumers add the
 // three planes (ld3).  W bf16 row-major [N][K] (w_kn = false) or [K][N]
@@ -602,8 +634,7 @@ extern "C" ffb_status ffb_prefill(ffb_model* m, const int64_t* tokens, int64_t n
                                   int64_t* greedy) {
     if (!m || !tokens || n <= 0) return fail(FFB_USAGE, "prefill: NULL argument or n <= 0");
     const auto& c = m->cfg;
-    if (c.kind != 0 || m->ops->kc != 0 || m->tp_size != 1)
-        return fail(FFB_UNSUPPORTED, "prefill: decoder with batch < 8 on one GPU");
+    if (c.kind != 0 || m->tp_size != 1) return fail(FFB_UNSUPPORTED, "prefill: decoder on one GPU");
     if (!cublas()) return fail(FFB_UNSUPPORTED, "prefill: cuBLAS not available (dlopen libcublas.so.12)");
     for (int64_t l = 0; l < c.layers; ++l)
         if (m->kv_len[l] != pos0)
@@ -630,13 +661,13 @@ extern "C" ffb_status ffb_prefill(ffb_model* m, const int64_t* tokens, int64_t n
     // planes), the RoPE table, token ids, argmax candidates
     const int Kmax = std::max({D, AD, DI});
     const size_t Cn = 3 * std::max<size_t>((size_t)rows * std::max({QKVR, 2 * DI, D}), (size_t)B * V);
-    const bool quant = m->ops->QB != 0;
+    const bool quant = m->ops->QB != 0, kcp = m->ops->kc != 0;
     // quantized weights: a chunk of kQChunk rows dequantised into three bf16
     // planes (W3) per projection
-    const size_t w3n = quant ? 3 * std::max<size_t>((size_t)std::min(kQChunk, std::max({QKVR, 2 * DI, D, V})) *
+    const size_t w3n = quant || kcp ? 3 * std::max<size_t>((size_t)std::min(kQChunk, std::max({QKVR, 2 * DI, D, V})) *
                                                         std::max(D, AD),
                                                     (size_t)DI * D)
-                             : 0;
+                                    : 0;
     size_t need = 0;
     auto carve = [&](size_t bytes) {  // 256-byte aligned sub-buffers
         const size_t at = need;
@@ -684,17 +715,23 @@ extern "C" ffb_status ffb_prefill(ffb_model* m, const int64_t* tokens, int64_t n
     const int nt = at;                       // planes of a projection's output the consumers add
     // one projection: Y3 (rows x K activations, split) . W^T -> C
     auto proj = [&](int K, const uint8_t* W, size_t row_bytes, int N, bool kn, int tc) -> ffb_status {
-        if (!quant) return gemm3(h, Y3, (int)rows, K, W, N, kn, C, at);
+        if (!quant && !kcp) return gemm3(h, Y3, (int)rows, K, W, N, kn, C, at);
         const float one = 1.f, zero = 0.f;
+        const int wpl = quant ? 3 : 1;  // bf16 planes of the stored weight
         for (int n0 = 0; n0 < N; n0 += kn ? N : kQChunk) {
             const int nc = kn ? N : std::min(kQChunk, N - n0);
             // kn (Wffn2^T): the packed rows are the GEMM's K, their columns N
-            if (kn) k_dequant3<<<4 * m->grid, 256, 0, s>>>(W, row_bytes, 0, K, N, RB->QB, tc, W3);
-            else k_dequant3<<<4 * m->grid, 256, 0, s>>>(W, row_bytes, n0, nc, K, RB->QB, tc, W3);
+            if (kcp)
+                k_unpack_kc<<<4 * m->grid, 256, 0, s>>>(reinterpret_cast<const __half*>(W), N, n0, nc, K, RB->kc,
+                                                        RB->kc_layout, W3);
+            else if (kn)
+                k_dequant3<<<4 * m->grid, 256, 0, s>>>(W, row_bytes, 0, K, N, RB->QB, tc, W3);
+            else
+                k_dequant3<<<4 * m->grid, 256, 0, s>>>(W, row_bytes, n0, nc, K, RB->QB, tc, W3);
             // weight plane pw against activation terms a < at - pw, summed
             // into the activation-term planes of C (beta = 1 after plane 0):
             // C[a] = W_hi y_a + W_mid y_a + W_lo y_a over the significant pairs
-            for (int pw = 0; pw < 3 && pw < at; ++pw) {
+            for (int pw = 0; pw < wpl && pw < at; ++pw) {
                 const int na = at - pw;
                 const __nv_bfloat16* A = W3 + (size_t)pw * nc * K;
                 // C planes [a][rows][N] are the rows a * rows + r of one

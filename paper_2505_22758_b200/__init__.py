@@ -180,15 +180,15 @@ def pack_quant_rows(values: np.ndarray, quant_bits: int, layout: int = 0) -> tup
 def tc_code_positions(quant_bits: int) -> np.ndarray:
     """Column i of a 128-column group -> nibble (int4) / byte (int8)
     position in the tensor-core code order (runtime.cu: tc_nibble_index,
-    tc_byte_index; decode_kernel.cuh: tc_slot)."""
+    tc_byte_index; decode_kernel.cuh: tc_slot, the mma.sync m16n8k32 u8 A
+    fragments): lane quad q of k32-step s owns columns 32s + 4q + j (low
+    nibbles / first 4 bytes) and 32s + 16 + 4q + j (high nibbles / last 4)."""
     i = np.arange(128)
-    s, r = i // 16, i % 16
-    q, hi, plus8 = (r % 8) // 2, r % 2, (r >= 8).astype(int)
+    s, r = i // 32, i % 32
+    half, q, j = r // 16, (r % 16) // 4, r % 4
     if quant_bits == 4:
-        t, u = s // 2, s % 2
-        bit = hi * 16 + plus8 * 4 + u * 8
-        return (q * 4 + t) * 8 + bit // 4
-    return q * 32 + s * 4 + plus8 * 2 + hi
+        return q * 32 + s * 8 + 2 * j + half
+    return q * 32 + s * 8 + half * 4 + j
 
 
 def unpack_quant_rows(packed: np.ndarray, cols: int, quant_bits: int,

@@ -393,6 +393,27 @@ def run_ours(args):
         torch.cuda.synchronize(dev)
         variants["decode_loop_ms_per_token"] = round(
             max_over_ranks(g0.elapsed_time(g1) / (k * n_gen)) / cfg.batch, 5)
+        if tp == 1:
+            # prompt ingestion as GEMMs (ffb_prefill): a 512-token
+            # prompt (per batch row) ending at the bench context, host wall
+            # clock around the synchronous call (prompt copy and last logits
+            # included), best of 3 after one warm-up
+            import time as _time
+            n_pf = min(512, 1024 // cfg.batch, ctx)
+            prompt = np.random.default_rng(3).integers(0, cfg.vocab_size, size=(n_pf, cfg.batch))
+            best = float("inf")
+            for r in range(4):
+                for l in range(cfg.layers):
+                    m.set_length(l, ctx - n_pf)
+                t0 = _time.perf_counter()
+                m.prefill(prompt, ctx - n_pf, logits=False)
+                if r:
+                    best = min(best, _time.perf_counter() - t0)
+            variants["prefill_prompt_tokens"] = int(n_pf * cfg.batch)
+            variants["prefill_ms"] = round(best * 1e3, 3)
+            variants["prefill_tokens_per_s"] = round(n_pf * cfg.batch / best, 1)
+            for l in range(cfg.layers):
+                m.set_length(l, ctx)
 
     algo = algorithmic_bytes(cfg, ctx)
     peak, peak_kind = measured_peak()

@@ -1,6 +1,7 @@
 """Batch 8 / 16 (config E lists batch 16): every projection on tensor cores,
 streamed in K chunks (decode_kernel.cuh: Shape::KCP, gemv_kc), the FFN in two
-phases, activations as bf16 hi/lo MMA A-fragment tables.  Same bars as the
+phases, the weights as fp16 (the bf16 values; exact in the fp16 normal
+range) and the activations as fp16 hi/lo MMA A-fragment tables.  Same bars as the
 batch 1-4 parity suite (tests/test_gpu_parity.py): with the device's K/V rows
 fed to the oracle rel_err < 2e-5, without that hook the reference's 1e-4
 whenever no bf16 rounding flip occurred; all run modes bit-identical."""

@@ -278,7 +278,10 @@ ffb_status ffb_decode_loop(ffb_model *m, const int64_t *d_tokens, int64_t pos, i
  * of the LAST position.  Decoders on one GPU (batch >= 8: the fp16
  * tensor-core weight layout is unpacked per projection; tensor-parallel
  * shards return FFB_UNSUPPORTED); n * batch <= 1024 per call (longer prompts:
- * call again with pos0 advanced).  Synchronous. */
+ * call again with pos0 advanced).  Synchronous; the scratch (activations,
+ * split planes, expanded weight chunks: ~1-2 GB at the 8B shape and 1024
+ * rows) is allocated on first use, grown as needed and freed with the
+ * handle; cuBLAS is loaded at run time (libcublas.so.12). */
 ffb_status ffb_prefill(ffb_model *m, const int64_t *tokens, int64_t n, int64_t pos0,
                        float *logits_out, int64_t *greedy_out);
 

@@ -1001,11 +1001,12 @@ struct DecodeCta {
                 }
             }
         }
-        float inv[B];
-#pragma unroll
-        for (int b = 0; b < B; ++b) inv[b] = 1.f;
-        if (gain != nullptr) {  // RMSNorm statistics over the whole row, numerics.hpp:14-24
-            float* ns = norm_s();
+        // RMSNorm statistics over the whole row (numerics.hpp:14-24): the
+        // warp partials go to smem now, the row's 1/rms is formed after the
+        // table barrier below -- the int8 terms of gain * x do not depend on
+        // it (the block scale absorbs it: dq = inv * max|gain * x| / 127)
+        float* ns = norm_s();
+        if (gain != nullptr) {
 #pragma unroll
             for (int b = 0; b < B; ++b) {
                 float sq = 0.f;
@@ -1014,14 +1015,6 @@ struct DecodeCta {
                 sq = warp_sum(sq);
                 if (lane == 0) ns[warp * B + b] = sq;
             }
-            consumer_sync(NCT);
-#pragma unroll
-            for (int b = 0; b < B; ++b) {
-                float t = 0.f;
-                for (int w = 0; w < NCW; ++w) t += ns[w * B + b];
-                inv[b] = 1.0f / sqrtf(t / static_cast<float>(M::K) + p.eps);
-            }
-            consumer_sync(NCT);  // ns reusable afterwards
         }
         // MMA B fragments (m16n8k32 "col", s8, batch 1): each 128-column
         // group of activations as three int8 terms of one block scale,
@@ -1040,7 +1033,7 @@ struct DecodeCta {
         float mx = 0.f;
 #pragma unroll
         for (int c = 0; c < PL; ++c) {
-            x[c] = gain ? gl[c] * v[0][c] * inv[0] : v[0][c];
+            x[c] = gain ? gl[c] * v[0][c] : v[0][c];
             mx = fmaxf(mx, fabsf(x[c]));
         }
 #pragma unroll
@@ -1097,7 +1090,13 @@ struct DecodeCta {
         if (lane % LPG == 0)
             ginfo[warp * (M::KW / kQuantGroup) + lane / LPG] =
                 make_float2(mx / 127.f, s0 + s1 * (1.f / 254.f) + s2 * (1.f / 64516.f));
-        consumer_sync(NCT);  // tables complete before any warp's first MMA
+        consumer_sync(NCT);  // tables (and the norm partials) complete before any warp's first MMA
+        act.sum[0] = 1.f;  // the row's 1/rms (1 without a gain): scales every group's dq in tc_slot
+        if (gain != nullptr) {
+            float t = 0.f;
+            for (int w = 0; w < NCW; ++w) t += ns[w * B];
+            act.sum[0] = 1.0f / sqrtf(t / static_cast<float>(M::K) + p.eps);
+        }
     }
 
     // per-group (dq, zero-point sum) of the TC activation tables
@@ -1149,7 +1148,7 @@ struct DecodeCta {
     // zero point folded through the group's activation sum.  out[0] / out[2]
     // = rows g / g + 8 (lanes q == 0), out[1] = out[3] = 0.
     template <class M>
-    __device__ __forceinline__ void tc_slot(const uint8_t* base, float (&out)[4]) {
+    __device__ __forceinline__ void tc_slot(const uint8_t* base, float inv, float (&out)[4]) {
         const int ctid = threadIdx.x, warp = ctid / 32, lane = ctid % 32, g = lane / 4, q = lane % 4;
         const uint32_t* tab = reinterpret_cast<const uint32_t*>(wpart()) + warp * M::KW;
         const float2* ginfo = tc_ginfo<M>() + warp * (M::KW / kQuantGroup);
@@ -1190,15 +1189,16 @@ struct DecodeCta {
             const int t2A = __shfl_down_sync(0xffffffffu, acc[0], 1);
             const int t2B = __shfl_down_sync(0xffffffffu, acc[2], 1);
             const float2 gf = ginfo[gi];
+            const float dq = gf.x * inv;
             const float xA = fmaf(static_cast<float>(t2A), 1.f / 64516.f,
                                   fmaf(static_cast<float>(acc[1]), 1.f / 254.f, static_cast<float>(acc[0])));
-            out[0] = fmaf(sA * gf.x, fmaf(-zA, gf.y, xA), out[0]);
+            out[0] = fmaf(sA * dq, fmaf(-zA, gf.y, xA), out[0]);
             if constexpr (M::QB == 4) {
                 const float sB = *reinterpret_cast<const float*>(rB + M::CODE_BYTES + 4 * G);
                 const float zB = static_cast<float>(rB[M::CODE_BYTES + 4 * M::NG + G]);
                 const float xB = fmaf(static_cast<float>(t2B), 1.f / 64516.f,
                                       fmaf(static_cast<float>(acc[3]), 1.f / 254.f, static_cast<float>(acc[2])));
-                out[2] = fmaf(sB * gf.x, fmaf(-zB, gf.y, xB), out[2]);
+                out[2] = fmaf(sB * dq, fmaf(-zB, gf.y, xB), out[2]);
             } else {
                 (void)t2B;
             }
@@ -1425,7 +1425,7 @@ struct DecodeCta {
             const uint32_t slot = it % T::NSLOTS, par = (it / T::NSLOTS) & 1;
             wait_full(slot, par);
             float c[4];
-            tc_slot<M>(ring + slot * T::SLOT_BYTES, c);
+            tc_slot<M>(ring + slot * T::SLOT_BYTES, act.sum[0], c);
             __syncwarp();
             if (lane == 0) mbar_arrive(&empty[slot]);
             ++it;

@@ -331,7 +331,9 @@ ffb_status ffb_calibrate(ffb_model *m, int32_t iterations);
 /* Current per-SM plan weights (mean 1); returns the count (grid) or -1. */
 int64_t ffb_get_plan_weights(const ffb_model *m, double *out, int64_t n);
 
-/* Device pointer to the most recent logits (batch x vocab f32). */
+/* Device pointer to the most recent logits (batch x vocab f32) of
+ * ffb_decode_step_device / ffb_decode_loop (ffb_decode_step with host logits
+ * writes them straight into pinned host memory instead). */
 const float *ffb_logits_device(const ffb_model *m);
 
 #ifdef __cplusplus

@@ -1554,11 +1554,24 @@ ffb_status ffb_decode_step(ffb_model* m, const int64_t* tokens, int64_t pos, flo
     std::memcpy(m->tokens_pinned, tokens, sizeof(int64_t) * c.batch);
     CUDA_TRY(cudaMemcpyAsync(m->tokens_dev, m->tokens_pinned, sizeof(int64_t) * c.batch,
                              cudaMemcpyHostToDevice, s));
-    st = launch_step(m, pos, m->tokens_dev, nullptr, nullptr, s);
-    if (st) return st;
+    // logits straight into pinned host memory (the caller's buffer when it is
+    // pinned, else the handle's staging buffer): the LM head's stores cross
+    // PCIe while the stage still streams, instead of a D2H copy after the
+    // kernel (zero-copy; the device logits buffer is then not written)
     const size_t lbytes = sizeof(float) * c.batch * c.vocab_size;
     const bool direct = logits_out && pinned(logits_out);
-    if (logits_out)
+    float* d_logits = nullptr;
+    if (logits_out) {
+        void* dp = nullptr;
+        if (cudaHostGetDevicePointer(&dp, direct ? static_cast<void*>(logits_out) : m->logits_pinned, 0) ==
+            cudaSuccess)
+            d_logits = static_cast<float*>(dp);
+        else
+            cudaGetLastError();  // not mapped: copy after the kernel below
+    }
+    st = launch_step(m, pos, m->tokens_dev, d_logits, nullptr, s);
+    if (st) return st;
+    if (logits_out && !d_logits)
         CUDA_TRY(cudaMemcpyAsync(direct ? logits_out : m->logits_pinned, m->logits, lbytes,
                                  cudaMemcpyDeviceToHost, s));
     // greedy ids and the device error latch behind them in one copy

@@ -613,22 +613,33 @@ class DecodeModel:
                                      1 if teacher_forced else 0, C.c_void_p(d_out),
                                      C.c_void_p(stream or None)))
 
-    def generate(self, tokens, pos: int, n_steps: int, prompt=None) -> np.ndarray:
+    def generate(self, tokens, pos: int, n_steps: int, prompt=None, use_prefill: bool = False) -> np.ndarray:
         """Greedy generation on the device (decode_loop): returns the n_steps
         produced tokens int64 [n_steps][batch].  With `prompt` ([n][batch],
-        teacher-forced from `pos`), token 0 is the prediction after the
-        prompt; otherwise `tokens` ([batch]) is consumed at `pos` first.  The
-        cache ends holding every consumed token."""
+        from `pos`), token 0 is the prediction after the prompt -- ingested
+        teacher-forced through the decode loop (the reference's
+        decode-as-prefill), or with `use_prefill` through ffb_prefill's GEMMs;
+        otherwise `tokens` ([batch]) is consumed at `pos` first.  The cache
+        ends holding every consumed token."""
         import torch
         dev = f"cuda:{self.device}"
         B = self.cfg.batch
         stream = torch.cuda.Stream(device=self.device)  # (0 would mean the handle's own stream)
         with torch.cuda.stream(stream):
-            return self._generate(torch, dev, B, stream.cuda_stream, tokens, pos, n_steps, prompt)
+            return self._generate(torch, dev, B, stream.cuda_stream, tokens, pos, n_steps, prompt,
+                                  use_prefill)
 
-    def _generate(self, torch, dev, B, st, tokens, pos, n_steps, prompt):
+    def _generate(self, torch, dev, B, st, tokens, pos, n_steps, prompt, use_prefill=False):
         out = torch.empty((n_steps, B), dtype=torch.int64, device=dev)
-        if prompt is not None:
+        if prompt is not None and use_prefill:
+            pr = np.asarray(prompt, np.int64).reshape(-1, B)
+            _, g = self.prefill(pr, pos, logits=False)
+            out[0] = torch.as_tensor(g, device=dev)
+            if n_steps > 1:
+                torch.cuda.current_stream().synchronize()
+                self.decode_loop(out[0].data_ptr(), pos + pr.shape[0], n_steps - 1,
+                                 out[1:].data_ptr(), False, st)
+        elif prompt is not None:
             pr = torch.as_tensor(np.asarray(prompt, np.int64).reshape(-1, B), device=dev)
             po = torch.empty_like(pr)
             self.decode_loop(pr.data_ptr(), pos, pr.shape[0], po.data_ptr(), True, st)

@@ -168,6 +168,21 @@ def test_prefill_batch8_16_tensor_core_layout_matches_oracle(name, batch, ctx, n
     print(f"b{batch} {name} ctx {ctx} n {n}: rel_err {e_plain:.2e}, same-KV {e_strict:.2e}, flips {flips}")
 
 
+def test_generate_with_prefill_matches_decode_loop_generation():
+    """DecodeModel.generate(prompt=..., use_prefill=True): the prompt through
+    ffb_prefill, then the device-resident decode loop -- the same tokens as
+    the all-decode-loop generation on the tiny model."""
+    cfg = O.preset("tiny").replace(layers=2)
+    prompt = O.tiny_prompt(20, cfg.vocab_size)
+    gens = []
+    for use_prefill in (True, False):
+        st = O.OracleStore(cfg, 42, 64)
+        with device_from_store(st, 64) as m:
+            gens.append([int(t) for t in m.generate(None, 0, 10, prompt=prompt, use_prefill=use_prefill)[:, 0]])
+            assert m.length(0) == len(prompt) + 9
+    assert gens[0] == gens[1], gens
+
+
 def test_prefill_greedy_continuation_matches_decode_as_prefill():
     """Greedy generation after a GEMM prefill equals generation after the
     reference's decode-as-prefill (the persistent kernel stepping through the

@@ -15,8 +15,15 @@ import oracle as O
 from gpu_helpers import device_from_store, rel_err
 from paper_2505_22758_b200 import RunMode
 
+# optional: QB to run the 8B-width int4 / int8 shape (1 layer) -- the
+# integer-MMA tensor-core GEMV (decode_kernel.cuh tc_slot) only exists there
+QB = int(sys.argv[1]) if len(sys.argv) > 1 else 0
 cfg = O.preset("llama31_8b-toy")
-for mode in (RunMode.FUSED_OVERLAP, RunMode.FUSED, RunMode.BASELINE):
+modes = (RunMode.FUSED_OVERLAP, RunMode.FUSED, RunMode.BASELINE)
+if QB:
+    cfg = O.preset("llama31_8b").replace(layers=1, vocab_size=4096, quant_bits=QB)
+    modes = (RunMode.FUSED_OVERLAP,)
+for mode in modes:
     st = O.OracleStore(cfg, 42, 40)
     st.synthetic_prefill(9, 7)
     with device_from_store(st) as m:

@@ -278,12 +278,15 @@ ffb_status build_plan(ffb_model* m) {
     m->n_units = static_cast<int>(c.batch * c.n_kv_heads);
     if (m->n_units > G) return fail(FFB_UNSUPPORTED, "batch * n_kv_heads exceeds the SM count");
     // split-K group per (batch row, kv head): as many SMs as fit, at most
-    // kMaxGroup so the last-arriver combine keeps every load in flight, and
-    // no more than give each member ~64 KiB of the cache's K/V (256 positions
-    // at d_head 64, 128 at 128): below that the combine outweighs the split
-    // (same box, 1B at 1k context: 18 CTAs 0.652, 5 CTAs 0.630 ms; 8B / 1B
-    // at 4k keep 18, the SM bound)
-    const int64_t kv_group = std::max<int64_t>(1, (m->max_seq * c.d_head + 16383) / 16384);
+    // kMaxGroup so the last-arriver combine keeps every load in flight, and,
+    // for d_head 64 (1B-class shapes), no more than give each member ~64 KiB
+    // of the cache's K/V (256 positions): below that the combine outweighs
+    // the split (same box, 1B at 1k context: 18 CTAs 0.652, 5 CTAs 0.630 ms;
+    // at 4k the SM bound, 18, stays).  d_head 128 shapes keep the SM bound:
+    // their 4k-context optimum, and the group size fixes the summation order
+    // the full-depth greedy-identity tests were pinned with.
+    const int64_t kv_group = c.d_head <= 64 ? std::max<int64_t>(1, (m->max_seq * c.d_head + 16383) / 16384)
+                                            : kMaxGroup;
     m->attn_group = static_cast<int>(std::min<int64_t>({G / m->n_units, kMaxGroup, kv_group}));
     if (m->attn_group_max > 0) m->attn_group = std::min(m->attn_group, m->attn_group_max);
     std::vector<CtaPlan> plan(G);

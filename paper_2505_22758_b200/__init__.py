@@ -339,8 +339,8 @@ def lib():
     L.ffb_set_trace.argtypes = [C.c_void_p, C.c_int]
     L.ffb_get_trace.argtypes = [C.c_void_p, C.POINTER(C.c_uint64), C.c_int64]
     L.ffb_get_trace.restype = C.c_int64
-    L.ffb_decode_step.argtypes = [C.c_void_p, P(C.c_int64), C.c_int64, P(C.c_float),
-                                  P(C.c_int64), C.c_void_p]
+    # (raw addresses: the per-token host path avoids ctypes pointer objects)
+    L.ffb_decode_step.argtypes = [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p]
     L.ffb_decode_step_device.argtypes = [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p,
                                          C.c_void_p, C.c_void_p]
     L.ffb_get_info.argtypes = [C.c_void_p, P(_Info)]
@@ -556,12 +556,17 @@ class DecodeModel:
             raise ValidationError("execute_program: one token per batch row required")
         if out is None and logits:  # a TP rank returns its vocabulary slice
             out = np.empty((c.batch, c.vocab_size // self.tp_size), np.float32)
+        elif out is not None:
+            if (out.dtype != np.float32 or not out.flags.c_contiguous
+                    or out.size != c.batch * (c.vocab_size // self.tp_size)):
+                raise UsageError("step: out must be C-contiguous f32 [batch][vocab]")
         if greedy is None:
             greedy = np.empty(c.batch, np.int64)
-        _check(lib().ffb_decode_step(self._h, tok.ctypes.data_as(C.POINTER(C.c_int64)), pos,
-                                     _fp(out) if out is not None else None,
-                                     greedy.ctypes.data_as(C.POINTER(C.c_int64)),
-                                     C.c_void_p(stream or None)))
+        elif greedy.dtype != np.int64 or not greedy.flags.c_contiguous or greedy.size != c.batch:
+            raise UsageError("step: greedy must be C-contiguous int64 [batch]")
+        addr = lambda a: a.__array_interface__["data"][0]  # noqa: E731
+        _check(lib().ffb_decode_step(self._h, addr(tok), pos, addr(out) if out is not None else None,
+                                     addr(greedy), stream or None))
         return out, greedy
 
     def forward(self, tokens, pos: int) -> np.ndarray:

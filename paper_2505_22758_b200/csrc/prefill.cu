@@ -10,17 +10,22 @@
 // cache lengths end exactly where n decode steps would leave them, so decoding
 // continues with the persistent kernel at pos0 + n.
 //
-// Numerics.  The bf16 weights are exact in bf16; every GEMM input activation
-// (f32) is split into three bf16 terms (hi + mid + lo carry 24 bits, the
-// f32 mantissa) and the GEMM runs three bf16 x bf16 products accumulated in
-// f32 (cublasGemmEx, CUBLAS_COMPUTE_32F) -- f32-accurate products on the
-// bf16 tensor cores.  Attention and everything elementwise is f32 (the
-// online softmax in f32, like the decode kernel); K/V are rounded to bf16 at
-// append, as reference.hpp / KVCache::append do.
+// Numerics.  Every GEMM input activation (f32) is split into three bf16
+// terms (hi + mid + lo carry 24 bits, the f32 mantissa; option
+// "prefill_terms" = 2 keeps hi + lo) and ONE GEMM over the stacked terms runs
+// the bf16 x bf16 products with f32 accumulation (cublasGemmEx,
+// CUBLAS_COMPUTE_32F) -- f32-accurate products on the bf16 tensor cores; the
+// consumers add the term planes.  The weights enter exactly: bf16 as stored;
+// int4 / int8 expanded per projection into three bf16 planes of
+// (code - zero) * scale (k_dequant3; three accumulated GEMMs); batch >= 8
+// unpacked from the decode kernel's fp16 tensor-core layouts (k_unpack_kc).
+// Attention (mma.sync, q and P as bf16 hi + lo like the decode kernel's) and
+// everything elementwise is f32; K/V are rounded to bf16 at append, as
+// reference.hpp / KVCache::append do.
 //
 // cuBLAS is loaded at run time (dlopen "libcublas.so.12"): plain library
-// GEMMs only, the decode path never touches it.  bf16 weights in the
-// row-major layout only (batch < 8, no quantisation, one GPU).
+// GEMMs only, the decode path never touches it.  One GPU (tensor-parallel
+// shards return FFB_UNSUPPORTED).
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <dlfcn.h>

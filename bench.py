@@ -277,9 +277,25 @@ def run_ours(args):
             "baseline": RunMode.BASELINE}[args.mode]
     m = DecodeModel(cfg, ctx + 8, device=dev, mode=mode, tp_rank=rank if tp > 1 else 0,
                     tp_size=tp, grid=grid)
-    if tp > 1:  # wire the TP group: all-gather every rank's exchange-buffer blob
+    # the in-kernel exchange stores into peer GPUs' memory (NVLink P2P); a box
+    # without P2P between the group's GPUs runs the host-NCCL multi-kernel
+    # TP path instead (RunMode.BASELINE_NCCL), flagged in the line
+    p2p_ok = share or tp == 1 or all(torch.cuda.can_device_access_peer(dev, j)
+                                     for j in range(min(world, n_dev)) if j != dev)
+    if tp > 1 and world > 1:
+        import torch.distributed as dist
+        flag = torch.tensor([1 if p2p_ok else 0], dtype=torch.int32,
+                            device="cpu" if share else f"cuda:{dev}")
+        dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+        p2p_ok = bool(flag.item())
+    if tp > 1 and p2p_ok:  # wire the TP group: all-gather every rank's exchange-buffer blob
         from paper_2505_22758_b200 import all_gather_tp_blobs
         m.tp_connect(all_gather_tp_blobs(m.tp_blob()))
+    elif tp > 1:
+        from paper_2505_22758_b200 import broadcast_nccl_id
+        m.tp_nccl_init(broadcast_nccl_id())
+        mode = RunMode.BASELINE_NCCL
+        m.set_mode(mode)
     m.init_synthetic(1234)
     if args.calibrate and tp == 1 and not share:  # per-SM load balance (setup, outside the timed region)
         for l in range(cfg.layers):
@@ -357,13 +373,16 @@ def run_ours(args):
     if not args.no_variants:
         for name, rm in (("baseline", RunMode.BASELINE), ("fused", RunMode.FUSED),
                          ("fused_overlap", RunMode.FUSED_OVERLAP)):
+            if tp > 1 and not p2p_ok:  # these exchange in-kernel over peer memory
+                break
             k = max(10, args.steps // 4)
             variants[name + "_ms_per_step"] = round(max_over_ranks(timed(rm, k)), 5)
         if tp > 1 and not share and torch.cuda.device_count() >= tp:
+            if p2p_ok:  # (else already initialised as the main mode)
+                from paper_2505_22758_b200 import broadcast_nccl_id
+                m.tp_nccl_init(broadcast_nccl_id())
             # the host-NCCL multi-kernel baseline: the same
             # per-stage launches, residual sums as ncclAllReduce between them
-            from paper_2505_22758_b200 import broadcast_nccl_id
-            m.tp_nccl_init(broadcast_nccl_id())
             k = max(10, args.steps // 4)
             variants["baseline_nccl_ms_per_step"] = round(
                 max_over_ranks(timed(RunMode.BASELINE_NCCL, k)), 5)
@@ -437,6 +456,8 @@ def run_ours(args):
             "ms_per_step": round(ms, 5), "higher_is_better": False,
             "scaling": "strong" if tp > 1 else "weak", "vs_baseline": None,
             "n_ranks_tp": tp,
+            **({"tp_exchange": "in-kernel over NVLink peer memory" if p2p_ok
+                else "host NCCL between per-stage launches (no P2P between the GPUs)"} if tp > 1 else {}),
             **({"shared_gpu": f"{world} ranks on {n_dev} GPU(s): functional check, not a "
                               f"per-GPU timing"} if share else {}),
             "dtype": f"int{args.quant} weights, f32 math" if args.quant else "bf16",

@@ -22,6 +22,7 @@ ap.add_argument("--reverse", action="store_true", help="plan_reverse option")
 ap.add_argument("--calibrate", type=int, default=0, help="ffb_calibrate iterations first")
 ap.add_argument("--mask", type=lambda v: int(v, 0), default=0x1f, help="stage_mask (component ablation)")
 ap.add_argument("--vocab", type=int, default=0, help="vocabulary rows (0: the preset's)")
+ap.add_argument("--opt", action="append", default=[], help="ffb_set_option key=value (repeatable)")
 a = ap.parse_args()
 cfg = model_preset(a.model).replace(batch=a.batch, quant_bits=a.quant)
 if a.vocab:
@@ -31,6 +32,9 @@ m = DecodeModel(cfg, a.ctx + 8, mode={"fused_overlap": RunMode.FUSED_OVERLAP, "f
 m.init_synthetic(1)
 if a.mask != 0x1f:
     m.set_option("stage_mask", a.mask)
+for kv in a.opt:
+    k, v = kv.split("=")
+    m.set_option(k, int(v, 0))
 if a.reverse:
     m.set_option("plan_reverse", 1)
 if a.calibrate:
@@ -91,6 +95,18 @@ for s_name, s_idx in (("qkv", 0), ("aout", 2)):
     o = np.argsort(-dr.mean(1))
     print(f"{s_name}: done spread {np.mean(dr.max(0)):.2f} us; slowest ctas {list(o[:6])}; "
           f"corr(done, cta)={np.corrcoef(dr.mean(1), np.arange(len(sm)))[0,1]:.2f}")
+if os.environ.get("QKV_CTAS"):  # per-CTA QKV timeline of the slowest / a typical CTA
+    ss = [s for s in range(S - 1) if s % 5 == 0]
+    base = np.stack([tr[:, s, 1].astype(np.int64) for s in ss], 1)
+    base = base - base.min(0, keepdims=True)
+    for c in list(np.argsort(-np.stack([tr[:, s, 2] - tr[:, s, 2].min() for s in ss], 1).mean(1))[:6]) + [10, 60]:
+        ent = np.mean([(tr[c, s, 0] - tr[:, s, 1].min()) / 1e3 for s in ss])
+        met = np.mean([(tr[c, s, 1] - tr[:, s, 1].min()) / 1e3 for s in ss])
+        mk = np.mean([(tr[c, s, 3] - tr[:, s, 1].min()) / 1e3 for s in ss])
+        dn = np.mean([(tr[c, s, 2] - tr[:, s, 1].min()) / 1e3 for s in ss])
+        stv = np.mean([tr[c, s, 4] / 1e3 for s in ss])
+        print(f"  qkv cta {c:3d} sm {int(tr[c, S - 1, 6]):3d} unit {'attn' if c < 144 else 'idle'}: entry {ent:6.2f} met {met:6.2f} mark {mk:6.2f} done {dn:6.2f} starve {stv:5.2f} us "
+              f"(rel. to the first CTA's dependency met)")
 # attention breakdown (slots 5: q staged, 6: ring slots ready, 3: pass done,
 # 7: partial written; 2: combine done, last arriver only)
 att = [s for s in range(S - 1) if s % 5 == 1]

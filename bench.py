@@ -456,7 +456,8 @@ def run_ours(args):
             "ms_per_step": round(ms, 5), "higher_is_better": False,
             "scaling": "strong" if tp > 1 else "weak", "vs_baseline": None,
             "n_ranks_tp": tp,
-            **({"tp_exchange": "in-kernel over NVLink peer memory" if p2p_ok
+            **({"tp_exchange": ("in-kernel over CUDA-IPC memory on the shared GPU" if share
+                                else "in-kernel over NVLink peer memory") if p2p_ok
                 else "host NCCL between per-stage launches (no P2P between the GPUs)"} if tp > 1 else {}),
             **({"shared_gpu": f"{world} ranks on {n_dev} GPU(s): functional check, not a "
                               f"per-GPU timing"} if share else {}),

@@ -558,11 +558,11 @@ class DecodeModel:
             out = np.empty((c.batch, c.vocab_size // self.tp_size), np.float32)
         elif out is not None:
             if (out.dtype != np.float32 or not out.flags.c_contiguous
-                    or out.size != c.batch * (c.vocab_size // self.tp_size)):
-                raise UsageError("step: out must be C-contiguous f32 [batch][vocab]")
+                    or out.size < c.batch * (c.vocab_size // self.tp_size)):
+                raise UsageError("step: out must be C-contiguous f32 with room for [batch][vocab / tp]")
         if greedy is None:
             greedy = np.empty(c.batch, np.int64)
-        elif greedy.dtype != np.int64 or not greedy.flags.c_contiguous or greedy.size != c.batch:
+        elif greedy.dtype != np.int64 or not greedy.flags.c_contiguous or greedy.size < c.batch:
             raise UsageError("step: greedy must be C-contiguous int64 [batch]")
         addr = lambda a: a.__array_interface__["data"][0]  # noqa: E731
         _check(lib().ffb_decode_step(self._h, addr(tok), pos, addr(out) if out is not None else None,

@@ -78,3 +78,21 @@ def test_tp2_two_processes_cuda_ipc_matches_oracle(mps_env):
         assert int(res[0]["greedy"][i]) == int(np.argmax(want)), i
     print(f"TP2 across two processes (CUDA IPC, MPS): {N_STEPS} greedy steps identical, "
           f"max rel_err {worst:.2e}")
+
+
+def test_bench_two_ranks_tp2_under_mps(mps_env):
+    """bench.py's N > 1 contract (torchrun, one process per rank, the TP-2
+    sharded model, max over ranks) on a one-GPU box: both ranks on the GPU
+    under MPS; checks the JSON line, not the timing."""
+    env, d = mps_env
+    root = os.path.dirname(HERE)
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+                        "--master-addr", "127.0.0.1", "--master-port", "29533", "bench.py", "--gpus", "2",
+                        "--model", "tiny", "--ctx", "192", "--steps", "5", "--warmup", "3", "--no-cpu-baseline"],
+                       cwd=root, env=env, capture_output=True, text=True, timeout=600)
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert r.returncode == 0 and lines, r.stdout[-2000:] + r.stderr[-2000:]
+    import json
+    line = json.loads(lines[-1])
+    assert line["n_gpus"] == 2 and line["n_ranks_tp"] == 2 and line["value"] > 0
+    assert line["config"]["parallelism"] == "tp2" and "shared_gpu" in line

@@ -89,9 +89,10 @@ def measured_peak():
         return 6650.0, "fallback"
 
 
-def ncu_traffic(model: str, batch: int, ctx: int):
+def ncu_traffic(model: str, batch: int, ctx: int, quant: int = 0):
     """dram bytes per launch of the decode kernel from the committed ncu
-    --set full summary (profiles/), or None."""
+    --set full summary (profiles/) of the same model / batch / context /
+    weight format, or None."""
     import glob
     best = None
     for p in sorted(glob.glob(os.path.join(ROOT, "profiles", "ncu_*.json"))):
@@ -99,7 +100,8 @@ def ncu_traffic(model: str, batch: int, ctx: int):
             d = json.load(open(p))
         except Exception:
             continue
-        if d.get("model") == model and d.get("batch") == batch and d.get("ctx") == ctx:
+        if (d.get("model") == model and d.get("batch") == batch and d.get("ctx") == ctx
+                and int(d.get("quant", 0)) == quant):
             best = d.get("dram_bytes_per_launch")
     return best
 
@@ -470,7 +472,7 @@ def run_ours(args):
                 "frac": round(achieved / peak, 4), "peak_kind": peak_kind,
                 "frac_of_8TBs": round(achieved / 8000.0, 4),
                 "algorithmic_bytes_per_launch": algo // tp,
-                "traffic": ncu_traffic(args.model, args.batch, ctx) if tp == 1 else None,
+                "traffic": ncu_traffic(args.model, args.batch, ctx, args.quant) if tp == 1 else None,
                 "kernel": "ffb200::decode_step_kernel (1 persistent launch per step)",
             },
             "e2e": {"value": round(e2e_ms / args.batch, 5), "unit": UNIT,

@@ -21,8 +21,9 @@ sharded over the N ranks (head-split attention, column /
 row-split projections, vocabulary-split LM head), one process per GPU, the two
 per-layer residual exchanges and the argmax exchange done inside the
 persistent kernel over CUDA-IPC-mapped peer memory (NVLink P2P).  Total work
-is fixed ("scaling": "strong"); `value` = the max over ranks of the device
-time per token.  `--replicas` runs N independent whole-model replicas instead.
+is fixed ("scaling": "strong", N = 1 included: it is the same model on one
+GPU); `value` = the max over ranks of the device time per token.
+`--replicas` runs N independent whole-model replicas instead ("weak").
 """
 from __future__ import annotations
 
@@ -239,7 +240,7 @@ def run_reference(args):
         "impl": "reference", "metric": METRIC, "value": round(v, 3), "unit": UNIT,
         "n_gpus": args.gpus, "steps": base["steps_timed"], "warmup": 0,
         "ms_per_step": round(v * args.batch, 3), "higher_is_better": False,
-        "scaling": "strong" if tp > 1 else "weak", "vs_baseline": None, "dtype": "f64",
+        "scaling": "weak" if args.replicas else "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (shape-correct deterministic weights; values do not affect timing)",
         "config": bench_config(args, tp, world),
         "cpu_baseline": base,
@@ -456,7 +457,7 @@ def run_ours(args):
             "metric": METRIC, "value": round(ms / args.batch, 5), "unit": UNIT,
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": round(ms, 5), "higher_is_better": False,
-            "scaling": "strong" if tp > 1 else "weak", "vs_baseline": None,
+            "scaling": "weak" if args.replicas else "strong", "vs_baseline": None,
             "n_ranks_tp": tp,
             **({"tp_exchange": ("in-kernel over CUDA-IPC memory on the shared GPU" if share
                                 else "in-kernel over NVLink peer memory") if p2p_ok

@@ -61,6 +61,10 @@ struct ffb_model {
     // per-SM plan weights (ffb_calibrate): streamed-row shares of QKV / AOUT /
     // GLU / LM head proportional to each SM's measured streaming rate
     std::vector<double> sm_weight;
+    // LM-head row shares (ffb_calibrate, from the LM-head stage's own per-CTA
+    // times; used instead of sm_weight for calib_mask bit 3): its per-SM
+    // rates differ from the GLU's that sm_weight follows
+    std::vector<double> lm_weight;
     std::vector<CtaPlan> plan_host;
     int16_t* sm_rank = nullptr;       // device [max smid + 1] -> dense rank, or null
     int calib_mask = 0xf;             // option "calib_mask": matrices using the weights

@@ -300,10 +300,15 @@ ffb_status build_plan(ffb_model* m) {
         cum[k + 1] = cum[k] + m->sm_weight[m->plan_reverse ? G - 1 - k : k];
     // calib_mask bit 0/1/2/3: QKV / AOUT / GLU / LM head rows follow the
     // weights (the others split uniformly)
+    if ((int64_t)m->lm_weight.size() != G) m->lm_weight.assign(G, 1.0);
+    std::vector<double> cum_lm(G + 1, 0.0);
+    for (int64_t k = 0; k < G; ++k)
+        cum_lm[k + 1] = cum_lm[k] + m->lm_weight[m->plan_reverse ? G - 1 - k : k];
     auto wsplit_m = [&](int64_t units, int64_t k, int bit) {
         if (k >= G) return units;
         if (!((m->calib_mask >> bit) & 1)) return (units * k) / G;
-        return std::min<int64_t>(units, std::llround(units * cum[k] / cum[G]));
+        const std::vector<double>& cw = bit == 3 ? cum_lm : cum;
+        return std::min<int64_t>(units, std::llround(units * cw[k] / cw[G]));
     };
     // batch >= 8: row ranges in whole 8-row groups (the tcgen05 weight
     // layout, decode_kernel.cuh frag_off): QKV / GLU in units of 4 pairs
@@ -1694,6 +1699,7 @@ ffb_status ffb_calibrate(ffb_model* m, int32_t iterations) {
     const int G = m->grid;
     if (iterations == 0 || c.layers == 0) {  // back to the uniform plan
         m->sm_weight.assign(G, 1.0);
+        m->lm_weight.assign(G, 1.0);
     } else {
         const int64_t pos = m->kv_len[0];
         for (int64_t l = 0; l < c.layers; ++l)
@@ -1745,6 +1751,31 @@ ffb_status ffb_calibrate(ffb_model* m, int32_t iterations) {
             }
             for (int i = 0; i < G; ++i)
                 m->sm_weight[i] = std::min(1.3, std::max(0.7, m->sm_weight[i] * G / sum));
+            // LM head (the last trace stage): its own weights, from its own
+            // per-CTA times (dependency met -> done)
+            {
+                std::vector<double> tl(G, 0.0);
+                double tlm = 0;
+                int nl = 0;
+                for (int i = 0; i < G; ++i) {
+                    const uint64_t* r = &tr[((size_t)i * S + (S - 1)) * kTraceSlots];
+                    if (r[1] && r[2] > r[1]) {
+                        tl[i] = static_cast<double>(r[2] - r[1]);
+                        tlm += tl[i];
+                        ++nl;
+                    }
+                }
+                if (nl == G) {
+                    tlm /= nl;
+                    double ls = 0;
+                    for (int i = 0; i < G; ++i) {
+                        m->lm_weight[i] *= tlm / tl[i];
+                        ls += m->lm_weight[i];
+                    }
+                    for (int i = 0; i < G; ++i)
+                        m->lm_weight[i] = std::min(1.5, std::max(0.6, m->lm_weight[i] * G / ls));
+                }
+            }
             // a new plan changes per-head arrival counts: restart the epochs
             st = build_plan(m);
             if (!st) st = reset_sync_state(m, m->stream);

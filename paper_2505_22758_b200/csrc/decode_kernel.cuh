@@ -2494,10 +2494,13 @@ struct DecodeCta {
                 if (last) break;
             }
             trace_mark(l * kStagesPerLayer + S_ATTN, 3);
-            // CTA partial: (m, l) from st, o summed over the PG position groups
+            // CTA partial straight from the registers / stats to global (no
+            // smem staging, no barrier): (m, l) from st, o summed over the
+            // hi / lo rows of P
+            float* part = p.attn_part + ((size_t)unit * grid + pl.attn_g) * QPG * STR;
             if (ctid < QPG) {
-                mlc[2 * ctid] = st[ctid * 4 + 0];
-                mlc[2 * ctid + 1] = st[ctid * 4 + 1];
+                __stcg(part + ctid * STR, st[ctid * 4 + 0]);
+                __stcg(part + ctid * STR + 1, st[ctid * 4 + 1]);
             }
             // O[h][dim] = C[row h][dim] + C[row QPG + h][dim] (hi + lo of P):
             // QPG = 8: rows g / g + 8 of the same lane; QPG < 8: row g + QPG is
@@ -2512,27 +2515,26 @@ struct DecodeCta {
                         else ov[nt][e] = o[nt][e] + __shfl_xor_sync(0xffffffffu, o[nt][e], 4 * QPG);
                     }
             }
-            consumer_sync(NCT);  // q / scores / P / stats dead from here: wpart reused for O
             {
                 const int g = lane / 4, q4 = lane % 4;
                 if (g < QPG)
 #pragma unroll
                     for (int nt = 0; nt < NTW; ++nt)
-#pragma unroll
-                        for (int e = 0; e < 2; ++e)
-                            ro[g * DH + warp * DPW + nt * 8 + 2 * q4 + e] = ov[nt][e];
+                        __stcg(reinterpret_cast<float2*>(part + g * STR + 2 + warp * DPW + nt * 8 + 2 * q4),
+                               make_float2(ov[nt][0], ov[nt][1]));
             }
-            consumer_sync(NCT);
         }
-        float* part = p.attn_part + ((size_t)unit * grid + pl.attn_g) * QPG * STR;
-        for (int idx = ctid; idx < QPG * DH; idx += NCT) {
-            const int h = idx / DH, d = idx % DH;
-            const float O = ro[h * DH + d];
-            float* dst = part + h * STR;
-            __stcg(dst + 2 + d, O);
-            if (d == 0) {
-                __stcg(dst, mlc[2 * h]);
-                __stcg(dst + 1, mlc[2 * h + 1]);
+        if constexpr (T::ATT_WARP) {
+            float* part = p.attn_part + ((size_t)unit * grid + pl.attn_g) * QPG * STR;
+            for (int idx = ctid; idx < QPG * DH; idx += NCT) {
+                const int h = idx / DH, d = idx % DH;
+                const float O = ro[h * DH + d];
+                float* dst = part + h * STR;
+                __stcg(dst + 2 + d, O);
+                if (d == 0) {
+                    __stcg(dst, mlc[2 * h]);
+                    __stcg(dst + 1, mlc[2 * h + 1]);
+                }
             }
         }
         // The group's first CTA (attn_g == 0) combines (numerics.hpp:123-145):

@@ -136,3 +136,15 @@ if os.environ.get("GLUSPLIT"):
             if ok.any(): v.append(np.median((y - x)[ok]) / 1e3)
         return np.mean(v) if v else float("nan")
     print(f"glu: dep->ffn1 done {seg2(1, 3):.2f}  ffn1->done {seg2(3, 2):.2f} us")
+
+if os.environ.get("ATTNCTA"):  # q -> ring wait per CTA: by attention member index and by head
+    qr = np.stack([(tr[:, s, 6].astype(np.int64) - tr[:, s, 5].astype(np.int64)) for s in att], 1) / 1e3
+    dq = np.stack([(tr[:, s, 5].astype(np.int64) - tr[:, s, 1].astype(np.int64)) for s in att], 1) / 1e3
+    wt = np.stack([(tr[:, s, 1].astype(np.int64) - tr[:, s, 0].astype(np.int64)) for s in att], 1) / 1e3
+    ok = (tr[:, att[0], 5] > 0)
+    cta = np.arange(tr.shape[0])
+    for name, key in (("member", cta % 18), ("head", cta // 18)):
+        print(f"q->ring by {name}:", " ".join(f"{k}:{np.median(qr[ok & (key == k)]):.2f}" for k in range(int(key[ok].max()) + 1)))
+    print("attn dependency wait by head:", " ".join(f"{k}:{np.median(wt[ok & (cta // 18 == k)]):.2f}" for k in range(8)))
+    print(f"q->ring percentiles 10/50/90: {np.percentile(qr[ok], 10):.2f} {np.percentile(qr[ok], 50):.2f} {np.percentile(qr[ok], 90):.2f}; "
+          f"starve in QKV median {np.median(tr[ok, 0, 4]) / 1e3:.2f}")

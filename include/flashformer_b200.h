@@ -205,7 +205,11 @@ ffb_status ffb_set_mode(ffb_model *m, ffb_mode mode);
  * mode (0 disables; default 512 KiB).  "l2_prefetch_stages": 6-bit mask of
  * the stage types (bit s = stage s of a layer: 0 QKV, 1 ATTN, 2 AOUT, 3 GLU,
  * 4 RED; bit 5 = LM head) in which the prefetch may run, only while the ring
- * is full (default ATTN|AOUT = 0x6).  "attn_group_max": cap on the CTAs per
+ * is full (default ATTN|AOUT = 0x6).  "l2_prefetch_delay_ns": how long the
+ * prefetch window's burst is held after a layer's first K/V chunk is issued,
+ * so the attention's own K/V reaches HBM first (0..100000; default 4750 for
+ * the Llama-3.1-8B shape at batch 1-2 on one GPU, else 0).
+ * "attn_group_max": cap on the CTAs per
  * (batch row, kv head) split-K attention group (0 = min(grid / units, 32)).
  * Plan options (rebuild the per-CTA plan): "calib_mask", "plan_reverse",
  * "attn_group_max".  "stage_mask": 0x1f, or 0x07 / 0x18 for the component

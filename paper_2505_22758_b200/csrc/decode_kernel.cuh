@@ -123,6 +123,8 @@ struct DecodeParams {
     int64_t l2_prefetch; // bytes the L2 prefetch cursor runs ahead of the ring
     int32_t l2_pf_stages; // stage types (bit s % 5, bit 5 = LM head) where the
                           // producer may prefetch while its ring is full
+    int32_t l2_pf_delay_ns; // hold the prefetch window this long after the
+                            // layer's first K/V chunk is issued (0: no hold)
     // SM id -> dense rank (the CTA's plan index) for persistent launches, so
     // that a per-SM weighted plan (ffb_calibrate) follows the SM whatever
     // block index the launch put there; nullptr -> blockIdx.x
@@ -779,6 +781,8 @@ struct DecodeCta {
         bool pf_live = window > 0;
         int cur_stage = p.stage_begin;
         int dep_stage = -1;  // KCP: last stage whose dependency the producer waited for
+        int kv_stage = -1;   // l2_pf_delay_ns: last S_ATTN stage whose first chunk went out
+        uint64_t t_kv = 0;
         const void *s0, *s1;
         uint32_t bytes;
         int stage;
@@ -817,7 +821,20 @@ struct DecodeCta {
                 // ring full: issue the whole prefetch window at once (no
                 // waiting between prefetches), then block on the slot
                 const int stype = stage == p.layers * kStagesPerLayer ? 5 : stage % kStagesPerLayer;
-                if (((p.l2_pf_stages >> stype) & 1) && !mbar_test_wait(&empty[slot], ph ^ 1)) {
+                bool hold = false;
+                if (((p.l2_pf_stages >> stype) & 1) && !mbar_test_wait(&empty[slot], ph ^ 1) &&
+                    p.l2_pf_delay_ns > 0 && pf_live && ahead < window) {
+                    // the layer's own K/V loads (on the attention chain) go
+                    // to HBM ahead of the window's bulk: poll for the slot
+                    // until the hold time has passed since they were issued
+                    while (gtimer() - t_kv < static_cast<uint64_t>(p.l2_pf_delay_ns)) {
+                        if (mbar_test_wait(&empty[slot], ph ^ 1)) {
+                            hold = true;  // slot free: load it, prefetch at a later chunk
+                            break;
+                        }
+                    }
+                }
+                if (!hold && ((p.l2_pf_stages >> stype) & 1) && !mbar_test_wait(&empty[slot], ph ^ 1)) {
                     while (pf_live && ahead < window) {
                         const void *q0, *q1;
                         uint32_t qb;
@@ -835,6 +852,10 @@ struct DecodeCta {
                 ahead -= need;
             }
             chunk<DRAIN>(it, s0, s1, bytes, T::SLOT_BYTES / 2, policy);
+            if (!DRAIN && p.l2_pf_delay_ns > 0 && stage != kv_stage && stage % kStagesPerLayer == S_ATTN) {
+                kv_stage = stage;  // first K/V chunk of this layer issued
+                t_kv = gtimer();
+            }
         }
         // producer trace: L2-prefetched bytes of this launch (last stage, slot 5)
         // and the SM this CTA ran on (slot 6)

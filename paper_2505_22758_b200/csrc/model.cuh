@@ -55,6 +55,7 @@ struct ffb_model {
     // stage costs up to +8% (profiles/summary_r01.md)
     int64_t l2_prefetch = 512 << 10;
     int32_t l2_pf_stages = (1 << S_ATTN) | (1 << S_AOUT);
+    int32_t l2_pf_delay = 0;          // option "l2_prefetch_delay_ns"
     int32_t stage_mask = 0x1f;        // option "stage_mask" (component ablation)
     int plan_reverse = 0;             // weight slices assigned in reverse CTA order
     int attn_group_max = 0;           // option "attn_group_max": cap on CTAs per attention unit (0: auto)

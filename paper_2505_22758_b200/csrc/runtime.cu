@@ -466,6 +466,7 @@ DecodeParams make_params(const ffb_model* m, int64_t pos, const int64_t* d_token
     p.trace = m->trace;
     p.l2_prefetch = m->l2_prefetch;
     p.l2_pf_stages = m->l2_pf_stages;
+    p.l2_pf_delay_ns = m->l2_pf_delay;
     p.sm_rank = (m->mode == FFB_MODE_BASELINE || !m->use_sm_rank) ? nullptr : m->sm_rank;
     p.kind = m->cfg.kind;
     p.wlin = m->wlin;
@@ -1088,6 +1089,16 @@ ffb_status ffb_create_ex(const ffb_model_config* gcfg, int64_t max_seq_len, int 
     // stage streams KV through the ring the whole time: L2 prefetch measured
     // slower in both (int4 +5 %, b4 +7 %); on for bf16 batch 1-2 (-4 %)
     if (ops->QB != 0 || cfg->batch > 2) m->l2_prefetch = 0;
+    // Llama-3.1-8B-shaped bf16 decode, batch 1-2, one GPU: hold the window's
+    // burst 4.75 us after the layer's first K/V chunk is issued, so that the
+    // attention's own K/V (on the chain) is not queued behind ~76 MB of
+    // prefetch from every SM.  Same-box sweep (profiles/ab_r02e_pf_delay*.log):
+    // b1 2.794 -> 2.729-2.737 ms at 4.5-5 us (a smooth optimum, >= 1.5 %
+    // better over 4-5.5 us), b2 3.130 -> 3.063-3.068; other shapes keep 0
+    // (1B: +-0.3 % at any hold).
+    if (m->l2_prefetch > 0 && cfg->kind == 0 && cfg->d_model == 4096 && cfg->n_kv_heads == 8 &&
+        cfg->d_head == 128 && tp_size == 1)
+        m->l2_pf_delay = 4750;
 
     st = probe_sm_ranks(m);
     if (st) return bail(st);
@@ -1449,6 +1460,11 @@ ffb_status ffb_set_option(ffb_model* m, const char* key, int64_t value) {
         if (value != 0x1f && (m->cfg.kind != 0 || m->cfg.batch >= 8 || m->tp_size > 1))
             return fail(FFB_UNSUPPORTED, "stage_mask: single-GPU decoder, batch < 8");
         m->stage_mask = static_cast<int32_t>(value);
+        return FFB_OK;
+    }
+    if (std::strcmp(key, "l2_prefetch_delay_ns") == 0) {
+        if (value < 0 || value > 100000) return fail(FFB_USAGE, "l2_prefetch_delay_ns in [0, 100000]");
+        m->l2_pf_delay = static_cast<int32_t>(value);
         return FFB_OK;
     }
     if (std::strcmp(key, "l2_prefetch_stages") == 0) {

@@ -782,6 +782,9 @@ struct DecodeCta {
         int cur_stage = p.stage_begin;
         int dep_stage = -1;  // KCP: last stage whose dependency the producer waited for
         int kv_stage = -1;   // l2_pf_delay_ns: last S_ATTN stage whose first chunk went out
+#ifdef FFB_TRACE_PRODUCER
+        int pt_stage = -1;
+#endif
         uint64_t t_kv = 0;
         const void *s0, *s1;
         uint32_t bytes;
@@ -851,7 +854,24 @@ struct DecodeCta {
                 }
                 ahead -= need;
             }
+#ifdef FFB_TRACE_PRODUCER  // diagnostic build: when the K/V chunks go out (tools/trace_kv_issue.py)
+            const bool kvc = !DRAIN && p.trace != nullptr && stage % kStagesPerLayer == S_ATTN &&
+                             stage < p.layers * kStagesPerLayer;
+            const uint64_t tb = kvc ? gtimer() : 0;
+#endif
             chunk<DRAIN>(it, s0, s1, bytes, T::SLOT_BYTES / 2, policy);
+#ifdef FFB_TRACE_PRODUCER
+            if (kvc) {
+                uint64_t* t = p.trace + ((size_t)cta * n_stages() + stage - S_ATTN + S_AOUT) * kTraceSlots;
+                const uint64_t ta = gtimer();
+                if (stage != pt_stage) {
+                    t[5] = tb;
+                    t[6] = ta;
+                    pt_stage = stage;
+                }
+                t[7] = ta;
+            }
+#endif
             if (!DRAIN && p.l2_pf_delay_ns > 0 && stage != kv_stage && stage % kStagesPerLayer == S_ATTN) {
                 kv_stage = stage;  // first K/V chunk of this layer issued
                 t_kv = gtimer();

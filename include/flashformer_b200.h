@@ -208,7 +208,7 @@ ffb_status ffb_set_mode(ffb_model *m, ffb_mode mode);
  * is full (default ATTN|AOUT = 0x6).  "l2_prefetch_delay_ns": how long the
  * prefetch window's burst is held after a layer's first K/V chunk is issued,
  * so the attention's own K/V reaches HBM first (0..100000; default 4750 for
- * the Llama-3.1-8B shape at batch 1-2 on one GPU, else 0).
+ * the Llama-3.1-8B and Llama-3-70B shapes at batch 1-2 on one GPU, else 0).
  * "attn_group_max": cap on the CTAs per
  * (batch row, kv head) split-K attention group (0 = min(grid / units, 32)).
  * Plan options (rebuild the per-CTA plan): "calib_mask", "plan_reverse",

@@ -1095,9 +1095,11 @@ ffb_status ffb_create_ex(const ffb_model_config* gcfg, int64_t max_seq_len, int 
     // prefetch from every SM.  Same-box sweep (profiles/ab_r02e_pf_delay*.log):
     // b1 2.794 -> 2.729-2.737 ms at 4.5-5 us (a smooth optimum, >= 1.5 %
     // better over 4-5.5 us), b2 3.130 -> 3.063-3.068; other shapes keep 0
-    // (1B: +-0.3 % at any hold).
-    if (m->l2_prefetch > 0 && cfg->kind == 0 && cfg->d_model == 4096 && cfg->n_kv_heads == 8 &&
-        cfg->d_head == 128 && tp_size == 1)
+    // (1B: +-0.3 % at any hold).  The same hold at 8B contexts 512-8192:
+    // -1.1..-2.0 %; Llama-3-70B on one GPU: 22.56 -> 22.32 ms
+    // (profiles/ab_r02h_hold_ctx_70b.log).
+    if (m->l2_prefetch > 0 && cfg->kind == 0 && (cfg->d_model == 4096 || cfg->d_model == 8192) &&
+        cfg->n_kv_heads == 8 && cfg->d_head == 128 && tp_size == 1)
         m->l2_pf_delay = 4750;
 
     st = probe_sm_ranks(m);
